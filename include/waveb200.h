@@ -1,0 +1,179 @@
+/*
+ * waveb200 — C ABI of the B200-native superposed-adjoint hot path.
+ *
+ * The reference (waveopt, /root/reference/pkg/src/waveopt) has no native
+ * boundary: its hot loops are Numba functions called per time step from
+ * Python (kernels.py:136-152) inside the sweep loops of gradients.py and
+ * solver.py.  A per-step FFI call would serialise 2N host round trips, so
+ * this ABI exports SWEEP-level entry points that replace whole reference
+ * loops; per-step entries remain for propagate_step / run_backward.
+ *
+ * Conventions
+ *  - Plain C types only: host pointers + sizes.  Arrays are C-order
+ *    (axis 0 outermost, last axis contiguous), exactly numpy's default.
+ *  - Field dtype is chosen per context: itemsize 4 ("single") or 8
+ *    ("double"); void* field arrays use that dtype.  Costs, amplitudes,
+ *    measured traces and scalars are always double (fwi.py:57-63).
+ *  - A context owns its device buffers (gamma, two field levels,
+ *    accumulator — the four field buffers of gradients.py:302-303 — plus
+ *    compact support storage).  Calls are blocking and not thread-safe;
+ *    one context per GPU.
+ *  - Status codes mirror the CLI exit codes of cli.py:333-342.
+ */
+#ifndef WAVEB200_H
+#define WAVEB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WO_OK 0
+#define WO_ERR_CONFIG 1   /* ConfigError            (grids.py:20)  */
+#define WO_ERR_UNSTABLE 2 /* SolverInstabilityError (solver.py:34) */
+#define WO_ERR_BUDGET 3   /* ResourceBudgetError    (solver.py:44) */
+#define WO_ERR_CUDA 4     /* device / driver failure                */
+
+#define WO_RHO_SCALED 0   /* grids.py:99  */
+#define WO_ACOUSTIC 1     /* grids.py:100 */
+
+#define WO_SHOT_FWI 1     /* fwi.py:48-63  FwiShot  */
+#define WO_SHOT_TATO 2    /* tato.py:143-163 TatoShot */
+
+typedef struct wo_ctx wo_ctx;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int wo_version(void);
+/* Number of visible CUDA devices (0 when none). */
+int wo_device_count(void);
+/* Message of the last failed call on ctx (ctx == NULL: last wo_create). */
+const char* wo_last_error(const wo_ctx* ctx);
+
+/* Create a context for one grid (grids.py:31-72: 1 <= ndim <= 3) at one
+ * dtype on one device.  Replaces the allocations of gradients.py:302-303 and
+ * solver.py:138-143 (SolverWindow.zeros). */
+int wo_create(wo_ctx** out, int ndim, const int64_t* shape, double dx, int itemsize,
+              int device);
+/* Slab of a 3D grid for slab decomposition along axis 0: the context holds
+ * global planes [i_begin, i_end) plus one ghost plane on each side that has
+ * a neighbour. */
+int wo_create_slab(wo_ctx** out, const int64_t* global_shape, int64_t i_begin,
+                   int64_t i_end, double dx, int itemsize, int device);
+void wo_destroy(wo_ctx* ctx);
+
+/* Material: replaces prepare_material (solver.py:89-125).  gamma is fp64,
+ * C-order over the context's planes including ghosts (slab: planes
+ * [max(i_begin-1,0), min(i_end+1,n0)) ).  Coefficients are recomputed from
+ * gamma on the fly with the reference's exact operations.  ratio2 is the
+ * squared Courant-type ratio evaluated by the caller exactly as the
+ * reference does with Python's ** operator: (c0*dt/dx)**2 for rho_scaled
+ * (solver.py:96), (dt/dx)**2 for acoustic (solver.py:108). */
+int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, double rho1,
+                    double kappa1, double rho2, double kappa2, double dt, double ratio2);
+/* Kernel-increment scalars (gradients.py:117-129, kernels.py:149-152): the
+ * fp64 values cv, cg, 1/(2dt), 1/(2dx); cast to the field dtype here. */
+int wo_set_kernel_coefficients(wo_ctx* ctx, double cv, double cg, double inv2dt,
+                               double inv2dx);
+/* Support nodes (sensor or objective-region flat indices, strictly
+ * increasing, local to the context).  Device support order = this order. */
+int wo_set_support(wo_ctx* ctx, int64_t n_sup, const int64_t* flat_sorted);
+
+/* Window management (solver.py:128-151). */
+int wo_reset_window(wo_ctx* ctx);                                  /* u^0 = u^1 = 0 */
+int wo_set_window(wo_ctx* ctx, const void* u_prev, const void* u_cur);
+int wo_get_window(wo_ctx* ctx, void* u_prev, void* u_cur);
+int wo_swap_direction(wo_ctx* ctx);                                /* solver.py:149 */
+int wo_zero_accumulator(wo_ctx* ctx);
+int wo_get_accumulator(wo_ctx* ctx, void* out);
+int wo_set_accumulator(wo_ctx* ctx, const void* in);
+
+#define WO_FWD_ACCUMULATE 1 /* subtract the self-kernel (superposed engine) */
+#define WO_FWD_HISTORY 2    /* keep all N+1 levels on the device (reference engine) */
+
+/* Forward sweep n = 1..N-1 (gradients.py:214-250 _forward_pass;
+ * solver.py:282-340 run_forward): steps the window, injects the sources
+ * (src_flat[n_src], amplitudes src_amp[n_src][N] in fp64), records u^n on
+ * the support into the compact store when a support is set, subtracts the
+ * self-kernel when flags & WO_FWD_ACCUMULATE (sdt = -dt), records the full
+ * history when flags & WO_FWD_HISTORY, and checks stability every 50 steps
+ * and at the last one against 1e6*scale (scale <= 0: finiteness only).  On
+ * WO_ERR_UNSTABLE, *fail_step / *fail_max hold the first failing check.
+ * *peak_out = max over the checks. */
+int wo_sweep_forward(wo_ctx* ctx, int64_t n_steps, int n_src, const int64_t* src_flat,
+                     const double* src_amp, int flags, double dt, double scale,
+                     double* peak_out, int64_t* fail_step, double* fail_max);
+/* Standard-adjoint sweep of gradient_reference (gradients.py:371-386) using
+ * the recorded history and the unscaled compact adjoint store; accumulates
+ * the mixed kernel.  wo_free_history releases the history buffer. */
+int wo_sweep_adjoint_reference(wo_ctx* ctx, int64_t n_steps, double dt, int64_t* fail_step,
+                               double* fail_max);
+int wo_free_history(wo_ctx* ctx);
+
+/* Per-step shot cost and compact adjoint store from the recorded support
+ * values (fwi.py:57-63, tato.py:154-163, gradients.py:231-239, 263):
+ * cost_n = (((c1*dot)*c2)*c3)/c4; FWI uses measured[n_sup][N] (device
+ * support order), TATO adj = adj_coef*u.  When write_adj, the store becomes
+ * T(adj)*T(k).  *cost_out = sum over n in order. */
+int wo_shot_misfit(wo_ctx* ctx, int64_t n_steps, int kind, const double* measured,
+                   double c1, double c2, double c3, double c4, double adj_coef, int write_adj,
+                   double k, double* cost_out);
+/* Copy the compact store [N][n_sup] (traces, or adjoint after misfit). */
+int wo_get_store(wo_ctx* ctx, int64_t n_steps, void* out);
+
+/* Backward superposed sweep n = N-1..1 (gradients.py:253-281) on the
+ * swapped window: step + source + support injection of the k-scaled store
+ * + self-kernel (sdt = +dt); stability checked every 50 steps and at n=1. */
+int wo_sweep_backward(wo_ctx* ctx, int64_t n_steps, int64_t src_flat, const double* src_amp,
+                      int inject_support, int accumulate, double dt, int64_t* fail_step,
+                      double* fail_max);
+
+/* acc /= T(2k) in place, then copy out (gradients.py:315). */
+int wo_get_gradient(wo_ctx* ctx, double two_k, void* out);
+
+/* One explicit step with an optional sparse (idx, vals) or dense (fp64
+ * field) force and a finiteness max (solver.py:173-177, 189-202; the
+ * backward replay of solver.py:343-372).  Rotates the window. */
+int wo_step(wo_ctx* ctx, int64_t n_force, const int64_t* idx, const double* vals,
+            const double* dense_force, int want_max, double* max_out);
+
+/* Literal per-step drop-ins for kernels.apply_step / apply_kernel_increment
+ * (kernels.py:136-152) on host arrays with precomputed face weights. */
+int wo_apply_step(int ndim, const int64_t* shape, int itemsize, const void* u_prev,
+                  const void* u_cur, const void* wf0, const void* wf1, const void* wf2,
+                  const void* coef, void* out, int device);
+int wo_apply_kernel_increment(int ndim, const int64_t* shape, int itemsize, void* acc,
+                              const void* a_old, const void* a_mid, const void* a_new,
+                              const void* b_old, const void* b_mid, const void* b_new,
+                              double cv, double cg, double inv2dt, double inv2dx, double sdt,
+                              int device);
+
+/* Topology-optimisation design chain in fp64 (tato.py:61-140), host arrays
+ * in/out.  The filter footprint (offsets [n_fp][ndim], weights [n_fp]) is
+ * the non-zero part of the linear-decay kernel in C order; mask may be NULL
+ * (everything in the design region).
+ *   wo_design_filter  density_filter     (tato.py:78-94, bit-exact sums)
+ *   wo_design_project heaviside_project + design masking (tato.py:97-108, 226);
+ *                     t_be = tanh(beta*eta), denom = t_be + tanh(beta*(1-eta))
+ *   wo_design_chain   chain_rule         (tato.py:124-140) */
+int wo_design_filter(int ndim, const int64_t* shape, const double* gamma,
+                     const unsigned char* mask, int n_fp, const int* offsets,
+                     const double* weights, double* out, int device);
+int wo_design_project(int64_t n, const double* g_tilde, double beta, double eta, double t_be,
+                      double denom, const unsigned char* mask, double* out, int device);
+int wo_design_chain(int ndim, const int64_t* shape, const double* dcdbar, const double* g_tilde,
+                    double beta, double eta, double denom, const unsigned char* mask, int n_fp,
+                    const int* offsets, const double* weights, double* out, int device);
+
+/* Profiling: when on, every fused step launch is bracketed by CUDA events
+ * on the context stream; wo_stats returns launches and summed kernel ms. */
+int wo_set_profiling(wo_ctx* ctx, int on);
+int wo_stats(wo_ctx* ctx, int64_t* launches, int64_t* step_launches, double* step_kernel_ms);
+int wo_reset_stats(wo_ctx* ctx);
+/* Device bytes held by the context (fields + support storage). */
+int64_t wo_device_bytes(const wo_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WAVEB200_H */

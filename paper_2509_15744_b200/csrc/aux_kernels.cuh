@@ -1,0 +1,108 @@
+// Small per-shot / per-sweep kernels around the fused step:
+//   misfit_kernel   fwi.py:57-63, tato.py:154-163 — per-step shot cost (fp64)
+//                   and the k-scaled adjoint store (gradients.py:239, 263)
+//   cost_sum_kernel gradients.py:231-238 — sequential per-step cost sum
+//   scale_div_kernel gradients.py:315 — acc /= T(2k)
+//   inject_kernel   solver.py:167-170 — sparse nodal += for >MAX_SRC nodes
+//   dense_force_kernel solver.py:163-165 — out += fc * T(force)
+#pragma once
+
+#include "common.cuh"
+
+namespace wb {
+
+enum ShotKind : int { SHOT_NONE = 0, SHOT_FWI = 1, SHOT_TATO = 2 };
+
+// One block per time step n.  store is [N][n_sup] (row n = trace entry n,
+// i.e. u^n on the support, device support order).  measured is [n_sup][N]
+// fp64 (the reference's layout, rows permuted to device support order).
+// cost_n = (((c1 * dot) * c2) * c3) / c4 with
+//   FWI : dot = sum r^2, r = double(u) - measured ; (c1..c4) = (0.5, dt, 1, 1)
+//   TATO: dot = sum u^2                           ; (sign, cell, dt, area)
+// adj (written in place over the trace when write_adj):
+//   FWI : T(-r) * T(k)      TATO: T(adj_coef * double(u)) * T(k)
+template <typename T>
+__global__ void misfit_kernel(T* store, const double* measured, long long n_steps, int n_sup,
+                              int kind, double c1, double c2, double c3, double c4,
+                              double adj_coef, int write_adj, T k_t, double* partial) {
+    __shared__ double sred[256];
+    const long long n = blockIdx.x;
+    double dot = 0.0;
+    // per-thread partial sums in a fixed order, then a fixed tree: deterministic
+    for (int s = threadIdx.x; s < n_sup; s += blockDim.x) {
+        const double u = (double)store[n * n_sup + s];
+        double v;
+        if (kind == SHOT_FWI) {
+            const double r = u - measured[(long long)s * n_steps + n];
+            dot += r * r;
+            v = -r;
+        } else {
+            dot += u * u;
+            v = adj_coef * u;
+        }
+        if (write_adj) store[n * n_sup + s] = (n == 0) ? T(0) : (T)v * k_t;
+    }
+    sred[threadIdx.x] = dot;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sred[threadIdx.x] += sred[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[n] = (((c1 * sred[0]) * c2) * c3) / c4;
+}
+
+__global__ void cost_sum_kernel(const double* partial, long long n_steps, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double c = 0.0;
+        for (long long n = 0; n < n_steps; ++n) c = (n == 0) ? partial[0] : c + partial[n];
+        *out = c;
+    }
+}
+
+template <typename T>
+__global__ void scale_div_kernel(T* acc, long long n, T denom) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        acc[i] = FTraits<T>::div(acc[i], denom);
+}
+
+// out[idx[s]] += fc[idx[s]] * vals[s] for deduplicated idx (last occurrence
+// kept by the host, matching numpy fancy-index +=).
+template <typename T>
+__global__ void inject_kernel(T* out, const T* gamma, MatScalars<T> M, const long long* idx,
+                              const T* vals, int n) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const long long c = idx[s];
+    T kappa;
+    (void)mat_coef(M, gamma[c], kappa);
+    out[c] = out[c] + mat_fc(M, gamma[c], kappa) * vals[s];
+}
+
+template <typename T>
+__global__ void dense_force_kernel(T* out, const T* gamma, MatScalars<T> M, const double* f,
+                                   long long n) {
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+         c += (long long)gridDim.x * blockDim.x) {
+        T kappa;
+        (void)mat_coef(M, gamma[c], kappa);
+        out[c] = out[c] + mat_fc(M, gamma[c], kappa) * (T)f[c];
+    }
+}
+
+template <typename T>
+__global__ void max_abs_kernel(const T* u, long long n, typename FTraits<T>::Bits* slot) {
+    typename FTraits<T>::Bits m = 0;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+         c += (long long)gridDim.x * blockDim.x) {
+        typename FTraits<T>::Bits b = FTraits<T>::abs_bits(u[c]);
+        m = b > m ? b : m;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        typename FTraits<T>::Bits v = __shfl_xor_sync(0xffffffffu, m, o);
+        m = v > m ? v : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(slot, m);
+}
+
+}  // namespace wb

@@ -1,0 +1,1131 @@
+// waveb200 C ABI implementation (include/waveb200.h).
+//
+// Host-side driver of the fused sweeps: owns the device buffers of one grid,
+// builds the per-step launch arguments (pointer rotation of the 3-level
+// window, source values, support rows, check slots) and evaluates the
+// stability checks after each sweep in the reference's order.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/waveb200.h"
+#include "aux_kernels.cuh"
+#include "common.cuh"
+#include "design_kernels.cuh"
+#include "dropin_kernels.cuh"
+#include "step_kernel.cuh"
+
+using namespace wb;
+
+namespace {
+
+constexpr int STABILITY_CHECK_INTERVAL = 50;     // solver.py:29
+constexpr double STABILITY_GROWTH_FACTOR = 1e6;  // solver.py:30
+thread_local std::string g_create_error;
+
+}  // namespace
+
+struct wo_ctx {
+    int device = 0;
+    int ndim = 0;
+    int64_t shape[3] = {1, 1, 1};      // caller's shape (local for slabs)
+    int kn0 = 1, kn1 = 1, kn2 = 1;     // kernel-space local extents
+    int i_off = 0, n0g = 1;            // slab placement along axis 0
+    int has_lo = 0, has_hi = 0;        // ghost planes present
+    int itemsize = 8;
+    double dx = 0.0;
+    cudaStream_t stream = nullptr;
+
+    char* gamma = nullptr;             // allocation bases (ghost planes first)
+    char* u[2] = {nullptr, nullptr};
+    char* acc = nullptr;
+    int cur = 0;                       // u[cur] = u^n, u[1-cur] = u^{n-1}
+
+    bool material_set = false;
+    int flavor = 0;
+    double rho0 = 0, rho1 = 0, kappa1 = 0, rho2 = 0, kappa2 = 0, dt_mat = 0, ratio2 = 0;
+    double cv = 0, cg = 0, inv2dt = 0, inv2dx = 0;
+
+    int64_t n_sup = 0;
+    unsigned int* mask = nullptr;
+    int* prefix = nullptr;
+    char* store = nullptr;
+    size_t store_bytes = 0;
+    double* measured = nullptr;
+    size_t measured_bytes = 0;
+    double* partial = nullptr;
+    size_t partial_bytes = 0;
+    double* cost = nullptr;
+    char* maxslots = nullptr;
+    size_t maxslot_bytes = 0;
+    long long* f_idx = nullptr;
+    size_t f_idx_cap = 0;
+    char* f_vals = nullptr;
+    size_t f_vals_cap = 0;
+    double* f_dense = nullptr;
+    size_t f_dense_cap = 0;
+    char* hist = nullptr;              // full forward history (reference engine)
+    size_t hist_bytes = 0;
+    char* u3 = nullptr;                // third adjoint level (reference engine)
+    size_t u3_bytes = 0;
+
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_free, ev_used;
+    int64_t launches = 0, step_launches = 0;
+    double step_ms = 0.0;
+    int64_t dev_bytes = 0;
+    std::string err;
+
+    int64_t plane() const { return (int64_t)kn1 * kn2; }
+    int64_t cells() const { return (int64_t)kn0 * plane(); }
+    int64_t alloc_cells() const { return (int64_t)(kn0 + has_lo + has_hi) * plane(); }
+    size_t field_bytes() const { return (size_t)cells() * itemsize; }
+    char* base0(char* p) const { return p + (size_t)has_lo * plane() * itemsize; }
+    char* ucur() const { return base0(u[cur]); }
+    char* uprev() const { return base0(u[1 - cur]); }
+};
+
+#define CK(call)                                                                     \
+    do {                                                                             \
+        cudaError_t e_ = (call);                                                     \
+        if (e_ != cudaSuccess) {                                                     \
+            ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);           \
+            return WO_ERR_CUDA;                                                      \
+        }                                                                            \
+    } while (0)
+
+#define REQUIRE(cond, msg)                   \
+    do {                                     \
+        if (!(cond)) {                       \
+            ctx->err = (msg);                \
+            return WO_ERR_CONFIG;            \
+        }                                    \
+    } while (0)
+
+namespace {
+
+int dev_alloc(wo_ctx* ctx, void** p, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+        ctx->err = std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e);
+        return e == cudaErrorMemoryAllocation ? WO_ERR_BUDGET : WO_ERR_CUDA;
+    }
+    ctx->dev_bytes += (int64_t)bytes;
+    return WO_OK;
+}
+
+template <typename P>
+int ensure(wo_ctx* ctx, P** p, size_t* cap, size_t bytes) {
+    if (*cap >= bytes && *p) return WO_OK;
+    if (*p) {
+        cudaFree(*p);
+        ctx->dev_bytes -= (int64_t)*cap;
+    }
+    *p = nullptr;
+    *cap = 0;
+    int rc = dev_alloc(ctx, (void**)p, bytes);
+    if (rc == WO_OK) *cap = bytes;
+    return rc;
+}
+
+template <typename T>
+MatScalars<T> mat_scalars(const wo_ctx* ctx) {
+    MatScalars<T> M{};
+    M.flavor = ctx->flavor;
+    const double dt = ctx->dt_mat;
+    if (ctx->flavor == RHO_SCALED) {
+        const T r2 = (T)ctx->ratio2;          // dtype.type((c0*dt/dx)**2), solver.py:96
+        M.two_r2 = T(2) * r2;                 // dtype.type(2.0) * r2, solver.py:97
+        M.rho0 = (T)ctx->rho0;
+    } else {
+        M.irho1 = (T)(1.0 / ctx->rho1);       // grids.py:252 (python floats, then weak cast)
+        M.drho = (T)(1.0 / ctx->rho2 - 1.0 / ctx->rho1);
+        M.ikap1 = (T)(1.0 / ctx->kappa1);
+        M.dkap = (T)(1.0 / ctx->kappa2 - 1.0 / ctx->kappa1);
+        M.s2 = (T)ctx->ratio2;                // dtype.type((dt/dx)**2), solver.py:108
+    }
+    M.dt2 = (T)(dt * dt);
+    return M;
+}
+
+int choose_chunk(const wo_ctx* ctx) {
+    const int tiles = ((ctx->kn2 + BX - 1) / BX) * ((ctx->kn1 + BY - 1) / BY);
+    const int target = 148 * 8;  // CTAs in flight we aim to offer per launch
+    int nz = std::max(1, target / std::max(1, tiles));
+    int chunk = (ctx->kn0 + nz - 1) / nz;
+    chunk = std::max(chunk, std::min(ctx->kn0, 16));
+    return std::max(chunk, 1);
+}
+
+cudaEvent_t take_event(wo_ctx* ctx) {
+    cudaEvent_t e;
+    if (!ctx->ev_free.empty()) {
+        e = ctx->ev_free.back();
+        ctx->ev_free.pop_back();
+    } else {
+        cudaEventCreate(&e);
+    }
+    ctx->ev_used.push_back(e);
+    return e;
+}
+
+// after a stream sync: fold the bracketed step-kernel times into the stats
+void harvest_events(wo_ctx* ctx) {
+    for (size_t i = 0; i + 1 < ctx->ev_used.size(); i += 2) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, ctx->ev_used[i], ctx->ev_used[i + 1]) == cudaSuccess)
+            ctx->step_ms += ms;
+    }
+    for (auto e : ctx->ev_used) ctx->ev_free.push_back(e);
+    ctx->ev_used.clear();
+}
+
+struct StepSpec {
+    bool acc = false;
+    bool check = false;
+    int backward = 0;
+    double sdt = 0.0;
+    int n_src = 0;
+    const long long* src_flat = nullptr;
+    const double* src_val = nullptr;   // fp64 values, cast to T here
+    int sup_mode = SUP_NONE;
+    int64_t row = 0;                   // store row (trace entry / adjoint step)
+    int64_t slot = 0;                  // max slot index
+    char* prev = nullptr;              // overrides of the window pointers
+    char* cur = nullptr;
+    char* out = nullptr;
+    char* hist = nullptr;              // history row receiving a copy of out
+};
+
+template <typename T>
+int launch_step(wo_ctx* ctx, const StepSpec& sp) {
+    StepArgs<T> a{};
+    a.gamma = reinterpret_cast<const T*>(ctx->base0(ctx->gamma));
+    a.u_prev = reinterpret_cast<const T*>(sp.prev ? sp.prev : ctx->uprev());
+    a.u_cur = reinterpret_cast<const T*>(sp.cur ? sp.cur : ctx->ucur());
+    a.u_out = reinterpret_cast<T*>(sp.out ? sp.out : ctx->uprev());
+    a.hist_out = reinterpret_cast<T*>(sp.hist);
+    a.acc = reinterpret_cast<T*>(ctx->acc);
+    a.n0 = ctx->kn0;
+    a.n1 = ctx->kn1;
+    a.n2 = ctx->kn2;
+    a.i_off = ctx->i_off;
+    a.n0g = ctx->n0g;
+    a.chunk = choose_chunk(ctx);
+    a.mat = mat_scalars<T>(ctx);
+    a.cv = (T)ctx->cv;
+    a.cg = (T)ctx->cg;
+    a.inv2dt = (T)ctx->inv2dt;
+    a.inv2dx = (T)ctx->inv2dx;
+    a.sdt = (T)sp.sdt;
+    a.backward = sp.backward;
+    a.n_src = sp.n_src;
+    for (int s = 0; s < sp.n_src; ++s) {
+        a.src_flat[s] = sp.src_flat[s];
+        a.src_val[s] = (T)sp.src_val[s];
+    }
+    a.sup_mode = sp.sup_mode;
+    a.sup_mask = ctx->mask;
+    a.sup_prefix = ctx->prefix;
+    if (sp.sup_mode != SUP_NONE) {
+        T* st = reinterpret_cast<T*>(ctx->store) + sp.row * ctx->n_sup;
+        a.trace_row = st;
+        a.adj_row = st;
+    }
+    a.max_slot = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots) + sp.slot;
+
+    dim3 block(BX, BY, 1);
+    dim3 grid((ctx->kn2 + BX - 1) / BX, (ctx->kn1 + BY - 1) / BY,
+              (ctx->kn0 + a.chunk - 1) / a.chunk);
+    const bool one_d = ctx->ndim == 1;
+    if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
+#define LAUNCH(ACC, CHK, ONED) step_kernel<T, ACC, CHK, ONED><<<grid, block, 0, ctx->stream>>>(a)
+    if (sp.acc) {
+        if (sp.check) { if (one_d) LAUNCH(true, true, true); else LAUNCH(true, true, false); }
+        else { if (one_d) LAUNCH(true, false, true); else LAUNCH(true, false, false); }
+    } else {
+        if (sp.check) { if (one_d) LAUNCH(false, true, true); else LAUNCH(false, true, false); }
+        else { if (one_d) LAUNCH(false, false, true); else LAUNCH(false, false, false); }
+    }
+#undef LAUNCH
+    if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
+    ctx->launches++;
+    ctx->step_launches++;
+    CK(cudaGetLastError());
+    return WO_OK;
+}
+
+template <typename T>
+double slot_value(const char* host_slots, int64_t idx) {
+    using Bits = typename FTraits<T>::Bits;
+    Bits b;
+    std::memcpy(&b, host_slots + idx * sizeof(Bits), sizeof(Bits));
+    T v;
+    std::memcpy(&v, &b, sizeof(T));
+    return (double)v;
+}
+
+// deduplicate nodal injections, keeping the LAST occurrence of a node
+// (numpy fancy-index += semantics, solver.py:170)
+void dedupe_last(int n, const int64_t* idx, std::vector<long long>& out_idx,
+                 std::vector<int>& out_pos) {
+    out_idx.clear();
+    out_pos.clear();
+    for (int s = 0; s < n; ++s) {
+        bool later = false;
+        for (int t = s + 1; t < n; ++t)
+            if (idx[t] == idx[s]) { later = true; break; }
+        if (!later) {
+            out_idx.push_back((long long)idx[s]);
+            out_pos.push_back(s);
+        }
+    }
+}
+
+int check_ctx(wo_ctx* ctx) {
+    if (!ctx) return WO_ERR_CONFIG;
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) {
+        ctx->err = cudaGetErrorString(e);
+        return WO_ERR_CUDA;
+    }
+    return WO_OK;
+}
+
+int ensure_slots(wo_ctx* ctx, int64_t n) {
+    return ensure(ctx, &ctx->maxslots, &ctx->maxslot_bytes, (size_t)(n + 2) * 8);
+}
+
+template <typename T>
+int inject_host_list(wo_ctx* ctx, int n, const long long* idx, const double* vals) {
+    // > MAX_SRC nodes: separate injection kernel after the step (no kernel
+    // increment follows in these modes, so the order matches solver.py:173-177)
+    int rc = ensure(ctx, &ctx->f_idx, &ctx->f_idx_cap, (size_t)n * 8);
+    if (rc) return rc;
+    rc = ensure(ctx, &ctx->f_vals, &ctx->f_vals_cap, (size_t)n * sizeof(T));
+    if (rc) return rc;
+    std::vector<T> tv(n);
+    for (int s = 0; s < n; ++s) tv[s] = (T)vals[s];
+    CK(cudaMemcpyAsync(ctx->f_idx, idx, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->f_vals, tv.data(), (size_t)n * sizeof(T), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    // u_out was written into the prev buffer; after rotation it is ucur
+    inject_kernel<T><<<(n + 127) / 128, 128, 0, ctx->stream>>>(
+        reinterpret_cast<T*>(ctx->uprev()), reinterpret_cast<const T*>(ctx->base0(ctx->gamma)),
+        mat_scalars<T>(ctx), ctx->f_idx, reinterpret_cast<const T*>(ctx->f_vals), n);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));  // host vector lifetime
+    return WO_OK;
+}
+
+template <typename T>
+int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
+                    const double* src_amp, int flags, double dt, double scale,
+                    double* peak_out, int64_t* fail_step, double* fail_max) {
+    const int accumulate = flags & WO_FWD_ACCUMULATE;
+    const bool record = (flags & WO_FWD_HISTORY) != 0;
+    if (record) {
+        REQUIRE(!ctx->has_lo && !ctx->has_hi, "history recording is single-domain only");
+        int rc0 = ensure(ctx, &ctx->hist, &ctx->hist_bytes, (size_t)(N + 1) * ctx->field_bytes());
+        if (rc0) return rc0;
+        // history[0] = u_prev, history[1] = u_cur (gradients.py:233-235)
+        CK(cudaMemcpyAsync(ctx->hist, ctx->uprev(), ctx->field_bytes(), cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+        CK(cudaMemcpyAsync(ctx->hist + ctx->field_bytes(), ctx->ucur(), ctx->field_bytes(),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    std::vector<long long> sidx;
+    std::vector<int> spos;
+    dedupe_last(n_src, src_flat, sidx, spos);
+    const int ns = (int)sidx.size();
+    REQUIRE(ns <= MAX_SRC || !accumulate, "at most 8 source nodes per accumulating sweep");
+    int rc = ensure_slots(ctx, N);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(ctx->maxslots, 0, (size_t)(N + 2) * 8, ctx->stream));
+    const bool gather = ctx->n_sup > 0;
+    if (gather) {
+        rc = ensure(ctx, &ctx->store, &ctx->store_bytes, (size_t)N * ctx->n_sup * sizeof(T));
+        if (rc) return rc;
+        CK(cudaMemsetAsync(ctx->store, 0, (size_t)N * ctx->n_sup * sizeof(T), ctx->stream));
+    }
+    std::vector<double> vals(std::max(ns, 1));
+    for (int64_t n = 1; n < N; ++n) {
+        StepSpec sp;
+        sp.acc = accumulate != 0;
+        sp.check = (n % STABILITY_CHECK_INTERVAL == 0) || (n == N - 1);
+        sp.backward = 0;
+        sp.sdt = -dt;
+        for (int s = 0; s < ns; ++s) vals[s] = src_amp[(int64_t)spos[s] * N + n];
+        const bool in_kernel = ns <= MAX_SRC;
+        sp.n_src = in_kernel ? ns : 0;
+        sp.src_flat = sidx.data();
+        sp.src_val = vals.data();
+        sp.sup_mode = gather ? SUP_GATHER : SUP_NONE;
+        sp.row = n;
+        sp.slot = n;
+        if (record) {
+            REQUIRE(in_kernel, "history recording supports at most 8 source nodes");
+            sp.hist = ctx->hist + (size_t)(n + 1) * ctx->field_bytes();
+        }
+        if (!in_kernel && sp.check) {
+            // stability max must see the injected values: check separately
+            sp.check = false;
+            rc = launch_step<T>(ctx, sp);
+            if (rc) return rc;
+            rc = inject_host_list<T>(ctx, ns, sidx.data(), vals.data());
+            if (rc) return rc;
+            max_abs_kernel<T><<<296, 256, 0, ctx->stream>>>(
+                reinterpret_cast<const T*>(ctx->uprev()), ctx->cells(),
+                reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots) + n);
+            ctx->launches++;
+        } else {
+            rc = launch_step<T>(ctx, sp);
+            if (rc) return rc;
+            if (!in_kernel) {
+                rc = inject_host_list<T>(ctx, ns, sidx.data(), vals.data());
+                if (rc) return rc;
+            }
+        }
+        ctx->cur = 1 - ctx->cur;  // rotate (u^{n+1} was written over u^{n-1})
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->prof) harvest_events(ctx);
+    std::vector<char> hs((size_t)(N + 2) * 8);
+    CK(cudaMemcpy(hs.data(), ctx->maxslots, hs.size(), cudaMemcpyDeviceToHost));
+    double peak = 0.0;
+    for (int64_t n = 1; n < N; ++n) {
+        if (!((n % STABILITY_CHECK_INTERVAL == 0) || (n == N - 1))) continue;
+        const double m = slot_value<T>(hs.data(), n);
+        if (!std::isfinite(m) || (scale > 0.0 && m > STABILITY_GROWTH_FACTOR * scale)) {
+            *fail_step = n + 1;
+            *fail_max = m;
+            ctx->err = "unstable field";
+            return WO_ERR_UNSTABLE;
+        }
+        peak = std::max(peak, m);
+    }
+    if (peak_out) *peak_out = peak;
+    return WO_OK;
+}
+
+template <typename T>
+int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src_amp,
+                     int inject, int accumulate, double dt, int64_t* fail_step,
+                     double* fail_max) {
+    REQUIRE(!inject || ctx->n_sup > 0, "backward support injection without a support");
+    REQUIRE(!inject || ctx->store_bytes >= (size_t)N * ctx->n_sup * sizeof(T),
+            "adjoint store not populated for this N");
+    int rc = ensure_slots(ctx, N);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(ctx->maxslots, 0, (size_t)(N + 2) * 8, ctx->stream));
+    ctx->cur = 1 - ctx->cur;  // swap_direction: u_prev <- u^N, u_cur <- u^{N-1}
+    long long sf = (long long)src_flat;
+    double val = 0.0;
+    for (int64_t n = N - 1; n >= 1; --n) {
+        StepSpec sp;
+        sp.acc = accumulate != 0;
+        sp.check = (n % STABILITY_CHECK_INTERVAL == 0) || (n == 1);
+        sp.backward = 1;
+        sp.sdt = dt;
+        if (src_flat >= 0) {
+            val = src_amp[n];
+            sp.n_src = 1;
+            sp.src_flat = &sf;
+            sp.src_val = &val;
+        }
+        sp.sup_mode = inject ? SUP_INJECT : SUP_NONE;
+        sp.row = n;
+        sp.slot = n;
+        rc = launch_step<T>(ctx, sp);
+        if (rc) return rc;
+        ctx->cur = 1 - ctx->cur;
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->prof) harvest_events(ctx);
+    std::vector<char> hs((size_t)(N + 2) * 8);
+    CK(cudaMemcpy(hs.data(), ctx->maxslots, hs.size(), cudaMemcpyDeviceToHost));
+    for (int64_t n = N - 1; n >= 1; --n) {
+        if (!((n % STABILITY_CHECK_INTERVAL == 0) || (n == 1))) continue;
+        const double m = slot_value<T>(hs.data(), n);
+        if (!std::isfinite(m)) {
+            *fail_step = n - 1;
+            *fail_max = m;
+            ctx->err = "unstable field";
+            return WO_ERR_UNSTABLE;
+        }
+    }
+    return WO_OK;
+}
+
+// gradient_reference adjoint sweep (gradients.py:371-386): a separate
+// 3-level adjoint window from zero end conditions, no source, support
+// injection of the UNSCALED adjoint store, mixed increment against the
+// recorded forward history.
+template <typename T>
+int sweep_adjoint_reference_t(wo_ctx* ctx, int64_t N, double dt, int64_t* fail_step,
+                              double* fail_max) {
+    REQUIRE(ctx->hist_bytes >= (size_t)(N + 1) * ctx->field_bytes(), "no forward history recorded");
+    REQUIRE(ctx->n_sup > 0 && ctx->store_bytes >= (size_t)N * ctx->n_sup * sizeof(T),
+            "adjoint store not populated");
+    int rc = ensure(ctx, &ctx->u3, &ctx->u3_bytes, ctx->field_bytes());
+    if (rc) return rc;
+    rc = ensure_slots(ctx, N);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(ctx->maxslots, 0, (size_t)(N + 2) * 8, ctx->stream));
+    char* lv[3] = {ctx->uprev(), ctx->ucur(), ctx->u3};   // (prev, cur, next)
+    for (char* p : lv) CK(cudaMemsetAsync(p, 0, ctx->field_bytes(), ctx->stream));
+    int n0, n1, n2;
+    n0 = ctx->kn0; n1 = ctx->kn1; n2 = ctx->kn2;
+    const size_t fb = ctx->field_bytes();
+    for (int64_t n = N - 1; n >= 1; --n) {
+        StepSpec sp;
+        sp.check = (n % STABILITY_CHECK_INTERVAL == 0) || (n == 1);
+        sp.sup_mode = SUP_INJECT;
+        sp.row = n;
+        sp.slot = n;
+        sp.prev = lv[0];
+        sp.cur = lv[1];
+        sp.out = lv[2];
+        rc = launch_step<T>(ctx, sp);
+        if (rc) return rc;
+        const T* h = reinterpret_cast<const T*>(ctx->hist);
+        const size_t C = (size_t)ctx->cells();
+        dropin_ki_kernel<T><<<592, 256, 0, ctx->stream>>>(
+            ctx->ndim, n0, n1, n2, reinterpret_cast<T*>(ctx->acc), h + (n - 1) * C, h + n * C,
+            h + (n + 1) * C, reinterpret_cast<const T*>(lv[2]), reinterpret_cast<const T*>(lv[1]),
+            reinterpret_cast<const T*>(lv[0]), (T)ctx->cv, (T)ctx->cg, (T)ctx->inv2dt,
+            (T)ctx->inv2dx, (T)dt);
+        ctx->launches++;
+        CK(cudaGetLastError());
+        char* t = lv[0];   // rotate: (prev, cur, next) <- (cur, next, prev)
+        lv[0] = lv[1];
+        lv[1] = lv[2];
+        lv[2] = t;
+    }
+    (void)fb;
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->prof) harvest_events(ctx);
+    std::vector<char> hs((size_t)(N + 2) * 8);
+    CK(cudaMemcpy(hs.data(), ctx->maxslots, hs.size(), cudaMemcpyDeviceToHost));
+    for (int64_t n = N - 1; n >= 1; --n) {
+        if (!((n % STABILITY_CHECK_INTERVAL == 0) || (n == 1))) continue;
+        const double m = slot_value<T>(hs.data(), n);
+        if (!std::isfinite(m)) {
+            *fail_step = n - 1;
+            *fail_max = m;
+            ctx->err = "unstable field";
+            return WO_ERR_UNSTABLE;
+        }
+    }
+    return WO_OK;
+}
+
+template <typename T>
+int step_t(wo_ctx* ctx, int64_t n_force, const int64_t* idx, const double* vals,
+           const double* dense, int want_max, double* max_out) {
+    int rc = ensure_slots(ctx, 1);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(ctx->maxslots, 0, 8, ctx->stream));
+    std::vector<long long> sidx;
+    std::vector<int> spos;
+    dedupe_last((int)n_force, idx, sidx, spos);
+    std::vector<double> sv(sidx.size());
+    for (size_t s = 0; s < sidx.size(); ++s) sv[s] = vals[spos[s]];
+    const int ns = (int)sidx.size();
+    const bool in_kernel = ns <= MAX_SRC && !dense;
+    StepSpec sp;
+    sp.check = want_max && in_kernel;
+    sp.n_src = in_kernel ? ns : 0;
+    sp.src_flat = sidx.data();
+    sp.src_val = sv.data();
+    sp.slot = 0;
+    rc = launch_step<T>(ctx, sp);
+    if (rc) return rc;
+    if (dense) {
+        rc = ensure(ctx, &ctx->f_dense, &ctx->f_dense_cap, (size_t)ctx->cells() * 8);
+        if (rc) return rc;
+        double* d = ctx->f_dense;
+        CK(cudaMemcpyAsync(d, dense, (size_t)ctx->cells() * 8, cudaMemcpyHostToDevice, ctx->stream));
+        dense_force_kernel<T><<<592, 256, 0, ctx->stream>>>(
+            reinterpret_cast<T*>(ctx->uprev()), reinterpret_cast<const T*>(ctx->base0(ctx->gamma)),
+            mat_scalars<T>(ctx), d, ctx->cells());
+        ctx->launches++;
+        CK(cudaGetLastError());
+    }
+    if (!in_kernel && ns > 0) {
+        rc = inject_host_list<T>(ctx, ns, sidx.data(), sv.data());
+        if (rc) return rc;
+    }
+    if (want_max && !in_kernel) {
+        max_abs_kernel<T><<<296, 256, 0, ctx->stream>>>(
+            reinterpret_cast<const T*>(ctx->uprev()), ctx->cells(),
+            reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots));
+        ctx->launches++;
+        CK(cudaGetLastError());
+    }
+    ctx->cur = 1 - ctx->cur;
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->prof) harvest_events(ctx);
+    if (want_max && max_out) {
+        char hs[8];
+        CK(cudaMemcpy(hs, ctx->maxslots, 8, cudaMemcpyDeviceToHost));
+        *max_out = slot_value<T>(hs, 0);
+    }
+    return WO_OK;
+}
+
+template <typename T>
+int misfit_t(wo_ctx* ctx, int64_t N, int kind, const double* measured, double c1, double c2,
+             double c3, double c4, double adj_coef, int write_adj, double k, double* cost_out) {
+    REQUIRE(ctx->n_sup > 0, "shot misfit needs a support");
+    REQUIRE(ctx->store_bytes >= (size_t)N * ctx->n_sup * sizeof(T), "no recorded support values");
+    int rc;
+    if (kind == SHOT_FWI) {
+        rc = ensure(ctx, &ctx->measured, &ctx->measured_bytes, (size_t)N * ctx->n_sup * 8);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(ctx->measured, measured, (size_t)N * ctx->n_sup * 8,
+                           cudaMemcpyHostToDevice, ctx->stream));
+    }
+    rc = ensure(ctx, &ctx->partial, &ctx->partial_bytes, (size_t)N * 8 + 8);
+    if (rc) return rc;
+    if (!ctx->cost) {
+        rc = dev_alloc(ctx, (void**)&ctx->cost, 8);
+        if (rc) return rc;
+    }
+    misfit_kernel<T><<<(unsigned)N, 256, 0, ctx->stream>>>(
+        reinterpret_cast<T*>(ctx->store), ctx->measured, (long long)N, (int)ctx->n_sup, kind, c1,
+        c2, c3, c4, adj_coef, write_adj, (T)k, ctx->partial);
+    cost_sum_kernel<<<1, 32, 0, ctx->stream>>>(ctx->partial, (long long)N, ctx->cost);
+    ctx->launches += 2;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(cost_out, ctx->cost, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return WO_OK;
+}
+
+template <typename T>
+int gradient_t(wo_ctx* ctx, double two_k, void* out) {
+    scale_div_kernel<T><<<592, 256, 0, ctx->stream>>>(reinterpret_cast<T*>(ctx->acc), ctx->cells(),
+                                                      (T)two_k);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, ctx->acc, ctx->field_bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return WO_OK;
+}
+
+int create_common(wo_ctx* ctx) {
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    const size_t ab = (size_t)ctx->alloc_cells() * ctx->itemsize;
+    int rc;
+    if ((rc = dev_alloc(ctx, (void**)&ctx->gamma, ab))) return rc;
+    if ((rc = dev_alloc(ctx, (void**)&ctx->u[0], ab))) return rc;
+    if ((rc = dev_alloc(ctx, (void**)&ctx->u[1], ab))) return rc;
+    if ((rc = dev_alloc(ctx, (void**)&ctx->acc, ctx->field_bytes()))) return rc;
+    CK(cudaMemsetAsync(ctx->u[0], 0, ab, ctx->stream));
+    CK(cudaMemsetAsync(ctx->u[1], 0, ab, ctx->stream));
+    CK(cudaMemsetAsync(ctx->acc, 0, ctx->field_bytes(), ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return WO_OK;
+}
+
+}  // namespace
+
+#define DISPATCH(ctx, FN, ...) \
+    ((ctx)->itemsize == 4 ? FN<float>(__VA_ARGS__) : FN<double>(__VA_ARGS__))
+
+extern "C" {
+
+int wo_version(void) { return 100; }
+
+int wo_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+const char* wo_last_error(const wo_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+int wo_create(wo_ctx** out, int ndim, const int64_t* shape, double dx, int itemsize, int device) {
+    *out = nullptr;
+    if (ndim < 1 || ndim > 3 || (itemsize != 4 && itemsize != 8) || !(dx > 0)) {
+        g_create_error = "invalid grid / dtype";
+        return WO_ERR_CONFIG;
+    }
+    for (int a = 0; a < ndim; ++a)
+        if (shape[a] < 3 || shape[a] > (1ll << 30)) {
+            g_create_error = "every axis needs at least 3 nodes";
+            return WO_ERR_CONFIG;
+        }
+    wo_ctx* ctx = new wo_ctx();
+    ctx->device = device;
+    ctx->ndim = ndim;
+    ctx->itemsize = itemsize;
+    ctx->dx = dx;
+    for (int a = 0; a < ndim; ++a) ctx->shape[a] = shape[a];
+    if (ndim == 3) { ctx->kn0 = (int)shape[0]; ctx->kn1 = (int)shape[1]; ctx->kn2 = (int)shape[2]; }
+    else if (ndim == 2) { ctx->kn0 = 1; ctx->kn1 = (int)shape[0]; ctx->kn2 = (int)shape[1]; }
+    else { ctx->kn0 = 1; ctx->kn1 = 1; ctx->kn2 = (int)shape[0]; }
+    ctx->n0g = ctx->kn0;
+    int rc = create_common(ctx);
+    if (rc) {
+        g_create_error = ctx->err;
+        wo_destroy(ctx);
+        return rc;
+    }
+    *out = ctx;
+    return WO_OK;
+}
+
+int wo_create_slab(wo_ctx** out, const int64_t* gshape, int64_t i_begin, int64_t i_end, double dx,
+                   int itemsize, int device) {
+    *out = nullptr;
+    if (!(0 <= i_begin && i_begin < i_end && i_end <= gshape[0]) || gshape[0] < 3 ||
+        gshape[1] < 3 || gshape[2] < 3 || (itemsize != 4 && itemsize != 8)) {
+        g_create_error = "invalid slab";
+        return WO_ERR_CONFIG;
+    }
+    wo_ctx* ctx = new wo_ctx();
+    ctx->device = device;
+    ctx->ndim = 3;
+    ctx->itemsize = itemsize;
+    ctx->dx = dx;
+    ctx->shape[0] = i_end - i_begin;
+    ctx->shape[1] = gshape[1];
+    ctx->shape[2] = gshape[2];
+    ctx->kn0 = (int)(i_end - i_begin);
+    ctx->kn1 = (int)gshape[1];
+    ctx->kn2 = (int)gshape[2];
+    ctx->i_off = (int)i_begin;
+    ctx->n0g = (int)gshape[0];
+    ctx->has_lo = i_begin > 0;
+    ctx->has_hi = i_end < gshape[0];
+    int rc = create_common(ctx);
+    if (rc) {
+        g_create_error = ctx->err;
+        wo_destroy(ctx);
+        return rc;
+    }
+    *out = ctx;
+    return WO_OK;
+}
+
+void wo_destroy(wo_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    void* bufs[] = {ctx->gamma, ctx->u[0], ctx->u[1], ctx->acc, ctx->mask, ctx->prefix,
+                    ctx->store, ctx->measured, ctx->partial, ctx->cost, ctx->maxslots,
+                    ctx->f_idx, ctx->f_vals, ctx->f_dense, ctx->hist, ctx->u3};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    for (auto e : ctx->ev_free) cudaEventDestroy(e);
+    for (auto e : ctx->ev_used) cudaEventDestroy(e);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, double rho1,
+                    double kappa1, double rho2, double kappa2, double dt, double ratio2) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(flavor == WO_RHO_SCALED || flavor == WO_ACOUSTIC, "unknown material flavor");
+    ctx->flavor = flavor;
+    ctx->rho0 = rho0; ctx->rho1 = rho1; ctx->kappa1 = kappa1;
+    ctx->rho2 = rho2; ctx->kappa2 = kappa2; ctx->dt_mat = dt; ctx->ratio2 = ratio2;
+    // gamma.astype(T) (solver.py:94/100) on the host: halves H2D bytes in fp32
+    const int64_t n = ctx->alloc_cells();
+    if (ctx->itemsize == 4) {
+        std::vector<float> g(n);
+        for (int64_t i = 0; i < n; ++i) g[i] = (float)gamma[i];
+        CK(cudaMemcpy(ctx->gamma, g.data(), n * 4, cudaMemcpyHostToDevice));
+    } else {
+        CK(cudaMemcpy(ctx->gamma, gamma, n * 8, cudaMemcpyHostToDevice));
+    }
+    ctx->material_set = true;
+    return WO_OK;
+}
+
+int wo_set_kernel_coefficients(wo_ctx* ctx, double cv, double cg, double inv2dt, double inv2dx) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    ctx->cv = cv; ctx->cg = cg; ctx->inv2dt = inv2dt; ctx->inv2dx = inv2dx;
+    return WO_OK;
+}
+
+int wo_set_support(wo_ctx* ctx, int64_t n_sup, const int64_t* flat) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    const int64_t C = ctx->cells();
+    for (int64_t s = 0; s < n_sup; ++s) {
+        REQUIRE(flat[s] >= 0 && flat[s] < C, "support index outside the grid");
+        REQUIRE(s == 0 || flat[s] > flat[s - 1], "support indices must be strictly increasing");
+    }
+    const int64_t words = (C + 31) / 32;
+    if (!ctx->mask) {
+        if ((rc = dev_alloc(ctx, (void**)&ctx->mask, words * 4))) return rc;
+        if ((rc = dev_alloc(ctx, (void**)&ctx->prefix, words * 4))) return rc;
+    }
+    std::vector<unsigned int> m(words, 0u);
+    std::vector<int> p(words, 0);
+    for (int64_t s = 0; s < n_sup; ++s) m[flat[s] >> 5] |= 1u << (flat[s] & 31);
+    int run = 0;
+    for (int64_t w = 0; w < words; ++w) {
+        p[w] = run;
+        run += __builtin_popcount(m[w]);
+    }
+    CK(cudaMemcpy(ctx->mask, m.data(), words * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->prefix, p.data(), words * 4, cudaMemcpyHostToDevice));
+    ctx->n_sup = n_sup;
+    return WO_OK;
+}
+
+int wo_reset_window(wo_ctx* ctx) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    const size_t ab = (size_t)ctx->alloc_cells() * ctx->itemsize;
+    CK(cudaMemsetAsync(ctx->u[0], 0, ab, ctx->stream));
+    CK(cudaMemsetAsync(ctx->u[1], 0, ab, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return WO_OK;
+}
+
+int wo_set_window(wo_ctx* ctx, const void* u_prev, const void* u_cur) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    CK(cudaMemcpy(ctx->uprev(), u_prev, ctx->field_bytes(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->ucur(), u_cur, ctx->field_bytes(), cudaMemcpyHostToDevice));
+    return WO_OK;
+}
+
+int wo_get_window(wo_ctx* ctx, void* u_prev, void* u_cur) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (u_prev) CK(cudaMemcpy(u_prev, ctx->uprev(), ctx->field_bytes(), cudaMemcpyDeviceToHost));
+    if (u_cur) CK(cudaMemcpy(u_cur, ctx->ucur(), ctx->field_bytes(), cudaMemcpyDeviceToHost));
+    return WO_OK;
+}
+
+int wo_swap_direction(wo_ctx* ctx) {
+    if (!ctx) return WO_ERR_CONFIG;
+    ctx->cur = 1 - ctx->cur;
+    return WO_OK;
+}
+
+int wo_zero_accumulator(wo_ctx* ctx) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(ctx->acc, 0, ctx->field_bytes(), ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return WO_OK;
+}
+
+int wo_get_accumulator(wo_ctx* ctx, void* out) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(out, ctx->acc, ctx->field_bytes(), cudaMemcpyDeviceToHost));
+    return WO_OK;
+}
+
+int wo_set_accumulator(wo_ctx* ctx, const void* in) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    CK(cudaMemcpy(ctx->acc, in, ctx->field_bytes(), cudaMemcpyHostToDevice));
+    return WO_OK;
+}
+
+int wo_sweep_forward(wo_ctx* ctx, int64_t n_steps, int n_src, const int64_t* src_flat,
+                     const double* src_amp, int flags, double dt, double scale,
+                     double* peak_out, int64_t* fail_step, double* fail_max) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(ctx->material_set, "material not set");
+    REQUIRE(n_steps >= 2, "need at least 2 time steps");
+    return DISPATCH(ctx, sweep_forward_t, ctx, n_steps, n_src, src_flat, src_amp, flags, dt,
+                    scale, peak_out, fail_step, fail_max);
+}
+
+int wo_sweep_adjoint_reference(wo_ctx* ctx, int64_t n_steps, double dt, int64_t* fail_step,
+                               double* fail_max) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(ctx->material_set, "material not set");
+    return DISPATCH(ctx, sweep_adjoint_reference_t, ctx, n_steps, dt, fail_step, fail_max);
+}
+
+int wo_free_history(wo_ctx* ctx) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->hist) {
+        cudaFree(ctx->hist);
+        ctx->dev_bytes -= (int64_t)ctx->hist_bytes;
+        ctx->hist = nullptr;
+        ctx->hist_bytes = 0;
+    }
+    if (ctx->u3) {
+        cudaFree(ctx->u3);
+        ctx->dev_bytes -= (int64_t)ctx->u3_bytes;
+        ctx->u3 = nullptr;
+        ctx->u3_bytes = 0;
+    }
+    return WO_OK;
+}
+
+int wo_shot_misfit(wo_ctx* ctx, int64_t n_steps, int kind, const double* measured, double c1,
+                   double c2, double c3, double c4, double adj_coef, int write_adj, double k,
+                   double* cost_out) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(kind == WO_SHOT_FWI || kind == WO_SHOT_TATO, "unknown shot kind");
+    return DISPATCH(ctx, misfit_t, ctx, n_steps, kind, measured, c1, c2, c3, c4, adj_coef,
+                    write_adj, k, cost_out);
+}
+
+int wo_get_store(wo_ctx* ctx, int64_t n_steps, void* out) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    const size_t b = (size_t)n_steps * ctx->n_sup * ctx->itemsize;
+    REQUIRE(ctx->store_bytes >= b, "store smaller than requested");
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(out, ctx->store, b, cudaMemcpyDeviceToHost));
+    return WO_OK;
+}
+
+int wo_sweep_backward(wo_ctx* ctx, int64_t n_steps, int64_t src_flat, const double* src_amp,
+                      int inject_support, int accumulate, double dt, int64_t* fail_step,
+                      double* fail_max) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(ctx->material_set, "material not set");
+    return DISPATCH(ctx, sweep_backward_t, ctx, n_steps, src_flat, src_amp, inject_support,
+                    accumulate, dt, fail_step, fail_max);
+}
+
+int wo_get_gradient(wo_ctx* ctx, double two_k, void* out) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    return DISPATCH(ctx, gradient_t, ctx, two_k, out);
+}
+
+int wo_step(wo_ctx* ctx, int64_t n_force, const int64_t* idx, const double* vals,
+            const double* dense_force, int want_max, double* max_out) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(ctx->material_set, "material not set");
+    return DISPATCH(ctx, step_t, ctx, n_force, idx, vals, dense_force, want_max, max_out);
+}
+
+int wo_set_profiling(wo_ctx* ctx, int on) {
+    if (!ctx) return WO_ERR_CONFIG;
+    ctx->prof = on != 0;
+    return WO_OK;
+}
+
+int wo_stats(wo_ctx* ctx, int64_t* launches, int64_t* step_launches, double* step_kernel_ms) {
+    if (!ctx) return WO_ERR_CONFIG;
+    if (launches) *launches = ctx->launches;
+    if (step_launches) *step_launches = ctx->step_launches;
+    if (step_kernel_ms) *step_kernel_ms = ctx->step_ms;
+    return WO_OK;
+}
+
+int wo_reset_stats(wo_ctx* ctx) {
+    if (!ctx) return WO_ERR_CONFIG;
+    ctx->launches = ctx->step_launches = 0;
+    ctx->step_ms = 0.0;
+    return WO_OK;
+}
+
+int64_t wo_device_bytes(const wo_ctx* ctx) { return ctx ? ctx->dev_bytes : 0; }
+
+// ---------------------------------------------------------------- drop-ins
+namespace {
+struct Scratch {
+    std::vector<void*> p;
+    ~Scratch() {
+        for (void* q : p) cudaFree(q);
+    }
+    void* put(const void* h, size_t b) {
+        void* d = nullptr;
+        if (cudaMalloc(&d, b ? b : 16) != cudaSuccess) return nullptr;
+        p.push_back(d);
+        if (h) cudaMemcpy(d, h, b, cudaMemcpyHostToDevice);
+        return d;
+    }
+};
+
+void map3(int ndim, const int64_t* shape, int& n0, int& n1, int& n2) {
+    if (ndim == 3) { n0 = (int)shape[0]; n1 = (int)shape[1]; n2 = (int)shape[2]; }
+    else if (ndim == 2) { n0 = 1; n1 = (int)shape[0]; n2 = (int)shape[1]; }
+    else { n0 = 1; n1 = 1; n2 = (int)shape[0]; }
+}
+}  // namespace
+
+int wo_apply_step(int ndim, const int64_t* shape, int itemsize, const void* u_prev,
+                  const void* u_cur, const void* wf0, const void* wf1, const void* wf2,
+                  const void* coef, void* out, int device) {
+    if (ndim < 1 || ndim > 3 || (itemsize != 4 && itemsize != 8)) return WO_ERR_CONFIG;
+    if (cudaSetDevice(device) != cudaSuccess) return WO_ERR_CUDA;
+    int n0, n1, n2;
+    map3(ndim, shape, n0, n1, n2);
+    const long long C = (long long)n0 * n1 * n2;
+    const size_t fb = (size_t)C * itemsize;
+    // face arrays in kernel space: axis a of the reference -> kernel axis
+    const void* wf[3] = {wf0, wf1, wf2};
+    const void* kw[3] = {nullptr, nullptr, nullptr};
+    const int first = 3 - ndim;
+    for (int a = 0; a < ndim; ++a) kw[first + a] = wf[a];
+    size_t wb_[3];
+    wb_[0] = (size_t)(n0 - 1) * n1 * n2 * itemsize;
+    wb_[1] = (size_t)n0 * (n1 - 1) * n2 * itemsize;
+    wb_[2] = (size_t)n0 * n1 * (n2 - 1) * itemsize;
+    Scratch s;
+    void* d_up = s.put(u_prev, fb);
+    void* d_u = s.put(u_cur, fb);
+    void* d_c = s.put(coef, fb);
+    void* d_o = s.put(nullptr, fb);
+    void* d_w[3] = {nullptr, nullptr, nullptr};
+    for (int a = 0; a < 3; ++a)
+        if (kw[a]) d_w[a] = s.put(kw[a], wb_[a]);
+    if (!d_up || !d_u || !d_c || !d_o) return WO_ERR_CUDA;
+    if (itemsize == 4)
+        dropin_step_kernel<float><<<592, 256>>>(n0, n1, n2, (const float*)d_up, (const float*)d_u,
+                                                (const float*)d_w[0], (const float*)d_w[1],
+                                                (const float*)d_w[2], (const float*)d_c, (float*)d_o);
+    else
+        dropin_step_kernel<double><<<592, 256>>>(n0, n1, n2, (const double*)d_up,
+                                                 (const double*)d_u, (const double*)d_w[0],
+                                                 (const double*)d_w[1], (const double*)d_w[2],
+                                                 (const double*)d_c, (double*)d_o);
+    if (cudaGetLastError() != cudaSuccess) return WO_ERR_CUDA;
+    if (cudaMemcpy(out, d_o, fb, cudaMemcpyDeviceToHost) != cudaSuccess) return WO_ERR_CUDA;
+    return WO_OK;
+}
+
+int wo_apply_kernel_increment(int ndim, const int64_t* shape, int itemsize, void* acc,
+                              const void* a_old, const void* a_mid, const void* a_new,
+                              const void* b_old, const void* b_mid, const void* b_new, double cv,
+                              double cg, double inv2dt, double inv2dx, double sdt, int device) {
+    if (ndim < 1 || ndim > 3 || (itemsize != 4 && itemsize != 8)) return WO_ERR_CONFIG;
+    if (cudaSetDevice(device) != cudaSuccess) return WO_ERR_CUDA;
+    int n0, n1, n2;
+    map3(ndim, shape, n0, n1, n2);
+    const size_t fb = (size_t)n0 * n1 * n2 * itemsize;
+    Scratch s;
+    void* d[7] = {s.put(acc, fb), s.put(a_old, fb), s.put(a_mid, fb), s.put(a_new, fb),
+                  s.put(b_old, fb), s.put(b_mid, fb), s.put(b_new, fb)};
+    for (void* q : d)
+        if (!q) return WO_ERR_CUDA;
+    if (itemsize == 4)
+        dropin_ki_kernel<float><<<592, 256>>>(
+            ndim, n0, n1, n2, (float*)d[0], (const float*)d[1], (const float*)d[2],
+            (const float*)d[3], (const float*)d[4], (const float*)d[5], (const float*)d[6],
+            (float)cv, (float)cg, (float)inv2dt, (float)inv2dx, (float)sdt);
+    else
+        dropin_ki_kernel<double><<<592, 256>>>(
+            ndim, n0, n1, n2, (double*)d[0], (const double*)d[1], (const double*)d[2],
+            (const double*)d[3], (const double*)d[4], (const double*)d[5], (const double*)d[6], cv,
+            cg, inv2dt, inv2dx, sdt);
+    if (cudaGetLastError() != cudaSuccess) return WO_ERR_CUDA;
+    if (cudaMemcpy(acc, d[0], fb, cudaMemcpyDeviceToHost) != cudaSuccess) return WO_ERR_CUDA;
+    return WO_OK;
+}
+
+// ------------------------------------------------------------ design chain
+namespace {
+struct DevFootprint {
+    Scratch s;
+    Footprint fp{};
+    bool ok = false;
+    DevFootprint(int ndim, int n, const int* off, const double* w) {
+        std::vector<int> o3((size_t)n * 3, 0);
+        for (int f = 0; f < n; ++f)
+            for (int a = 0; a < ndim; ++a) o3[(size_t)f * 3 + (3 - ndim) + a] = off[(size_t)f * ndim + a];
+        fp.n = n;
+        fp.off = (const int*)s.put(o3.data(), o3.size() * sizeof(int));
+        fp.w = (const double*)s.put(w, (size_t)n * sizeof(double));
+        ok = fp.off && fp.w;
+    }
+};
+}  // namespace
+
+int wo_design_filter(int ndim, const int64_t* shape, const double* gamma,
+                     const unsigned char* mask, int n_fp, const int* offsets,
+                     const double* weights, double* out, int device) {
+    if (ndim < 1 || ndim > 3 || n_fp < 1) return WO_ERR_CONFIG;
+    if (cudaSetDevice(device) != cudaSuccess) return WO_ERR_CUDA;
+    int n0, n1, n2;
+    map3(ndim, shape, n0, n1, n2);
+    const long long N = (long long)n0 * n1 * n2;
+    DevFootprint F(ndim, n_fp, offsets, weights);
+    Scratch s;
+    double* d_g = (double*)s.put(gamma, N * 8);
+    unsigned char* d_m = mask ? (unsigned char*)s.put(mask, N) : nullptr;
+    double* d_num = (double*)s.put(nullptr, N * 8);
+    double* d_den = (double*)s.put(nullptr, N * 8);
+    double* d_o = (double*)s.put(nullptr, N * 8);
+    if (!F.ok || !d_g || !d_num || !d_den || !d_o || (mask && !d_m)) return WO_ERR_CUDA;
+    masked_correlate_kernel<<<592, 256>>>(n0, n1, n2, d_g, d_m, 1, F.fp, d_num, d_den);
+    filter_finish_kernel<<<592, 256>>>(N, d_g, d_m, d_num, d_den, d_o);
+    if (cudaGetLastError() != cudaSuccess) return WO_ERR_CUDA;
+    if (cudaMemcpy(out, d_o, N * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return WO_ERR_CUDA;
+    return WO_OK;
+}
+
+int wo_design_project(int64_t n, const double* g_tilde, double beta, double eta, double t_be,
+                      double denom, const unsigned char* mask, double* out, int device) {
+    if (cudaSetDevice(device) != cudaSuccess) return WO_ERR_CUDA;
+    Scratch s;
+    double* d_g = (double*)s.put(g_tilde, n * 8);
+    unsigned char* d_m = mask ? (unsigned char*)s.put(mask, n) : nullptr;
+    double* d_o = (double*)s.put(nullptr, n * 8);
+    if (!d_g || !d_o || (mask && !d_m)) return WO_ERR_CUDA;
+    heaviside_kernel<<<592, 256>>>(n, d_g, beta, eta, t_be, denom, d_m, d_o);
+    if (cudaGetLastError() != cudaSuccess) return WO_ERR_CUDA;
+    if (cudaMemcpy(out, d_o, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return WO_ERR_CUDA;
+    return WO_OK;
+}
+
+int wo_design_chain(int ndim, const int64_t* shape, const double* dcdbar, const double* g_tilde,
+                    double beta, double eta, double denom, const unsigned char* mask, int n_fp,
+                    const int* offsets, const double* weights, double* out, int device) {
+    if (ndim < 1 || ndim > 3 || n_fp < 1) return WO_ERR_CONFIG;
+    if (cudaSetDevice(device) != cudaSuccess) return WO_ERR_CUDA;
+    int n0, n1, n2;
+    map3(ndim, shape, n0, n1, n2);
+    const long long N = (long long)n0 * n1 * n2;
+    DevFootprint F(ndim, n_fp, offsets, weights);
+    Scratch s;
+    double* d_g = (double*)s.put(dcdbar, N * 8);
+    double* d_t = (double*)s.put(g_tilde, N * 8);
+    unsigned char* d_m = mask ? (unsigned char*)s.put(mask, N) : nullptr;
+    double* d_inner = (double*)s.put(nullptr, N * 8);
+    double* d_den = (double*)s.put(nullptr, N * 8);
+    double* d_ratio = (double*)s.put(nullptr, N * 8);
+    double* d_o = (double*)s.put(nullptr, N * 8);
+    if (!F.ok || !d_g || !d_t || !d_inner || !d_den || !d_ratio || !d_o || (mask && !d_m))
+        return WO_ERR_CUDA;
+    chain_inner_kernel<<<592, 256>>>(N, d_g, d_t, beta, eta, denom, d_m, d_inner);
+    masked_correlate_kernel<<<592, 256>>>(n0, n1, n2, d_inner, d_m, 1, F.fp, nullptr, d_den);
+    chain_ratio_kernel<<<592, 256>>>(N, d_inner, d_den, d_m, d_ratio);
+    masked_correlate_kernel<<<592, 256>>>(n0, n1, n2, d_ratio, nullptr, 0, F.fp, d_o, nullptr);
+    mask_zero_kernel<<<592, 256>>>(N, d_m, d_o);
+    if (cudaGetLastError() != cudaSuccess) return WO_ERR_CUDA;
+    if (cudaMemcpy(out, d_o, N * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return WO_ERR_CUDA;
+    return WO_OK;
+}
+
+}  // extern "C"

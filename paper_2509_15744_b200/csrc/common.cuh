@@ -1,0 +1,77 @@
+// Shared device helpers for the waveb200 sweep kernels.
+//
+// Arithmetic contract (parity with the reference's Numba kernels,
+// /root/reference/pkg/src/waveopt/kernels.py): the whole library is compiled
+// with -fmad=false -prec-div=true -ftz=false, so every + - * / below is one
+// IEEE-754 round-to-nearest operation in the run dtype, in source order.
+// Divisions and reciprocals go through the _rn intrinsics explicitly.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace wb {
+
+template <typename T> struct FTraits;
+template <> struct FTraits<float> {
+    using Bits = unsigned int;
+    __device__ static __forceinline__ float rcp(float x) { return __frcp_rn(x); }
+    __device__ static __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+    __device__ static __forceinline__ Bits abs_bits(float x) {
+        return __float_as_uint(x) & 0x7fffffffu;
+    }
+};
+template <> struct FTraits<double> {
+    using Bits = unsigned long long;
+    __device__ static __forceinline__ double rcp(double x) { return __drcp_rn(x); }
+    __device__ static __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+    __device__ static __forceinline__ Bits abs_bits(double x) {
+        return (Bits)__double_as_longlong(x) & 0x7fffffffffffffffull;
+    }
+};
+
+// Material flavors (grids.py:99-100)
+enum Flavor : int { RHO_SCALED = 0, ACOUSTIC = 1 };
+
+// Per-run material scalars, all already rounded to T on the host exactly as
+// solver.py:93-110 rounds them (dtype.type(python_float)).
+template <typename T> struct MatScalars {
+    int flavor;
+    T two_r2;   // rho_scaled: dtype.type(2.0) * r2, r2 = T((c0*dt/dx)**2)
+    T dt2;      // T(dt*dt)
+    T rho0;     // rho_scaled: T(rho0)
+    T irho1;    // acoustic: T(1/rho1)
+    T drho;     // acoustic: T(1/rho2 - 1/rho1)
+    T ikap1;    // acoustic: T(1/kappa1)
+    T dkap;     // acoustic: T(1/kappa2 - 1/kappa1)
+    T s2;       // acoustic: T((dt/dx)**2)
+};
+
+// m: reciprocal flux coefficient used by the face weights (solver.py:95,107)
+template <typename T>
+__device__ __forceinline__ T mat_m(const MatScalars<T>& M, T g) {
+    if (M.flavor == RHO_SCALED) return FTraits<T>::rcp(g);            // T(1)/gamma
+    T ir = M.irho1 + g * M.drho;                                       // grids.py:252
+    return FTraits<T>::rcp(ir);                                        // T(1)/inv_rho
+}
+
+// coef multiplying the face sum (solver.py:97, 109).  kappa returned for fc.
+template <typename T>
+__device__ __forceinline__ T mat_coef(const MatScalars<T>& M, T g, T& kappa) {
+    if (M.flavor == RHO_SCALED) {
+        kappa = T(0);
+        return FTraits<T>::div(M.two_r2, g);                           // (2*r2)/gamma
+    }
+    T ik = M.ikap1 + g * M.dkap;                                       // grids.py:253
+    kappa = FTraits<T>::rcp(ik);                                       // T(1)/inv_kappa
+    return (T(2) * kappa) * M.s2;                                      // (2*kappa)*s2
+}
+
+// nodal force coefficient (solver.py:98, 110)
+template <typename T>
+__device__ __forceinline__ T mat_fc(const MatScalars<T>& M, T g, T kappa) {
+    if (M.flavor == RHO_SCALED) return FTraits<T>::div(M.dt2, M.rho0 * g);
+    return kappa * M.dt2;
+}
+
+}  // namespace wb

@@ -1,0 +1,312 @@
+"""Device context: one grid at one dtype on one GPU (wraps ``wo_ctx``).
+
+This is the only module that talks to the native library; the API modules
+(solver, gradients, fwi, tato) describe WHAT to run in the reference's terms
+and call the sweep-level entry points here.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from collections import OrderedDict
+
+import numpy as np
+
+from . import _native as N
+from .grids import ACOUSTIC, RHO_SCALED, ConfigError, Grid, MaterialModel
+
+
+class SolverInstabilityError(RuntimeError):
+    """Blow-up or NaN/Inf during time integration (CLI exit code 2; solver.py:34-41)."""
+
+    def __init__(self, step, max_abs, detail=""):
+        self.step = step
+        self.max_abs = max_abs
+        msg = f"unstable field at step {step}: max|u| = {max_abs:g}"
+        super().__init__(msg + (f" ({detail})" if detail else ""))
+
+
+class ResourceBudgetError(RuntimeError):
+    """Allocation exceeds the configured budget (CLI exit code 3; solver.py:44-45)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA / driver failure inside the native library."""
+
+
+def _raise(ctx_handle, rc, what):
+    L = N.load()
+    msg = L.wo_last_error(ctx_handle)
+    msg = msg.decode() if msg else ""
+    text = f"{what}: {msg}"
+    if rc == N.WO_ERR_CONFIG:
+        raise ConfigError(text)
+    if rc == N.WO_ERR_BUDGET:
+        raise ResourceBudgetError(text)
+    raise DeviceError(text)
+
+
+def source_amplitude_table(sources, dt, n_steps):
+    """[n_src][N] fp64 table of burst_amplitude(n*dt) (solver.py:48-54),
+    evaluated with math.sin exactly like the reference."""
+    out = np.zeros((len(sources), n_steps), dtype=np.float64)
+    for s, src in enumerate(sources):
+        w = src.omega
+        dur = src.duration
+        amp = src.amplitude
+        half = 2 * src.cycles
+        for n in range(n_steps):
+            t = n * dt
+            if t < 0 or t > dur:
+                continue
+            out[s, n] = amp * math.sin(w * t) * math.sin(w * t / half) ** 2
+    return out
+
+
+def force_coef_at(material: MaterialModel, dt, dtype, node):
+    """force_coef[node] of prepare_material (solver.py:98,110), as a T scalar."""
+    T = np.dtype(dtype).type
+    g = T(material.gamma[tuple(node)])
+    if material.flavor == RHO_SCALED:
+        return T(dt * dt) / (T(material.rho0) * g)
+    ik = 1.0 / material.kappa1 + g * (1.0 / material.kappa2 - 1.0 / material.kappa1)
+    return (T(1.0) / T(ik)) * T(dt * dt)
+
+
+def material_ratio2(material: MaterialModel, dt, dx):
+    """The squared ratio the reference evaluates with ** (solver.py:96,108)."""
+    if material.flavor == RHO_SCALED:
+        return (material.c0 * dt / dx) ** 2
+    return (dt / dx) ** 2
+
+
+def kernel_coefficients(material: MaterialModel):
+    """(velocity, gradient) kernel coefficients (gradients.py:117-129)."""
+    if material.flavor == RHO_SCALED:
+        return -material.rho0, material.rho0 * material.c0**2
+    dk = 1.0 / material.kappa2 - 1.0 / material.kappa1
+    dr = 1.0 / material.rho2 - 1.0 / material.rho1
+    return -dk, dr
+
+
+class DeviceGrid:
+    """Device buffers + sweeps for one grid at one dtype (include/waveb200.h)."""
+
+    def __init__(self, grid: Grid, dtype, device=0):
+        self.L = N.load(require_device=True)
+        self.grid = grid
+        self.dtype = np.dtype(dtype)
+        self.device = device
+        h = ctypes.c_void_p()
+        rc = self.L.wo_create(ctypes.byref(h), grid.ndim, N.shape3(grid.shape), float(grid.dx),
+                              self.dtype.itemsize, device)
+        if rc:
+            _raise(None, rc, "wo_create")
+        self.h = h
+        self._support_key = None
+        self.n_sup = 0
+
+    # --------------------------------------------------------------- basics
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.wo_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ck(self, rc, what):
+        if rc:
+            _raise(self.h, rc, what)
+
+    def _field(self, a):
+        a = np.ascontiguousarray(a, dtype=self.dtype)
+        if a.shape != self.grid.shape:
+            raise ConfigError(f"field shape {a.shape} != grid {self.grid.shape}")
+        return a
+
+    def set_material(self, material: MaterialModel, dt):
+        if material.grid.shape != self.grid.shape:
+            raise ConfigError("material lives on a different grid")
+        flavor = N.WO_RHO_SCALED if material.flavor == RHO_SCALED else N.WO_ACOUSTIC
+        gamma = np.ascontiguousarray(material.gamma, dtype=np.float64)
+        ratio2 = material_ratio2(material, float(dt), self.grid.dx)
+        self._ck(self.L.wo_set_material(self.h, flavor, N.ptr(gamma), float(material.rho0),
+                                        float(material.rho1), float(material.kappa1),
+                                        float(material.rho2), float(material.kappa2),
+                                        float(dt), float(ratio2)), "wo_set_material")
+        cv, cg = kernel_coefficients(material)
+        self._ck(self.L.wo_set_kernel_coefficients(
+            self.h, float(cv), float(cg), 1.0 / (2.0 * float(dt)), 1.0 / (2.0 * self.grid.dx)),
+            "wo_set_kernel_coefficients")
+
+    def set_support(self, flat_idx):
+        """Set the support; returns the permutation sorting flat_idx (device
+        order = increasing flat index)."""
+        flat_idx = np.asarray(flat_idx, dtype=np.int64)
+        order = np.argsort(flat_idx, kind="stable")
+        srt = np.ascontiguousarray(flat_idx[order])
+        key = srt.tobytes()
+        if key != self._support_key:
+            self._ck(self.L.wo_set_support(self.h, len(srt), N.ptr(srt)), "wo_set_support")
+            self._support_key = key
+        self.n_sup = len(srt)
+        return order
+
+    def clear_support(self):
+        self.set_support(np.zeros(0, dtype=np.int64))
+
+    def reset_window(self):
+        self._ck(self.L.wo_reset_window(self.h), "wo_reset_window")
+
+    def set_window(self, u_prev, u_cur):
+        self._ck(self.L.wo_set_window(self.h, N.ptr(self._field(u_prev)),
+                                      N.ptr(self._field(u_cur))), "wo_set_window")
+
+    def get_window(self):
+        up = np.empty(self.grid.shape, self.dtype)
+        uc = np.empty(self.grid.shape, self.dtype)
+        self._ck(self.L.wo_get_window(self.h, N.ptr(up), N.ptr(uc)), "wo_get_window")
+        return up, uc
+
+    def swap_direction(self):
+        self._ck(self.L.wo_swap_direction(self.h), "wo_swap_direction")
+
+    def zero_accumulator(self):
+        self._ck(self.L.wo_zero_accumulator(self.h), "wo_zero_accumulator")
+
+    def get_accumulator(self):
+        out = np.empty(self.grid.shape, self.dtype)
+        self._ck(self.L.wo_get_accumulator(self.h, N.ptr(out)), "wo_get_accumulator")
+        return out
+
+    def set_accumulator(self, values):
+        self._ck(self.L.wo_set_accumulator(self.h, N.ptr(self._field(values))),
+                 "wo_set_accumulator")
+
+    # --------------------------------------------------------------- sweeps
+    def sweep_forward(self, n_steps, src_flat, amp_table, accumulate, dt, scale,
+                      detail_on_fail="", history=False):
+        src = np.ascontiguousarray(np.asarray(src_flat, dtype=np.int64).reshape(-1))
+        amp = np.ascontiguousarray(np.asarray(amp_table, dtype=np.float64))
+        peak = ctypes.c_double(0.0)
+        fstep = ctypes.c_int64(0)
+        fmax = ctypes.c_double(0.0)
+        flags = (N.WO_FWD_ACCUMULATE if accumulate else 0) | (N.WO_FWD_HISTORY if history else 0)
+        rc = self.L.wo_sweep_forward(self.h, int(n_steps), len(src), N.ptr(src), N.ptr(amp),
+                                     flags, float(dt), float(scale),
+                                     ctypes.byref(peak), ctypes.byref(fstep), ctypes.byref(fmax))
+        if rc == N.WO_ERR_UNSTABLE:
+            m = fmax.value
+            detail = detail_on_fail
+            if math.isfinite(m) and scale > 0:
+                detail = f"exceeds 1e6 x scale {scale:g}"
+            raise SolverInstabilityError(int(fstep.value), m, detail=detail)
+        self._ck(rc, "wo_sweep_forward")
+        return peak.value
+
+    def shot_misfit(self, n_steps, kind, measured, c, adj_coef, write_adj, k):
+        meas = (np.ascontiguousarray(measured, dtype=np.float64) if measured is not None
+                else None)
+        cost = ctypes.c_double(0.0)
+        self._ck(self.L.wo_shot_misfit(self.h, int(n_steps), int(kind), N.ptr(meas),
+                                       float(c[0]), float(c[1]), float(c[2]), float(c[3]),
+                                       float(adj_coef), int(bool(write_adj)), float(k),
+                                       ctypes.byref(cost)), "wo_shot_misfit")
+        return cost.value
+
+    def get_store(self, n_steps):
+        out = np.empty((int(n_steps), self.n_sup), self.dtype)
+        self._ck(self.L.wo_get_store(self.h, int(n_steps), N.ptr(out)), "wo_get_store")
+        return out
+
+    def sweep_backward(self, n_steps, src_flat, amp_row, inject, accumulate, dt,
+                       detail_on_fail=""):
+        amp = np.ascontiguousarray(np.asarray(amp_row, dtype=np.float64))
+        fstep = ctypes.c_int64(0)
+        fmax = ctypes.c_double(0.0)
+        rc = self.L.wo_sweep_backward(self.h, int(n_steps), int(src_flat), N.ptr(amp),
+                                      int(bool(inject)), int(bool(accumulate)), float(dt),
+                                      ctypes.byref(fstep), ctypes.byref(fmax))
+        if rc == N.WO_ERR_UNSTABLE:
+            raise SolverInstabilityError(int(fstep.value), fmax.value, detail=detail_on_fail)
+        self._ck(rc, "wo_sweep_backward")
+
+    def sweep_adjoint_reference(self, n_steps, dt):
+        fstep = ctypes.c_int64(0)
+        fmax = ctypes.c_double(0.0)
+        rc = self.L.wo_sweep_adjoint_reference(self.h, int(n_steps), float(dt),
+                                               ctypes.byref(fstep), ctypes.byref(fmax))
+        if rc == N.WO_ERR_UNSTABLE:
+            raise SolverInstabilityError(int(fstep.value), fmax.value)
+        self._ck(rc, "wo_sweep_adjoint_reference")
+
+    def free_history(self):
+        self._ck(self.L.wo_free_history(self.h), "wo_free_history")
+
+    def gradient(self, two_k):
+        out = np.empty(self.grid.shape, self.dtype)
+        self._ck(self.L.wo_get_gradient(self.h, float(two_k), N.ptr(out)), "wo_get_gradient")
+        return out
+
+    def step(self, force=None, want_max=False):
+        """One step with a sparse/dense/None force; returns max|u_new| or None."""
+        idx = vals = dense = None
+        n = 0
+        if isinstance(force, np.ndarray):
+            dense = np.ascontiguousarray(force, dtype=np.float64)
+            if dense.shape != self.grid.shape:
+                raise ConfigError("dense force shape does not match the grid")
+        elif force is not None:
+            idx = np.ascontiguousarray(np.asarray(force[0], dtype=np.int64).reshape(-1))
+            vals = np.ascontiguousarray(np.asarray(force[1], dtype=np.float64).reshape(-1))
+            n = len(idx)
+        m = ctypes.c_double(0.0)
+        self._ck(self.L.wo_step(self.h, n, N.ptr(idx), N.ptr(vals), N.ptr(dense),
+                                int(bool(want_max)), ctypes.byref(m)), "wo_step")
+        return m.value if want_max else None
+
+    # ---------------------------------------------------------- profiling
+    def set_profiling(self, on):
+        self._ck(self.L.wo_set_profiling(self.h, int(bool(on))), "wo_set_profiling")
+
+    def stats(self):
+        a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
+        self._ck(self.L.wo_stats(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)),
+                 "wo_stats")
+        return {"launches": a.value, "step_launches": b.value, "step_kernel_ms": c.value}
+
+    def reset_stats(self):
+        self._ck(self.L.wo_reset_stats(self.h), "wo_reset_stats")
+
+    def device_bytes(self):
+        return int(self.L.wo_device_bytes(self.h))
+
+
+_CACHE: OrderedDict = OrderedDict()
+_CACHE_MAX = 3
+
+
+def get_context(grid: Grid, dtype, device=0) -> DeviceGrid:
+    """Cached DeviceGrid per (shape, dx, dtype, device)."""
+    key = (grid.shape, float(grid.dx), np.dtype(dtype).str, device)
+    ctx = _CACHE.get(key)
+    if ctx is None:
+        while len(_CACHE) >= _CACHE_MAX:
+            _, old = _CACHE.popitem(last=False)
+            old.close()
+        ctx = DeviceGrid(grid, dtype, device)
+        _CACHE[key] = ctx
+    else:
+        _CACHE.move_to_end(key)
+    return ctx
+
+
+def release_contexts():
+    while _CACHE:
+        _, c = _CACHE.popitem()
+        c.close()

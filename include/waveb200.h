@@ -113,8 +113,9 @@ int wo_free_history(wo_ctx* ctx);
 /* Per-step shot cost and compact adjoint store from the recorded support
  * values (fwi.py:57-63, tato.py:154-163, gradients.py:231-239, 263):
  * cost_n = (((c1*dot)*c2)*c3)/c4; FWI uses measured[n_sup][N] (device
- * support order), TATO adj = adj_coef*u.  When write_adj, the store becomes
- * T(adj)*T(k).  *cost_out = sum over n in order. */
+ * support order; NULL reuses the traces of the previous call), TATO adj =
+ * adj_coef*u.  When write_adj, the store becomes T(adj)*T(k).  *cost_out =
+ * sum over n in order. */
 int wo_shot_misfit(wo_ctx* ctx, int64_t n_steps, int kind, const double* measured,
                    double c1, double c2, double c3, double c4, double adj_coef, int write_adj,
                    double k, double* cost_out);
@@ -128,7 +129,8 @@ int wo_sweep_backward(wo_ctx* ctx, int64_t n_steps, int64_t src_flat, const doub
                       int inject_support, int accumulate, double dt, int64_t* fail_step,
                       double* fail_max);
 
-/* acc /= T(2k) in place, then copy out (gradients.py:315). */
+/* acc /= T(2k) in place, then copy out (gradients.py:315); out == NULL
+ * leaves the gradient resident on the device. */
 int wo_get_gradient(wo_ctx* ctx, double two_k, void* out);
 
 /* One explicit step with an optional sparse (idx, vals) or dense (fp64
@@ -172,6 +174,13 @@ int wo_stats(wo_ctx* ctx, int64_t* launches, int64_t* step_launches, double* ste
 int wo_reset_stats(wo_ctx* ctx);
 /* Device bytes held by the context (fields + support storage). */
 int64_t wo_device_bytes(const wo_ctx* ctx);
+/* CUDA-event marks on the context stream (8 slots) for device timing. */
+int wo_timer_mark(wo_ctx* ctx, int idx);
+int wo_timer_elapsed(wo_ctx* ctx, int a, int b, double* ms);
+int wo_synchronize(wo_ctx* ctx);
+/* Device address of the accumulator (C-order field at the context dtype),
+ * for collectives that sum per-shot accumulators across GPUs in place. */
+void* wo_accumulator_ptr(wo_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -26,7 +26,8 @@ EXPORTS = (
     "wo_shot_misfit", "wo_get_store", "wo_sweep_backward", "wo_get_gradient", "wo_step",
     "wo_apply_step", "wo_apply_kernel_increment", "wo_set_profiling", "wo_stats",
     "wo_reset_stats", "wo_device_bytes", "wo_sweep_adjoint_reference", "wo_free_history",
-    "wo_design_filter", "wo_design_project", "wo_design_chain",
+    "wo_design_filter", "wo_design_project", "wo_design_chain", "wo_timer_mark",
+    "wo_timer_elapsed", "wo_synchronize", "wo_accumulator_ptr",
 )
 
 
@@ -77,6 +78,10 @@ _SIGS = {
     "wo_design_project": (c_int, [c_i64, c_vp, c_dbl, c_dbl, c_dbl, c_dbl, c_vp, c_vp, c_int]),
     "wo_design_chain": (c_int, [c_int, P_i64, c_vp, c_vp, c_dbl, c_dbl, c_dbl, c_vp, c_int,
                                 c_vp, c_vp, c_vp, c_int]),
+    "wo_timer_mark": (c_int, [c_vp, c_int]),
+    "wo_timer_elapsed": (c_int, [c_vp, c_int, c_int, P_dbl]),
+    "wo_synchronize": (c_int, [c_vp]),
+    "wo_accumulator_ptr": (c_vp, [c_vp]),
 }
 
 

@@ -75,6 +75,7 @@ struct wo_ctx {
     size_t u3_bytes = 0;
 
     bool prof = false;
+    cudaEvent_t marks[8] = {};
     std::vector<cudaEvent_t> ev_free, ev_used;
     int64_t launches = 0, step_launches = 0;
     double step_ms = 0.0;
@@ -587,12 +588,15 @@ int misfit_t(wo_ctx* ctx, int64_t N, int kind, const double* measured, double c1
     REQUIRE(ctx->n_sup > 0, "shot misfit needs a support");
     REQUIRE(ctx->store_bytes >= (size_t)N * ctx->n_sup * sizeof(T), "no recorded support values");
     int rc;
-    if (kind == SHOT_FWI) {
+    if (kind == SHOT_FWI && measured) {
         rc = ensure(ctx, &ctx->measured, &ctx->measured_bytes, (size_t)N * ctx->n_sup * 8);
         if (rc) return rc;
         CK(cudaMemcpyAsync(ctx->measured, measured, (size_t)N * ctx->n_sup * 8,
                            cudaMemcpyHostToDevice, ctx->stream));
     }
+    // measured == NULL: reuse the traces uploaded by the previous call
+    REQUIRE(kind != SHOT_FWI || ctx->measured_bytes >= (size_t)N * ctx->n_sup * 8,
+            "FWI misfit without measured traces");
     rc = ensure(ctx, &ctx->partial, &ctx->partial_bytes, (size_t)N * 8 + 8);
     if (rc) return rc;
     if (!ctx->cost) {
@@ -616,8 +620,39 @@ int gradient_t(wo_ctx* ctx, double two_k, void* out) {
                                                       (T)two_k);
     ctx->launches++;
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(out, ctx->acc, ctx->field_bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+    if (out)
+        CK(cudaMemcpyAsync(out, ctx->acc, ctx->field_bytes(), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    return WO_OK;
+}
+
+// gamma.astype(T) (solver.py:94,100) on the device: fp64 host data goes up
+// through a fixed double-buffered staging area and is cast by a kernel, so
+// the host never loops over the field and big grids need no fp64 twin.
+template <typename T>
+__global__ void cast_kernel(const double* src, T* dst, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        dst[i] = (T)src[i];
+}
+
+template <typename T>
+int upload_cast_t(wo_ctx* ctx, const double* host, char* dev, int64_t n) {
+    const int64_t chunk = 4 << 20;  // doubles per staging half (32 MiB)
+    double* stage = nullptr;
+    int rc = dev_alloc(ctx, (void**)&stage, (size_t)std::min(n, 2 * chunk) * 8);
+    if (rc) return rc;
+    int half = 0;  // stream order keeps a half busy until its cast kernel ran
+    for (int64_t off = 0; off < n; off += chunk, half ^= 1) {
+        const int64_t m = std::min(chunk, n - off);
+        double* s = stage + (size_t)half * chunk;
+        CK(cudaMemcpyAsync(s, host + off, (size_t)m * 8, cudaMemcpyHostToDevice, ctx->stream));
+        cast_kernel<T><<<296, 256, 0, ctx->stream>>>(s, reinterpret_cast<T*>(dev) + off, m);
+        ctx->launches++;
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(stage);
+    ctx->dev_bytes -= (int64_t)std::min(n, 2 * chunk) * 8;
     return WO_OK;
 }
 
@@ -729,6 +764,8 @@ void wo_destroy(wo_ctx* ctx) {
                     ctx->f_idx, ctx->f_vals, ctx->f_dense, ctx->hist, ctx->u3};
     for (void* b : bufs)
         if (b) cudaFree(b);
+    for (auto e : ctx->marks)
+        if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_free) cudaEventDestroy(e);
     for (auto e : ctx->ev_used) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -746,11 +783,11 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
     // gamma.astype(T) (solver.py:94/100) on the host: halves H2D bytes in fp32
     const int64_t n = ctx->alloc_cells();
     if (ctx->itemsize == 4) {
-        std::vector<float> g(n);
-        for (int64_t i = 0; i < n; ++i) g[i] = (float)gamma[i];
-        CK(cudaMemcpy(ctx->gamma, g.data(), n * 4, cudaMemcpyHostToDevice));
+        rc = upload_cast_t<float>(ctx, gamma, ctx->gamma, n);
+        if (rc) return rc;
     } else {
-        CK(cudaMemcpy(ctx->gamma, gamma, n * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(ctx->gamma, gamma, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
     }
     ctx->material_set = true;
     return WO_OK;
@@ -950,6 +987,36 @@ int wo_reset_stats(wo_ctx* ctx) {
 }
 
 int64_t wo_device_bytes(const wo_ctx* ctx) { return ctx ? ctx->dev_bytes : 0; }
+
+int wo_timer_mark(wo_ctx* ctx, int idx) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(idx >= 0 && idx < 8, "timer slot out of range");
+    if (!ctx->marks[idx]) CK(cudaEventCreate(&ctx->marks[idx]));
+    CK(cudaEventRecord(ctx->marks[idx], ctx->stream));
+    return WO_OK;
+}
+
+int wo_timer_elapsed(wo_ctx* ctx, int a, int b, double* ms) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(a >= 0 && a < 8 && b >= 0 && b < 8 && ctx->marks[a] && ctx->marks[b],
+            "timer slots not recorded");
+    CK(cudaEventSynchronize(ctx->marks[b]));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, ctx->marks[a], ctx->marks[b]));
+    *ms = f;
+    return WO_OK;
+}
+
+void* wo_accumulator_ptr(wo_ctx* ctx) { return ctx ? (void*)ctx->acc : nullptr; }
+
+int wo_synchronize(wo_ctx* ctx) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return WO_OK;
+}
 
 // ---------------------------------------------------------------- drop-ins
 namespace {

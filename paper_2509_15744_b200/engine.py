@@ -248,10 +248,23 @@ class DeviceGrid:
     def free_history(self):
         self._ck(self.L.wo_free_history(self.h), "wo_free_history")
 
-    def gradient(self, two_k):
-        out = np.empty(self.grid.shape, self.dtype)
+    def gradient(self, two_k, copy=True):
+        """acc /= T(2k); returns the host copy (copy=False: stays on the device)."""
+        out = np.empty(self.grid.shape, self.dtype) if copy else None
         self._ck(self.L.wo_get_gradient(self.h, float(two_k), N.ptr(out)), "wo_get_gradient")
         return out
+
+    def timer_mark(self, idx):
+        self._ck(self.L.wo_timer_mark(self.h, int(idx)), "wo_timer_mark")
+
+    def timer_elapsed_ms(self, a, b):
+        ms = ctypes.c_double(0.0)
+        self._ck(self.L.wo_timer_elapsed(self.h, int(a), int(b), ctypes.byref(ms)),
+                 "wo_timer_elapsed")
+        return ms.value
+
+    def synchronize(self):
+        self._ck(self.L.wo_synchronize(self.h), "wo_synchronize")
 
     def step(self, force=None, want_max=False):
         """One step with a sparse/dense/None force; returns max|u_new| or None."""

@@ -71,6 +71,13 @@ void wo_destroy(wo_ctx* ctx);
  * (solver.py:96), (dt/dx)**2 for acoustic (solver.py:108). */
 int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, double rho1,
                     double kappa1, double rho2, double kappa2, double dt, double ratio2);
+/* Options.  WO_OPT_FAST_DIV (default 1): let wo_set_material enable the
+ * branch-free division path when it verifies bit-identical to the IEEE
+ * intrinsics for every coefficient of the material (0 = always intrinsics).
+ * wo_fast_div_active reports the path in use. */
+#define WO_OPT_FAST_DIV 1
+int wo_set_option(wo_ctx* ctx, int option, int value);
+int wo_fast_div_active(const wo_ctx* ctx);
 /* Kernel-increment scalars (gradients.py:117-129, kernels.py:149-152): the
  * fp64 values cv, cg, 1/(2dt), 1/(2dx); cast to the field dtype here. */
 int wo_set_kernel_coefficients(wo_ctx* ctx, double cv, double cg, double inv2dt,

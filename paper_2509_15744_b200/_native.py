@@ -27,7 +27,8 @@ EXPORTS = (
     "wo_apply_step", "wo_apply_kernel_increment", "wo_set_profiling", "wo_stats",
     "wo_reset_stats", "wo_device_bytes", "wo_sweep_adjoint_reference", "wo_free_history",
     "wo_design_filter", "wo_design_project", "wo_design_chain", "wo_timer_mark",
-    "wo_timer_elapsed", "wo_synchronize", "wo_accumulator_ptr",
+    "wo_timer_elapsed", "wo_synchronize", "wo_accumulator_ptr", "wo_set_option",
+    "wo_fast_div_active",
 )
 
 
@@ -82,7 +83,10 @@ _SIGS = {
     "wo_timer_elapsed": (c_int, [c_vp, c_int, c_int, P_dbl]),
     "wo_synchronize": (c_int, [c_vp]),
     "wo_accumulator_ptr": (c_vp, [c_vp]),
+    "wo_set_option": (c_int, [c_vp, c_int, c_int]),
+    "wo_fast_div_active": (c_int, [c_vp]),
 }
+WO_OPT_FAST_DIV = 1
 
 
 def load(require_device=False):

@@ -47,6 +47,9 @@ struct wo_ctx {
     int cur = 0;                       // u[cur] = u^n, u[1-cur] = u^{n-1}
 
     bool material_set = false;
+    bool fast_div = false;             // verify_material_kernel passed for this material
+    int allow_fast_div = 1;            // wo_set_option(WO_OPT_FAST_DIV)
+    unsigned char* sup_plane = nullptr;   // per local plane: holds a support node
     int flavor = 0;
     double rho0 = 0, rho1 = 0, kappa1 = 0, rho2 = 0, kappa2 = 0, dt_mat = 0, ratio2 = 0;
     double cv = 0, cg = 0, inv2dt = 0, inv2dx = 0;
@@ -226,14 +229,23 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     a.inv2dx = (T)ctx->inv2dx;
     a.sdt = (T)sp.sdt;
     a.backward = sp.backward;
-    a.n_src = sp.n_src;
+    a.one_d = ctx->ndim == 1;
+    a.n_src = 0;
     for (int s = 0; s < sp.n_src; ++s) {
-        a.src_flat[s] = sp.src_flat[s];
-        a.src_val[s] = (T)sp.src_val[s];
+        // local kernel-space (i, j, k) of the node; skip nodes outside the slab
+        const long long f = sp.src_flat[s];
+        const long long pl = ctx->plane();
+        if (f < 0 || f >= ctx->cells()) continue;
+        a.src_i[a.n_src] = (int)(f / pl);
+        a.src_j[a.n_src] = (int)((f % pl) / ctx->kn2);
+        a.src_k[a.n_src] = (int)(f % ctx->kn2);
+        a.src_val[a.n_src] = (T)sp.src_val[s];
+        a.n_src++;
     }
     a.sup_mode = sp.sup_mode;
     a.sup_mask = ctx->mask;
     a.sup_prefix = ctx->prefix;
+    a.sup_plane = ctx->sup_plane;
     if (sp.sup_mode != SUP_NONE) {
         T* st = reinterpret_cast<T*>(ctx->store) + sp.row * ctx->n_sup;
         a.trace_row = st;
@@ -244,16 +256,22 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     dim3 block(BX, BY, 1);
     dim3 grid((ctx->kn2 + BX - 1) / BX, (ctx->kn1 + BY - 1) / BY,
               (ctx->kn0 + a.chunk - 1) / a.chunk);
-    const bool one_d = ctx->ndim == 1;
     if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
-#define LAUNCH(ACC, CHK, ONED) step_kernel<T, ACC, CHK, ONED><<<grid, block, 0, ctx->stream>>>(a)
-    if (sp.acc) {
-        if (sp.check) { if (one_d) LAUNCH(true, true, true); else LAUNCH(true, true, false); }
-        else { if (one_d) LAUNCH(true, false, true); else LAUNCH(true, false, false); }
+#define LAUNCH(FL, FAST, ACC, CHK) \
+    step_kernel<T, FL, FAST, ACC, CHK><<<grid, block, 0, ctx->stream>>>(a)
+#define LAUNCH_AC(FL, FAST)                                                   \
+    do {                                                                      \
+        if (sp.acc) { if (sp.check) LAUNCH(FL, FAST, true, true);             \
+                      else LAUNCH(FL, FAST, true, false); }                   \
+        else { if (sp.check) LAUNCH(FL, FAST, false, true);                   \
+               else LAUNCH(FL, FAST, false, false); }                         \
+    } while (0)
+    if (ctx->flavor == RHO_SCALED) {
+        if (ctx->fast_div) LAUNCH_AC(RHO_SCALED, true); else LAUNCH_AC(RHO_SCALED, false);
     } else {
-        if (sp.check) { if (one_d) LAUNCH(false, true, true); else LAUNCH(false, true, false); }
-        else { if (one_d) LAUNCH(false, false, true); else LAUNCH(false, false, false); }
+        if (ctx->fast_div) LAUNCH_AC(ACOUSTIC, true); else LAUNCH_AC(ACOUSTIC, false);
     }
+#undef LAUNCH_AC
 #undef LAUNCH
     if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
     ctx->launches++;
@@ -677,6 +695,40 @@ int create_common(wo_ctx* ctx) {
 #define DISPATCH(ctx, FN, ...) \
     ((ctx)->itemsize == 4 ? FN<float>(__VA_ARGS__) : FN<double>(__VA_ARGS__))
 
+// Decide the division path of the step kernel for the current material
+// (fastdiv.cuh): branch-free sequences only if every derived coefficient is
+// bit-identical to the IEEE intrinsic, checked over the whole allocation
+// (ghost planes included).
+template <typename T>
+static int verify_fast_div_t(wo_ctx* ctx) {
+    ctx->fast_div = false;
+    if (!ctx->allow_fast_div) return WO_OK;
+    int* d_ok = nullptr;
+    int rc = dev_alloc(ctx, (void**)&d_ok, sizeof(int));
+    if (rc) return rc;
+    const int one = 1;
+    CK(cudaMemcpyAsync(d_ok, &one, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    const int n0 = ctx->kn0 + ctx->has_lo + ctx->has_hi;
+    const T* g = reinterpret_cast<const T*>(ctx->gamma);
+    if (ctx->flavor == RHO_SCALED)
+        verify_material_kernel<T, RHO_SCALED><<<592, 256, 0, ctx->stream>>>(
+            g, n0, ctx->kn1, ctx->kn2, mat_scalars<T>(ctx), d_ok);
+    else
+        verify_material_kernel<T, ACOUSTIC><<<592, 256, 0, ctx->stream>>>(
+            g, n0, ctx->kn1, ctx->kn2, mat_scalars<T>(ctx), d_ok);
+    ctx->launches++;
+    int ok = 0;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_ok);
+    ctx->dev_bytes -= (int64_t)sizeof(int);
+    ctx->fast_div = ok != 0;
+    return WO_OK;
+}
+
+static int verify_fast_div(wo_ctx* ctx) { return DISPATCH(ctx, verify_fast_div_t, ctx); }
+
 extern "C" {
 
 int wo_version(void) { return 100; }
@@ -761,7 +813,7 @@ void wo_destroy(wo_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     void* bufs[] = {ctx->gamma, ctx->u[0], ctx->u[1], ctx->acc, ctx->mask, ctx->prefix,
                     ctx->store, ctx->measured, ctx->partial, ctx->cost, ctx->maxslots,
-                    ctx->f_idx, ctx->f_vals, ctx->f_dense, ctx->hist, ctx->u3};
+                    ctx->f_idx, ctx->f_vals, ctx->f_dense, ctx->hist, ctx->u3, ctx->sup_plane};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (auto e : ctx->marks)
@@ -790,6 +842,20 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
         CK(cudaStreamSynchronize(ctx->stream));
     }
     ctx->material_set = true;
+    return verify_fast_div(ctx);
+}
+
+int wo_set_option(wo_ctx* ctx, int option, int value) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(option == WO_OPT_FAST_DIV, "unknown option");
+    ctx->allow_fast_div = value != 0;
+    if (ctx->material_set) return verify_fast_div(ctx);
+    ctx->fast_div = false;
+    return WO_OK;
+}
+
+int wo_fast_div_active(const wo_ctx* ctx) { return ctx && ctx->fast_div ? 1 : 0;
     return WO_OK;
 }
 
@@ -812,10 +878,15 @@ int wo_set_support(wo_ctx* ctx, int64_t n_sup, const int64_t* flat) {
     if (!ctx->mask) {
         if ((rc = dev_alloc(ctx, (void**)&ctx->mask, words * 4))) return rc;
         if ((rc = dev_alloc(ctx, (void**)&ctx->prefix, words * 4))) return rc;
+        if ((rc = dev_alloc(ctx, (void**)&ctx->sup_plane, (size_t)ctx->kn0))) return rc;
     }
     std::vector<unsigned int> m(words, 0u);
     std::vector<int> p(words, 0);
-    for (int64_t s = 0; s < n_sup; ++s) m[flat[s] >> 5] |= 1u << (flat[s] & 31);
+    std::vector<unsigned char> pl(ctx->kn0, 0);
+    for (int64_t s = 0; s < n_sup; ++s) {
+        m[flat[s] >> 5] |= 1u << (flat[s] & 31);
+        pl[flat[s] / ctx->plane()] = 1;
+    }
     int run = 0;
     for (int64_t w = 0; w < words; ++w) {
         p[w] = run;
@@ -823,6 +894,7 @@ int wo_set_support(wo_ctx* ctx, int64_t n_sup, const int64_t* flat) {
     }
     CK(cudaMemcpy(ctx->mask, m.data(), words * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->prefix, p.data(), words * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->sup_plane, pl.data(), pl.size(), cudaMemcpyHostToDevice));
     ctx->n_sup = n_sup;
     return WO_OK;
 }

@@ -15,14 +15,20 @@
 // Layout: C-order [n0][n1][n2], axis 2 contiguous.  2D grids run as
 // (1, n0, n1) and 1D as (1, 1, n0) — the skipped axis contributes no
 // stencil term and a +0 gradient term, which leaves every result bit
-// unchanged (see DESIGN.md "Dimension mapping").
+// unchanged (DESIGN.md "Dimension mapping").
 //
-// Parallelisation: a CTA owns a BY x BX tile of the (axis1, axis2) plane and
-// marches a chunk of axis 0.  The centre column lives in a register queue
-// (u[i-1], u[i], u[i+1]; m[i], m[i+1]); the current plane of u and m, with a
-// one-cell halo, is staged in double-buffered shared memory, so each plane
-// costs one __syncthreads.  Output u^{n+1} is written in place over u^{n-1}
-// (each cell reads its own u^{n-1} before writing), which is what keeps the
+// Parallelisation (2.5D march): a CTA owns a BY x BX tile of the
+// (axis1, axis2) plane and marches a chunk of axis 0.  Per plane i, with ONE
+// __syncthreads:
+//   A  stage u(i) and m(i+1) (centre + one-cell halo) in shared memory
+//   C  compute the in-plane face weights of plane i+1 once per face
+//   D  stencil + injections + kernel increment of plane i, reading the
+//      faces of plane i computed one iteration earlier
+// The centre column lives in a register queue (u[i-1..i+1], gamma[i..i+1],
+// m, axis-0 face); loads for plane i+1/i+2 are issued one iteration ahead.
+// Halo cells are spread over the first 2*(BX+BY) threads so halo work costs
+// whole warps, not one divergent lane per warp.  Output u^{n+1} is written
+// in place over u^{n-1} (each cell reads its own u^{n-1} first), keeping the
 // device footprint at four field buffers: gamma, two levels, accumulator.
 #pragma once
 
@@ -32,6 +38,8 @@ namespace wb {
 
 constexpr int BX = 32;
 constexpr int BY = 8;
+constexpr int NTHREADS = BX * BY;
+constexpr int NHALO = 2 * (BX + BY);
 constexpr int MAX_SRC = 8;
 
 enum SupportMode : int { SUP_NONE = 0, SUP_GATHER = 1, SUP_INJECT = 2 };
@@ -51,14 +59,16 @@ template <typename T> struct StepArgs {
     // kernel-increment scalars, cast to T on the host (kernels.py:149-152)
     T cv, cg, inv2dt, inv2dx, sdt;
     int backward;       // 1: physical window is (out, cur, prev)
-    // nodal sources: local flat index (-1 = not owned) and T(value)
+    int one_d;          // reference ndim == 1: (cg*ga)*gb ordering (kernels.py:83)
+    // nodal sources at local (i, j, k); i = -1: not owned by this context
     int n_src;
-    long long src_flat[MAX_SRC];
+    int src_i[MAX_SRC], src_j[MAX_SRC], src_k[MAX_SRC];
     T src_val[MAX_SRC];
     // support (sensors / objective region)
     int sup_mode;
     const unsigned int* sup_mask;   // bit per cell
     const int* sup_prefix;          // set bits before each mask word
+    const unsigned char* sup_plane; // 1 if local plane i holds a support node
     T* trace_row;                   // SUP_GATHER: row n of the [N][n_sup] store
     const T* adj_row;               // SUP_INJECT: row n of the k-scaled store
     // stability max (CHECK only): atomicMax on |out| bit patterns
@@ -68,17 +78,21 @@ template <typename T> struct StepArgs {
 template <typename T>
 __device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
 
-template <typename T, bool ACC, bool CHECK, bool ONE_D>
-__global__ void __launch_bounds__(BX * BY)
+template <typename T, int FLAVOR, bool FAST, bool ACC, bool CHECK>
+__global__ void __launch_bounds__(NTHREADS)
 step_kernel(const StepArgs<T> a) {
     using Tr = FTraits<T>;
+    using MT = Mat<T, FLAVOR, FAST>;
     __shared__ T su[2][BY + 2][BX + 2];
     __shared__ T sm[2][BY + 2][BX + 2];
-    __shared__ typename Tr::Bits smax[BX * BY / 32];
+    __shared__ T sfk[2][BY][BX + 1];      // face (k-1, k) at [ty][tx]
+    __shared__ T sfj[2][BY + 1][BX];      // face (j-1, j) at [ty][tx]
+    __shared__ typename Tr::Bits smax[NTHREADS / 32];
 
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const int k = blockIdx.x * BX + tx;
-    const int j = blockIdx.y * BY + ty;
+    const int tid = ty * BX + tx;
+    const int k0 = blockIdx.x * BX, j0 = blockIdx.y * BY;
+    const int k = k0 + tx, j = j0 + ty;
     const int n1 = a.n1, n2 = a.n2;
     const bool inb = (j < n1) && (k < n2);
     const long long plane = (long long)n1 * n2;
@@ -86,138 +100,144 @@ step_kernel(const StepArgs<T> a) {
     const int i1 = min(i0 + a.chunk, a.n0);
     const MatScalars<T>& M = a.mat;
 
-    // halo roles (the 5-point in-plane stencil needs no corners)
-    const int hk = (tx == 0) ? k - 1 : ((tx == BX - 1) ? k + 1 : -1);
-    const int hj = (ty == 0) ? j - 1 : ((ty == BY - 1) ? j + 1 : -1);
-    const bool has_hk = (hk >= 0) && (hk < n2) && (j < n1);
-    const bool has_hj = (hj >= 0) && (hj < n1) && (k < n2);
-    const int sxk = (tx == 0) ? 0 : BX + 1;   // smem column of the k-halo
-    const int syj = (ty == 0) ? 0 : BY + 1;   // smem row of the j-halo
+    // ---- halo role of this thread (threads 0 .. NHALO-1) ----
+    int hj = -1, hk = -1, hsy = 0, hsx = 0;
+    if (tid < BY) { hj = j0 + tid; hk = k0 - 1; hsy = tid + 1; hsx = 0; }
+    else if (tid < 2 * BY) { hj = j0 + tid - BY; hk = k0 + BX; hsy = tid - BY + 1; hsx = BX + 1; }
+    else if (tid < 2 * BY + BX) { hj = j0 - 1; hk = k0 + tid - 2 * BY; hsy = 0; hsx = tid - 2 * BY + 1; }
+    else if (tid < NHALO) { hj = j0 + BY; hk = k0 + tid - 2 * BY - BX; hsy = BY + 1; hsx = tid - 2 * BY - BX + 1; }
+    const bool hval = hj >= 0 && hj < n1 && hk >= 0 && hk < n2;
+    const long long hofs = (long long)hj * n2 + hk;
     const long long cofs = (long long)j * n2 + k;
-    const long long hkofs = (long long)j * n2 + hk;
-    const long long hjofs = (long long)hj * n2 + k;
 
-    // prologue: centre column queue for plane i0
-    T u_m1 = T(0), u_0 = T(0), u_p1 = T(0);
-    T g_0 = T(1), g_p1 = T(1);
-    T m_0 = T(0), wf0_lo = T(0);
-    T hu_k = T(0), hg_k = T(1), hu_j = T(0), hg_j = T(1);
+    const int gi0 = i0 + a.i_off;
+    // ---- prologue: plane i0 queue, m(i0) in smem, faces of plane i0 ----
+    T u_m1 = T(0), u_0 = T(0), u_p1 = T(0), g_0 = T(1), g_p1 = T(1), wf0_lo = T(0);
+    T up = T(0), acc_old = T(0);
+    T hu = T(0), hg = T(1);
     if (inb) {
         const long long c = (long long)i0 * plane + cofs;
         u_0 = ldg(a.u_cur + c);
         g_0 = ldg(a.gamma + c);
-        if (i0 + a.i_off > 0) {
-            u_m1 = ldg(a.u_cur + c - plane);
-            const T g_m1 = ldg(a.gamma + c - plane);
-            m_0 = mat_m(M, g_0);
-            wf0_lo = Tr::rcp(mat_m(M, g_m1) + m_0);
-        } else {
-            m_0 = mat_m(M, g_0);
-        }
-        if (i0 + a.i_off < a.n0g - 1) {
+        up = ldg(a.u_prev + c);
+        if (ACC) acc_old = a.acc[c];
+        if (gi0 > 0) u_m1 = ldg(a.u_cur + c - plane);
+        if (gi0 + 1 < a.n0g) {
             u_p1 = ldg(a.u_cur + c + plane);
             g_p1 = ldg(a.gamma + c + plane);
         }
     }
-    if (has_hk) {
-        hu_k = ldg(a.u_cur + (long long)i0 * plane + hkofs);
-        hg_k = ldg(a.gamma + (long long)i0 * plane + hkofs);
+    T m_0 = MT::m(M, g_0);
+    if (inb && gi0 > 0) {
+        const T g_m1 = ldg(a.gamma + (long long)i0 * plane + cofs - plane);
+        wf0_lo = MT::face(MT::m(M, g_m1), m_0);
     }
-    if (has_hj) {
-        hu_j = ldg(a.u_cur + (long long)i0 * plane + hjofs);
-        hg_j = ldg(a.gamma + (long long)i0 * plane + hjofs);
+    {
+        const int b = i0 & 1;
+        sm[b][ty + 1][tx + 1] = m_0;
+        if (hval) {
+            sm[b][hsy][hsx] = MT::m(M, ldg(a.gamma + (long long)i0 * plane + hofs));
+            hu = ldg(a.u_cur + (long long)i0 * plane + hofs);
+            if (gi0 + 1 < a.n0g) hg = ldg(a.gamma + (long long)(i0 + 1) * plane + hofs);
+        }
+        __syncthreads();
+        sfk[b][ty][tx] = MT::face(sm[b][ty + 1][tx], sm[b][ty + 1][tx + 1]);
+        sfj[b][ty][tx] = MT::face(sm[b][ty][tx + 1], sm[b][ty + 1][tx + 1]);
+        if (tid < BY) sfk[b][tid][BX] = MT::face(sm[b][tid + 1][BX], sm[b][tid + 1][BX + 1]);
+        else if (tid >= 32 && tid < 32 + BX)
+            sfj[b][BY][tid - 32] = MT::face(sm[b][BY][tid - 31], sm[b][BY + 1][tid - 31]);
     }
 
     typename Tr::Bits local_max = 0;
 
     for (int i = i0; i < i1; ++i) {
         const int gi = i + a.i_off;
-        const int buf = i & 1;
+        const int b = i & 1, nb = b ^ 1;
+        const bool next = i + 1 < i1;
         const long long c = (long long)i * plane + cofs;
-        // loads for this plane's epilogue and the next plane's queue
-        T up = T(0), acc_old = T(0);
-        T u_p2 = T(0), g_p2 = T(1);
-        T nhu_k = T(0), nhg_k = T(1), nhu_j = T(0), nhg_j = T(1);
-        if (inb) {
-            up = ldg(a.u_prev + c);
-            if (ACC) acc_old = a.acc[c];
-            if (gi + 2 < a.n0g && i + 1 < i1) {
-                u_p2 = ldg(a.u_cur + c + 2 * plane);
-                g_p2 = ldg(a.gamma + c + 2 * plane);
+
+        // ---- loads for the next iteration (one plane ahead) ----
+        T u_p2 = T(0), g_p2 = T(1), up_n = T(0), acc_n = T(0), hu_n = T(0), hg_n = T(1);
+        if (next) {
+            if (inb) {
+                up_n = ldg(a.u_prev + c + plane);
+                if (ACC) acc_n = a.acc[c + plane];
+                if (gi + 2 < a.n0g) {
+                    u_p2 = ldg(a.u_cur + c + 2 * plane);
+                    g_p2 = ldg(a.gamma + c + 2 * plane);
+                }
             }
-        }
-        if (i + 1 < i1) {
-            if (has_hk) {
-                nhu_k = ldg(a.u_cur + (long long)(i + 1) * plane + hkofs);
-                nhg_k = ldg(a.gamma + (long long)(i + 1) * plane + hkofs);
-            }
-            if (has_hj) {
-                nhu_j = ldg(a.u_cur + (long long)(i + 1) * plane + hjofs);
-                nhg_j = ldg(a.gamma + (long long)(i + 1) * plane + hjofs);
+            if (hval) {
+                hu_n = ldg(a.u_cur + (long long)(i + 1) * plane + hofs);
+                if (gi + 2 < a.n0g) hg_n = ldg(a.gamma + (long long)(i + 2) * plane + hofs);
             }
         }
 
-        // stage plane i (u and m) with its halo
-        su[buf][ty + 1][tx + 1] = u_0;
-        sm[buf][ty + 1][tx + 1] = m_0;
-        if (has_hk) {
-            su[buf][ty + 1][sxk] = hu_k;
-            sm[buf][ty + 1][sxk] = mat_m(M, hg_k);
-        }
-        if (has_hj) {
-            su[buf][syj][tx + 1] = hu_j;
-            sm[buf][syj][tx + 1] = mat_m(M, hg_j);
+        // ---- A: stage u(i) and m(i+1) ----
+        su[b][ty + 1][tx + 1] = u_0;
+        if (hval) su[b][hsy][hsx] = hu;
+        const bool has_p = gi < a.n0g - 1, has_m = gi > 0;
+        const T m_p1 = has_p ? MT::m(M, g_p1) : T(0);
+        if (next) {
+            sm[nb][ty + 1][tx + 1] = m_p1;
+            if (hval) sm[nb][hsy][hsx] = MT::m(M, hg);
         }
         __syncthreads();
 
-        if (inb) {
-            const bool has_p = gi < a.n0g - 1, has_m = gi > 0;
-            const bool jp = j < n1 - 1, jm = j > 0, kp = k < n2 - 1, km = k > 0;
-            T m_p1 = T(0), wf0_hi = T(0);
-            if (has_p) {
-                m_p1 = mat_m(M, g_p1);
-                wf0_hi = Tr::rcp(m_0 + m_p1);
-            }
-            const T u_jp = jp ? su[buf][ty + 2][tx + 1] : u_0;
-            const T u_jm = jm ? su[buf][ty][tx + 1] : u_0;
-            const T u_kp = kp ? su[buf][ty + 1][tx + 2] : u_0;
-            const T u_km = km ? su[buf][ty + 1][tx] : u_0;
+        // ---- C: in-plane faces of plane i+1 ----
+        if (next) {
+            sfk[nb][ty][tx] = MT::face(sm[nb][ty + 1][tx], sm[nb][ty + 1][tx + 1]);
+            sfj[nb][ty][tx] = MT::face(sm[nb][ty][tx + 1], sm[nb][ty + 1][tx + 1]);
+            if (tid < BY) sfk[nb][tid][BX] = MT::face(sm[nb][tid + 1][BX], sm[nb][tid + 1][BX + 1]);
+            else if (tid >= 32 && tid < 32 + BX)
+                sfj[nb][BY][tid - 32] = MT::face(sm[nb][BY][tid - 31], sm[nb][BY + 1][tid - 31]);
+        }
 
-            // ---- stencil, kernels.py:56-69 ----
+        // ---- D: plane i ----
+        T wf0_hi = T(0);
+        if (inb) {
+            const bool jp = j < n1 - 1, jm = j > 0, kp = k < n2 - 1, km = k > 0;
+            const T u_jp = jp ? su[b][ty + 2][tx + 1] : u_0;
+            const T u_jm = jm ? su[b][ty][tx + 1] : u_0;
+            const T u_kp = kp ? su[b][ty + 1][tx + 2] : u_0;
+            const T u_km = km ? su[b][ty + 1][tx] : u_0;
+            if (has_p) wf0_hi = MT::face(m_0, m_p1);
+
+            // stencil, kernels.py:56-69
             T accf = u_0 - u_0;
             if (has_p) accf += (u_p1 - u_0) * wf0_hi;
             if (has_m) accf -= (u_0 - u_m1) * wf0_lo;
-            if (jp) accf += (u_jp - u_0) * Tr::rcp(m_0 + sm[buf][ty + 2][tx + 1]);
-            if (jm) accf -= (u_0 - u_jm) * Tr::rcp(sm[buf][ty][tx + 1] + m_0);
-            if (kp) accf += (u_kp - u_0) * Tr::rcp(m_0 + sm[buf][ty + 1][tx + 2]);
-            if (km) accf -= (u_0 - u_km) * Tr::rcp(sm[buf][ty + 1][tx] + m_0);
+            if (jp) accf += (u_jp - u_0) * sfj[b][ty + 1][tx];
+            if (jm) accf -= (u_0 - u_jm) * sfj[b][ty][tx];
+            if (kp) accf += (u_kp - u_0) * sfk[b][ty][tx + 1];
+            if (km) accf -= (u_0 - u_km) * sfk[b][ty][tx];
             T kappa;
-            const T coef = mat_coef(M, g_0, kappa);
+            const T coef = MT::coef(M, g_0, kappa);
             T out = ((u_0 + u_0) - up) + coef * accf;
 
-            // ---- nodal injections, solver.py:167-170 (source first) ----
-            const long long flat = (long long)i * plane + cofs;
+            // nodal injections, solver.py:167-170 (sources first, then support)
             for (int s = 0; s < a.n_src; ++s)
-                if (flat == a.src_flat[s]) out = out + mat_fc(M, g_0, kappa) * a.src_val[s];
-            if (a.sup_mode != SUP_NONE) {
+                if (i == a.src_i[s] && j == a.src_j[s] && k == a.src_k[s])
+                    out = out + MT::fc(M, g_0, kappa) * a.src_val[s];
+            if (a.sup_mode != SUP_NONE && a.sup_plane[i]) {
+                const long long flat = c;
                 const unsigned int w = __ldg(a.sup_mask + (flat >> 5));
-                const unsigned int b = (unsigned int)(flat & 31);
-                if ((w >> b) & 1u) {
-                    const int s = __ldg(a.sup_prefix + (flat >> 5)) + __popc(w & ((1u << b) - 1u));
+                const unsigned int bit = (unsigned int)(flat & 31);
+                if ((w >> bit) & 1u) {
+                    const int s = __ldg(a.sup_prefix + (flat >> 5)) + __popc(w & ((1u << bit) - 1u));
                     if (a.sup_mode == SUP_GATHER) a.trace_row[s] = u_0;
-                    else out = out + mat_fc(M, g_0, kappa) * ldg(a.adj_row + s);
+                    else out = out + MT::fc(M, g_0, kappa) * ldg(a.adj_row + s);
                 }
             }
 
-            // ---- self-kernel increment, kernels.py:105-128 ----
+            // self-kernel increment, kernels.py:105-128
             if (ACC) {
                 const T va = a.backward ? (up - out) * a.inv2dt : (out - up) * a.inv2dt;
-                const T gz = (has_p ? u_p1 : u_0) - (has_m ? u_m1 : u_0);
-                const T g0 = gz * a.inv2dx;
+                const T g0 = ((has_p ? u_p1 : u_0) - (has_m ? u_m1 : u_0)) * a.inv2dx;
                 const T g1 = (u_jp - u_jm) * a.inv2dx;
                 const T g2 = (u_kp - u_km) * a.inv2dx;
                 T inc;
-                if (ONE_D) inc = a.sdt * ((a.cv * va) * va + (a.cg * g2) * g2);
+                if (a.one_d) inc = a.sdt * ((a.cv * va) * va + (a.cg * g2) * g2);
                 else inc = a.sdt * ((a.cv * va) * va + a.cg * (((g0 * g0) + (g1 * g1)) + (g2 * g2)));
                 a.acc[c] = acc_old + inc;
             }
@@ -227,12 +247,13 @@ step_kernel(const StepArgs<T> a) {
                 const typename Tr::Bits bits = Tr::abs_bits(out);
                 local_max = bits > local_max ? bits : local_max;
             }
-            // advance the centre queue
-            u_m1 = u_0; u_0 = u_p1; u_p1 = u_p2;
-            g_0 = g_p1; g_p1 = g_p2;
-            m_0 = m_p1; wf0_lo = wf0_hi;
         }
-        hu_k = nhu_k; hg_k = nhg_k; hu_j = nhu_j; hg_j = nhg_j;
+        // advance the queue
+        u_m1 = u_0; u_0 = u_p1; u_p1 = u_p2;
+        g_0 = g_p1; g_p1 = g_p2;
+        m_0 = m_p1; wf0_lo = wf0_hi;
+        up = up_n; acc_old = acc_n;
+        hu = hu_n; hg = hg_n;
     }
 
     if (CHECK) {
@@ -241,11 +262,11 @@ step_kernel(const StepArgs<T> a) {
             typename Tr::Bits v = __shfl_xor_sync(0xffffffffu, local_max, o);
             local_max = v > local_max ? v : local_max;
         }
-        const int lane = (ty * BX + tx) & 31, warp = (ty * BX + tx) >> 5;
+        const int lane = tid & 31, warp = tid >> 5;
         if (lane == 0) smax[warp] = local_max;
         __syncthreads();
         if (warp == 0) {
-            typename Tr::Bits v = lane < (BX * BY / 32) ? smax[lane] : 0;
+            typename Tr::Bits v = lane < (NTHREADS / 32) ? smax[lane] : 0;
             for (int o = 16; o > 0; o >>= 1) {
                 typename Tr::Bits w = __shfl_xor_sync(0xffffffffu, v, o);
                 v = w > v ? w : v;
@@ -253,6 +274,39 @@ step_kernel(const StepArgs<T> a) {
             if (lane == 0 && v) atomicMax(a.max_slot, v);
         }
     }
+}
+
+// Fast-division admissibility for the current material: every coefficient
+// the step kernel derives from gamma (m, coef, the face weight of each +1
+// neighbour on every axis) computed with the branch-free sequences must be
+// bit-identical to the IEEE intrinsics.  Any mismatch clears *ok.
+template <typename T, int FLAVOR>
+__global__ void verify_material_kernel(const T* gamma, int n0, int n1, int n2, MatScalars<T> M,
+                                       int* ok) {
+    using F = Mat<T, FLAVOR, true>;
+    using P = Mat<T, FLAVOR, false>;
+    const long long N = (long long)n0 * n1 * n2;
+    const long long pl = (long long)n1 * n2;
+    bool good = true;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < N;
+         c += (long long)gridDim.x * blockDim.x) {
+        const T g = gamma[c];
+        T kf, kp;
+        const T mf = F::m(M, g), mp = P::m(M, g);
+        const T cf = F::coef(M, g, kf), cp = P::coef(M, g, kp);
+        good &= FTraits<T>::bits(mf) == FTraits<T>::bits(mp);
+        good &= FTraits<T>::bits(cf) == FTraits<T>::bits(cp);
+        good &= FTraits<T>::bits(kf) == FTraits<T>::bits(kp);
+        const int kk = (int)(c % n2), jj = (int)((c / n2) % n1), ii = (int)(c / pl);
+        const long long nbr[3] = {ii + 1 < n0 ? c + pl : -1, jj + 1 < n1 ? c + n2 : -1,
+                                  kk + 1 < n2 ? c + 1 : -1};
+        for (int ax = 0; ax < 3; ++ax) {
+            if (nbr[ax] < 0) continue;
+            const T mh = P::m(M, gamma[nbr[ax]]);
+            good &= FTraits<T>::bits(F::face(mp, mh)) == FTraits<T>::bits(P::face(mp, mh));
+        }
+    }
+    if (!good) atomicExch(ok, 0);
 }
 
 }  // namespace wb

@@ -263,6 +263,13 @@ class DeviceGrid:
                  "wo_timer_elapsed")
         return ms.value
 
+    def set_fast_div(self, allow):
+        self._ck(self.L.wo_set_option(self.h, N.WO_OPT_FAST_DIV, int(bool(allow))),
+                 "wo_set_option")
+
+    def fast_div_active(self):
+        return bool(self.L.wo_fast_div_active(self.h))
+
     def synchronize(self):
         self._ck(self.L.wo_synchronize(self.h), "wo_synchronize")
 

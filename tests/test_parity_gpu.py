@@ -111,6 +111,34 @@ def test_gradient_superposed_bitexact(W, golden, name, prec):
     assert res.counter.peak_fields == 4
 
 
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_division_paths_agree(W, golden, prec):
+    """The verified branch-free division path is active on the desk material
+    and gives the same bits as the IEEE-intrinsic path."""
+    from paper_2509_15744_b200 import engine
+
+    g = golden("fwi3d")
+    c = cases.fwi3d_case()
+    problem, mat = product_fwi_problem(W, c, g["gamma_model"], g["measured"])
+    ctx = engine.get_context(problem.grid, W.precision_dtype(prec))
+    ctx.set_material(mat, problem.time.dt)
+    assert ctx.fast_div_active()
+    fast = W.gradient_superposed(problem, mat, W.SuperpositionConfig(k=c["k"], precision=prec))
+    try:
+        ctx.set_fast_div(False)
+        assert not ctx.fast_div_active()
+        plan = W.gradients.SuperposedPlan(problem, mat, W.SuperpositionConfig(k=c["k"],
+                                                                            precision=prec))
+        plan.upload()
+        ctx.set_fast_div(False)          # upload re-verified; force the precise path
+        plan.run()
+        slow = plan.download()
+    finally:
+        ctx.set_fast_div(True)
+    assert bits_equal(fast.gradient, slow)
+    assert bits_equal(slow, g[f"sup_grad_{prec}"])
+
+
 @pytest.mark.parametrize("name", ["fwi3d", "desk_fwi"])
 @pytest.mark.parametrize("prec", ["double", "single"])
 def test_gradient_reference_bitexact(W, golden, name, prec):

@@ -49,7 +49,7 @@ struct wo_ctx {
     bool material_set = false;
     bool fast_div = false;             // verify_material_kernel passed for this material
     int allow_fast_div = 1;            // wo_set_option(WO_OPT_FAST_DIV)
-    unsigned char* sup_plane = nullptr;   // per local plane: holds a support node
+    int sup_lo = 0, sup_hi = -1;       // local planes holding support nodes
     int flavor = 0;
     double rho0 = 0, rho1 = 0, kappa1 = 0, rho2 = 0, kappa2 = 0, dt_mat = 0, ratio2 = 0;
     double cv = 0, cg = 0, inv2dt = 0, inv2dx = 0;
@@ -219,8 +219,8 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     a.n0 = ctx->kn0;
     a.n1 = ctx->kn1;
     a.n2 = ctx->kn2;
-    a.i_off = ctx->i_off;
-    a.n0g = ctx->n0g;
+    a.i_lo = ctx->has_lo ? -1 : 0;
+    a.i_hi = ctx->kn0 + ctx->has_hi;
     a.chunk = choose_chunk(ctx);
     a.mat = mat_scalars<T>(ctx);
     a.cv = (T)ctx->cv;
@@ -242,10 +242,11 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
         a.src_val[a.n_src] = (T)sp.src_val[s];
         a.n_src++;
     }
-    a.sup_mode = sp.sup_mode;
+    a.sup_mode = ctx->n_sup > 0 ? sp.sup_mode : SUP_NONE;
+    a.sup_lo = ctx->sup_lo;
+    a.sup_hi = ctx->sup_hi;
     a.sup_mask = ctx->mask;
     a.sup_prefix = ctx->prefix;
-    a.sup_plane = ctx->sup_plane;
     if (sp.sup_mode != SUP_NONE) {
         T* st = reinterpret_cast<T*>(ctx->store) + sp.row * ctx->n_sup;
         a.trace_row = st;
@@ -675,6 +676,9 @@ int upload_cast_t(wo_ctx* ctx, const double* host, char* dev, int64_t n) {
 }
 
 int create_common(wo_ctx* ctx) {
+    // the step kernel indexes a context with 32-bit offsets (ghost planes incl.)
+    REQUIRE(ctx->alloc_cells() < (1ll << 31),
+            "grid too large for one context (>= 2^31 cells): use slab decomposition");
     CK(cudaSetDevice(ctx->device));
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     const size_t ab = (size_t)ctx->alloc_cells() * ctx->itemsize;
@@ -813,7 +817,7 @@ void wo_destroy(wo_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     void* bufs[] = {ctx->gamma, ctx->u[0], ctx->u[1], ctx->acc, ctx->mask, ctx->prefix,
                     ctx->store, ctx->measured, ctx->partial, ctx->cost, ctx->maxslots,
-                    ctx->f_idx, ctx->f_vals, ctx->f_dense, ctx->hist, ctx->u3, ctx->sup_plane};
+                    ctx->f_idx, ctx->f_vals, ctx->f_dense, ctx->hist, ctx->u3};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (auto e : ctx->marks)
@@ -878,15 +882,12 @@ int wo_set_support(wo_ctx* ctx, int64_t n_sup, const int64_t* flat) {
     if (!ctx->mask) {
         if ((rc = dev_alloc(ctx, (void**)&ctx->mask, words * 4))) return rc;
         if ((rc = dev_alloc(ctx, (void**)&ctx->prefix, words * 4))) return rc;
-        if ((rc = dev_alloc(ctx, (void**)&ctx->sup_plane, (size_t)ctx->kn0))) return rc;
     }
     std::vector<unsigned int> m(words, 0u);
     std::vector<int> p(words, 0);
-    std::vector<unsigned char> pl(ctx->kn0, 0);
-    for (int64_t s = 0; s < n_sup; ++s) {
-        m[flat[s] >> 5] |= 1u << (flat[s] & 31);
-        pl[flat[s] / ctx->plane()] = 1;
-    }
+    for (int64_t s = 0; s < n_sup; ++s) m[flat[s] >> 5] |= 1u << (flat[s] & 31);
+    ctx->sup_lo = n_sup ? (int)(flat[0] / ctx->plane()) : 0;
+    ctx->sup_hi = n_sup ? (int)(flat[n_sup - 1] / ctx->plane()) : -1;
     int run = 0;
     for (int64_t w = 0; w < words; ++w) {
         p[w] = run;
@@ -894,7 +895,6 @@ int wo_set_support(wo_ctx* ctx, int64_t n_sup, const int64_t* flat) {
     }
     CK(cudaMemcpy(ctx->mask, m.data(), words * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->prefix, p.data(), words * 4, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->sup_plane, pl.data(), pl.size(), cudaMemcpyHostToDevice));
     ctx->n_sup = n_sup;
     return WO_OK;
 }

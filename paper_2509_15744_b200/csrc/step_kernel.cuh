@@ -13,9 +13,15 @@
 // material array streamed from HBM.
 //
 // Layout: C-order [n0][n1][n2], axis 2 contiguous.  2D grids run as
-// (1, n0, n1) and 1D as (1, 1, n0) — the skipped axis contributes no
-// stencil term and a +0 gradient term, which leaves every result bit
-// unchanged.
+// (1, n0, n1) and 1D as (1, 1, n0).
+//
+// Boundaries without predicates: every load is clamped into the domain, so a
+// missing neighbour reads the cell itself (mirror).  The reference SKIPS the
+// boundary face terms (kernels.py:56-65); here they are present but equal
+// (u - u) * w = +0, and adding +0 leaves the face sum unchanged (it starts at
+// u - u = +0 and can never become -0), so the sum is bit-identical.  The
+// clamped central differences of kernels.py:118-125 are exactly the mirrored
+// ones.  Threads of partial tiles compute a clamped duplicate and skip stores.
 //
 // Parallelisation (2.5D march): a CTA owns a BY x BX tile of the
 // (axis1, axis2) plane and marches a chunk of axis 0.  Per plane i, with ONE
@@ -27,9 +33,8 @@
 // The centre column lives in a register queue (u[i-1..i+1], gamma[i..i+1],
 // m, axis-0 face); loads for plane i+1/i+2 are issued one iteration ahead.
 // Halo cells are spread over the first 2*(BX+BY) threads so halo work costs
-// whole warps, not one divergent lane per warp.  Output u^{n+1} is written
-// in place over u^{n-1} (each cell reads its own u^{n-1} first), keeping the
-// device footprint at four field buffers: gamma, two levels, accumulator.
+// whole warps.  u^{n+1} is written in place over u^{n-1} (each cell reads its
+// own u^{n-1} first): device footprint gamma + two levels + accumulator.
 #pragma once
 
 #include "common.cuh"
@@ -52,23 +57,21 @@ template <typename T> struct StepArgs {
     T* hist_out;        // optional second copy of u_out (full-history recording)
     T* acc;             // kernel accumulator (ACC only)
     int n0, n1, n2;     // local extents (n0 = planes of this slab)
-    int i_off;          // global axis-0 index of local plane 0
-    int n0g;            // global axis-0 extent
+    int i_lo, i_hi;     // loadable local planes: [-1 if ghost below, n0 (+1 if ghost above))
     int chunk;          // axis-0 planes per CTA
     MatScalars<T> mat;
     // kernel-increment scalars, cast to T on the host (kernels.py:149-152)
     T cv, cg, inv2dt, inv2dx, sdt;
     int backward;       // 1: physical window is (out, cur, prev)
     int one_d;          // reference ndim == 1: (cg*ga)*gb ordering (kernels.py:83)
-    // nodal sources at local (i, j, k); i = -1: not owned by this context
+    // nodal sources at local (i, j, k) owned by this context
     int n_src;
     int src_i[MAX_SRC], src_j[MAX_SRC], src_k[MAX_SRC];
     T src_val[MAX_SRC];
-    // support (sensors / objective region)
-    int sup_mode;
+    // support (sensors / objective region): planes [sup_lo, sup_hi] hold nodes
+    int sup_mode, sup_lo, sup_hi;
     const unsigned int* sup_mask;   // bit per cell
     const int* sup_prefix;          // set bits before each mask word
-    const unsigned char* sup_plane; // 1 if local plane i holds a support node
     T* trace_row;                   // SUP_GATHER: row n of the [N][n_sup] store
     const T* adj_row;               // SUP_INJECT: row n of the k-scaled store
     // stability max (CHECK only): atomicMax on |out| bit patterns
@@ -95,92 +98,88 @@ step_kernel(const StepArgs<T> a) {
     const int k = k0 + tx, j = j0 + ty;
     const int n1 = a.n1, n2 = a.n2;
     const bool inb = (j < n1) && (k < n2);
-    const long long plane = (long long)n1 * n2;
+    const int plane = n1 * n2;
     const int i0 = blockIdx.z * a.chunk;
     const int i1 = min(i0 + a.chunk, a.n0);
     const MatScalars<T>& M = a.mat;
 
-    // ---- halo role of this thread (threads 0 .. NHALO-1) ----
-    int hj = -1, hk = -1, hsy = 0, hsx = 0;
+    // clamped (mirror) coordinates of this thread's cell and halo cell
+    const int jc = min(j, n1 - 1), kc = min(k, n2 - 1);
+    int hj = 0, hk = 0, hsy = 0, hsx = 0;
+    const bool hal = tid < NHALO;
     if (tid < BY) { hj = j0 + tid; hk = k0 - 1; hsy = tid + 1; hsx = 0; }
     else if (tid < 2 * BY) { hj = j0 + tid - BY; hk = k0 + BX; hsy = tid - BY + 1; hsx = BX + 1; }
     else if (tid < 2 * BY + BX) { hj = j0 - 1; hk = k0 + tid - 2 * BY; hsy = 0; hsx = tid - 2 * BY + 1; }
     else if (tid < NHALO) { hj = j0 + BY; hk = k0 + tid - 2 * BY - BX; hsy = BY + 1; hsx = tid - 2 * BY - BX + 1; }
-    const bool hval = hj >= 0 && hj < n1 && hk >= 0 && hk < n2;
-    const long long hofs = (long long)hj * n2 + hk;
-    const long long cofs = (long long)j * n2 + k;
+    hj = min(max(hj, 0), n1 - 1);
+    hk = min(max(hk, 0), n2 - 1);
+    const int cofs = jc * n2 + kc;
+    const int hofs = hj * n2 + hk;
 
-    const int gi0 = i0 + a.i_off;
+    // sources inside this CTA's tile and chunk (uniform bitmask)
+    unsigned my_src = 0;
+    for (int s = 0; s < a.n_src; ++s)
+        if (a.src_i[s] >= i0 && a.src_i[s] < i1 && a.src_j[s] >= j0 && a.src_j[s] < j0 + BY &&
+            a.src_k[s] >= k0 && a.src_k[s] < k0 + BX)
+            my_src |= 1u << s;
+
+    // plane offsets, clamped to the loadable planes (mirror at global ends)
+    auto pofs = [&](int i) { return min(max(i, a.i_lo), a.i_hi - 1) * plane; };
+
     // ---- prologue: plane i0 queue, m(i0) in smem, faces of plane i0 ----
-    T u_m1 = T(0), u_0 = T(0), u_p1 = T(0), g_0 = T(1), g_p1 = T(1), wf0_lo = T(0);
-    T up = T(0), acc_old = T(0);
-    T hu = T(0), hg = T(1);
-    if (inb) {
-        const long long c = (long long)i0 * plane + cofs;
-        u_0 = ldg(a.u_cur + c);
-        g_0 = ldg(a.gamma + c);
-        up = ldg(a.u_prev + c);
-        if (ACC) acc_old = a.acc[c];
-        if (gi0 > 0) u_m1 = ldg(a.u_cur + c - plane);
-        if (gi0 + 1 < a.n0g) {
-            u_p1 = ldg(a.u_cur + c + plane);
-            g_p1 = ldg(a.gamma + c + plane);
-        }
-    }
+    const int o0 = i0 * plane + cofs;
+    T u_0 = ldg(a.u_cur + o0);
+    const T u_m1 = ldg(a.u_cur + pofs(i0 - 1) + cofs);
+    T g_0 = ldg(a.gamma + o0);
+    T u_p1 = ldg(a.u_cur + pofs(i0 + 1) + cofs);
+    T g_p1 = ldg(a.gamma + pofs(i0 + 1) + cofs);
+    T up = ldg(a.u_prev + o0);
+    T acc_old = ACC ? a.acc[o0] : T(0);
     T m_0 = MT::m(M, g_0);
-    if (inb && gi0 > 0) {
-        const T g_m1 = ldg(a.gamma + (long long)i0 * plane + cofs - plane);
-        wf0_lo = MT::face(MT::m(M, g_m1), m_0);
+    T wf0_lo = MT::face(MT::m(M, ldg(a.gamma + pofs(i0 - 1) + cofs)), m_0);
+    T u_mq = u_m1;
+    T hu = T(0), hg = T(1);
+    sm[0][ty + 1][tx + 1] = m_0;
+    if (hal) {
+        sm[0][hsy][hsx] = MT::m(M, ldg(a.gamma + i0 * plane + hofs));
+        hu = ldg(a.u_cur + i0 * plane + hofs);
+        hg = ldg(a.gamma + pofs(i0 + 1) + hofs);
     }
-    {
-        const int b = i0 & 1;
-        sm[b][ty + 1][tx + 1] = m_0;
-        if (hval) {
-            sm[b][hsy][hsx] = MT::m(M, ldg(a.gamma + (long long)i0 * plane + hofs));
-            hu = ldg(a.u_cur + (long long)i0 * plane + hofs);
-            if (gi0 + 1 < a.n0g) hg = ldg(a.gamma + (long long)(i0 + 1) * plane + hofs);
-        }
-        __syncthreads();
-        sfk[b][ty][tx] = MT::face(sm[b][ty + 1][tx], sm[b][ty + 1][tx + 1]);
-        sfj[b][ty][tx] = MT::face(sm[b][ty][tx + 1], sm[b][ty + 1][tx + 1]);
-        if (tid < BY) sfk[b][tid][BX] = MT::face(sm[b][tid + 1][BX], sm[b][tid + 1][BX + 1]);
-        else if (tid >= 32 && tid < 32 + BX)
-            sfj[b][BY][tid - 32] = MT::face(sm[b][BY][tid - 31], sm[b][BY + 1][tid - 31]);
-    }
+    __syncthreads();
+    sfk[0][ty][tx] = MT::face(sm[0][ty + 1][tx], sm[0][ty + 1][tx + 1]);
+    sfj[0][ty][tx] = MT::face(sm[0][ty][tx + 1], sm[0][ty + 1][tx + 1]);
+    if (tid < BY) sfk[0][tid][BX] = MT::face(sm[0][tid + 1][BX], sm[0][tid + 1][BX + 1]);
+    else if (tid >= 32 && tid < 32 + BX)
+        sfj[0][BY][tid - 32] = MT::face(sm[0][BY][tid - 31], sm[0][BY + 1][tid - 31]);
 
     typename Tr::Bits local_max = 0;
 
     for (int i = i0; i < i1; ++i) {
-        const int gi = i + a.i_off;
-        const int b = i & 1, nb = b ^ 1;
+        const int b = (i - i0) & 1, nb = b ^ 1;
         const bool next = i + 1 < i1;
-        const long long c = (long long)i * plane + cofs;
+        const int oc = i * plane + cofs;
 
         // ---- loads for the next iteration (one plane ahead) ----
-        T u_p2 = T(0), g_p2 = T(1), up_n = T(0), acc_n = T(0), hu_n = T(0), hg_n = T(1);
+        T u_p2 = u_p1, g_p2 = g_p1, up_n = T(0), acc_n = T(0), hu_n = T(0), hg_n = T(1);
         if (next) {
-            if (inb) {
-                up_n = ldg(a.u_prev + c + plane);
-                if (ACC) acc_n = a.acc[c + plane];
-                if (gi + 2 < a.n0g) {
-                    u_p2 = ldg(a.u_cur + c + 2 * plane);
-                    g_p2 = ldg(a.gamma + c + 2 * plane);
-                }
-            }
-            if (hval) {
-                hu_n = ldg(a.u_cur + (long long)(i + 1) * plane + hofs);
-                if (gi + 2 < a.n0g) hg_n = ldg(a.gamma + (long long)(i + 2) * plane + hofs);
+            up_n = ldg(a.u_prev + oc + plane);
+            if (ACC) acc_n = a.acc[oc + plane];
+            const int o2 = pofs(i + 2);
+            u_p2 = ldg(a.u_cur + o2 + cofs);
+            g_p2 = ldg(a.gamma + o2 + cofs);
+            if (hal) {
+                hu_n = ldg(a.u_cur + oc - cofs + plane + hofs);
+                hg_n = ldg(a.gamma + o2 + hofs);
             }
         }
 
         // ---- A: stage u(i) and m(i+1) ----
         su[b][ty + 1][tx + 1] = u_0;
-        if (hval) su[b][hsy][hsx] = hu;
-        const bool has_p = gi < a.n0g - 1, has_m = gi > 0;
-        const T m_p1 = has_p ? MT::m(M, g_p1) : T(0);
+        if (hal) su[b][hsy][hsx] = hu;
+        const T m_p1 = MT::m(M, g_p1);
         if (next) {
             sm[nb][ty + 1][tx + 1] = m_p1;
-            if (hval) sm[nb][hsy][hsx] = MT::m(M, hg);
+            if (hal) sm[nb][hsy][hsx] = MT::m(M, hg);
         }
         __syncthreads();
 
@@ -193,63 +192,61 @@ step_kernel(const StepArgs<T> a) {
                 sfj[nb][BY][tid - 32] = MT::face(sm[nb][BY][tid - 31], sm[nb][BY + 1][tid - 31]);
         }
 
-        // ---- D: plane i ----
-        T wf0_hi = T(0);
-        if (inb) {
-            const bool jp = j < n1 - 1, jm = j > 0, kp = k < n2 - 1, km = k > 0;
-            const T u_jp = jp ? su[b][ty + 2][tx + 1] : u_0;
-            const T u_jm = jm ? su[b][ty][tx + 1] : u_0;
-            const T u_kp = kp ? su[b][ty + 1][tx + 2] : u_0;
-            const T u_km = km ? su[b][ty + 1][tx] : u_0;
-            if (has_p) wf0_hi = MT::face(m_0, m_p1);
+        // ---- D: plane i (terms in the order of kernels.py:56-69) ----
+        const T u_jp = su[b][ty + 2][tx + 1];
+        const T u_jm = su[b][ty][tx + 1];
+        const T u_kp = su[b][ty + 1][tx + 2];
+        const T u_km = su[b][ty + 1][tx];
+        const T wf0_hi = MT::face(m_0, m_p1);
+        T accf = u_0 - u_0;
+        accf += (u_p1 - u_0) * wf0_hi;
+        accf -= (u_0 - u_mq) * wf0_lo;
+        accf += (u_jp - u_0) * sfj[b][ty + 1][tx];
+        accf -= (u_0 - u_jm) * sfj[b][ty][tx];
+        accf += (u_kp - u_0) * sfk[b][ty][tx + 1];
+        accf -= (u_0 - u_km) * sfk[b][ty][tx];
+        T kappa;
+        const T coef = MT::coef(M, g_0, kappa);
+        T out = ((u_0 + u_0) - up) + coef * accf;
 
-            // stencil, kernels.py:56-69
-            T accf = u_0 - u_0;
-            if (has_p) accf += (u_p1 - u_0) * wf0_hi;
-            if (has_m) accf -= (u_0 - u_m1) * wf0_lo;
-            if (jp) accf += (u_jp - u_0) * sfj[b][ty + 1][tx];
-            if (jm) accf -= (u_0 - u_jm) * sfj[b][ty][tx];
-            if (kp) accf += (u_kp - u_0) * sfk[b][ty][tx + 1];
-            if (km) accf -= (u_0 - u_km) * sfk[b][ty][tx];
-            T kappa;
-            const T coef = MT::coef(M, g_0, kappa);
-            T out = ((u_0 + u_0) - up) + coef * accf;
-
-            // nodal injections, solver.py:167-170 (sources first, then support)
+        // nodal injections, solver.py:167-170 (sources first, then support)
+        if (my_src) {
             for (int s = 0; s < a.n_src; ++s)
-                if (i == a.src_i[s] && j == a.src_j[s] && k == a.src_k[s])
+                if (((my_src >> s) & 1u) && i == a.src_i[s] && j == a.src_j[s] && k == a.src_k[s])
                     out = out + MT::fc(M, g_0, kappa) * a.src_val[s];
-            if (a.sup_mode != SUP_NONE && a.sup_plane[i]) {
-                const long long flat = c;
-                const unsigned int w = __ldg(a.sup_mask + (flat >> 5));
-                const unsigned int bit = (unsigned int)(flat & 31);
-                if ((w >> bit) & 1u) {
-                    const int s = __ldg(a.sup_prefix + (flat >> 5)) + __popc(w & ((1u << bit) - 1u));
-                    if (a.sup_mode == SUP_GATHER) a.trace_row[s] = u_0;
-                    else out = out + MT::fc(M, g_0, kappa) * ldg(a.adj_row + s);
-                }
+        }
+        if (a.sup_mode != SUP_NONE && i >= a.sup_lo && i <= a.sup_hi && inb) {
+            const unsigned int flat = (unsigned int)oc;
+            const unsigned int w = __ldg(a.sup_mask + (flat >> 5));
+            const unsigned int bit = flat & 31u;
+            if ((w >> bit) & 1u) {
+                const int s = __ldg(a.sup_prefix + (flat >> 5)) + __popc(w & ((1u << bit) - 1u));
+                if (a.sup_mode == SUP_GATHER) a.trace_row[s] = u_0;
+                else out = out + MT::fc(M, g_0, kappa) * ldg(a.adj_row + s);
             }
+        }
 
-            // self-kernel increment, kernels.py:105-128
-            if (ACC) {
-                const T va = a.backward ? (up - out) * a.inv2dt : (out - up) * a.inv2dt;
-                const T g0 = ((has_p ? u_p1 : u_0) - (has_m ? u_m1 : u_0)) * a.inv2dx;
-                const T g1 = (u_jp - u_jm) * a.inv2dx;
-                const T g2 = (u_kp - u_km) * a.inv2dx;
-                T inc;
-                if (a.one_d) inc = a.sdt * ((a.cv * va) * va + (a.cg * g2) * g2);
-                else inc = a.sdt * ((a.cv * va) * va + a.cg * (((g0 * g0) + (g1 * g1)) + (g2 * g2)));
-                a.acc[c] = acc_old + inc;
-            }
-            a.u_out[c] = out;
-            if (a.hist_out) a.hist_out[c] = out;
+        // self-kernel increment, kernels.py:105-128 (clamped differences)
+        if (ACC) {
+            const T va = a.backward ? (up - out) * a.inv2dt : (out - up) * a.inv2dt;
+            const T g0 = (u_p1 - u_mq) * a.inv2dx;
+            const T g1 = (u_jp - u_jm) * a.inv2dx;
+            const T g2 = (u_kp - u_km) * a.inv2dx;
+            T inc;
+            if (a.one_d) inc = a.sdt * ((a.cv * va) * va + (a.cg * g2) * g2);
+            else inc = a.sdt * ((a.cv * va) * va + a.cg * (((g0 * g0) + (g1 * g1)) + (g2 * g2)));
+            if (inb) a.acc[oc] = acc_old + inc;
+        }
+        if (inb) {
+            a.u_out[oc] = out;
+            if (a.hist_out) a.hist_out[oc] = out;
             if (CHECK) {
                 const typename Tr::Bits bits = Tr::abs_bits(out);
                 local_max = bits > local_max ? bits : local_max;
             }
         }
         // advance the queue
-        u_m1 = u_0; u_0 = u_p1; u_p1 = u_p2;
+        u_mq = u_0; u_0 = u_p1; u_p1 = u_p2;
         g_0 = g_p1; g_p1 = g_p2;
         m_0 = m_p1; wf0_lo = wf0_hi;
         up = up_n; acc_old = acc_n;
@@ -277,9 +274,10 @@ step_kernel(const StepArgs<T> a) {
 }
 
 // Fast-division admissibility for the current material: every coefficient
-// the step kernel derives from gamma (m, coef, the face weight of each +1
-// neighbour on every axis) computed with the branch-free sequences must be
-// bit-identical to the IEEE intrinsics.  Any mismatch clears *ok.
+// the step kernel derives from gamma (m, coef, kappa, the face weight of each
+// +1 neighbour on every axis and the mirrored boundary face) computed with
+// the branch-free sequences must be bit-identical to the IEEE intrinsics.
+// Any mismatch clears *ok.
 template <typename T, int FLAVOR>
 __global__ void verify_material_kernel(const T* gamma, int n0, int n1, int n2, MatScalars<T> M,
                                        int* ok) {
@@ -297,6 +295,7 @@ __global__ void verify_material_kernel(const T* gamma, int n0, int n1, int n2, M
         good &= FTraits<T>::bits(mf) == FTraits<T>::bits(mp);
         good &= FTraits<T>::bits(cf) == FTraits<T>::bits(cp);
         good &= FTraits<T>::bits(kf) == FTraits<T>::bits(kp);
+        good &= FTraits<T>::bits(F::face(mp, mp)) == FTraits<T>::bits(P::face(mp, mp));
         const int kk = (int)(c % n2), jj = (int)((c / n2) % n1), ii = (int)(c / pl);
         const long long nbr[3] = {ii + 1 < n0 ? c + pl : -1, jj + 1 < n1 ? c + n2 : -1,
                                   kk + 1 < n2 ? c + 1 : -1};

@@ -37,6 +37,8 @@
 // own u^{n-1} first): device footprint gamma + two levels + accumulator.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace wb {
@@ -123,27 +125,35 @@ step_kernel(const StepArgs<T> a) {
             a.src_k[s] >= k0 && a.src_k[s] < k0 + BX)
             my_src |= 1u << s;
 
-    // plane offsets, clamped to the loadable planes (mirror at global ends)
-    auto pofs = [&](int i) { return min(max(i, a.i_lo), a.i_hi - 1) * plane; };
+    // plane index clamped to the loadable planes (mirror at the global ends)
+    auto pc = [&](int i) { return min(max(i, a.i_lo), a.i_hi - 1) * plane; };
+    // per-thread stream bases: every plane access is one IMAD.WIDE
+    const T* __restrict__ pU = a.u_cur + cofs;
+    const T* __restrict__ pG = a.gamma + cofs;
+    const T* __restrict__ pP = a.u_prev + cofs;
+    const T* __restrict__ hU = a.u_cur + hofs;
+    const T* __restrict__ hG = a.gamma + hofs;
+    T* pA = a.acc + cofs;
+    T* pO = a.u_out + cofs;
+    T* pH = a.hist_out ? a.hist_out + cofs : nullptr;
+    const int last = a.n0 - 1;
 
     // ---- prologue: plane i0 queue, m(i0) in smem, faces of plane i0 ----
-    const int o0 = i0 * plane + cofs;
-    T u_0 = ldg(a.u_cur + o0);
-    const T u_m1 = ldg(a.u_cur + pofs(i0 - 1) + cofs);
-    T g_0 = ldg(a.gamma + o0);
-    T u_p1 = ldg(a.u_cur + pofs(i0 + 1) + cofs);
-    T g_p1 = ldg(a.gamma + pofs(i0 + 1) + cofs);
-    T up = ldg(a.u_prev + o0);
-    T acc_old = ACC ? a.acc[o0] : T(0);
+    T u_0 = ldg(pU + i0 * plane);
+    T u_m1 = ldg(pU + pc(i0 - 1));
+    T g_0 = ldg(pG + i0 * plane);
+    T u_p1 = ldg(pU + pc(i0 + 1));
+    T g_p1 = ldg(pG + pc(i0 + 1));
+    T up = ldg(pP + i0 * plane);
+    T acc_old = ACC ? pA[i0 * plane] : T(0);
     T m_0 = MT::m(M, g_0);
-    T wf0_lo = MT::face(MT::m(M, ldg(a.gamma + pofs(i0 - 1) + cofs)), m_0);
-    T u_mq = u_m1;
+    T wf0_lo = MT::face(MT::m(M, ldg(pG + pc(i0 - 1))), m_0);
     T hu = T(0), hg = T(1);
     sm[0][ty + 1][tx + 1] = m_0;
     if (hal) {
-        sm[0][hsy][hsx] = MT::m(M, ldg(a.gamma + i0 * plane + hofs));
-        hu = ldg(a.u_cur + i0 * plane + hofs);
-        hg = ldg(a.gamma + pofs(i0 + 1) + hofs);
+        sm[0][hsy][hsx] = MT::m(M, ldg(hG + i0 * plane));
+        hu = ldg(hU + i0 * plane);
+        hg = ldg(hG + pc(i0 + 1));
     }
     __syncthreads();
     sfk[0][ty][tx] = MT::face(sm[0][ty + 1][tx], sm[0][ty + 1][tx + 1]);
@@ -154,23 +164,23 @@ step_kernel(const StepArgs<T> a) {
 
     typename Tr::Bits local_max = 0;
 
-    for (int i = i0; i < i1; ++i) {
-        const int b = (i - i0) & 1, nb = b ^ 1;
+    // one plane; B = buffer parity (compile time, the loop is unrolled by 2)
+    auto body = [&](auto parity, int i) {
+        constexpr int b = decltype(parity)::value, nb = b ^ 1;
         const bool next = i + 1 < i1;
-        const int oc = i * plane + cofs;
+        const int oc = i * plane;
 
-        // ---- loads for the next iteration (one plane ahead) ----
-        T u_p2 = u_p1, g_p2 = g_p1, up_n = T(0), acc_n = T(0), hu_n = T(0), hg_n = T(1);
-        if (next) {
-            up_n = ldg(a.u_prev + oc + plane);
-            if (ACC) acc_n = a.acc[oc + plane];
-            const int o2 = pofs(i + 2);
-            u_p2 = ldg(a.u_cur + o2 + cofs);
-            g_p2 = ldg(a.gamma + o2 + cofs);
-            if (hal) {
-                hu_n = ldg(a.u_cur + oc - cofs + plane + hofs);
-                hg_n = ldg(a.gamma + o2 + hofs);
-            }
+        // ---- loads for the next iteration (clamped: always in bounds) ----
+        const int on = min(i + 1, last) * plane;
+        const int o2 = pc(i + 2);
+        const T up_n = ldg(pP + on);
+        const T acc_n = ACC ? pA[on] : T(0);
+        const T u_p2 = ldg(pU + o2);
+        const T g_p2 = ldg(pG + o2);
+        T hu_n = T(0), hg_n = T(1);
+        if (hal) {
+            hu_n = ldg(hU + on);
+            hg_n = ldg(hG + o2);
         }
 
         // ---- A: stage u(i) and m(i+1) ----
@@ -200,7 +210,7 @@ step_kernel(const StepArgs<T> a) {
         const T wf0_hi = MT::face(m_0, m_p1);
         T accf = u_0 - u_0;
         accf += (u_p1 - u_0) * wf0_hi;
-        accf -= (u_0 - u_mq) * wf0_lo;
+        accf -= (u_0 - u_m1) * wf0_lo;
         accf += (u_jp - u_0) * sfj[b][ty + 1][tx];
         accf -= (u_0 - u_jm) * sfj[b][ty][tx];
         accf += (u_kp - u_0) * sfk[b][ty][tx + 1];
@@ -216,7 +226,7 @@ step_kernel(const StepArgs<T> a) {
                     out = out + MT::fc(M, g_0, kappa) * a.src_val[s];
         }
         if (a.sup_mode != SUP_NONE && i >= a.sup_lo && i <= a.sup_hi && inb) {
-            const unsigned int flat = (unsigned int)oc;
+            const unsigned int flat = (unsigned int)(oc + cofs);
             const unsigned int w = __ldg(a.sup_mask + (flat >> 5));
             const unsigned int bit = flat & 31u;
             if ((w >> bit) & 1u) {
@@ -229,28 +239,33 @@ step_kernel(const StepArgs<T> a) {
         // self-kernel increment, kernels.py:105-128 (clamped differences)
         if (ACC) {
             const T va = a.backward ? (up - out) * a.inv2dt : (out - up) * a.inv2dt;
-            const T g0 = (u_p1 - u_mq) * a.inv2dx;
+            const T g0 = (u_p1 - u_m1) * a.inv2dx;
             const T g1 = (u_jp - u_jm) * a.inv2dx;
             const T g2 = (u_kp - u_km) * a.inv2dx;
             T inc;
             if (a.one_d) inc = a.sdt * ((a.cv * va) * va + (a.cg * g2) * g2);
             else inc = a.sdt * ((a.cv * va) * va + a.cg * (((g0 * g0) + (g1 * g1)) + (g2 * g2)));
-            if (inb) a.acc[oc] = acc_old + inc;
+            if (inb) pA[oc] = acc_old + inc;
         }
         if (inb) {
-            a.u_out[oc] = out;
-            if (a.hist_out) a.hist_out[oc] = out;
+            pO[oc] = out;
+            if (pH) pH[oc] = out;
             if (CHECK) {
                 const typename Tr::Bits bits = Tr::abs_bits(out);
                 local_max = bits > local_max ? bits : local_max;
             }
         }
         // advance the queue
-        u_mq = u_0; u_0 = u_p1; u_p1 = u_p2;
+        u_m1 = u_0; u_0 = u_p1; u_p1 = u_p2;
         g_0 = g_p1; g_p1 = g_p2;
         m_0 = m_p1; wf0_lo = wf0_hi;
         up = up_n; acc_old = acc_n;
         hu = hu_n; hg = hg_n;
+    };
+
+    for (int i = i0; i < i1; i += 2) {
+        body(std::integral_constant<int, 0>{}, i);
+        if (i + 1 < i1) body(std::integral_constant<int, 1>{}, i + 1);
     }
 
     if (CHECK) {

@@ -1,0 +1,11 @@
+#!/bin/bash
+# One build-measure cycle on the GPU box (run under gpurun from the repo root):
+#   parity tests, a short bench, then ncu on the fused step kernel.
+#   profiles/gpu_cycle.sh <tag> [bench args...]
+tag=${1:-cycle}; shift
+out=gpurun_out
+timeout 600 python -m pytest tests -x -q -m gpu > $out/${tag}_tests.log 2>&1; echo "tests rc $?"; tail -2 $out/${tag}_tests.log
+timeout 600 python bench.py --steps 5 --warmup 3 --cpu-sample-steps 4 "$@" > $out/${tag}_bench.json 2> $out/${tag}_bench.err; echo "bench rc $?"
+python profiles/profile_step.py > $out/${tag}_prof_plain.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 10 -c 1 \
+      -o $out/${tag}_step python profiles/profile_step.py > $out/${tag}_ncu.log 2>&1; echo "ncu rc $?"

@@ -87,6 +87,7 @@ _SIGS = {
     "wo_fast_div_active": (c_int, [c_vp]),
 }
 WO_OPT_FAST_DIV = 1
+WO_OPT_PAIR_KERNEL = 2
 
 
 def load(require_device=False):

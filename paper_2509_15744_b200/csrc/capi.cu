@@ -19,6 +19,7 @@
 #include "design_kernels.cuh"
 #include "dropin_kernels.cuh"
 #include "step_kernel.cuh"
+#include "step_kernel_v2.cuh"
 
 using namespace wb;
 
@@ -49,6 +50,7 @@ struct wo_ctx {
     bool material_set = false;
     bool fast_div = false;             // verify_material_kernel passed for this material
     int allow_fast_div = 1;            // wo_set_option(WO_OPT_FAST_DIV)
+    int use_pair = 1;                  // wo_set_option(WO_OPT_PAIR_KERNEL)
     int sup_lo = 0, sup_hi = -1;       // local planes holding support nodes
     int flavor = 0;
     double rho0 = 0, rho1 = 0, kappa1 = 0, rho2 = 0, kappa2 = 0, dt_mat = 0, ratio2 = 0;
@@ -254,12 +256,17 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     }
     a.max_slot = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots) + sp.slot;
 
-    dim3 block(BX, BY, 1);
-    dim3 grid((ctx->kn2 + BX - 1) / BX, (ctx->kn1 + BY - 1) / BY,
-              (ctx->kn0 + a.chunk - 1) / a.chunk);
+    // even rows: the pair-vectorised kernel; odd rows: the scalar kernel
+    const bool pair = (ctx->kn2 % 2 == 0) && ctx->use_pair;
+    dim3 block(pair ? 32 : BX, BY, 1);
+    dim3 grid(pair ? (ctx->kn2 + PBX - 1) / PBX : (ctx->kn2 + BX - 1) / BX,
+              (ctx->kn1 + BY - 1) / BY, (ctx->kn0 + a.chunk - 1) / a.chunk);
     if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
-#define LAUNCH(FL, FAST, ACC, CHK) \
-    step_kernel<T, FL, FAST, ACC, CHK><<<grid, block, 0, ctx->stream>>>(a)
+#define LAUNCH(FL, FAST, ACC, CHK)                                                    \
+    do {                                                                              \
+        if (pair) step_kernel_pair<T, FL, FAST, ACC, CHK><<<grid, block, 0, ctx->stream>>>(a); \
+        else step_kernel<T, FL, FAST, ACC, CHK><<<grid, block, 0, ctx->stream>>>(a);   \
+    } while (0)
 #define LAUNCH_AC(FL, FAST)                                                   \
     do {                                                                      \
         if (sp.acc) { if (sp.check) LAUNCH(FL, FAST, true, true);             \
@@ -852,7 +859,11 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
 int wo_set_option(wo_ctx* ctx, int option, int value) {
     int rc = check_ctx(ctx);
     if (rc) return rc;
-    REQUIRE(option == WO_OPT_FAST_DIV, "unknown option");
+    REQUIRE(option == WO_OPT_FAST_DIV || option == WO_OPT_PAIR_KERNEL, "unknown option");
+    if (option == WO_OPT_PAIR_KERNEL) {
+        ctx->use_pair = value != 0;
+        return WO_OK;
+    }
     ctx->allow_fast_div = value != 0;
     if (ctx->material_set) return verify_fast_div(ctx);
     ctx->fast_div = false;

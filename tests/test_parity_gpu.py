@@ -227,7 +227,8 @@ def test_calibrate_k_tato(W, golden):
 
 
 # ------------------------------------------------------ oracle comparisons
-@pytest.mark.parametrize("shape", [(40, 9, 70), (5, 64, 33), (130, 3, 3), (200,), (3, 257)])
+@pytest.mark.parametrize("shape", [(40, 9, 70), (5, 64, 33), (130, 3, 3), (200,), (3, 257),
+                                   (17, 13, 66), (6, 9, 130), (3, 64), (33, 4)])
 @pytest.mark.parametrize("prec", ["single", "double"])
 def test_odd_shapes_vs_oracle(W, shape, prec):
     """Ragged tiles, tiny axes and chunk boundaries: bit-exact vs the oracle."""
@@ -252,6 +253,27 @@ def test_odd_shapes_vs_oracle(W, shape, prec):
     cost, grad, _ = O.gradient_superposed(omat, dt, n_steps, shots, 1e13, prec)
     assert bits_equal(res.gradient, grad)
     assert abs(res.cost - cost) <= COST_RTOL * abs(cost)
+
+
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_pair_and_scalar_kernels_agree(W, golden, prec):
+    """Even last axis: the pair-vectorised kernel and the scalar kernel give
+    identical bits (fwi3d has n2 = 26)."""
+    from paper_2509_15744_b200 import engine
+
+    g = golden("fwi3d")
+    c = cases.fwi3d_case()
+    problem, mat = product_fwi_problem(W, c, g["gamma_model"], g["measured"])
+    cfg = W.SuperpositionConfig(k=c["k"], precision=prec)
+    ctx = engine.get_context(problem.grid, W.precision_dtype(prec))
+    try:
+        ctx.set_pair_kernel(False)
+        scalar = W.gradient_superposed(problem, mat, cfg).gradient
+    finally:
+        ctx.set_pair_kernel(True)
+    pair = W.gradient_superposed(problem, mat, cfg).gradient
+    assert bits_equal(pair, scalar)
+    assert bits_equal(pair, g[f"sup_grad_{prec}"])
 
 
 def test_instability_reported_like_reference(W):

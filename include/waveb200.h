@@ -79,6 +79,9 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
 /* WO_OPT_PAIR_KERNEL (default 1): two-cells-per-thread vectorised step kernel
  * on grids with an even last axis (0 = scalar kernel everywhere). */
 #define WO_OPT_PAIR_KERNEL 2
+/* WO_OPT_TMA_KERNEL (default 1): TMA/mbarrier-pipelined step kernel when the
+ * grid tiles exactly into 64 x 8 cells (0 = never). */
+#define WO_OPT_TMA_KERNEL 3
 int wo_set_option(wo_ctx* ctx, int option, int value);
 int wo_fast_div_active(const wo_ctx* ctx);
 /* Kernel-increment scalars (gradients.py:117-129, kernels.py:149-152): the

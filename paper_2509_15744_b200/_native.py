@@ -88,6 +88,7 @@ _SIGS = {
 }
 WO_OPT_FAST_DIV = 1
 WO_OPT_PAIR_KERNEL = 2
+WO_OPT_TMA_KERNEL = 3
 
 
 def load(require_device=False):

@@ -19,7 +19,10 @@
 #include "design_kernels.cuh"
 #include "dropin_kernels.cuh"
 #include "step_kernel.cuh"
+#include "step_kernel_tma.cuh"
 #include "step_kernel_v2.cuh"
+
+#include <cudaTypedefs.h>
 
 using namespace wb;
 
@@ -51,6 +54,9 @@ struct wo_ctx {
     bool fast_div = false;             // verify_material_kernel passed for this material
     int allow_fast_div = 1;            // wo_set_option(WO_OPT_FAST_DIV)
     int use_pair = 1;                  // wo_set_option(WO_OPT_PAIR_KERNEL)
+    int use_tma = 1;                   // wo_set_option(WO_OPT_TMA_KERNEL)
+    int tma_state = 0;                 // 0 not built, 1 maps ready, -1 not eligible
+    TmaMaps tmaps;                     // tensor maps of gamma, u[0], u[1], acc
     int sup_lo = 0, sup_hi = -1;       // local planes holding support nodes
     int flavor = 0;
     double rho0 = 0, rho1 = 0, kappa1 = 0, rho2 = 0, kappa2 = 0, dt_mat = 0, ratio2 = 0;
@@ -192,6 +198,62 @@ void harvest_events(wo_ctx* ctx) {
     ctx->ev_used.clear();
 }
 
+// ---- TMA tensor maps (driver entry point; no libcuda link dependency) ----
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+bool make_map(CUtensorMap* m, void* base, int itemsize, uint64_t n2, uint64_t n1, uint64_t np,
+              uint32_t bw, uint32_t bh) {
+    auto enc = tma_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {n2, n1, np};
+    const cuuint64_t strides[2] = {n2 * (cuuint64_t)itemsize, n1 * n2 * (cuuint64_t)itemsize};
+    const cuuint32_t box[3] = {bw, bh, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = enc(m, itemsize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                            : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                           3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// whole 64 x 8 tiles and 16-byte pitches: the TMA kernel applies
+bool tma_ready(wo_ctx* ctx) {
+    if (ctx->tma_state == 0) {
+        ctx->tma_state = -1;
+        if (ctx->kn2 % PBX == 0 && ctx->kn1 % BY == 0) {
+            const uint64_t np = (uint64_t)(ctx->kn0 + ctx->has_lo + ctx->has_hi);
+            bool ok = true;
+            for (int b = 0; b < 2; ++b) {
+                ok &= make_map(&ctx->tmaps.u_halo[b], ctx->u[b], ctx->itemsize, ctx->kn2, ctx->kn1,
+                               np, TH_W, TH_H);
+                ok &= make_map(&ctx->tmaps.u_ctr[b], ctx->u[b], ctx->itemsize, ctx->kn2, ctx->kn1,
+                               np, PBX, BY);
+            }
+            ok &= make_map(&ctx->tmaps.g_halo, ctx->gamma, ctx->itemsize, ctx->kn2, ctx->kn1, np,
+                           TH_W, TH_H);
+            ok &= make_map(&ctx->tmaps.a_ctr, ctx->acc, ctx->itemsize, ctx->kn2, ctx->kn1,
+                           (uint64_t)ctx->kn0, PBX, BY);
+            ctx->tmaps.lo = ctx->has_lo;
+            if (ok) ctx->tma_state = 1;
+        }
+    }
+    return ctx->tma_state == 1;
+}
+
 struct StepSpec {
     bool acc = false;
     bool check = false;
@@ -256,16 +318,31 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     }
     a.max_slot = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots) + sp.slot;
 
-    // even rows: the pair-vectorised kernel; odd rows: the scalar kernel
-    const bool pair = (ctx->kn2 % 2 == 0) && ctx->use_pair;
+    // whole 64x8 tiles on the default window: TMA pipeline; even rows: the
+    // pair-vectorised kernel; otherwise the scalar kernel
+    const bool tma = ctx->use_tma && ctx->use_pair && !sp.prev && !sp.cur && !sp.out &&
+                     tma_ready(ctx);
+    const bool pair = tma || ((ctx->kn2 % 2 == 0) && ctx->use_pair);
     dim3 block(pair ? 32 : BX, BY, 1);
     dim3 grid(pair ? (ctx->kn2 + PBX - 1) / PBX : (ctx->kn2 + BX - 1) / BX,
               (ctx->kn1 + BY - 1) / BY, (ctx->kn0 + a.chunk - 1) / a.chunk);
+    if (tma) ctx->tmaps.cur = ctx->cur;
+    const size_t tsm = tma_smem_bytes<T>();
     if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
-#define LAUNCH(FL, FAST, ACC, CHK)                                                    \
-    do {                                                                              \
-        if (pair) step_kernel_pair<T, FL, FAST, ACC, CHK><<<grid, block, 0, ctx->stream>>>(a); \
-        else step_kernel<T, FL, FAST, ACC, CHK><<<grid, block, 0, ctx->stream>>>(a);   \
+#define LAUNCH(FL, FAST, ACC, CHK)                                                        \
+    do {                                                                                  \
+        if (tma) {                                                                        \
+            static bool attr_set = false;                                                 \
+            if (!attr_set) {                                                              \
+                cudaFuncSetAttribute(step_kernel_tma<T, FL, FAST, ACC, CHK>,              \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm); \
+                attr_set = true;                                                          \
+            }                                                                             \
+            step_kernel_tma<T, FL, FAST, ACC, CHK><<<grid, block, tsm, ctx->stream>>>(a, ctx->tmaps); \
+        } else if (pair)                                                                  \
+            step_kernel_pair<T, FL, FAST, ACC, CHK><<<grid, block, 0, ctx->stream>>>(a);  \
+        else                                                                              \
+            step_kernel<T, FL, FAST, ACC, CHK><<<grid, block, 0, ctx->stream>>>(a);       \
     } while (0)
 #define LAUNCH_AC(FL, FAST)                                                   \
     do {                                                                      \
@@ -859,9 +936,15 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
 int wo_set_option(wo_ctx* ctx, int option, int value) {
     int rc = check_ctx(ctx);
     if (rc) return rc;
-    REQUIRE(option == WO_OPT_FAST_DIV || option == WO_OPT_PAIR_KERNEL, "unknown option");
+    REQUIRE(option == WO_OPT_FAST_DIV || option == WO_OPT_PAIR_KERNEL ||
+                option == WO_OPT_TMA_KERNEL,
+            "unknown option");
     if (option == WO_OPT_PAIR_KERNEL) {
         ctx->use_pair = value != 0;
+        return WO_OK;
+    }
+    if (option == WO_OPT_TMA_KERNEL) {
+        ctx->use_tma = value != 0;
         return WO_OK;
     }
     ctx->allow_fast_div = value != 0;

@@ -1,0 +1,354 @@
+// TMA-pipelined fused step (the production kernel on aligned grids).
+//
+// Same arithmetic, op order and boundary semantics as step_kernel /
+// step_kernel_pair (see step_kernel.cuh for the reference mapping).  What is
+// B200-specific is the data movement:
+//   * one producer thread streams, per plane p, four boxes into a ring of
+//     S shared-memory stages with cp.async.bulk.tensor (TMA):
+//       U  u^n   (64+4) x (8+2) cells, halo included   [read: stencil]
+//       G  gamma (64+4) x (8+2) cells                    [read: material]
+//       P  u^{n-1} 64 x 8                                 [read: pointwise]
+//       A  accumulator 64 x 8 (ACC only)
+//     completion is tracked by one mbarrier (expect_tx) per stage, and the
+//     producer runs S-1 planes ahead, so HBM latency is hidden by bytes in
+//     flight instead of by occupancy;
+//   * consumers (all 256 threads, two cells each) read the stages, compute
+//     m = 1/gamma once per cell into a double-buffered m-plane, share the
+//     j-faces through shared memory and keep the k-faces in registers;
+//   * results go out with 8/16-byte coalesced stores.
+// Domain boundaries: TMA fills out-of-range box elements with zeros; those
+// are never read — every thread addresses its neighbours through clamped
+// (mirrored) shared-memory offsets fixed at kernel start, and the axis-0
+// neighbours at the global ends are the cell itself.  The mirrored boundary
+// terms are exactly +0 (step_kernel.cuh header), so results are bit-identical
+// to the reference.  Requires n2 % 64 == 0, n1 % 8 == 0 (whole tiles) and
+// 16-byte row pitch; other grids use the pair / scalar kernels.
+#pragma once
+
+#include <cuda.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "step_kernel.cuh"
+#include "step_kernel_v2.cuh"
+
+namespace wb {
+
+constexpr int TS = 4;                 // pipeline stages
+constexpr int TH_W = PBX + 4;         // halo box width (k0-2 .. k0+65)
+constexpr int TH_H = BY + 2;          // halo box height (j0-1 .. j0+8)
+
+struct TmaMaps {
+    CUtensorMap u_halo[2];   // u buffers 0/1, (TH_W, TH_H, 1) boxes
+    CUtensorMap u_ctr[2];    // u buffers 0/1, (PBX, BY, 1) boxes
+    CUtensorMap g_halo;      // gamma, (TH_W, TH_H, 1)
+    CUtensorMap a_ctr;       // accumulator, (PBX, BY, 1)
+    int cur;                 // index of the buffer holding u^n
+    int lo;                  // ghost planes below plane 0 (map plane = p + lo)
+};
+
+template <typename T> struct TmaStage {   // every TMA destination 128-byte aligned
+    alignas(128) T U[TH_H][TH_W];
+    alignas(128) T G[TH_H][TH_W];
+    alignas(128) T P[BY][PBX];
+    alignas(128) T A[BY][PBX];
+};
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2),
+        "r"(smem_addr(bar))
+        : "memory");
+}
+
+template <typename T, int FLAVOR, bool FAST, bool ACC, bool CHECK>
+__global__ void __launch_bounds__(NTHREADS)
+step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ TmaMaps maps) {
+    using Tr = FTraits<T>;
+    using MT = Mat<T, FLAVOR, FAST>;
+    using V = typename Pair<T>::V;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    TmaStage<T>* st = reinterpret_cast<TmaStage<T>*>(smem_raw);
+    T(*SM)[TH_H][TH_W] = reinterpret_cast<T(*)[TH_H][TH_W]>(smem_raw + TS * sizeof(TmaStage<T>));
+    T(*SF)[BY + 1][PBX] = reinterpret_cast<T(*)[BY + 1][PBX]>(
+        smem_raw + TS * sizeof(TmaStage<T>) + 2 * sizeof(T) * TH_H * TH_W);
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(
+        smem_raw + TS * sizeof(TmaStage<T>) + 2 * sizeof(T) * TH_H * TH_W +
+        2 * sizeof(T) * (BY + 1) * PBX);
+    __shared__ typename Tr::Bits smax[NTHREADS / 32];
+
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = ty * 32 + tx;
+    const int k0 = blockIdx.x * PBX, j0 = blockIdx.y * BY;
+    const int kA = k0 + 2 * tx, j = j0 + ty;
+    const int n1 = a.n1, n2 = a.n2;
+    const int plane = n1 * n2;
+    const int i0 = blockIdx.z * a.chunk;
+    const int i1 = min(i0 + a.chunk, a.n0);
+    const int plast = a.i_hi - 1;              // last loadable local plane
+    const int pend = min(i1, plast);           // last plane streamed by this CTA
+    const MatScalars<T>& M = a.mat;
+
+    // smem coordinates (halo boxes start at k0-2, j0-1): own pair and the
+    // clamped (mirrored) neighbours
+    const int r0 = ty + 1, cA = 2 + 2 * tx;
+    const int rU = j > 0 ? r0 - 1 : r0, rD = j < n1 - 1 ? r0 + 1 : r0;
+    const int cL = kA > 0 ? cA - 1 : cA, cR = kA + 2 < n2 ? cA + 2 : cA + 1;
+    // halo roles for the m-plane: 16 k-halo cells, 64 j-halo pairs
+    const bool hk_role = tid < 2 * BY;
+    const bool hj_role = tid >= 2 * BY && tid < 2 * BY + 64;
+    int hr = 0, hc = 0;
+    if (hk_role) { hr = (tid < BY ? tid : tid - BY) + 1; hc = tid < BY ? 1 : PBX + 2; }
+    else if (hj_role) { const int q = tid - 2 * BY; hr = q < 32 ? 0 : BY + 1; hc = 2 + 2 * (q & 31); }
+
+    unsigned my_src = 0;
+    for (int s = 0; s < a.n_src; ++s)
+        if (a.src_i[s] >= i0 && a.src_i[s] < i1 && a.src_j[s] >= j0 && a.src_j[s] < j0 + BY &&
+            a.src_k[s] >= k0 && a.src_k[s] < k0 + PBX)
+            my_src |= 1u << s;
+
+    constexpr unsigned STAGE_BYTES = (unsigned)(sizeof(T) * (2 * TH_H * TH_W + (ACC ? 2 : 1) * BY * PBX));
+    const CUtensorMap* mU = &maps.u_halo[maps.cur];
+    const CUtensorMap* mP = &maps.u_ctr[maps.cur ^ 1];
+    auto issue = [&](int p) {   // producer: plane p into its stage
+        const int s = (p - i0) % TS;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar[s], STAGE_BYTES);
+        tma_load_3d(&st[s].U[0][0], mU, k0 - 2, j0 - 1, p + maps.lo, &bar[s]);
+        tma_load_3d(&st[s].G[0][0], &maps.g_halo, k0 - 2, j0 - 1, p + maps.lo, &bar[s]);
+        tma_load_3d(&st[s].P[0][0], mP, k0, j0, p + maps.lo, &bar[s]);
+        if (ACC) tma_load_3d(&st[s].A[0][0], &maps.a_ctr, k0, j0, p, &bar[s]);
+    };
+    auto wait_plane = [&](int p) {
+        const int n = p - i0;
+        mbar_wait(&bar[n % TS], (unsigned)((n / TS) & 1));
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < TS; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int p = i0; p <= min(i0 + TS - 1, pend); ++p) issue(p);
+
+    // ---- prologue: plane i0 queue, m(i0), faces of plane i0 ----
+    const int cofs = j * n2 + kA;
+    const bool has_m0 = i0 > a.i_lo;          // plane i0-1 exists (real or ghost)
+    V u_m1 = {T(0), T(0)}, g_m1 = {T(1), T(1)};
+    if (has_m0) {
+        u_m1 = __ldg(reinterpret_cast<const V*>(a.u_cur + (i0 - 1) * plane + cofs));
+        g_m1 = __ldg(reinterpret_cast<const V*>(a.gamma + (i0 - 1) * plane + cofs));
+    }
+    wait_plane(i0);
+    V u_0 = *reinterpret_cast<const V*>(&st[0].U[r0][cA]);
+    V g_0 = *reinterpret_cast<const V*>(&st[0].G[r0][cA]);
+    if (!has_m0) { u_m1 = u_0; g_m1 = g_0; }
+    V m_0 = {MT::m(M, g_0.x), MT::m(M, g_0.y)};
+    V wf0_lo = {MT::face(MT::m(M, g_m1.x), m_0.x), MT::face(MT::m(M, g_m1.y), m_0.y)};
+    *reinterpret_cast<V*>(&SM[0][r0][cA]) = m_0;
+    if (hk_role) SM[0][hr][hc] = MT::m(M, st[0].G[hr][hc]);
+    else if (hj_role) {
+        const V hg = *reinterpret_cast<const V*>(&st[0].G[hr][hc]);
+        *reinterpret_cast<V*>(&SM[0][hr][hc]) = V{MT::m(M, hg.x), MT::m(M, hg.y)};
+    }
+    __syncthreads();
+    T fkL, fkI, fkR;
+    V fj_lo;
+    auto faces = [&](T (*smb)[TH_W], T (*sfb)[PBX], V m_c, T& oL, T& oI, T& oR, V& ojlo) {
+        oL = MT::face(smb[r0][cL], m_c.x);
+        oI = MT::face(m_c.x, m_c.y);
+        oR = MT::face(m_c.y, smb[r0][cR]);
+        const V mu = *reinterpret_cast<const V*>(&smb[rU][cA]);
+        ojlo.x = MT::face(mu.x, m_c.x);
+        ojlo.y = MT::face(mu.y, m_c.y);
+        *reinterpret_cast<V*>(&sfb[ty][cA - 2]) = ojlo;
+        if (tid >= 32 && tid < 64) {
+            // hi face of the tile's last row: (j0+BY-1, j0+BY), mirrored at the domain end
+            const int p = tid - 32;
+            const int rb = j0 + BY < n1 ? BY + 1 : BY;
+            const V ma = *reinterpret_cast<const V*>(&smb[BY][2 + 2 * p]);
+            const V mb = *reinterpret_cast<const V*>(&smb[rb][2 + 2 * p]);
+            *reinterpret_cast<V*>(&sfb[BY][2 * p]) = V{MT::face(ma.x, mb.x), MT::face(ma.y, mb.y)};
+        }
+    };
+    faces(SM[0], SF[0], m_0, fkL, fkI, fkR, fj_lo);
+
+    typename Tr::Bits local_max = 0;
+
+    auto body = [&](auto parity, int i) {
+        constexpr int b = decltype(parity)::value, nb = b ^ 1;
+        const bool next = i + 1 < i1;
+        const int sc = (i - i0) % TS;
+        // ---- plane i+1 from its stage (mirror beyond the global end) ----
+        V u_p1 = u_0, g_p1 = g_0;
+        const bool have_p1 = i + 1 <= plast;
+        int sn = 0;
+        if (have_p1) {
+            wait_plane(i + 1);
+            sn = (i + 1 - i0) % TS;
+            u_p1 = *reinterpret_cast<const V*>(&st[sn].U[r0][cA]);
+            g_p1 = *reinterpret_cast<const V*>(&st[sn].G[r0][cA]);
+        }
+        const V m_p1 = {MT::m(M, g_p1.x), MT::m(M, g_p1.y)};
+        if (next) {
+            *reinterpret_cast<V*>(&SM[nb][r0][cA]) = m_p1;
+            if (hk_role) SM[nb][hr][hc] = MT::m(M, st[sn].G[hr][hc]);
+            else if (hj_role) {
+                const V hg = *reinterpret_cast<const V*>(&st[sn].G[hr][hc]);
+                *reinterpret_cast<V*>(&SM[nb][hr][hc]) = V{MT::m(M, hg.x), MT::m(M, hg.y)};
+            }
+        }
+        __syncthreads();
+        // producer: the stage of plane i-1 is free now (every thread is past it)
+        if (tid == 0 && i > i0 && i - 1 + TS <= pend) issue(i - 1 + TS);
+
+        // ---- faces of plane i+1 ----
+        T nL = fkL, nI = fkI, nR = fkR;
+        V njlo = fj_lo;
+        if (next) faces(SM[nb], SF[nb], m_p1, nL, nI, nR, njlo);
+
+        // ---- plane i ----
+        const TmaStage<T>& S = st[sc];
+        const V uj_m = *reinterpret_cast<const V*>(&S.U[rU][cA]);
+        const V uj_p = *reinterpret_cast<const V*>(&S.U[rD][cA]);
+        const T uL = S.U[r0][cL];
+        const T uR = S.U[r0][cR];
+        const V up = *reinterpret_cast<const V*>(&S.P[ty][2 * tx]);
+        const V fj_hi = *reinterpret_cast<const V*>(&SF[b][ty + 1][cA - 2]);
+        const V wf0_hi = {MT::face(m_0.x, m_p1.x), MT::face(m_0.y, m_p1.y)};
+        T kapA, kapB;
+        const T coefA = MT::coef(M, g_0.x, kapA);
+        const T coefB = MT::coef(M, g_0.y, kapB);
+        T accA = u_0.x - u_0.x;
+        accA += (u_p1.x - u_0.x) * wf0_hi.x;
+        accA -= (u_0.x - u_m1.x) * wf0_lo.x;
+        accA += (uj_p.x - u_0.x) * fj_hi.x;
+        accA -= (u_0.x - uj_m.x) * fj_lo.x;
+        accA += (u_0.y - u_0.x) * fkI;
+        accA -= (u_0.x - uL) * fkL;
+        T accB = u_0.y - u_0.y;
+        accB += (u_p1.y - u_0.y) * wf0_hi.y;
+        accB -= (u_0.y - u_m1.y) * wf0_lo.y;
+        accB += (uj_p.y - u_0.y) * fj_hi.y;
+        accB -= (u_0.y - uj_m.y) * fj_lo.y;
+        accB += (uR - u_0.y) * fkR;
+        accB -= (u_0.y - u_0.x) * fkI;
+        V out;
+        out.x = ((u_0.x + u_0.x) - up.x) + coefA * accA;
+        out.y = ((u_0.y + u_0.y) - up.y) + coefB * accB;
+
+        if (my_src) {
+            for (int s = 0; s < a.n_src; ++s) {
+                if (!((my_src >> s) & 1u) || i != a.src_i[s] || j != a.src_j[s]) continue;
+                if (kA == a.src_k[s]) out.x = out.x + MT::fc(M, g_0.x, kapA) * a.src_val[s];
+                if (kA + 1 == a.src_k[s]) out.y = out.y + MT::fc(M, g_0.y, kapB) * a.src_val[s];
+            }
+        }
+        const int oc = i * plane + cofs;
+        if (a.sup_mode != SUP_NONE && i >= a.sup_lo && i <= a.sup_hi) {
+            const unsigned int flat = (unsigned int)oc;
+            const unsigned int w = __ldg(a.sup_mask + (flat >> 5));
+            const unsigned int bit = flat & 31u;
+            const unsigned int two = (w >> bit) & 3u;
+            if (two) {
+                const int s = __ldg(a.sup_prefix + (flat >> 5)) + __popc(w & ((1u << bit) - 1u));
+                if (a.sup_mode == SUP_GATHER) {
+                    if (two & 1u) a.trace_row[s] = u_0.x;
+                    if (two & 2u) a.trace_row[s + (two & 1u)] = u_0.y;
+                } else {
+                    if (two & 1u) out.x = out.x + MT::fc(M, g_0.x, kapA) * ldg(a.adj_row + s);
+                    if (two & 2u)
+                        out.y = out.y + MT::fc(M, g_0.y, kapB) * ldg(a.adj_row + s + (two & 1u));
+                }
+            }
+        }
+        if (ACC) {
+            const V acc_old = *reinterpret_cast<const V*>(&S.A[ty][2 * tx]);
+            const T vaA = a.backward ? (up.x - out.x) * a.inv2dt : (out.x - up.x) * a.inv2dt;
+            const T vaB = a.backward ? (up.y - out.y) * a.inv2dt : (out.y - up.y) * a.inv2dt;
+            const T g0A = (u_p1.x - u_m1.x) * a.inv2dx, g0B = (u_p1.y - u_m1.y) * a.inv2dx;
+            const T g1A = (uj_p.x - uj_m.x) * a.inv2dx, g1B = (uj_p.y - uj_m.y) * a.inv2dx;
+            const T g2A = (u_0.y - uL) * a.inv2dx, g2B = (uR - u_0.x) * a.inv2dx;
+            V nacc;
+            if (a.one_d) {
+                nacc.x = acc_old.x + a.sdt * ((a.cv * vaA) * vaA + (a.cg * g2A) * g2A);
+                nacc.y = acc_old.y + a.sdt * ((a.cv * vaB) * vaB + (a.cg * g2B) * g2B);
+            } else {
+                nacc.x = acc_old.x + a.sdt * ((a.cv * vaA) * vaA +
+                                              a.cg * (((g0A * g0A) + (g1A * g1A)) + (g2A * g2A)));
+                nacc.y = acc_old.y + a.sdt * ((a.cv * vaB) * vaB +
+                                              a.cg * (((g0B * g0B) + (g1B * g1B)) + (g2B * g2B)));
+            }
+            *reinterpret_cast<V*>(a.acc + oc) = nacc;
+        }
+        *reinterpret_cast<V*>(a.u_out + oc) = out;
+        if (a.hist_out) *reinterpret_cast<V*>(a.hist_out + oc) = out;
+        if (CHECK) {
+            typename Tr::Bits bx = Tr::abs_bits(out.x), by = Tr::abs_bits(out.y);
+            bx = bx > by ? bx : by;
+            local_max = bx > local_max ? bx : local_max;
+        }
+        u_m1 = u_0; u_0 = u_p1;
+        g_0 = g_p1;
+        m_0 = m_p1; wf0_lo = wf0_hi;
+        fkL = nL; fkI = nI; fkR = nR; fj_lo = njlo;
+    };
+
+    for (int i = i0; i < i1; i += 2) {
+        body(std::integral_constant<int, 0>{}, i);
+        if (i + 1 < i1) body(std::integral_constant<int, 1>{}, i + 1);
+    }
+
+    if (CHECK) {
+        for (int o = 16; o > 0; o >>= 1) {
+            typename Tr::Bits v = __shfl_xor_sync(0xffffffffu, local_max, o);
+            local_max = v > local_max ? v : local_max;
+        }
+        const int lane = tid & 31, warp = tid >> 5;
+        if (lane == 0) smax[warp] = local_max;
+        __syncthreads();
+        if (warp == 0) {
+            typename Tr::Bits v = lane < (NTHREADS / 32) ? smax[lane] : 0;
+            for (int o = 16; o > 0; o >>= 1) {
+                typename Tr::Bits w = __shfl_xor_sync(0xffffffffu, v, o);
+                v = w > v ? w : v;
+            }
+            if (lane == 0 && v) atomicMax(a.max_slot, v);
+        }
+    }
+}
+
+template <typename T>
+constexpr size_t tma_smem_bytes() {
+    return TS * sizeof(TmaStage<T>) + 2 * sizeof(T) * TH_H * TH_W + 2 * sizeof(T) * (BY + 1) * PBX +
+           TS * sizeof(unsigned long long);
+}
+
+}  // namespace wb

@@ -228,7 +228,8 @@ def test_calibrate_k_tato(W, golden):
 
 # ------------------------------------------------------ oracle comparisons
 @pytest.mark.parametrize("shape", [(40, 9, 70), (5, 64, 33), (130, 3, 3), (200,), (3, 257),
-                                   (17, 13, 66), (6, 9, 130), (3, 64), (33, 4)])
+                                   (17, 13, 66), (6, 9, 130), (3, 64), (33, 4),
+                                   (12, 16, 64), (9, 24, 128), (64, 128), (3, 8, 64)])
 @pytest.mark.parametrize("prec", ["single", "double"])
 def test_odd_shapes_vs_oracle(W, shape, prec):
     """Ragged tiles, tiny axes and chunk boundaries: bit-exact vs the oracle."""
@@ -274,6 +275,42 @@ def test_pair_and_scalar_kernels_agree(W, golden, prec):
     pair = W.gradient_superposed(problem, mat, cfg).gradient
     assert bits_equal(pair, scalar)
     assert bits_equal(pair, g[f"sup_grad_{prec}"])
+
+
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_tma_pair_scalar_kernels_agree(W, prec):
+    """A grid of whole 64x8 tiles runs the TMA pipeline; it must match the
+    pair and scalar kernels and the oracle bit for bit (sensor plane and a
+    source on tile edges, random heterogeneous gamma)."""
+    from paper_2509_15744_b200 import engine
+
+    shape, dx, n_steps = (20, 16, 128), 1e-4, 90
+    dt = 0.45 * dx / 6000.0 / np.sqrt(3)
+    rng = np.random.default_rng(5)
+    gamma = rng.uniform(0.2, 1.0, size=shape)
+    grid = W.build_grid(shape, dx)
+    mat = W.MaterialModel.rho_scaled(gamma, grid, rho0=2700.0, c0=6000.0)
+    src = W.SourceSpec(node=(4, 8, 63), amplitude=1e12, frequency=5e6, cycles=2)
+    sens = [(15, j, k) for j in (0, 7, 8, 15) for k in (0, 1, 63, 64, 127)]
+    measured = rng.normal(scale=1e-10, size=(1, len(sens), n_steps))
+    problem = W.FwiProblem(grid=grid, time=W.TimeConfig(n_steps, dt), material=mat,
+                           sources=[src], sensors=W.SensorArray(nodes=sens), measured=measured)
+    cfg = W.SuperpositionConfig(k=1e13, precision=prec)
+    ctx = engine.get_context(grid, W.precision_dtype(prec))
+    out = {}
+    for name, tma, pair in (("tma", True, True), ("pair", False, True), ("scalar", False, False)):
+        ctx.set_tma_kernel(tma)
+        ctx.set_pair_kernel(pair)
+        out[name] = W.gradient_superposed(problem, mat, cfg)
+    ctx.set_tma_kernel(True)
+    ctx.set_pair_kernel(True)
+    omat = O.Material("rho_scaled", gamma, dx, rho0=2700.0, c0=6000.0)
+    support = np.array([grid.flat_index(n) for n in sens], dtype=np.int64)
+    shots = [(O.Source(src.node, 1e12, 5e6, 2), O.FwiShot(support, measured[0], dt))]
+    cost, grad, _ = O.gradient_superposed(omat, dt, n_steps, shots, 1e13, prec)
+    for name, res in out.items():
+        assert bits_equal(res.gradient, grad), name
+        assert abs(res.cost - cost) <= COST_RTOL * abs(cost), name
 
 
 def test_instability_reported_like_reference(W):

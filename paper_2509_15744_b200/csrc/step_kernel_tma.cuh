@@ -93,7 +93,11 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
     using Tr = FTraits<T>;
     using MT = Mat<T, FLAVOR, FAST>;
     using V = typename Pair<T>::V;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_dyn[];
+    // TMA destinations need 128-byte alignment: align the dynamic base
+    // explicitly (static shared memory may precede it)
+    unsigned char* smem_raw = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<unsigned long long>(smem_dyn) + 127ull) & ~127ull);
     TmaStage<T>* st = reinterpret_cast<TmaStage<T>*>(smem_raw);
     T(*SM)[TH_H][TH_W] = reinterpret_cast<T(*)[TH_H][TH_W]>(smem_raw + TS * sizeof(TmaStage<T>));
     T(*SF)[BY + 1][PBX] = reinterpret_cast<T(*)[BY + 1][PBX]>(
@@ -134,8 +138,9 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
             my_src |= 1u << s;
 
     constexpr unsigned STAGE_BYTES = (unsigned)(sizeof(T) * (2 * TH_H * TH_W + (ACC ? 2 : 1) * BY * PBX));
-    const CUtensorMap* mU = &maps.u_halo[maps.cur];
-    const CUtensorMap* mP = &maps.u_ctr[maps.cur ^ 1];
+    // constant-offset selects keep the descriptors in parameter space
+    const CUtensorMap* mU = maps.cur ? &maps.u_halo[1] : &maps.u_halo[0];
+    const CUtensorMap* mP = maps.cur ? &maps.u_ctr[0] : &maps.u_ctr[1];
     auto issue = [&](int p) {   // producer: plane p into its stage
         const int s = (p - i0) % TS;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -348,7 +353,7 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
 template <typename T>
 constexpr size_t tma_smem_bytes() {
     return TS * sizeof(TmaStage<T>) + 2 * sizeof(T) * TH_H * TH_W + 2 * sizeof(T) * (BY + 1) * PBX +
-           TS * sizeof(unsigned long long);
+           TS * sizeof(unsigned long long) + 128 /* alignment slack */;
 }
 
 }  // namespace wb

@@ -236,15 +236,16 @@ bool tma_ready(wo_ctx* ctx) {
         ctx->tma_state = -1;
         if (ctx->kn2 % PBX == 0 && ctx->kn1 % BY == 0) {
             const uint64_t np = (uint64_t)(ctx->kn0 + ctx->has_lo + ctx->has_hi);
+            const uint32_t hw = ctx->itemsize == 4 ? th_w<float>() : th_w<double>();
             bool ok = true;
             for (int b = 0; b < 2; ++b) {
                 ok &= make_map(&ctx->tmaps.u_halo[b], ctx->u[b], ctx->itemsize, ctx->kn2, ctx->kn1,
-                               np, TH_W, TH_H);
+                               np, hw, TH_H);
                 ok &= make_map(&ctx->tmaps.u_ctr[b], ctx->u[b], ctx->itemsize, ctx->kn2, ctx->kn1,
                                np, PBX, BY);
             }
             ok &= make_map(&ctx->tmaps.g_halo, ctx->gamma, ctx->itemsize, ctx->kn2, ctx->kn1, np,
-                           TH_W, TH_H);
+                           hw, TH_H);
             ok &= make_map(&ctx->tmaps.a_ctr, ctx->acc, ctx->itemsize, ctx->kn2, ctx->kn1,
                            (uint64_t)ctx->kn0, PBX, BY);
             ctx->tmaps.lo = ctx->has_lo;

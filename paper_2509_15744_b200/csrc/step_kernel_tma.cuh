@@ -36,21 +36,26 @@
 namespace wb {
 
 constexpr int TS = 4;                 // pipeline stages
-constexpr int TH_W = PBX + 4;         // halo box width (k0-2 .. k0+65)
 constexpr int TH_H = BY + 2;          // halo box height (j0-1 .. j0+8)
+// The innermost TMA box coordinate must be 16-byte aligned (measured: an
+// offset of -2 floats traps), so the halo box starts HO = 16/sizeof(T) cells
+// left of the tile and is PBX + 2*HO wide.
+template <typename T> constexpr int th_ho() { return 16 / (int)sizeof(T); }
+template <typename T> constexpr int th_w() { return PBX + 2 * th_ho<T>(); }
+constexpr int TH_WMAX = PBX + 8;
 
 struct TmaMaps {
-    CUtensorMap u_halo[2];   // u buffers 0/1, (TH_W, TH_H, 1) boxes
+    CUtensorMap u_halo[2];   // u buffers 0/1, (th_w, TH_H, 1) boxes
     CUtensorMap u_ctr[2];    // u buffers 0/1, (PBX, BY, 1) boxes
-    CUtensorMap g_halo;      // gamma, (TH_W, TH_H, 1)
+    CUtensorMap g_halo;      // gamma, (th_w, TH_H, 1)
     CUtensorMap a_ctr;       // accumulator, (PBX, BY, 1)
     int cur;                 // index of the buffer holding u^n
     int lo;                  // ghost planes below plane 0 (map plane = p + lo)
 };
 
 template <typename T> struct TmaStage {   // every TMA destination 128-byte aligned
-    alignas(128) T U[TH_H][TH_W];
-    alignas(128) T G[TH_H][TH_W];
+    alignas(128) T U[TH_H][th_w<T>()];
+    alignas(128) T G[TH_H][th_w<T>()];
     alignas(128) T P[BY][PBX];
     alignas(128) T A[BY][PBX];
 };
@@ -99,11 +104,12 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
     unsigned char* smem_raw = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<unsigned long long>(smem_dyn) + 127ull) & ~127ull);
     TmaStage<T>* st = reinterpret_cast<TmaStage<T>*>(smem_raw);
-    T(*SM)[TH_H][TH_W] = reinterpret_cast<T(*)[TH_H][TH_W]>(smem_raw + TS * sizeof(TmaStage<T>));
+    constexpr int W = th_w<T>(), HO = th_ho<T>();
+    T(*SM)[TH_H][W] = reinterpret_cast<T(*)[TH_H][W]>(smem_raw + TS * sizeof(TmaStage<T>));
     T(*SF)[BY + 1][PBX] = reinterpret_cast<T(*)[BY + 1][PBX]>(
-        smem_raw + TS * sizeof(TmaStage<T>) + 2 * sizeof(T) * TH_H * TH_W);
+        smem_raw + TS * sizeof(TmaStage<T>) + 2 * sizeof(T) * TH_H * W);
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(
-        smem_raw + TS * sizeof(TmaStage<T>) + 2 * sizeof(T) * TH_H * TH_W +
+        smem_raw + TS * sizeof(TmaStage<T>) + 2 * sizeof(T) * TH_H * W +
         2 * sizeof(T) * (BY + 1) * PBX);
     __shared__ typename Tr::Bits smax[NTHREADS / 32];
 
@@ -121,15 +127,15 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
 
     // smem coordinates (halo boxes start at k0-2, j0-1): own pair and the
     // clamped (mirrored) neighbours
-    const int r0 = ty + 1, cA = 2 + 2 * tx;
+    const int r0 = ty + 1, cA = HO + 2 * tx;
     const int rU = j > 0 ? r0 - 1 : r0, rD = j < n1 - 1 ? r0 + 1 : r0;
     const int cL = kA > 0 ? cA - 1 : cA, cR = kA + 2 < n2 ? cA + 2 : cA + 1;
     // halo roles for the m-plane: 16 k-halo cells, 64 j-halo pairs
     const bool hk_role = tid < 2 * BY;
     const bool hj_role = tid >= 2 * BY && tid < 2 * BY + 64;
     int hr = 0, hc = 0;
-    if (hk_role) { hr = (tid < BY ? tid : tid - BY) + 1; hc = tid < BY ? 1 : PBX + 2; }
-    else if (hj_role) { const int q = tid - 2 * BY; hr = q < 32 ? 0 : BY + 1; hc = 2 + 2 * (q & 31); }
+    if (hk_role) { hr = (tid < BY ? tid : tid - BY) + 1; hc = tid < BY ? HO - 1 : HO + PBX; }
+    else if (hj_role) { const int q = tid - 2 * BY; hr = q < 32 ? 0 : BY + 1; hc = HO + 2 * (q & 31); }
 
     unsigned my_src = 0;
     for (int s = 0; s < a.n_src; ++s)
@@ -137,7 +143,7 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
             a.src_k[s] >= k0 && a.src_k[s] < k0 + PBX)
             my_src |= 1u << s;
 
-    constexpr unsigned STAGE_BYTES = (unsigned)(sizeof(T) * (2 * TH_H * TH_W + (ACC ? 2 : 1) * BY * PBX));
+    constexpr unsigned STAGE_BYTES = (unsigned)(sizeof(T) * (2 * TH_H * W + (ACC ? 2 : 1) * BY * PBX));
     // constant-offset selects keep the descriptors in parameter space
     const CUtensorMap* mU = maps.cur ? &maps.u_halo[1] : &maps.u_halo[0];
     const CUtensorMap* mP = maps.cur ? &maps.u_ctr[0] : &maps.u_ctr[1];
@@ -145,8 +151,8 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
         const int s = (p - i0) % TS;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[s], STAGE_BYTES);
-        tma_load_3d(&st[s].U[0][0], mU, k0 - 2, j0 - 1, p + maps.lo, &bar[s]);
-        tma_load_3d(&st[s].G[0][0], &maps.g_halo, k0 - 2, j0 - 1, p + maps.lo, &bar[s]);
+        tma_load_3d(&st[s].U[0][0], mU, k0 - HO, j0 - 1, p + maps.lo, &bar[s]);
+        tma_load_3d(&st[s].G[0][0], &maps.g_halo, k0 - HO, j0 - 1, p + maps.lo, &bar[s]);
         tma_load_3d(&st[s].P[0][0], mP, k0, j0, p + maps.lo, &bar[s]);
         if (ACC) tma_load_3d(&st[s].A[0][0], &maps.a_ctr, k0, j0, p, &bar[s]);
     };
@@ -186,20 +192,20 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
     __syncthreads();
     T fkL, fkI, fkR;
     V fj_lo;
-    auto faces = [&](T (*smb)[TH_W], T (*sfb)[PBX], V m_c, T& oL, T& oI, T& oR, V& ojlo) {
+    auto faces = [&](T (*smb)[W], T (*sfb)[PBX], V m_c, T& oL, T& oI, T& oR, V& ojlo) {
         oL = MT::face(smb[r0][cL], m_c.x);
         oI = MT::face(m_c.x, m_c.y);
         oR = MT::face(m_c.y, smb[r0][cR]);
         const V mu = *reinterpret_cast<const V*>(&smb[rU][cA]);
         ojlo.x = MT::face(mu.x, m_c.x);
         ojlo.y = MT::face(mu.y, m_c.y);
-        *reinterpret_cast<V*>(&sfb[ty][cA - 2]) = ojlo;
+        *reinterpret_cast<V*>(&sfb[ty][cA - HO]) = ojlo;
         if (tid >= 32 && tid < 64) {
             // hi face of the tile's last row: (j0+BY-1, j0+BY), mirrored at the domain end
             const int p = tid - 32;
             const int rb = j0 + BY < n1 ? BY + 1 : BY;
-            const V ma = *reinterpret_cast<const V*>(&smb[BY][2 + 2 * p]);
-            const V mb = *reinterpret_cast<const V*>(&smb[rb][2 + 2 * p]);
+            const V ma = *reinterpret_cast<const V*>(&smb[BY][HO + 2 * p]);
+            const V mb = *reinterpret_cast<const V*>(&smb[rb][HO + 2 * p]);
             *reinterpret_cast<V*>(&sfb[BY][2 * p]) = V{MT::face(ma.x, mb.x), MT::face(ma.y, mb.y)};
         }
     };
@@ -246,7 +252,7 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
         const T uL = S.U[r0][cL];
         const T uR = S.U[r0][cR];
         const V up = *reinterpret_cast<const V*>(&S.P[ty][2 * tx]);
-        const V fj_hi = *reinterpret_cast<const V*>(&SF[b][ty + 1][cA - 2]);
+        const V fj_hi = *reinterpret_cast<const V*>(&SF[b][ty + 1][cA - HO]);
         const V wf0_hi = {MT::face(m_0.x, m_p1.x), MT::face(m_0.y, m_p1.y)};
         T kapA, kapB;
         const T coefA = MT::coef(M, g_0.x, kapA);
@@ -352,7 +358,7 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
 
 template <typename T>
 constexpr size_t tma_smem_bytes() {
-    return TS * sizeof(TmaStage<T>) + 2 * sizeof(T) * TH_H * TH_W + 2 * sizeof(T) * (BY + 1) * PBX +
+    return TS * sizeof(TmaStage<T>) + 2 * sizeof(T) * TH_H * th_w<T>() + 2 * sizeof(T) * (BY + 1) * PBX +
            TS * sizeof(unsigned long long) + 128 /* alignment slack */;
 }
 

@@ -40,8 +40,8 @@ constexpr int TH_H = BY + 2;          // halo box height (j0-1 .. j0+8)
 // The innermost TMA box coordinate must be 16-byte aligned (measured: an
 // offset of -2 floats traps), so the halo box starts HO = 16/sizeof(T) cells
 // left of the tile and is PBX + 2*HO wide.
-template <typename T> constexpr int th_ho() { return 16 / (int)sizeof(T); }
-template <typename T> constexpr int th_w() { return PBX + 2 * th_ho<T>(); }
+template <typename T> __host__ __device__ constexpr int th_ho() { return 16 / (int)sizeof(T); }
+template <typename T> __host__ __device__ constexpr int th_w() { return PBX + 2 * th_ho<T>(); }
 constexpr int TH_WMAX = PBX + 8;
 
 struct TmaMaps {

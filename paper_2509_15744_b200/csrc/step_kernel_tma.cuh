@@ -93,7 +93,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 }
 
 template <typename T, int FLAVOR, bool FAST, bool ACC, bool CHECK>
-__global__ void __launch_bounds__(NTHREADS)
+__global__ void __launch_bounds__(NTHREADS, sizeof(T) == 4 ? 3 : 2)
 step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ TmaMaps maps) {
     using Tr = FTraits<T>;
     using MT = Mat<T, FLAVOR, FAST>;
@@ -101,8 +101,9 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
     extern __shared__ __align__(128) unsigned char smem_dyn[];
     // TMA destinations need 128-byte alignment: align the dynamic base
     // explicitly (static shared memory may precede it)
-    unsigned char* smem_raw = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<unsigned long long>(smem_dyn) + 127ull) & ~127ull);
+    // (pointer arithmetic on the __shared__ array keeps LDS/STS addressing)
+    unsigned char* smem_raw =
+        smem_dyn + ((128u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_dyn)) & 127u)) & 127u);
     TmaStage<T>* st = reinterpret_cast<TmaStage<T>*>(smem_raw);
     constexpr int W = th_w<T>(), HO = th_ho<T>();
     T(*SM)[TH_H][W] = reinterpret_cast<T(*)[TH_H][W]>(smem_raw + TS * sizeof(TmaStage<T>));

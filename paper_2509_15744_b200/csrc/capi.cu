@@ -255,6 +255,17 @@ bool tma_ready(wo_ctx* ctx) {
     return ctx->tma_state == 1;
 }
 
+template <typename T, int FL, bool FAST, bool ACC, bool CHK, int SUP>
+void launch_tma(dim3 grid, dim3 block, size_t tsm, wo_ctx* ctx, const StepArgs<T>& a) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(step_kernel_tma<T, FL, FAST, ACC, CHK, SUP>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+        attr_set = true;
+    }
+    step_kernel_tma<T, FL, FAST, ACC, CHK, SUP><<<grid, block, tsm, ctx->stream>>>(a, ctx->tmaps);
+}
+
 struct StepSpec {
     bool acc = false;
     bool check = false;
@@ -322,7 +333,7 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     // whole 64x8 tiles on the default window: TMA pipeline; even rows: the
     // pair-vectorised kernel; otherwise the scalar kernel
     const bool tma = ctx->use_tma && ctx->use_pair && !sp.prev && !sp.cur && !sp.out &&
-                     tma_ready(ctx);
+                     !sp.hist && tma_ready(ctx);
     const bool pair = tma || ((ctx->kn2 % 2 == 0) && ctx->use_pair);
     dim3 block(pair ? 32 : BX, BY, 1);
     dim3 grid(pair ? (ctx->kn2 + PBX - 1) / PBX : (ctx->kn2 + BX - 1) / BX,
@@ -333,13 +344,12 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
 #define LAUNCH(FL, FAST, ACC, CHK)                                                        \
     do {                                                                                  \
         if (tma) {                                                                        \
-            static bool attr_set = false;                                                 \
-            if (!attr_set) {                                                              \
-                cudaFuncSetAttribute(step_kernel_tma<T, FL, FAST, ACC, CHK>,              \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm); \
-                attr_set = true;                                                          \
-            }                                                                             \
-            step_kernel_tma<T, FL, FAST, ACC, CHK><<<grid, block, tsm, ctx->stream>>>(a, ctx->tmaps); \
+            if (a.sup_mode == SUP_GATHER)                                                 \
+                launch_tma<T, FL, FAST, ACC, CHK, SUP_GATHER>(grid, block, tsm, ctx, a);  \
+            else if (a.sup_mode == SUP_INJECT)                                            \
+                launch_tma<T, FL, FAST, ACC, CHK, SUP_INJECT>(grid, block, tsm, ctx, a);  \
+            else                                                                          \
+                launch_tma<T, FL, FAST, ACC, CHK, SUP_NONE>(grid, block, tsm, ctx, a);    \
         } else if (pair)                                                                  \
             step_kernel_pair<T, FL, FAST, ACC, CHK><<<grid, block, 0, ctx->stream>>>(a);  \
         else                                                                              \

@@ -92,7 +92,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-template <typename T, int FLAVOR, bool FAST, bool ACC, bool CHECK>
+template <typename T, int FLAVOR, bool FAST, bool ACC, bool CHECK, int SUP>
 __global__ void __launch_bounds__(NTHREADS, sizeof(T) == 4 ? 3 : 2)
 step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ TmaMaps maps) {
     using Tr = FTraits<T>;
@@ -284,14 +284,14 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
             }
         }
         const int oc = i * plane + cofs;
-        if (a.sup_mode != SUP_NONE && i >= a.sup_lo && i <= a.sup_hi) {
+        if (SUP != SUP_NONE && i >= a.sup_lo && i <= a.sup_hi) {
             const unsigned int flat = (unsigned int)oc;
             const unsigned int w = __ldg(a.sup_mask + (flat >> 5));
             const unsigned int bit = flat & 31u;
             const unsigned int two = (w >> bit) & 3u;
             if (two) {
                 const int s = __ldg(a.sup_prefix + (flat >> 5)) + __popc(w & ((1u << bit) - 1u));
-                if (a.sup_mode == SUP_GATHER) {
+                if (SUP == SUP_GATHER) {
                     if (two & 1u) a.trace_row[s] = u_0.x;
                     if (two & 2u) a.trace_row[s + (two & 1u)] = u_0.y;
                 } else {
@@ -303,25 +303,23 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
         }
         if (ACC) {
             const V acc_old = *reinterpret_cast<const V*>(&S.A[ty][2 * tx]);
-            const T vaA = a.backward ? (up.x - out.x) * a.inv2dt : (out.x - up.x) * a.inv2dt;
-            const T vaB = a.backward ? (up.y - out.y) * a.inv2dt : (out.y - up.y) * a.inv2dt;
+            // The physical window order only flips the sign of va (backward:
+            // (u^{n+1} - u^{n-1}) with roles swapped); (cv*va)*va is invariant
+            // under va -> -va bit for bit (IEEE negation is exact), so one
+            // expression serves both sweeps.  n1 >= 8 here: never 1D.
+            const T vaA = (out.x - up.x) * a.inv2dt;
+            const T vaB = (out.y - up.y) * a.inv2dt;
             const T g0A = (u_p1.x - u_m1.x) * a.inv2dx, g0B = (u_p1.y - u_m1.y) * a.inv2dx;
             const T g1A = (uj_p.x - uj_m.x) * a.inv2dx, g1B = (uj_p.y - uj_m.y) * a.inv2dx;
             const T g2A = (u_0.y - uL) * a.inv2dx, g2B = (uR - u_0.x) * a.inv2dx;
             V nacc;
-            if (a.one_d) {
-                nacc.x = acc_old.x + a.sdt * ((a.cv * vaA) * vaA + (a.cg * g2A) * g2A);
-                nacc.y = acc_old.y + a.sdt * ((a.cv * vaB) * vaB + (a.cg * g2B) * g2B);
-            } else {
-                nacc.x = acc_old.x + a.sdt * ((a.cv * vaA) * vaA +
-                                              a.cg * (((g0A * g0A) + (g1A * g1A)) + (g2A * g2A)));
-                nacc.y = acc_old.y + a.sdt * ((a.cv * vaB) * vaB +
-                                              a.cg * (((g0B * g0B) + (g1B * g1B)) + (g2B * g2B)));
-            }
+            nacc.x = acc_old.x + a.sdt * ((a.cv * vaA) * vaA +
+                                          a.cg * (((g0A * g0A) + (g1A * g1A)) + (g2A * g2A)));
+            nacc.y = acc_old.y + a.sdt * ((a.cv * vaB) * vaB +
+                                          a.cg * (((g0B * g0B) + (g1B * g1B)) + (g2B * g2B)));
             *reinterpret_cast<V*>(a.acc + oc) = nacc;
         }
         *reinterpret_cast<V*>(a.u_out + oc) = out;
-        if (a.hist_out) *reinterpret_cast<V*>(a.hist_out + oc) = out;
         if (CHECK) {
             typename Tr::Bits bx = Tr::abs_bits(out.x), by = Tr::abs_bits(out.y);
             bx = bx > by ? bx : by;

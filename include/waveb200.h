@@ -116,6 +116,30 @@ int wo_set_accumulator(wo_ctx* ctx, const void* in);
 int wo_sweep_forward(wo_ctx* ctx, int64_t n_steps, int n_src, const int64_t* src_flat,
                      const double* src_amp, int flags, double dt, double scale,
                      double* peak_out, int64_t* fail_step, double* fail_max);
+/* Step ranges of the two sweeps, for drivers that exchange slab halos
+ * between steps (multi-GPU slab decomposition).  Forward: steps n in
+ * [n_begin, n_end); the range starting at n = 1 initialises the sweep.
+ * Backward: steps n = n_hi .. n_lo+1 descending; the range starting at
+ * n_hi = N-1 swaps the direction.  No stability evaluation: read the
+ * per-step max|u| with wo_check_maxima (out[n], n in [0, N+2), step n's
+ * check value) and combine across slabs.  Each call returns synchronised. */
+int wo_sweep_forward_range(wo_ctx* ctx, int64_t n_steps, int64_t n_begin, int64_t n_end,
+                           int n_src, const int64_t* src_flat, const double* src_amp, int flags,
+                           double dt);
+int wo_sweep_backward_range(wo_ctx* ctx, int64_t n_steps, int64_t n_hi, int64_t n_lo,
+                            int64_t src_flat, const double* src_amp, int inject_support,
+                            int accumulate, double dt);
+int wo_check_maxima(wo_ctx* ctx, int64_t n_steps, double* out);
+/* Device addresses of the current level's first/last local planes and its
+ * ghost planes (NULL when absent), plane size in bytes: the buffers a
+ * halo exchange (NCCL send/recv) reads and fills. */
+int wo_halo_planes(wo_ctx* ctx, void** first, void** last, void** ghost_lo, void** ghost_hi,
+                   int64_t* plane_bytes);
+/* Same-process halo exchange between adjacent slabs (same device or peer
+ * devices): lower's last plane -> upper's low ghost, upper's first plane ->
+ * lower's high ghost, on the current level. */
+int wo_exchange_local(wo_ctx* lower, wo_ctx* upper);
+
 /* Standard-adjoint sweep of gradient_reference (gradients.py:371-386) using
  * the recorded history and the unscaled compact adjoint store; accumulates
  * the mixed kernel.  wo_free_history releases the history buffer. */

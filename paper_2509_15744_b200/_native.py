@@ -28,7 +28,8 @@ EXPORTS = (
     "wo_reset_stats", "wo_device_bytes", "wo_sweep_adjoint_reference", "wo_free_history",
     "wo_design_filter", "wo_design_project", "wo_design_chain", "wo_timer_mark",
     "wo_timer_elapsed", "wo_synchronize", "wo_accumulator_ptr", "wo_set_option",
-    "wo_fast_div_active",
+    "wo_fast_div_active", "wo_sweep_forward_range", "wo_sweep_backward_range",
+    "wo_check_maxima", "wo_halo_planes", "wo_exchange_local",
 )
 
 
@@ -85,6 +86,13 @@ _SIGS = {
     "wo_accumulator_ptr": (c_vp, [c_vp]),
     "wo_set_option": (c_int, [c_vp, c_int, c_int]),
     "wo_fast_div_active": (c_int, [c_vp]),
+    "wo_sweep_forward_range": (c_int, [c_vp, c_i64, c_i64, c_i64, c_int, c_vp, c_vp, c_int,
+                                       c_dbl]),
+    "wo_sweep_backward_range": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_int, c_int,
+                                        c_dbl]),
+    "wo_check_maxima": (c_int, [c_vp, c_i64, c_vp]),
+    "wo_halo_planes": (c_int, [c_vp] + [ctypes.POINTER(c_vp)] * 4 + [P_i64]),
+    "wo_exchange_local": (c_int, [c_vp, c_vp]),
 }
 WO_OPT_FAST_DIV = 1
 WO_OPT_PAIR_KERNEL = 2

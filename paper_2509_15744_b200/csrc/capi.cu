@@ -440,13 +440,19 @@ int inject_host_list(wo_ctx* ctx, int n, const long long* idx, const double* val
     return WO_OK;
 }
 
+// forward steps n in [n_begin, n_end) of an N-step sweep; n_begin == 1
+// initialises the check slots / store / history, finish evaluates the checks
 template <typename T>
 int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
                     const double* src_amp, int flags, double dt, double scale,
-                    double* peak_out, int64_t* fail_step, double* fail_max) {
+                    double* peak_out, int64_t* fail_step, double* fail_max,
+                    int64_t n_begin = 1, int64_t n_end = -1, bool finish = true) {
+    if (n_end < 0) n_end = N;
+    REQUIRE(1 <= n_begin && n_begin <= n_end && n_end <= N, "bad forward step range");
     const int accumulate = flags & WO_FWD_ACCUMULATE;
     const bool record = (flags & WO_FWD_HISTORY) != 0;
-    if (record) {
+    const bool first = n_begin == 1;
+    if (record && first) {
         REQUIRE(!ctx->has_lo && !ctx->has_hi, "history recording is single-domain only");
         int rc0 = ensure(ctx, &ctx->hist, &ctx->hist_bytes, (size_t)(N + 1) * ctx->field_bytes());
         if (rc0) return rc0;
@@ -461,17 +467,25 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
     dedupe_last(n_src, src_flat, sidx, spos);
     const int ns = (int)sidx.size();
     REQUIRE(ns <= MAX_SRC || !accumulate, "at most 8 source nodes per accumulating sweep");
-    int rc = ensure_slots(ctx, N);
-    if (rc) return rc;
-    CK(cudaMemsetAsync(ctx->maxslots, 0, (size_t)(N + 2) * 8, ctx->stream));
+    REQUIRE(!record || ctx->hist_bytes >= (size_t)(N + 1) * ctx->field_bytes(),
+            "history not initialised");
+    int rc = WO_OK;
     const bool gather = ctx->n_sup > 0;
-    if (gather) {
-        rc = ensure(ctx, &ctx->store, &ctx->store_bytes, (size_t)N * ctx->n_sup * sizeof(T));
+    if (first) {
+        rc = ensure_slots(ctx, N);
         if (rc) return rc;
-        CK(cudaMemsetAsync(ctx->store, 0, (size_t)N * ctx->n_sup * sizeof(T), ctx->stream));
+        CK(cudaMemsetAsync(ctx->maxslots, 0, (size_t)(N + 2) * 8, ctx->stream));
+        if (gather) {
+            rc = ensure(ctx, &ctx->store, &ctx->store_bytes, (size_t)N * ctx->n_sup * sizeof(T));
+            if (rc) return rc;
+            CK(cudaMemsetAsync(ctx->store, 0, (size_t)N * ctx->n_sup * sizeof(T), ctx->stream));
+        }
     }
+    REQUIRE(ctx->maxslot_bytes >= (size_t)(N + 2) * 8 &&
+                (!gather || ctx->store_bytes >= (size_t)N * ctx->n_sup * sizeof(T)),
+            "sweep not initialised (first range must start at n = 1)");
     std::vector<double> vals(std::max(ns, 1));
-    for (int64_t n = 1; n < N; ++n) {
+    for (int64_t n = n_begin; n < n_end; ++n) {
         StepSpec sp;
         sp.acc = accumulate != 0;
         sp.check = (n % STABILITY_CHECK_INTERVAL == 0) || (n == N - 1);
@@ -512,6 +526,7 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
     }
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->prof) harvest_events(ctx);
+    if (!finish) return WO_OK;
     std::vector<char> hs((size_t)(N + 2) * 8);
     CK(cudaMemcpy(hs.data(), ctx->maxslots, hs.size(), cudaMemcpyDeviceToHost));
     double peak = 0.0;
@@ -530,20 +545,28 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
     return WO_OK;
 }
 
+// backward steps n = n_hi, n_hi-1, ..., n_lo+1 of an N-step sweep;
+// n_hi == N-1 swaps the direction and initialises the check slots
 template <typename T>
 int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src_amp,
                      int inject, int accumulate, double dt, int64_t* fail_step,
-                     double* fail_max) {
+                     double* fail_max, int64_t n_hi = -1, int64_t n_lo = 0, bool finish = true) {
+    if (n_hi < 0) n_hi = N - 1;
+    REQUIRE(0 <= n_lo && n_lo <= n_hi && n_hi <= N - 1, "bad backward step range");
     REQUIRE(!inject || ctx->n_sup > 0, "backward support injection without a support");
     REQUIRE(!inject || ctx->store_bytes >= (size_t)N * ctx->n_sup * sizeof(T),
             "adjoint store not populated for this N");
-    int rc = ensure_slots(ctx, N);
-    if (rc) return rc;
-    CK(cudaMemsetAsync(ctx->maxslots, 0, (size_t)(N + 2) * 8, ctx->stream));
-    ctx->cur = 1 - ctx->cur;  // swap_direction: u_prev <- u^N, u_cur <- u^{N-1}
+    int rc = WO_OK;
+    if (n_hi == N - 1) {
+        rc = ensure_slots(ctx, N);
+        if (rc) return rc;
+        CK(cudaMemsetAsync(ctx->maxslots, 0, (size_t)(N + 2) * 8, ctx->stream));
+        ctx->cur = 1 - ctx->cur;  // swap_direction: u_prev <- u^N, u_cur <- u^{N-1}
+    }
+    REQUIRE(ctx->maxslot_bytes >= (size_t)(N + 2) * 8, "sweep not initialised");
     long long sf = (long long)src_flat;
     double val = 0.0;
-    for (int64_t n = N - 1; n >= 1; --n) {
+    for (int64_t n = n_hi; n > n_lo; --n) {
         StepSpec sp;
         sp.acc = accumulate != 0;
         sp.check = (n % STABILITY_CHECK_INTERVAL == 0) || (n == 1);
@@ -564,6 +587,7 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
     }
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->prof) harvest_events(ctx);
+    if (!finish) return WO_OK;
     std::vector<char> hs((size_t)(N + 2) * 8);
     CK(cudaMemcpy(hs.data(), ctx->maxslots, hs.size(), cudaMemcpyDeviceToHost));
     for (int64_t n = N - 1; n >= 1; --n) {
@@ -1069,6 +1093,83 @@ int wo_sweep_forward(wo_ctx* ctx, int64_t n_steps, int n_src, const int64_t* src
     REQUIRE(n_steps >= 2, "need at least 2 time steps");
     return DISPATCH(ctx, sweep_forward_t, ctx, n_steps, n_src, src_flat, src_amp, flags, dt,
                     scale, peak_out, fail_step, fail_max);
+}
+
+int wo_sweep_forward_range(wo_ctx* ctx, int64_t n_steps, int64_t n_begin, int64_t n_end,
+                           int n_src, const int64_t* src_flat, const double* src_amp, int flags,
+                           double dt) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(ctx->material_set, "material not set");
+    REQUIRE(n_steps >= 2, "need at least 2 time steps");
+    int64_t fs = 0;
+    double fm = 0.0;
+    return DISPATCH(ctx, sweep_forward_t, ctx, n_steps, n_src, src_flat, src_amp, flags, dt, 0.0,
+                    nullptr, &fs, &fm, n_begin, n_end, false);
+}
+
+int wo_sweep_backward_range(wo_ctx* ctx, int64_t n_steps, int64_t n_hi, int64_t n_lo,
+                            int64_t src_flat, const double* src_amp, int inject_support,
+                            int accumulate, double dt) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(ctx->material_set, "material not set");
+    int64_t fs = 0;
+    double fm = 0.0;
+    return DISPATCH(ctx, sweep_backward_t, ctx, n_steps, src_flat, src_amp, inject_support,
+                    accumulate, dt, &fs, &fm, n_hi, n_lo, false);
+}
+
+int wo_check_maxima(wo_ctx* ctx, int64_t n_steps, double* out) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(ctx->maxslot_bytes >= (size_t)(n_steps + 2) * 8, "no sweep recorded");
+    CK(cudaStreamSynchronize(ctx->stream));
+    std::vector<char> hs((size_t)(n_steps + 2) * 8);
+    CK(cudaMemcpy(hs.data(), ctx->maxslots, hs.size(), cudaMemcpyDeviceToHost));
+    for (int64_t n = 0; n < n_steps + 2; ++n)
+        out[n] = ctx->itemsize == 4 ? slot_value<float>(hs.data(), n)
+                                    : slot_value<double>(hs.data(), n);
+    return WO_OK;
+}
+
+int wo_halo_planes(wo_ctx* ctx, void** first, void** last, void** ghost_lo, void** ghost_hi,
+                   int64_t* plane_bytes) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    const size_t pb = (size_t)ctx->plane() * ctx->itemsize;
+    char* c = ctx->ucur();
+    *first = c;
+    *last = c + (size_t)(ctx->kn0 - 1) * pb;
+    *ghost_lo = ctx->has_lo ? c - pb : nullptr;
+    *ghost_hi = ctx->has_hi ? c + (size_t)ctx->kn0 * pb : nullptr;
+    *plane_bytes = (int64_t)pb;
+    return WO_OK;
+}
+
+int wo_exchange_local(wo_ctx* lower, wo_ctx* upper) {
+    if (!lower || !upper) return WO_ERR_CONFIG;
+    wo_ctx* ctx = lower;
+    REQUIRE(lower->has_hi && upper->has_lo && lower->plane() == upper->plane() &&
+                lower->itemsize == upper->itemsize,
+            "contexts are not adjacent slabs");
+    const size_t pb = (size_t)lower->plane() * lower->itemsize;
+    CK(cudaStreamSynchronize(lower->stream));
+    CK(cudaSetDevice(upper->device));
+    CK(cudaStreamSynchronize(upper->stream));
+    char* lo_last = lower->ucur() + (size_t)(lower->kn0 - 1) * pb;
+    char* lo_ghost = lower->ucur() + (size_t)lower->kn0 * pb;
+    char* up_first = upper->ucur();
+    char* up_ghost = upper->ucur() - pb;
+    if (lower->device == upper->device) {
+        CK(cudaMemcpy(up_ghost, lo_last, pb, cudaMemcpyDeviceToDevice));
+        CK(cudaMemcpy(lo_ghost, up_first, pb, cudaMemcpyDeviceToDevice));
+    } else {
+        CK(cudaMemcpyPeer(up_ghost, upper->device, lo_last, lower->device, pb));
+        CK(cudaMemcpyPeer(lo_ghost, lower->device, up_first, upper->device, pb));
+    }
+    CK(cudaSetDevice(lower->device));
+    return WO_OK;
 }
 
 int wo_sweep_adjoint_reference(wo_ctx* ctx, int64_t n_steps, double dt, int64_t* fail_step,

@@ -1,20 +1,46 @@
 """Multi-GPU modes of the superposed gradient.
 
-shot-parallel: one process per GPU (torchrun, NCCL).  Rank r evaluates shots
-r, r+P, r+2P, ... into its own device accumulator; the unscaled accumulators
-and the costs are summed with one all-reduce per evaluation, then every rank
-applies acc /= T(2k).  Summation order differs from the reference's serial
-shared accumulator, so this mode is NOT bitwise (the reference itself notes
-shot concurrency); it is the throughput mode for multi-shot
-problems that fit one GPU.  ``shot_partition`` and ``reduce_plan`` hold the
-host logic and are exercised with gloo on CPU in tests/test_distributed_cpu.py.
+slab decomposition (SlabGradient)
+    The grid is cut along axis 0 (outermost, so a halo is one contiguous
+    n1*n2 plane).  Each slab context (``wo_create_slab``) holds its planes plus
+    one ghost plane per interior face; the step kernels read ghost planes
+    exactly like interior planes and mirror only at the global ends, so the
+    per-cell arithmetic is unchanged and the gradient, traces and adjoint
+    store are BITWISE equal to one GPU.  After every step each slab sends its
+    first/last plane of the new level to its neighbours' ghost planes:
+      * ``LoopbackHalo`` — all slabs in one process (same device or peer
+        devices), ``wo_exchange_local`` copies;
+      * ``TorchHalo`` — one slab per process (torchrun), torch.distributed
+        point-to-point send/recv of the plane tensors (NCCL over NVLink on
+        GPUs; the same code runs on gloo/CPU tensors in the tests).
+    Costs are summed per slab then across slabs (fp64, not bitwise: the
+    reference's BLAS dot order is unknown anyway); stability maxima are
+    combined with max before the reference's first-failure scan.
+
+shot-parallel (ShotParallelGradient)
+    Rank r evaluates shots r, r+P, ...; the unscaled accumulators and the
+    costs are summed with one all-reduce per evaluation, then acc /= T(2k).
+    Not bitwise (summation order), like the reference's own remark on shot
+    concurrency; the throughput mode for multi-shot problems
+    that fit one GPU.
 """
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
+from . import _native as N
+from . import engine
+from .engine import SolverInstabilityError, source_amplitude_table
+from .grids import ConfigError, precision_dtype
 
+STABILITY_CHECK_INTERVAL = 50
+STABILITY_GROWTH_FACTOR = 1e6
+
+
+# ------------------------------------------------------------- host logic
 def shot_partition(n_shots, rank, world):
     """Round-robin shot indices owned by rank."""
     if world < 1 or not 0 <= rank < world:
@@ -22,18 +48,263 @@ def shot_partition(n_shots, rank, world):
     return list(range(rank, n_shots, world))
 
 
-def accumulator_tensor(ctx):
-    """Zero-copy torch view of a DeviceGrid's accumulator (CUDA array interface)."""
+def slab_ranges(n0, parts):
+    """Balanced [i0, i1) plane ranges along axis 0 (each >= 1 plane)."""
+    if not 1 <= parts <= n0:
+        raise ConfigError(f"cannot cut {n0} planes into {parts} slabs")
+    base, extra = divmod(n0, parts)
+    out, i = [], 0
+    for p in range(parts):
+        n = base + (1 if p < extra else 0)
+        out.append((i, i + n))
+        i += n
+    return out
+
+
+def localize(flat, shape, i0, i1):
+    """Global C-order flat indices -> (owned mask, local flat indices) for
+    the slab of planes [i0, i1)."""
+    flat = np.asarray(flat, dtype=np.int64)
+    plane = int(shape[1]) * int(shape[2])
+    i = flat // plane
+    owned = (i >= i0) & (i < i1)
+    return owned, flat[owned] - i0 * plane
+
+
+def first_failure_forward(maxima, n_steps, scale):
+    """First failing forward check (solver.py:180-186, gradients.py:247-248):
+    (step, max) or None; also returns the peak over the checks."""
+    peak = 0.0
+    for n in range(1, n_steps):
+        if n % STABILITY_CHECK_INTERVAL and n != n_steps - 1:
+            continue
+        m = float(maxima[n])
+        if not math.isfinite(m) or (scale > 0.0 and m > STABILITY_GROWTH_FACTOR * scale):
+            return (n + 1, m), peak
+        peak = max(peak, m)
+    return None, peak
+
+
+def first_failure_backward(maxima, n_steps):
+    """First failing backward check (gradients.py:272-280): (step, max) or None."""
+    for n in range(n_steps - 1, 0, -1):
+        if n % STABILITY_CHECK_INTERVAL and n != 1:
+            continue
+        m = float(maxima[n])
+        if not math.isfinite(m):
+            return (n - 1, m)
+    return None
+
+
+def exchange_planes(first, last, ghost_lo, ghost_hi, rank, world, group=None):
+    """Halo exchange of one slab with torch.distributed P2P: first -> rank-1's
+    high ghost, last -> rank+1's low ghost (tensors: CUDA with NCCL, CPU with
+    gloo)."""
+    import torch.distributed as dist
+
+    ops = []
+    if rank > 0:
+        ops.append(dist.P2POp(dist.isend, first, rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, ghost_lo, rank - 1, group))
+    if rank < world - 1:
+        ops.append(dist.P2POp(dist.isend, last, rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, ghost_hi, rank + 1, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+def _device_view(ptr, nbytes, dtype, device):
+    """torch tensor over a device address (CUDA array interface, no copy)."""
     import torch
 
-    ptr = ctx.L.wo_accumulator_ptr(ctx.h)
-    typestr = "<f4" if ctx.dtype.itemsize == 4 else "<f8"
+    n = nbytes // np.dtype(dtype).itemsize
 
     class _View:
-        __cuda_array_interface__ = {"shape": tuple(ctx.grid.shape), "typestr": typestr,
+        __cuda_array_interface__ = {"shape": (n,), "typestr": np.dtype(dtype).str,
                                     "data": (int(ptr), False), "version": 3, "strides": None}
 
-    return torch.as_tensor(_View(), device=f"cuda:{ctx.device}")
+    return torch.as_tensor(_View(), device=f"cuda:{device}")
+
+
+# ----------------------------------------------------------- halo backends
+class LoopbackHalo:
+    """All slabs of the decomposition live in this process."""
+
+    def __init__(self, ctxs):
+        self.ctxs = ctxs
+
+    def exchange(self):
+        for lo, hi in zip(self.ctxs[:-1], self.ctxs[1:]):
+            rc = lo.L.wo_exchange_local(lo.h, hi.h)
+            if rc:
+                engine._raise(lo.h, rc, "wo_exchange_local")
+
+    def allreduce_max(self, arr):
+        return arr
+
+    def allreduce_sum(self, x):
+        return x
+
+
+class TorchHalo:
+    """One slab per process; neighbours are ranks r-1 and r+1."""
+
+    def __init__(self, ctx, rank, world, group=None):
+        self.ctx, self.rank, self.world, self.group = ctx, rank, world, group
+
+    def exchange(self):
+        import torch
+
+        (first, last, glo, ghi), pb = self.ctx.halo_planes()
+        dt, dev = self.ctx.dtype, self.ctx.device
+        view = lambda p: _device_view(p, pb, dt, dev) if p else None  # noqa: E731
+        exchange_planes(view(first), view(last), view(glo), view(ghi), self.rank, self.world,
+                        self.group)
+        torch.cuda.synchronize(dev)
+
+    def allreduce_max(self, arr):
+        import torch
+        import torch.distributed as dist
+
+        t = torch.from_numpy(np.ascontiguousarray(arr)).cuda(self.ctx.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return t.cpu().numpy()
+
+    def allreduce_sum(self, x):
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{self.ctx.device}")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return float(t.item())
+
+
+# ------------------------------------------------------------ slab driver
+class SlabGradient:
+    """gradient_superposed over axis-0 slabs (bitwise equal to one GPU).
+
+    slabs: list of (i0, i1) handled by THIS process; halo: 'loopback' (all
+    slabs here) or a TorchHalo-compatible object built by ``for_rank``."""
+
+    def __init__(self, problem, material, config, slabs, devices=None, halo="loopback"):
+        from .gradients import SuperpositionConfig, _misfit_spec, _shot_list
+
+        if not isinstance(config, SuperpositionConfig):
+            config = SuperpositionConfig(k=float(config))
+        grid = problem.grid
+        if grid.ndim != 3:
+            raise ConfigError("slab decomposition needs a 3D grid")
+        self.problem, self.material, self.config = problem, material, config
+        self.dtype = precision_dtype(config.precision)
+        devices = devices or [0] * len(slabs)
+        self.slabs = list(slabs)
+        self.ctxs = [engine.DeviceGrid(grid, self.dtype, d, slab=s)
+                     for s, d in zip(self.slabs, devices)]
+        self.halo = LoopbackHalo(self.ctxs) if halo == "loopback" else halo
+        self._misfit_spec = _misfit_spec
+        self._shots = _shot_list(problem)
+
+    @classmethod
+    def for_rank(cls, problem, material, config, rank, world, device=None, group=None):
+        """One slab per torchrun rank (NCCL halo exchange)."""
+        slab = slab_ranges(problem.grid.shape[0], world)[rank]
+        dev = rank if device is None else device
+        obj = cls(problem, material, config, [slab], [dev], halo=None)
+        obj.halo = TorchHalo(obj.ctxs[0], rank, world, group)
+        return obj
+
+    def upload(self):
+        dt = self.problem.time.dt
+        for c in self.ctxs:
+            c.set_material(self.material, dt)
+        return self
+
+    def run(self):
+        from .solver import injection_scale
+
+        problem, grid = self.problem, self.problem.grid
+        n_steps, dt, k = problem.time.n_steps, problem.time.dt, self.config.k
+        plane = grid.shape[1] * grid.shape[2]
+        for c in self.ctxs:
+            c.zero_accumulator()
+        total = 0.0
+        for source, shot in self._shots:
+            g_src = grid.flat_index(source.node)
+            amp = source_amplitude_table([source], dt, n_steps)
+            scale = injection_scale([source], self.material, dt, self.dtype) * n_steps
+            specs = []
+            for c in self.ctxs:
+                owned, local = localize(shot.support_idx, grid.shape, c.i_begin, c.i_end)
+                order = c.set_support(local)
+                kind, cc, adj_coef, meas = self._misfit_spec(shot, np.arange(len(owned)))
+                if meas is not None:
+                    meas = np.ascontiguousarray(meas[owned][order])
+                specs.append((len(local), kind, cc, adj_coef, meas))
+                c.reset_window()
+            src_local = [g_src - c.i_begin * plane if c.i_begin * plane <= g_src < c.i_end * plane
+                         else -1 for c in self.ctxs]
+            for n in range(1, n_steps):
+                for c, s in zip(self.ctxs, src_local):
+                    c.sweep_forward_range(n_steps, n, n + 1, [s] if s >= 0 else [], amp
+                                          if s >= 0 else np.zeros((0, n_steps)), True, dt)
+                self.halo.exchange()
+            maxima = self.halo.allreduce_max(
+                np.max([c.check_maxima(n_steps) for c in self.ctxs], axis=0))
+            fail, _ = first_failure_forward(maxima, n_steps, scale)
+            if fail:
+                raise SolverInstabilityError(*fail, detail=(
+                    f"exceeds 1e6 x scale {scale:g}" if math.isfinite(fail[1]) else ""))
+            cost = 0.0
+            for c, (nsup, kind, cc, adj_coef, meas) in zip(self.ctxs, specs):
+                if nsup:
+                    cost += c.shot_misfit(n_steps, kind, meas, cc, adj_coef, True, k)
+            total += self.halo.allreduce_sum(cost)
+            for n in range(n_steps - 1, 0, -1):
+                for c, s, spec in zip(self.ctxs, src_local, specs):
+                    c.sweep_backward_range(n_steps, n, n - 1, s, amp[0], spec[0] > 0, True, dt)
+                self.halo.exchange()
+            maxima = self.halo.allreduce_max(
+                np.max([c.check_maxima(n_steps) for c in self.ctxs], axis=0))
+            fail = first_failure_backward(maxima, n_steps)
+            if fail:
+                from .gradients import SUPERPOSED_DETAIL
+
+                raise SolverInstabilityError(*fail, detail=SUPERPOSED_DETAIL)
+        for c in self.ctxs:
+            c.gradient(2.0 * k, copy=False)
+        return total
+
+    def download(self):
+        """This process's slabs of the gradient, concatenated along axis 0."""
+        return np.concatenate([c.get_accumulator() for c in self.ctxs], axis=0)
+
+    def close(self):
+        for c in self.ctxs:
+            c.close()
+
+
+def gradient_superposed_slabs(problem, material, config, parts, devices=None):
+    """Single-process slab-decomposed gradient (loopback / peer halo)."""
+    from .gradients import GradientResult, BufferCounter
+
+    sg = SlabGradient(problem, material, config, slab_ranges(problem.grid.shape[0], parts),
+                      devices).upload()
+    try:
+        cost = sg.run()
+        grad = sg.download()
+    finally:
+        sg.close()
+    return GradientResult(cost=cost, gradient=grad, counter=BufferCounter(problem.grid),
+                          k=sg.config.k)
+
+
+# --------------------------------------------------------- shot-parallel
+def accumulator_tensor(ctx):
+    """Zero-copy torch view of a DeviceGrid's accumulator (CUDA array interface)."""
+    ptr = ctx.L.wo_accumulator_ptr(ctx.h)
+    t = _device_view(ptr, ctx.grid.n_nodes * ctx.dtype.itemsize, ctx.dtype, ctx.device)
+    return t.view(*ctx.grid.shape)
 
 
 def reduce_plan(acc, cost, group=None):

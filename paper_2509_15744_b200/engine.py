@@ -90,22 +90,51 @@ def kernel_coefficients(material: MaterialModel):
     return -dk, dr
 
 
+class _SlabShape:
+    """Minimal grid-like record for a slab's local planes."""
+
+    def __init__(self, shape, dx):
+        self.shape = tuple(int(n) for n in shape)
+        self.dx = float(dx)
+        self.ndim = len(self.shape)
+        self.n_nodes = int(np.prod(self.shape))
+
+
 class DeviceGrid:
     """Device buffers + sweeps for one grid at one dtype (include/waveb200.h)."""
 
-    def __init__(self, grid: Grid, dtype, device=0):
+    def __init__(self, grid: Grid, dtype, device=0, slab=None):
+        """slab=(i_begin, i_end): a slab of a 3D grid along axis 0 (global
+        planes [i_begin, i_end) plus ghost planes at interior faces)."""
         self.L = N.load(require_device=True)
-        self.grid = grid
         self.dtype = np.dtype(dtype)
         self.device = device
         h = ctypes.c_void_p()
-        rc = self.L.wo_create(ctypes.byref(h), grid.ndim, N.shape3(grid.shape), float(grid.dx),
-                              self.dtype.itemsize, device)
+        if slab is None:
+            self.global_grid = grid
+            self.i_begin, self.i_end = 0, grid.shape[0]
+            self.grid = grid
+            rc = self.L.wo_create(ctypes.byref(h), grid.ndim, N.shape3(grid.shape),
+                                  float(grid.dx), self.dtype.itemsize, device)
+        else:
+            if grid.ndim != 3:
+                raise ConfigError("slab decomposition needs a 3D grid")
+            self.global_grid = grid
+            self.i_begin, self.i_end = int(slab[0]), int(slab[1])
+            # local view: the slab's own planes (Grid needs >= 3 nodes per axis,
+            # so keep the dataclass-free shape separately)
+            self.grid = _SlabShape((self.i_end - self.i_begin,) + grid.shape[1:], grid.dx)
+            rc = self.L.wo_create_slab(ctypes.byref(h), N.shape3(grid.shape), self.i_begin,
+                                       self.i_end, float(grid.dx), self.dtype.itemsize, device)
         if rc:
             _raise(None, rc, "wo_create")
         self.h = h
         self._support_key = None
         self.n_sup = 0
+
+    @property
+    def is_slab(self):
+        return self.grid is not self.global_grid
 
     # --------------------------------------------------------------- basics
     def close(self):
@@ -130,10 +159,15 @@ class DeviceGrid:
         return a
 
     def set_material(self, material: MaterialModel, dt):
-        if material.grid.shape != self.grid.shape:
+        if material.grid.shape != self.global_grid.shape:
             raise ConfigError("material lives on a different grid")
         flavor = N.WO_RHO_SCALED if material.flavor == RHO_SCALED else N.WO_ACOUSTIC
-        gamma = np.ascontiguousarray(material.gamma, dtype=np.float64)
+        if self.is_slab:   # own planes plus the ghost planes (solver.py:94 per slab)
+            lo = max(self.i_begin - 1, 0)
+            hi = min(self.i_end + 1, self.global_grid.shape[0])
+            gamma = np.ascontiguousarray(material.gamma[lo:hi], dtype=np.float64)
+        else:
+            gamma = np.ascontiguousarray(material.gamma, dtype=np.float64)
         ratio2 = material_ratio2(material, float(dt), self.grid.dx)
         self._ck(self.L.wo_set_material(self.h, flavor, N.ptr(gamma), float(material.rho0),
                                         float(material.rho1), float(material.kappa1),
@@ -235,6 +269,36 @@ class DeviceGrid:
         if rc == N.WO_ERR_UNSTABLE:
             raise SolverInstabilityError(int(fstep.value), fmax.value, detail=detail_on_fail)
         self._ck(rc, "wo_sweep_backward")
+
+    def sweep_forward_range(self, n_steps, n_begin, n_end, src_flat, amp_table, accumulate, dt):
+        src = np.ascontiguousarray(np.asarray(src_flat, dtype=np.int64).reshape(-1))
+        amp = np.ascontiguousarray(np.asarray(amp_table, dtype=np.float64))
+        flags = N.WO_FWD_ACCUMULATE if accumulate else 0
+        self._ck(self.L.wo_sweep_forward_range(self.h, int(n_steps), int(n_begin), int(n_end),
+                                               len(src), N.ptr(src), N.ptr(amp), flags,
+                                               float(dt)), "wo_sweep_forward_range")
+
+    def sweep_backward_range(self, n_steps, n_hi, n_lo, src_flat, amp_row, inject, accumulate,
+                             dt):
+        amp = np.ascontiguousarray(np.asarray(amp_row, dtype=np.float64))
+        self._ck(self.L.wo_sweep_backward_range(self.h, int(n_steps), int(n_hi), int(n_lo),
+                                                int(src_flat), N.ptr(amp), int(bool(inject)),
+                                                int(bool(accumulate)), float(dt)),
+                 "wo_sweep_backward_range")
+
+    def check_maxima(self, n_steps):
+        out = np.empty(int(n_steps) + 2, dtype=np.float64)
+        self._ck(self.L.wo_check_maxima(self.h, int(n_steps), N.ptr(out)), "wo_check_maxima")
+        return out
+
+    def halo_planes(self):
+        """(first, last, ghost_lo, ghost_hi) device addresses of the current
+        level and the plane size in bytes."""
+        p = [ctypes.c_void_p() for _ in range(4)]
+        pb = ctypes.c_int64()
+        self._ck(self.L.wo_halo_planes(self.h, *[ctypes.byref(x) for x in p], ctypes.byref(pb)),
+                 "wo_halo_planes")
+        return tuple(x.value for x in p), pb.value
 
     def sweep_adjoint_reference(self, n_steps, dt):
         fstep = ctypes.c_int64(0)

@@ -1,0 +1,101 @@
+"""Multi-process host logic of the multi-GPU modes, on CPU with gloo
+(world_size 2): slab halo exchange protocol, shot partition, check
+combination.  The same exchange code drives NCCL on GPUs."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2509_15744_b200 import distributed as D
+
+
+def test_slab_ranges_and_localize():
+    assert D.slab_ranges(10, 3) == [(0, 4), (4, 7), (7, 10)]
+    assert D.slab_ranges(8, 8) == [(i, i + 1) for i in range(8)]
+    with pytest.raises(Exception):
+        D.slab_ranges(3, 4)
+    shape = (6, 4, 5)
+    flat = np.array([0, 19, 20, 59, 60, 119])
+    owned, local = D.localize(flat, shape, 1, 3)
+    assert owned.tolist() == [False, False, True, True, False, False]
+    assert local.tolist() == [0, 39]
+
+
+def test_shot_partition_covers_all():
+    for world in (1, 2, 3, 8):
+        got = sorted(s for r in range(world) for s in D.shot_partition(5, r, world))
+        assert got == list(range(5))
+
+
+def test_check_scans_follow_reference_order():
+    n = 120
+    m = np.zeros(n + 2)
+    m[50] = 1.0
+    m[100] = 5.0
+    assert D.first_failure_forward(m, n, scale=1e-6)[0] == (101, 5.0)
+    assert D.first_failure_forward(m, n, scale=1.0)[0] is None
+    m[100] = np.nan
+    assert D.first_failure_forward(m, n, 0.0)[0][0] == 101
+    b = np.zeros(n + 2)
+    b[50] = np.inf
+    b[100] = np.inf
+    assert D.first_failure_backward(b, n) == (99, np.inf)   # descending n: 100 first
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plane = 12
+        # slab r holds planes [2r, 2r+2) of a 2*world-plane field: value = 100*plane + j
+        field = torch.arange(2 * world * plane, dtype=torch.float64).view(2 * world, plane)
+        mine = field[2 * rank:2 * rank + 2].clone()
+        ghost_lo = torch.full((plane,), -1.0, dtype=torch.float64)
+        ghost_hi = torch.full((plane,), -1.0, dtype=torch.float64)
+        D.exchange_planes(mine[0].contiguous(), mine[1].contiguous(), ghost_lo, ghost_hi,
+                          rank, world)
+        ok = True
+        if rank > 0:
+            ok &= bool(torch.equal(ghost_lo, field[2 * rank - 1]))
+        if rank < world - 1:
+            ok &= bool(torch.equal(ghost_hi, field[2 * rank + 2]))
+        # cost / maxima reductions as the slab driver does them
+        c = torch.tensor([float(rank + 1)], dtype=torch.float64)
+        dist.all_reduce(c)
+        mx = torch.tensor([float(rank), 3.0 - rank], dtype=torch.float64)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        ok &= float(c.item()) == world * (world + 1) / 2
+        ok &= mx.tolist() == [world - 1.0, 3.0]
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_exchange_gloo(world):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res[r] for r in range(world)), res

@@ -20,6 +20,7 @@
 #include "dropin_kernels.cuh"
 #include "step_kernel.cuh"
 #include "step_kernel_tma.cuh"
+#include "step_kernel_tma4.cuh"
 #include "step_kernel_v2.cuh"
 
 #include <cudaTypedefs.h>
@@ -257,13 +258,26 @@ bool tma_ready(wo_ctx* ctx) {
 
 template <typename T, int FL, bool FAST, bool ACC, bool CHK, int SUP>
 void launch_tma(dim3 grid, dim3 block, size_t tsm, wo_ctx* ctx, const StepArgs<T>& a) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(step_kernel_tma<T, FL, FAST, ACC, CHK, SUP>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-        attr_set = true;
+    if (ctx->use_tma == 2) {   // v8 layout: 256 threads, 2 cells each
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaFuncSetAttribute(step_kernel_tma<T, FL, FAST, ACC, CHK, SUP>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+            attr_set = true;
+        }
+        step_kernel_tma<T, FL, FAST, ACC, CHK, SUP><<<grid, block, tsm, ctx->stream>>>(a, ctx->tmaps);
+        return;
     }
-    step_kernel_tma<T, FL, FAST, ACC, CHK, SUP><<<grid, block, tsm, ctx->stream>>>(a, ctx->tmaps);
+    // default: 128 threads, 2x2 cells each, statically unrolled stages
+    const size_t sm4 = tma4_smem_bytes<T>();
+    static bool attr4 = false;
+    if (!attr4) {
+        cudaFuncSetAttribute(step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
+        attr4 = true;
+    }
+    step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP><<<grid, dim3(32, 4, 1), sm4, ctx->stream>>>(
+        a, ctx->tmaps);
 }
 
 struct StepSpec {
@@ -979,7 +993,7 @@ int wo_set_option(wo_ctx* ctx, int option, int value) {
         return WO_OK;
     }
     if (option == WO_OPT_TMA_KERNEL) {
-        ctx->use_tma = value != 0;
+        ctx->use_tma = value;   // 0 off, 1 tma4 (default), 2 the 256-thread TMA kernel
         return WO_OK;
     }
     ctx->allow_fast_div = value != 0;

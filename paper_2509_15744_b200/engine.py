@@ -335,9 +335,9 @@ class DeviceGrid:
         self._ck(self.L.wo_set_option(self.h, N.WO_OPT_PAIR_KERNEL, int(bool(on))),
                  "wo_set_option")
 
-    def set_tma_kernel(self, on):
-        self._ck(self.L.wo_set_option(self.h, N.WO_OPT_TMA_KERNEL, int(bool(on))),
-                 "wo_set_option")
+    def set_tma_kernel(self, mode):
+        """0: never; 1/True: 2x2-cell TMA kernel (default); 2: 256-thread TMA kernel."""
+        self._ck(self.L.wo_set_option(self.h, N.WO_OPT_TMA_KERNEL, int(mode)), "wo_set_option")
 
     def fast_div_active(self):
         return bool(self.L.wo_fast_div_active(self.h))

@@ -311,9 +311,13 @@ def run_native(args):
     api_call()                                             # warm the API path
     barrier(world)
     t0 = time.perf_counter()
+    per_call = []
     for _ in range(args.steps):
+        tc = time.perf_counter()
         api_call()
+        per_call.append(time.perf_counter() - tc)
     e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps, world)
+    print(f"e2e per call (s): {[round(x, 4) for x in per_call]}", file=sys.stderr)
     e2e_value = world * updates / e2e_s / 1e9
     n_sup = len(problem.sensors)
     h2d = C * 8 + n_sup * n_steps * 8

@@ -25,9 +25,20 @@
 namespace wb {
 
 constexpr int T4_THREADS = 128;
+constexpr int NS = 3;                    // ring stages (2 planes in flight ahead)
+constexpr int U = NS % 2 ? 2 * NS : NS;  // planes per unrolled group: lcm(NS, 2)
+
+// body(q, plane) for q = 0..U-1 while the planes exist
+template <typename B, int... Q>
+__device__ __forceinline__ void unroll_planes(B& body, int i, int i1, unsigned gpar,
+                                              std::integer_sequence<int, Q...>) {
+    bool go = true;
+    ((go = go && (i + Q < i1), go ? (body(std::integral_constant<int, Q>{}, i + Q, gpar), 0) : 0),
+     ...);
+}
 
 template <typename T, int FLAVOR, bool FAST, bool ACC, bool CHECK, int SUP>
-__global__ void __launch_bounds__(T4_THREADS, sizeof(T) == 4 ? 4 : 2)
+__global__ void __launch_bounds__(T4_THREADS, sizeof(T) == 4 ? 5 : 2)
 step_kernel_tma4(const __grid_constant__ StepArgs<T> a, const __grid_constant__ TmaMaps maps) {
     using Tr = FTraits<T>;
     using MT = Mat<T, FLAVOR, FAST>;
@@ -37,9 +48,9 @@ step_kernel_tma4(const __grid_constant__ StepArgs<T> a, const __grid_constant__ 
     unsigned char* smem_raw =
         smem_dyn + ((128u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_dyn)) & 127u)) & 127u);
     TmaStage<T>* st = reinterpret_cast<TmaStage<T>*>(smem_raw);
-    T(*SM)[TH_H][W] = reinterpret_cast<T(*)[TH_H][W]>(smem_raw + TS * sizeof(TmaStage<T>));
+    T(*SM)[TH_H][W] = reinterpret_cast<T(*)[TH_H][W]>(smem_raw + NS * sizeof(TmaStage<T>));
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(
-        smem_raw + TS * sizeof(TmaStage<T>) + 2 * sizeof(T) * TH_H * W);
+        smem_raw + NS * sizeof(TmaStage<T>) + 2 * sizeof(T) * TH_H * W);
     __shared__ typename Tr::Bits smax[T4_THREADS / 32];
 
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -87,12 +98,12 @@ step_kernel_tma4(const __grid_constant__ StepArgs<T> a, const __grid_constant__ 
     };
 
     if (tid == 0) {
-        for (int s = 0; s < TS; ++s) mbar_init(&bar[s], 1);
+        for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (tid == 0)
-        for (int p = i0; p <= min(i0 + TS - 1, pend); ++p) issue(p, p - i0);
+        for (int p = i0; p <= min(i0 + NS - 1, pend); ++p) issue(p, p - i0);
 
     auto ldv = [](const T* p) { return *reinterpret_cast<const V*>(p); };
     auto stv = [](T* p, V v) { *reinterpret_cast<V*>(p) = v; };
@@ -167,14 +178,20 @@ step_kernel_tma4(const __grid_constant__ StepArgs<T> a, const __grid_constant__ 
         return accv + a.sdt * ((a.cv * va) * va + a.cg * (((g0 * g0) + (g1 * g1)) + (g2 * g2)));
     };
 
-    auto body = [&](auto stage, int i, unsigned par) {
-        constexpr int s = decltype(stage)::value;
-        constexpr int sn = (s + 1) & 3, sf = (s + 3) & 3, b = s & 1, nb = b ^ 1;
+    // body<q>: plane i = (group start) + q.  Stage of plane i is q % NS, the
+    // m-plane buffer q & 1; the mbarrier parity of plane i+1 is static within
+    // an unrolled group of U = lcm(NS, 2) planes up to the group parity gpar.
+    auto body = [&](auto stage, int i, unsigned gpar) {
+        constexpr int q = decltype(stage)::value;
+        constexpr int s = q % NS, sn = (q + 1) % NS, sf = (q + NS - 1) % NS;
+        constexpr int b = q & 1, nb = b ^ 1;
+        constexpr unsigned pnext = (unsigned)(((q + 1) / NS) & 1);   // within-group parity
+        constexpr unsigned gflip = (unsigned)((U / NS) & 1);          // parity step per group
         const bool next = i + 1 < i1;
         // ---- plane i+1 from its stage (mirror beyond the global end) ----
         V up1_a = u0_a, up1_b = u0_b, gp1_a = g0_a, gp1_b = g0_b;
         if (i + 1 <= plast) {
-            mbar_wait(&bar[sn], s == 3 ? par ^ 1u : par);
+            mbar_wait(&bar[sn], (q + 1 == U) ? (gpar ^ gflip) : (gpar ^ pnext));
             up1_a = ldv(&st[sn].U[ra][cA]);
             up1_b = ldv(&st[sn].U[rb][cA]);
             gp1_a = ldv(&st[sn].G[ra][cA]);
@@ -192,7 +209,7 @@ step_kernel_tma4(const __grid_constant__ StepArgs<T> a, const __grid_constant__ 
             }
         }
         __syncthreads();
-        if (tid == 0 && i > i0 && i - 1 + TS <= pend) issue(i - 1 + TS, sf);
+        if (tid == 0 && i > i0 && i - 1 + NS <= pend) issue(i - 1 + NS, sf);
         Faces Fn = F;
         if (next) Fn = faces(SM[nb], mp1_a, mp1_b);
 
@@ -282,13 +299,10 @@ step_kernel_tma4(const __grid_constant__ StepArgs<T> a, const __grid_constant__ 
         F = Fn;
     };
 
-    unsigned par = 0;
-    for (int i = i0; i < i1; i += TS) {
-        body(std::integral_constant<int, 0>{}, i, par);
-        if (i + 1 < i1) body(std::integral_constant<int, 1>{}, i + 1, par);
-        if (i + 2 < i1) body(std::integral_constant<int, 2>{}, i + 2, par);
-        if (i + 3 < i1) body(std::integral_constant<int, 3>{}, i + 3, par);
-        par ^= 1u;
+    unsigned gpar = 0;
+    for (int i = i0; i < i1; i += U) {
+        unroll_planes(body, i, i1, gpar, std::make_integer_sequence<int, U>{});
+        gpar ^= (unsigned)((U / NS) & 1);
     }
 
     if (CHECK) {
@@ -312,8 +326,8 @@ step_kernel_tma4(const __grid_constant__ StepArgs<T> a, const __grid_constant__ 
 
 template <typename T>
 constexpr size_t tma4_smem_bytes() {
-    return TS * sizeof(TmaStage<T>) + 2 * sizeof(T) * TH_H * th_w<T>() +
-           TS * sizeof(unsigned long long) + 128;
+    return NS * sizeof(TmaStage<T>) + 2 * sizeof(T) * TH_H * th_w<T>() +
+           NS * sizeof(unsigned long long) + 128;
 }
 
 }  // namespace wb

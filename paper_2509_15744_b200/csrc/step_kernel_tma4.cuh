@@ -25,7 +25,10 @@
 namespace wb {
 
 constexpr int T4_THREADS = 128;
-constexpr int NS = 3;                    // ring stages (2 planes in flight ahead)
+#ifndef WB_TMA_STAGES
+#define WB_TMA_STAGES 4
+#endif
+constexpr int NS = WB_TMA_STAGES;        // ring stages (NS-1 planes in flight ahead)
 constexpr int U = NS % 2 ? 2 * NS : NS;  // planes per unrolled group: lcm(NS, 2)
 
 // body(q, plane) for q = 0..U-1 while the planes exist
@@ -38,7 +41,7 @@ __device__ __forceinline__ void unroll_planes(B& body, int i, int i1, unsigned g
 }
 
 template <typename T, int FLAVOR, bool FAST, bool ACC, bool CHECK, int SUP>
-__global__ void __launch_bounds__(T4_THREADS, sizeof(T) == 4 ? 5 : 2)
+__global__ void __launch_bounds__(T4_THREADS, sizeof(T) == 4 ? 4 : 2)
 step_kernel_tma4(const __grid_constant__ StepArgs<T> a, const __grid_constant__ TmaMaps maps) {
     using Tr = FTraits<T>;
     using MT = Mat<T, FLAVOR, FAST>;

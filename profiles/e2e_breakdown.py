@@ -17,7 +17,16 @@ def main():
     wl = bench.workload(256, int(sys.argv[1]) if len(sys.argv) > 1 else 1024)
     problem, model = bench.build_problem(W, wl)
     cfg = W.SuperpositionConfig(k=wl["k"], precision="single")
-    for rep in range(3):
+    if "--pinned" in sys.argv:
+        import torch
+
+        gp = torch.empty(problem.grid.shape, dtype=torch.float64, pin_memory=True).numpy()
+        gp[...] = model.gamma
+        model = model.with_gamma(gp)
+        mp = torch.empty(problem.measured.shape, dtype=torch.float64, pin_memory=True).numpy()
+        mp[...] = problem.measured
+        problem.measured = mp
+    for rep in range(8):
         t0 = time.perf_counter()
         plan = G.SuperposedPlan(problem, model, cfg)
         t1 = time.perf_counter()

@@ -82,6 +82,11 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
 /* WO_OPT_TMA_KERNEL (default 1): TMA/mbarrier-pipelined step kernel when the
  * grid tiles exactly into 64 x 8 cells (0 = never). */
 #define WO_OPT_TMA_KERNEL 3
+/* WO_OPT_TWO_STEP (default 1): advance two time steps per pass over HBM
+ * (temporal blocking, identical arithmetic) on single-domain contexts whose
+ * grid tiles into 64 x 8 cells with the fast-division path active; sweeps
+ * fall back to single steps at odd range ends and everywhere else. */
+#define WO_OPT_TWO_STEP 4
 int wo_set_option(wo_ctx* ctx, int option, int value);
 int wo_fast_div_active(const wo_ctx* ctx);
 /* Kernel-increment scalars (gradients.py:117-129, kernels.py:149-152): the
@@ -211,6 +216,9 @@ int wo_stats(wo_ctx* ctx, int64_t* launches, int64_t* step_launches, double* ste
 int wo_reset_stats(wo_ctx* ctx);
 /* Device bytes held by the context (fields + support storage). */
 int64_t wo_device_bytes(const wo_ctx* ctx);
+/* Step launches since the last wo_reset_stats that were two-step passes
+ * (WO_OPT_TWO_STEP); the rest of wo_stats' step_launches are single steps. */
+int64_t wo_pair_launches(const wo_ctx* ctx);
 /* CUDA-event marks on the context stream (8 slots) for device timing. */
 int wo_timer_mark(wo_ctx* ctx, int idx);
 int wo_timer_elapsed(wo_ctx* ctx, int a, int b, double* ms);

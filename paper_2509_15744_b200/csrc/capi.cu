@@ -21,6 +21,7 @@
 #include "step_kernel.cuh"
 #include "step_kernel_tma.cuh"
 #include "step_kernel_tma4.cuh"
+#include "step2_kernel.cuh"
 #include "step_kernel_v2.cuh"
 
 #include <cudaTypedefs.h>
@@ -47,15 +48,19 @@ struct wo_ctx {
     cudaStream_t stream = nullptr;
 
     char* gamma = nullptr;             // allocation bases (ghost planes first)
-    char* u[2] = {nullptr, nullptr};
+    char* u[4] = {nullptr, nullptr, nullptr, nullptr};  // level buffers (2-3 only for two-step passes)
     char* acc = nullptr;
-    int cur = 0;                       // u[cur] = u^n, u[1-cur] = u^{n-1}
+    int cur = 0, prv = 1;              // u[cur] = u^n, u[prv] = u^{n-1}
 
     bool material_set = false;
     bool fast_div = false;             // verify_material_kernel passed for this material
     int allow_fast_div = 1;            // wo_set_option(WO_OPT_FAST_DIV)
     int use_pair = 1;                  // wo_set_option(WO_OPT_PAIR_KERNEL)
     int use_tma = 1;                   // wo_set_option(WO_OPT_TMA_KERNEL)
+    int use_two_step = 1;              // wo_set_option(WO_OPT_TWO_STEP)
+    int t2_state = 0;                  // two-step tensor maps: 0 not built, 1 ready, -1 no
+    Tma2Maps t2maps;
+    int64_t pair_launches = 0;
     int tma_state = 0;                 // 0 not built, 1 maps ready, -1 not eligible
     TmaMaps tmaps;                     // tensor maps of gamma, u[0], u[1], acc
     int sup_lo = 0, sup_hi = -1;       // local planes holding support nodes
@@ -100,7 +105,7 @@ struct wo_ctx {
     size_t field_bytes() const { return (size_t)cells() * itemsize; }
     char* base0(char* p) const { return p + (size_t)has_lo * plane() * itemsize; }
     char* ucur() const { return base0(u[cur]); }
-    char* uprev() const { return base0(u[1 - cur]); }
+    char* uprev() const { return base0(u[prv]); }
 };
 
 #define CK(call)                                                                     \
@@ -239,7 +244,8 @@ bool tma_ready(wo_ctx* ctx) {
             const uint64_t np = (uint64_t)(ctx->kn0 + ctx->has_lo + ctx->has_hi);
             const uint32_t hw = ctx->itemsize == 4 ? th_w<float>() : th_w<double>();
             bool ok = true;
-            for (int b = 0; b < 2; ++b) {
+            for (int b = 0; b < 4; ++b) {
+                if (!ctx->u[b]) continue;   // buffers 2/3 exist only after a two-step pass
                 ok &= make_map(&ctx->tmaps.u_halo[b], ctx->u[b], ctx->itemsize, ctx->kn2, ctx->kn1,
                                np, hw, TH_H);
                 ok &= make_map(&ctx->tmaps.u_ctr[b], ctx->u[b], ctx->itemsize, ctx->kn2, ctx->kn1,
@@ -352,7 +358,10 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     dim3 block(pair ? 32 : BX, BY, 1);
     dim3 grid(pair ? (ctx->kn2 + PBX - 1) / PBX : (ctx->kn2 + BX - 1) / BX,
               (ctx->kn1 + BY - 1) / BY, (ctx->kn0 + a.chunk - 1) / a.chunk);
-    if (tma) ctx->tmaps.cur = ctx->cur;
+    if (tma) {
+        ctx->tmaps.cur = ctx->cur;
+        ctx->tmaps.prev = ctx->prv;
+    }
     const size_t tsm = tma_smem_bytes<T>();
     if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
 #define LAUNCH(FL, FAST, ACC, CHK)                                                        \
@@ -431,6 +440,135 @@ int ensure_slots(wo_ctx* ctx, int64_t n) {
     return ensure(ctx, &ctx->maxslots, &ctx->maxslot_bytes, (size_t)(n + 2) * 8);
 }
 
+// ---- two-step passes (step2_kernel.cuh) ----
+int ensure_four(wo_ctx* ctx) {
+    const size_t ab = (size_t)ctx->alloc_cells() * ctx->itemsize;
+    for (int b = 2; b < 4; ++b) {
+        if (ctx->u[b]) continue;
+        int rc = dev_alloc(ctx, (void**)&ctx->u[b], ab);
+        if (rc) return rc;
+        CK(cudaMemsetAsync(ctx->u[b], 0, ab, ctx->stream));
+        ctx->tma_state = 0;   // single-step maps must cover the new buffers
+        ctx->t2_state = 0;
+    }
+    return WO_OK;
+}
+
+bool pair_ready(wo_ctx* ctx) {
+    if (!ctx->use_two_step || !ctx->use_tma || !ctx->use_pair || ctx->has_lo || ctx->has_hi ||
+        !ctx->fast_div || ctx->kn2 % PBX || ctx->kn1 % BY)
+        return false;
+    if (ensure_four(ctx)) return false;
+    if (ctx->t2_state == 0) {
+        ctx->t2_state = -1;
+        const uint64_t np = (uint64_t)ctx->kn0;
+        const uint32_t hw = ctx->itemsize == 4 ? th_w<float>() : th_w<double>();
+        bool ok = true;
+        for (int b = 0; b < 4; ++b) {
+            ok &= make_map(&ctx->t2maps.u_r2[b], ctx->u[b], ctx->itemsize, ctx->kn2, ctx->kn1, np,
+                           hw, R2_H);
+            ok &= make_map(&ctx->t2maps.u_r1[b], ctx->u[b], ctx->itemsize, ctx->kn2, ctx->kn1, np,
+                           hw, R1_H);
+        }
+        ok &= make_map(&ctx->t2maps.g_r2, ctx->gamma, ctx->itemsize, ctx->kn2, ctx->kn1, np, hw,
+                       R2_H);
+        ok &= make_map(&ctx->t2maps.a_ctr, ctx->acc, ctx->itemsize, ctx->kn2, ctx->kn1, np, PBX, BY);
+        if (ok) ctx->t2_state = 1;
+    }
+    return ctx->t2_state == 1 && tma_ready(ctx);
+}
+
+int choose_chunk2(const wo_ctx* ctx) {
+    const int tiles = (ctx->kn2 / PBX) * (ctx->kn1 / BY);
+    const int target = 148 * 3 * 2;   // two waves of 3 CTAs per SM
+    const int nz = std::max(1, target / std::max(1, tiles));
+    return std::max((ctx->kn0 + nz - 1) / nz, std::min(ctx->kn0, 8));
+}
+
+struct PairSpec {
+    bool acc = false, check1 = false, check2 = false;
+    double sdt = 0.0;
+    int n_src = 0;
+    const long long* src_flat = nullptr;
+    const double* val1 = nullptr;
+    const double* val2 = nullptr;
+    int sup_mode = SUP_NONE;
+    int64_t row1 = 0, row2 = 0, slot1 = 0, slot2 = 0;
+};
+
+template <typename T, int FL, bool ACC, int SUP>
+void launch_two(dim3 grid, wo_ctx* ctx, const Step2Args<T>& a) {
+    const size_t sm = step2_smem_bytes<T>();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(step2_kernel_tma<T, FL, true, ACC, SUP>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        attr = true;
+    }
+    step2_kernel_tma<T, FL, true, ACC, SUP><<<grid, dim3(32, 4, 1), sm, ctx->stream>>>(a, ctx->t2maps);
+}
+
+template <typename T>
+int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
+    int x[2], nx = 0;
+    for (int b = 0; b < 4 && nx < 2; ++b)
+        if (b != ctx->cur && b != ctx->prv) x[nx++] = b;
+    Step2Args<T> a{};
+    a.gamma = reinterpret_cast<const T*>(ctx->base0(ctx->gamma));
+    a.u_prev = reinterpret_cast<const T*>(ctx->uprev());
+    a.u_cur = reinterpret_cast<const T*>(ctx->ucur());
+    a.out1 = reinterpret_cast<T*>(ctx->base0(ctx->u[x[0]]));
+    a.out2 = reinterpret_cast<T*>(ctx->base0(ctx->u[x[1]]));
+    a.acc = reinterpret_cast<T*>(ctx->acc);
+    a.n0 = ctx->kn0; a.n1 = ctx->kn1; a.n2 = ctx->kn2;
+    a.chunk = choose_chunk2(ctx);
+    a.mat = mat_scalars<T>(ctx);
+    a.cv = (T)ctx->cv; a.cg = (T)ctx->cg; a.inv2dt = (T)ctx->inv2dt; a.inv2dx = (T)ctx->inv2dx;
+    a.sdt = (T)sp.sdt;
+    a.n_src = 0;
+    for (int s = 0; s < sp.n_src; ++s) {
+        const long long f = sp.src_flat[s];
+        const long long pl = ctx->plane();
+        if (f < 0 || f >= ctx->cells()) continue;
+        a.src_i[a.n_src] = (int)(f / pl);
+        a.src_j[a.n_src] = (int)((f % pl) / ctx->kn2);
+        a.src_k[a.n_src] = (int)(f % ctx->kn2);
+        a.src_val1[a.n_src] = (T)sp.val1[s];
+        a.src_val2[a.n_src] = (T)sp.val2[s];
+        a.n_src++;
+    }
+    const int sup = ctx->n_sup > 0 ? sp.sup_mode : SUP_NONE;
+    a.sup_lo = ctx->sup_lo; a.sup_hi = ctx->sup_hi;
+    a.sup_mask = ctx->mask; a.sup_prefix = ctx->prefix;
+    if (sup != SUP_NONE) {
+        a.row1 = reinterpret_cast<T*>(ctx->store) + sp.row1 * ctx->n_sup;
+        a.row2 = reinterpret_cast<T*>(ctx->store) + sp.row2 * ctx->n_sup;
+    }
+    a.check1 = sp.check1; a.check2 = sp.check2;
+    a.max1 = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots) + sp.slot1;
+    a.max2 = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots) + sp.slot2;
+    ctx->t2maps.prev = ctx->prv;
+    ctx->t2maps.cur = ctx->cur;
+    dim3 grid(ctx->kn2 / PBX, ctx->kn1 / BY, (ctx->kn0 + a.chunk - 1) / a.chunk);
+    if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
+#define L2(FL, ACC, SUP) launch_two<T, FL, ACC, SUP>(grid, ctx, a)
+#define L2S(FL, ACC) do { if (sup == SUP_GATHER) L2(FL, ACC, SUP_GATHER); \
+                          else if (sup == SUP_INJECT) L2(FL, ACC, SUP_INJECT); \
+                          else L2(FL, ACC, SUP_NONE); } while (0)
+    if (ctx->flavor == RHO_SCALED) { if (sp.acc) L2S(RHO_SCALED, true); else L2S(RHO_SCALED, false); }
+    else { if (sp.acc) L2S(ACOUSTIC, true); else L2S(ACOUSTIC, false); }
+#undef L2S
+#undef L2
+    if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
+    ctx->launches++;
+    ctx->step_launches++;
+    ctx->pair_launches++;
+    CK(cudaGetLastError());
+    ctx->prv = x[0];
+    ctx->cur = x[1];
+    return WO_OK;
+}
+
 template <typename T>
 int inject_host_list(wo_ctx* ctx, int n, const long long* idx, const double* vals) {
     // > MAX_SRC nodes: separate injection kernel after the step (no kernel
@@ -499,10 +637,34 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
                 (!gather || ctx->store_bytes >= (size_t)N * ctx->n_sup * sizeof(T)),
             "sweep not initialised (first range must start at n = 1)");
     std::vector<double> vals(std::max(ns, 1));
+    auto fcheck = [&](int64_t n) { return (n % STABILITY_CHECK_INTERVAL == 0) || (n == N - 1); };
+    const bool pairs = ns <= MAX_SRC && !record && pair_ready(ctx);
+    std::vector<double> vals2(std::max(ns, 1));
     for (int64_t n = n_begin; n < n_end; ++n) {
+        if (pairs && n + 1 < n_end) {   // steps n and n+1 in one pass
+            PairSpec ps;
+            ps.acc = accumulate != 0;
+            ps.check1 = fcheck(n);
+            ps.check2 = fcheck(n + 1);
+            ps.sdt = -dt;
+            for (int s = 0; s < ns; ++s) {
+                vals[s] = src_amp[(int64_t)spos[s] * N + n];
+                vals2[s] = src_amp[(int64_t)spos[s] * N + n + 1];
+            }
+            ps.n_src = ns;
+            ps.src_flat = sidx.data();
+            ps.val1 = vals.data();
+            ps.val2 = vals2.data();
+            ps.sup_mode = gather ? SUP_GATHER : SUP_NONE;
+            ps.row1 = n; ps.row2 = n + 1; ps.slot1 = n; ps.slot2 = n + 1;
+            rc = launch_pair<T>(ctx, ps);
+            if (rc) return rc;
+            ++n;
+            continue;
+        }
         StepSpec sp;
         sp.acc = accumulate != 0;
-        sp.check = (n % STABILITY_CHECK_INTERVAL == 0) || (n == N - 1);
+        sp.check = fcheck(n);
         sp.backward = 0;
         sp.sdt = -dt;
         for (int s = 0; s < ns; ++s) vals[s] = src_amp[(int64_t)spos[s] * N + n];
@@ -536,7 +698,7 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
                 if (rc) return rc;
             }
         }
-        ctx->cur = 1 - ctx->cur;  // rotate (u^{n+1} was written over u^{n-1})
+        std::swap(ctx->cur, ctx->prv);  // rotate (u^{n+1} was written over u^{n-1})
     }
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->prof) harvest_events(ctx);
@@ -575,15 +737,39 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
         rc = ensure_slots(ctx, N);
         if (rc) return rc;
         CK(cudaMemsetAsync(ctx->maxslots, 0, (size_t)(N + 2) * 8, ctx->stream));
-        ctx->cur = 1 - ctx->cur;  // swap_direction: u_prev <- u^N, u_cur <- u^{N-1}
+        std::swap(ctx->cur, ctx->prv);  // swap_direction: u_prev <- u^N, u_cur <- u^{N-1}
     }
     REQUIRE(ctx->maxslot_bytes >= (size_t)(N + 2) * 8, "sweep not initialised");
     long long sf = (long long)src_flat;
     double val = 0.0;
+    auto bcheck = [](int64_t n) { return (n % STABILITY_CHECK_INTERVAL == 0) || (n == 1); };
+    const bool pairs = pair_ready(ctx);
+    double val2 = 0.0;
     for (int64_t n = n_hi; n > n_lo; --n) {
+        if (pairs && n - 1 > n_lo) {   // steps n and n-1 in one pass
+            PairSpec ps;
+            ps.acc = accumulate != 0;
+            ps.check1 = bcheck(n);
+            ps.check2 = bcheck(n - 1);
+            ps.sdt = dt;
+            if (src_flat >= 0) {
+                val = src_amp[n];
+                val2 = src_amp[n - 1];
+                ps.n_src = 1;
+                ps.src_flat = &sf;
+                ps.val1 = &val;
+                ps.val2 = &val2;
+            }
+            ps.sup_mode = inject ? SUP_INJECT : SUP_NONE;
+            ps.row1 = n; ps.row2 = n - 1; ps.slot1 = n; ps.slot2 = n - 1;
+            rc = launch_pair<T>(ctx, ps);
+            if (rc) return rc;
+            --n;
+            continue;
+        }
         StepSpec sp;
         sp.acc = accumulate != 0;
-        sp.check = (n % STABILITY_CHECK_INTERVAL == 0) || (n == 1);
+        sp.check = bcheck(n);
         sp.backward = 1;
         sp.sdt = dt;
         if (src_flat >= 0) {
@@ -597,7 +783,7 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
         sp.slot = n;
         rc = launch_step<T>(ctx, sp);
         if (rc) return rc;
-        ctx->cur = 1 - ctx->cur;
+        std::swap(ctx->cur, ctx->prv);
     }
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->prof) harvest_events(ctx);
@@ -723,7 +909,7 @@ int step_t(wo_ctx* ctx, int64_t n_force, const int64_t* idx, const double* vals,
         ctx->launches++;
         CK(cudaGetLastError());
     }
-    ctx->cur = 1 - ctx->cur;
+    std::swap(ctx->cur, ctx->prv);
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->prof) harvest_events(ctx);
     if (want_max && max_out) {
@@ -948,7 +1134,7 @@ void wo_destroy(wo_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    void* bufs[] = {ctx->gamma, ctx->u[0], ctx->u[1], ctx->acc, ctx->mask, ctx->prefix,
+    void* bufs[] = {ctx->gamma, ctx->u[0], ctx->u[1], ctx->u[2], ctx->u[3], ctx->acc, ctx->mask, ctx->prefix,
                     ctx->store, ctx->measured, ctx->partial, ctx->cost, ctx->maxslots,
                     ctx->f_idx, ctx->f_vals, ctx->f_dense, ctx->hist, ctx->u3};
     for (void* b : bufs)
@@ -986,8 +1172,12 @@ int wo_set_option(wo_ctx* ctx, int option, int value) {
     int rc = check_ctx(ctx);
     if (rc) return rc;
     REQUIRE(option == WO_OPT_FAST_DIV || option == WO_OPT_PAIR_KERNEL ||
-                option == WO_OPT_TMA_KERNEL,
+                option == WO_OPT_TMA_KERNEL || option == WO_OPT_TWO_STEP,
             "unknown option");
+    if (option == WO_OPT_TWO_STEP) {
+        ctx->use_two_step = value != 0;
+        return WO_OK;
+    }
     if (option == WO_OPT_PAIR_KERNEL) {
         ctx->use_pair = value != 0;
         return WO_OK;
@@ -1046,8 +1236,8 @@ int wo_reset_window(wo_ctx* ctx) {
     int rc = check_ctx(ctx);
     if (rc) return rc;
     const size_t ab = (size_t)ctx->alloc_cells() * ctx->itemsize;
-    CK(cudaMemsetAsync(ctx->u[0], 0, ab, ctx->stream));
-    CK(cudaMemsetAsync(ctx->u[1], 0, ab, ctx->stream));
+    CK(cudaMemsetAsync(ctx->u[ctx->cur], 0, ab, ctx->stream));
+    CK(cudaMemsetAsync(ctx->u[ctx->prv], 0, ab, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return WO_OK;
 }
@@ -1071,7 +1261,7 @@ int wo_get_window(wo_ctx* ctx, void* u_prev, void* u_cur) {
 
 int wo_swap_direction(wo_ctx* ctx) {
     if (!ctx) return WO_ERR_CONFIG;
-    ctx->cur = 1 - ctx->cur;
+    std::swap(ctx->cur, ctx->prv);
     return WO_OK;
 }
 
@@ -1273,12 +1463,14 @@ int wo_stats(wo_ctx* ctx, int64_t* launches, int64_t* step_launches, double* ste
 
 int wo_reset_stats(wo_ctx* ctx) {
     if (!ctx) return WO_ERR_CONFIG;
-    ctx->launches = ctx->step_launches = 0;
+    ctx->launches = ctx->step_launches = ctx->pair_launches = 0;
     ctx->step_ms = 0.0;
     return WO_OK;
 }
 
 int64_t wo_device_bytes(const wo_ctx* ctx) { return ctx ? ctx->dev_bytes : 0; }
+
+int64_t wo_pair_launches(const wo_ctx* ctx) { return ctx ? ctx->pair_launches : 0; }
 
 int wo_timer_mark(wo_ctx* ctx, int idx) {
     int rc = check_ctx(ctx);

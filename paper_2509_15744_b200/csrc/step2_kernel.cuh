@@ -1,0 +1,580 @@
+// Two time steps per HBM pass (temporal blocking) on whole-tile grids.
+//
+// One launch advances the window by TWO steps, n and n+1 (forward: n, n+1;
+// backward: n, n-1), each with the exact per-cell arithmetic of step_kernel
+// (stencil, injections, support gather/inject, self-kernel increment,
+// stability max — see step_kernel.cuh for the reference mapping and the
+// mirrored-boundary argument).  Per plane p of the 2.5D march:
+//   a  wait for plane p+1 (TMA ring), m(p+1) on the tile + 2-cell ring
+//   b  __syncthreads
+//   d  step n at plane p on the tile AND a one-cell ring around it (the ring
+//      is recomputed redundantly so step n+1 never needs another CTA's data);
+//      u^{n+1}(p) goes to a shared-memory plane X
+//   c  step n+1 at plane p-1 on the tile, from X(p-1), the register queue of
+//      u^{n+1}, and the material coefficients kept from step n's plane p-1
+//   e  face weights of plane p+1 (registers)
+// HBM traffic per fp32 cell-update: (read u^{n-1}, u^n, gamma, acc + write
+// u^{n+1}, u^{n+2}, acc) / 2 = 14 B instead of 24 B, and m, coef and the face
+// weights are computed once for both steps.  u^{n+1} and u^{n+2} go to two
+// fresh buffers (other CTAs still read u^{n-1} / u^n rings), so the window
+// rotates through four level buffers.  Single-domain contexts only (a slab
+// would need ghost planes two deep).
+#pragma once
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "step_kernel.cuh"
+#include "step_kernel_tma.cuh"
+#include "step_kernel_v2.cuh"
+
+namespace wb {
+
+constexpr int T2_THREADS = 128;
+constexpr int T2_NS = 4;             // TMA ring stages
+constexpr int R2_H = BY + 4;         // rows j0-2 .. j0+9
+constexpr int R1_H = BY + 2;         // rows j0-1 .. j0+8
+constexpr int NRING = 2 * (PBX + 2) + 2 * BY;   // one-cell ring around a 64 x 8 tile
+
+template <typename T> struct Step2Args {
+    const T* gamma;
+    const T* u_prev;   // u^{n-1}
+    const T* u_cur;    // u^n
+    T* out1;           // u^{n+1}
+    T* out2;           // u^{n+2}
+    T* acc;
+    int n0, n1, n2, chunk;
+    MatScalars<T> mat;
+    T cv, cg, inv2dt, inv2dx, sdt;
+    int n_src;
+    int src_i[MAX_SRC], src_j[MAX_SRC], src_k[MAX_SRC];
+    T src_val1[MAX_SRC], src_val2[MAX_SRC];   // amplitudes of the two steps
+    int sup_lo, sup_hi;
+    const unsigned int* sup_mask;
+    const int* sup_prefix;
+    T* row1;           // store row of step 1 (gather: u^n; inject: adj of step 1)
+    T* row2;           // store row of step 2 (gather: u^{n+1}; inject: adj of step 2)
+    int check1, check2;
+    typename FTraits<T>::Bits* max1;
+    typename FTraits<T>::Bits* max2;
+};
+
+struct Tma2Maps {
+    CUtensorMap u_r2[4];   // level buffers, (W, R2_H) boxes at (k0-HO, j0-2)
+    CUtensorMap u_r1[4];   // level buffers, (W, R1_H) boxes at (k0-HO, j0-1)
+    CUtensorMap g_r2;      // gamma, (W, R2_H)
+    CUtensorMap a_ctr;     // accumulator, (PBX, BY)
+    int prev, cur;         // buffer indices of u^{n-1}, u^n
+};
+
+template <typename T> struct Tma2Stage {
+    alignas(128) T U[R2_H][th_w<T>()];
+    alignas(128) T G[R2_H][th_w<T>()];
+    alignas(128) T P[R1_H][th_w<T>()];
+    alignas(128) T A[BY][PBX];
+};
+
+template <typename T>
+constexpr size_t step2_smem_bytes() {
+    return T2_NS * sizeof(Tma2Stage<T>) + 2 * sizeof(T) * R2_H * th_w<T>() /* m planes */ +
+           2 * sizeof(T) * R2_H * th_w<T>() /* u^{n+1} planes */ +
+           T2_NS * sizeof(unsigned long long) + 128;
+}
+
+template <typename T, int FLAVOR, bool FAST, bool ACC, int SUP>
+__global__ void __launch_bounds__(T2_THREADS, sizeof(T) == 4 ? 3 : 1)
+step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__ Tma2Maps maps) {
+    using Tr = FTraits<T>;
+    using MT = Mat<T, FLAVOR, FAST>;
+    using V = typename Pair<T>::V;
+    using Bits = typename Tr::Bits;
+    constexpr int W = th_w<T>(), HO = th_ho<T>();
+    extern __shared__ __align__(128) unsigned char smem_dyn[];
+    unsigned char* smem_raw =
+        smem_dyn + ((128u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_dyn)) & 127u)) & 127u);
+    Tma2Stage<T>* st = reinterpret_cast<Tma2Stage<T>*>(smem_raw);
+    T(*SM)[R2_H][W] = reinterpret_cast<T(*)[R2_H][W]>(smem_raw + T2_NS * sizeof(Tma2Stage<T>));
+    T(*X)[R2_H][W] = reinterpret_cast<T(*)[R2_H][W]>(smem_raw + T2_NS * sizeof(Tma2Stage<T>) +
+                                                     2 * sizeof(T) * R2_H * W);
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(
+        smem_raw + T2_NS * sizeof(Tma2Stage<T>) + 4 * sizeof(T) * R2_H * W);
+    __shared__ Bits smax[2][T2_THREADS / 32];
+
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = ty * 32 + tx;
+    const int k0 = blockIdx.x * PBX, j0 = blockIdx.y * BY;
+    const int kA = k0 + 2 * tx, ja = j0 + 2 * ty;
+    const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
+    const int plane = n1 * n2;
+    const int i0 = blockIdx.z * a.chunk;
+    const int i1 = min(i0 + a.chunk, n0);
+    const int pbeg = max(i0 - 1, 0);           // step-n planes of this chunk
+    const int pfin = min(i1, n0 - 1);
+    const MatScalars<T>& M = a.mat;
+
+    // ---- geometry in the R2 frame (rows j0-2.., cols k0-HO..) ----
+    auto rowc = [&](int jj) { return min(max(jj, 0), n1 - 1) - j0 + 2; };
+    auto colc = [&](int kk) { return min(max(kk, 0), n2 - 1) - k0 + HO; };
+    const int ra = 2 * ty + 2, rb = ra + 1, cA = HO + 2 * tx;
+    const int rU = rowc(ja - 1), rD = rowc(ja + 2), cL = colc(kA - 1), cR = colc(kA + 2);
+    // ring cells: q = tid and q = tid + 128 (< NRING)
+    int rg_r[2], rg_c[2], rg_u[2], rg_d[2], rg_l[2], rg_rr[2];
+    bool rg_ok[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const int q = tid + t * T2_THREADS;
+        int jj = 0, kk = 0;
+        if (q < PBX + 2) { jj = j0 - 1; kk = k0 - 1 + q; }
+        else if (q < 2 * (PBX + 2)) { jj = j0 + BY; kk = k0 - 1 + (q - (PBX + 2)); }
+        else if (q < 2 * (PBX + 2) + BY) { jj = j0 + (q - 2 * (PBX + 2)); kk = k0 - 1; }
+        else { jj = j0 + (q - 2 * (PBX + 2) - BY); kk = k0 + PBX; }
+        rg_ok[t] = q < NRING && jj >= 0 && jj < n1 && kk >= 0 && kk < n2;
+        rg_r[t] = rowc(jj); rg_c[t] = colc(kk);
+        rg_u[t] = rowc(jj - 1); rg_d[t] = rowc(jj + 1);
+        rg_l[t] = colc(kk - 1); rg_rr[t] = colc(kk + 1);
+    }
+
+    unsigned my_src = 0;   // sources in tile + ring and the step-n plane range
+    for (int s = 0; s < a.n_src; ++s)
+        if (a.src_i[s] >= pbeg && a.src_i[s] <= pfin && a.src_j[s] >= j0 - 1 &&
+            a.src_j[s] <= j0 + BY && a.src_k[s] >= k0 - 1 && a.src_k[s] <= k0 + PBX)
+            my_src |= 1u << s;
+
+    constexpr unsigned STAGE_BYTES =
+        (unsigned)(sizeof(T) * ((2 * R2_H + R1_H) * W + (ACC ? BY * PBX : 0)));
+    const CUtensorMap* mU = pick_map(maps.u_r2, maps.cur);
+    const CUtensorMap* mP = pick_map(maps.u_r1, maps.prev);
+    auto issue = [&](int p) {
+        const int s = (p - pbeg) % T2_NS;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar[s], STAGE_BYTES);
+        tma_load_3d(&st[s].U[0][0], mU, k0 - HO, j0 - 2, p, &bar[s]);
+        tma_load_3d(&st[s].G[0][0], &maps.g_r2, k0 - HO, j0 - 2, p, &bar[s]);
+        tma_load_3d(&st[s].P[0][0], mP, k0 - HO, j0 - 1, p, &bar[s]);
+        if (ACC) tma_load_3d(&st[s].A[0][0], &maps.a_ctr, k0, j0, p, &bar[s]);
+    };
+    auto wait_plane = [&](int p) {
+        const int n = p - pbeg;
+        mbar_wait(&bar[n % T2_NS], (unsigned)((n / T2_NS) & 1));
+    };
+    if (tid == 0) {
+        for (int s = 0; s < T2_NS; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int p = pbeg; p <= min(pbeg + T2_NS - 1, pfin); ++p) issue(p);
+
+    auto ldv = [](const T* p) { return *reinterpret_cast<const V*>(p); };
+    auto stv = [](T* p, V v) { *reinterpret_cast<V*>(p) = v; };
+    auto face = [](T lo, T hi) { return MT::face(lo, hi); };
+
+    // m of the R2 region of a plane (uniform loop, no role divergence)
+    auto mplane = [&](const T (*G)[W], T (*D)[W]) {
+        for (int c = tid; c < R2_H * (PBX + 4); c += T2_THREADS) {
+            const int r = c / (PBX + 4), cc = HO - 2 + c % (PBX + 4);
+            D[r][cc] = MT::m(M, G[r][cc]);
+        }
+    };
+
+    // own faces of a plane (2x2 block) from its m-plane
+    struct Faces { T kLa, kIa, kRa, kLb, kIb, kRb; V jlo, jab, jhi; };
+    auto own_faces = [&](const T (*sm)[W]) {
+        Faces f;
+        const V ma = ldv(&sm[ra][cA]), mb = ldv(&sm[rb][cA]);
+        f.kLa = face(sm[ra][cL], ma.x); f.kIa = face(ma.x, ma.y); f.kRa = face(ma.y, sm[ra][cR]);
+        f.kLb = face(sm[rb][cL], mb.x); f.kIb = face(mb.x, mb.y); f.kRb = face(mb.y, sm[rb][cR]);
+        const V mu = ldv(&sm[rU][cA]), md = ldv(&sm[rD][cA]);
+        f.jlo = V{face(mu.x, ma.x), face(mu.y, ma.y)};
+        f.jab = V{face(ma.x, mb.x), face(ma.y, mb.y)};
+        f.jhi = V{face(mb.x, md.x), face(mb.y, md.y)};
+        return f;
+    };
+    // ring-cell in-plane faces (k lo, k hi, j lo, j hi)
+    struct RFaces { T kl, kh, jl, jh; };
+    auto ring_faces = [&](const T (*sm)[W], int t) {
+        RFaces f;
+        const T m = sm[rg_r[t]][rg_c[t]];
+        f.kl = face(sm[rg_r[t]][rg_l[t]], m); f.kh = face(m, sm[rg_r[t]][rg_rr[t]]);
+        f.jl = face(sm[rg_u[t]][rg_c[t]], m); f.jh = face(m, sm[rg_d[t]][rg_c[t]]);
+        return f;
+    };
+
+    auto cell = [&](T u0, T up1, T um1, T ujp, T ujm, T ukp, T ukm, T w0hi, T w0lo, T fjhi, T fjlo,
+                    T fkhi, T fklo, T coef, T up) {
+        T s = u0 - u0;
+        s += (up1 - u0) * w0hi;
+        s -= (u0 - um1) * w0lo;
+        s += (ujp - u0) * fjhi;
+        s -= (u0 - ujm) * fjlo;
+        s += (ukp - u0) * fkhi;
+        s -= (u0 - ukm) * fklo;
+        return ((u0 + u0) - up) + coef * s;
+    };
+    auto kinc = [&](T accv, T out, T up, T up1, T um1, T ujp, T ujm, T ukp, T ukm) {
+        const T va = (out - up) * a.inv2dt;    // sign-invariant: (cv*va)*va
+        const T g0 = (up1 - um1) * a.inv2dx;
+        const T g1 = (ujp - ujm) * a.inv2dx;
+        const T g2 = (ukp - ukm) * a.inv2dx;
+        return accv + a.sdt * ((a.cv * va) * va + a.cg * (((g0 * g0) + (g1 * g1)) + (g2 * g2)));
+    };
+    // nodal sources at (plane, j, k) for the step's amplitudes
+    auto inject_src = [&](int p, int jj, int kk, T g, T kap, const T* val, T& o) {
+        for (int q = 0; q < a.n_src; ++q)
+            if (((my_src >> q) & 1u) && p == a.src_i[q] && jj == a.src_j[q] && kk == a.src_k[q])
+                o = o + MT::fc(M, g, kap) * val[q];
+    };
+    // support bit / compact index of cell (p, jj, kk)
+    auto sup_index = [&](int p, int jj, int kk) -> int {
+        if (SUP == SUP_NONE || p < a.sup_lo || p > a.sup_hi) return -1;
+        const unsigned flat = (unsigned)(p * plane + jj * n2 + kk);
+        const unsigned w = __ldg(a.sup_mask + (flat >> 5));
+        const unsigned bit = flat & 31u;
+        if (!((w >> bit) & 1u)) return -1;
+        return __ldg(a.sup_prefix + (flat >> 5)) + __popc(w & ((1u << bit) - 1u));
+    };
+
+    // ---------------- prologue: plane pbeg ----------------
+    const int cofs = ja * n2 + kA;
+    const bool has_m0 = pbeg > 0;
+    V unm_a, unm_b, gm_a, gm_b;                  // plane pbeg-1 (mirror at 0)
+    if (has_m0) {
+        unm_a = __ldg(reinterpret_cast<const V*>(a.u_cur + (pbeg - 1) * plane + cofs));
+        unm_b = __ldg(reinterpret_cast<const V*>(a.u_cur + (pbeg - 1) * plane + cofs + n2));
+        gm_a = __ldg(reinterpret_cast<const V*>(a.gamma + (pbeg - 1) * plane + cofs));
+        gm_b = __ldg(reinterpret_cast<const V*>(a.gamma + (pbeg - 1) * plane + cofs + n2));
+    }
+    T rum[2] = {T(0), T(0)}, rgm[2] = {T(1), T(1)};
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+        if (has_m0 && rg_ok[t]) {
+            const int jj = rg_r[t] + j0 - 2, kk = rg_c[t] + k0 - HO;
+            rum[t] = __ldg(a.u_cur + (pbeg - 1) * plane + jj * n2 + kk);
+            rgm[t] = __ldg(a.gamma + (pbeg - 1) * plane + jj * n2 + kk);
+        }
+    wait_plane(pbeg);
+    const int s0 = 0;
+    V un0_a = ldv(&st[s0].U[ra][cA]), un0_b = ldv(&st[s0].U[rb][cA]);
+    V g0_a = ldv(&st[s0].G[ra][cA]), g0_b = ldv(&st[s0].G[rb][cA]);
+    T run0[2], rg0[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) { run0[t] = st[s0].U[rg_r[t]][rg_c[t]]; rg0[t] = st[s0].G[rg_r[t]][rg_c[t]]; }
+    if (!has_m0) {
+        unm_a = un0_a; unm_b = un0_b; gm_a = g0_a; gm_b = g0_b;
+        rum[0] = run0[0]; rum[1] = run0[1]; rgm[0] = rg0[0]; rgm[1] = rg0[1];
+    }
+    V m0_a = {MT::m(M, g0_a.x), MT::m(M, g0_a.y)}, m0_b = {MT::m(M, g0_b.x), MT::m(M, g0_b.y)};
+    V w0_a = {face(MT::m(M, gm_a.x), m0_a.x), face(MT::m(M, gm_a.y), m0_a.y)};
+    V w0_b = {face(MT::m(M, gm_b.x), m0_b.x), face(MT::m(M, gm_b.y), m0_b.y)};
+    T rm0[2], rw0[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) { rm0[t] = MT::m(M, rg0[t]); rw0[t] = face(MT::m(M, rgm[t]), rm0[t]); }
+    mplane(st[s0].G, SM[0]);
+    __syncthreads();
+    Faces F0 = own_faces(SM[0]);
+    RFaces RF0[2] = {ring_faces(SM[0], 0), ring_faces(SM[0], 1)};
+
+    // step n+1 state: material of the previous step-n plane, u^{n+1} queue
+    Faces F1 = F0;
+    V w1lo_a = w0_a, w1lo_b = w0_b, w1hi_a = w0_a, w1hi_b = w0_b;
+    T c1[4] = {T(0), T(0), T(0), T(0)}, kap1[4] = {T(0), T(0), T(0), T(0)};
+    V g1_a = g0_a, g1_b = g0_b;
+    V x_m1a = un0_a, x_m1b = un0_b, x_0a = un0_a, x_0b = un0_b;   // u^{n+1}(p-2), (p-1)
+    V un1_a = unm_a, un1_b = unm_b;                                // u^n(p-1)
+    V acc1_a = {T(0), T(0)}, acc1_b = acc1_a;                      // acc after step n at p-1
+    Bits lmax1 = 0, lmax2 = 0;
+
+    for (int p = pbeg; p <= pfin; ++p) {
+        const int sc = (p - pbeg) % T2_NS, sn = (p + 1 - pbeg) % T2_NS;
+        const int b = (p - pbeg) & 1, nb = b ^ 1;
+        const bool have_p1 = p + 1 <= pfin;         // step n needs plane p+1 (or mirror)
+        const bool exists_p1 = p + 1 <= n0 - 1;
+        // ---- a: plane p+1 ----
+        V unp_a = un0_a, unp_b = un0_b, gp_a = g0_a, gp_b = g0_b;
+        T runp[2] = {run0[0], run0[1]}, rgp[2] = {rg0[0], rg0[1]};
+        if (exists_p1) {
+            if (have_p1) {
+                wait_plane(p + 1);
+                unp_a = ldv(&st[sn].U[ra][cA]); unp_b = ldv(&st[sn].U[rb][cA]);
+                gp_a = ldv(&st[sn].G[ra][cA]); gp_b = ldv(&st[sn].G[rb][cA]);
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    runp[t] = st[sn].U[rg_r[t]][rg_c[t]];
+                    rgp[t] = st[sn].G[rg_r[t]][rg_c[t]];
+                }
+                mplane(st[sn].G, SM[nb]);
+            } else {   // chunk end inside the domain: plane p+1 straight from HBM
+                unp_a = __ldg(reinterpret_cast<const V*>(a.u_cur + (p + 1) * plane + cofs));
+                unp_b = __ldg(reinterpret_cast<const V*>(a.u_cur + (p + 1) * plane + cofs + n2));
+                gp_a = __ldg(reinterpret_cast<const V*>(a.gamma + (p + 1) * plane + cofs));
+                gp_b = __ldg(reinterpret_cast<const V*>(a.gamma + (p + 1) * plane + cofs + n2));
+#pragma unroll
+                for (int t = 0; t < 2; ++t)
+                    if (rg_ok[t]) {
+                        const int jj = rg_r[t] + j0 - 2, kk = rg_c[t] + k0 - HO;
+                        runp[t] = __ldg(a.u_cur + (p + 1) * plane + jj * n2 + kk);
+                        rgp[t] = __ldg(a.gamma + (p + 1) * plane + jj * n2 + kk);
+                    }
+            }
+        }
+        const V mp_a = {MT::m(M, gp_a.x), MT::m(M, gp_a.y)};
+        const V mp_b = {MT::m(M, gp_b.x), MT::m(M, gp_b.y)};
+        T rmp[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) rmp[t] = MT::m(M, rgp[t]);
+        __syncthreads();
+        if (tid == 0 && p > pbeg && p - 1 + T2_NS <= pfin) issue(p - 1 + T2_NS);
+
+        // ---- d: step n at plane p (tile + ring) -> X[b] ----
+        const Tma2Stage<T>& S = st[sc];
+        const V wh_a = {face(m0_a.x, mp_a.x), face(m0_a.y, mp_a.y)};
+        const V wh_b = {face(m0_b.x, mp_b.x), face(m0_b.y, mp_b.y)};
+        T kp[4];
+        const T cf[4] = {MT::coef(M, g0_a.x, kp[0]), MT::coef(M, g0_a.y, kp[1]),
+                         MT::coef(M, g0_b.x, kp[2]), MT::coef(M, g0_b.y, kp[3])};
+        const V uu = ldv(&S.U[rU][cA]), ud = ldv(&S.U[rD][cA]);
+        const T uLa = S.U[ra][cL], uRa = S.U[ra][cR], uLb = S.U[rb][cL], uRb = S.U[rb][cR];
+        const V pa = ldv(&S.P[ra - 1][cA]), pb = ldv(&S.P[rb - 1][cA]);
+        V oa, ob;
+        oa.x = cell(un0_a.x, unp_a.x, unm_a.x, un0_b.x, uu.x, un0_a.y, uLa, wh_a.x, w0_a.x,
+                    F0.jab.x, F0.jlo.x, F0.kIa, F0.kLa, cf[0], pa.x);
+        oa.y = cell(un0_a.y, unp_a.y, unm_a.y, un0_b.y, uu.y, uRa, un0_a.x, wh_a.y, w0_a.y,
+                    F0.jab.y, F0.jlo.y, F0.kRa, F0.kIa, cf[1], pa.y);
+        ob.x = cell(un0_b.x, unp_b.x, unm_b.x, ud.x, un0_a.x, un0_b.y, uLb, wh_b.x, w0_b.x,
+                    F0.jhi.x, F0.jab.x, F0.kIb, F0.kLb, cf[2], pb.x);
+        ob.y = cell(un0_b.y, unp_b.y, unm_b.y, ud.y, un0_a.y, uRb, un0_b.x, wh_b.y, w0_b.y,
+                    F0.jhi.y, F0.jab.y, F0.kRb, F0.kIb, cf[3], pb.y);
+        if (my_src) {
+            inject_src(p, ja, kA, g0_a.x, kp[0], a.src_val1, oa.x);
+            inject_src(p, ja, kA + 1, g0_a.y, kp[1], a.src_val1, oa.y);
+            inject_src(p, ja + 1, kA, g0_b.x, kp[2], a.src_val1, ob.x);
+            inject_src(p, ja + 1, kA + 1, g0_b.y, kp[3], a.src_val1, ob.y);
+        }
+        const bool own_plane = p >= i0 && p < i1;
+        if (SUP != SUP_NONE) {
+            const T uo[4] = {un0_a.x, un0_a.y, un0_b.x, un0_b.y};
+            T* oo[4] = {&oa.x, &oa.y, &ob.x, &ob.y};
+            const T gg[4] = {g0_a.x, g0_a.y, g0_b.x, g0_b.y};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int q = sup_index(p, ja + (c >> 1), kA + (c & 1));
+                if (q >= 0) {
+                    if (SUP == SUP_GATHER) { if (own_plane) a.row1[q] = uo[c]; }
+                    else *oo[c] = *oo[c] + MT::fc(M, gg[c], kp[c]) * ldg(a.row1 + q);
+                }
+            }
+        }
+        stv(&X[b][ra][cA], oa);
+        stv(&X[b][rb][cA], ob);
+        V nacc_a = acc1_a, nacc_b = acc1_b;
+        if (own_plane) {
+            if (ACC) {
+                const V aa = ldv(&S.A[2 * ty][2 * tx]), ab = ldv(&S.A[2 * ty + 1][2 * tx]);
+                nacc_a.x = kinc(aa.x, oa.x, pa.x, unp_a.x, unm_a.x, un0_b.x, uu.x, un0_a.y, uLa);
+                nacc_a.y = kinc(aa.y, oa.y, pa.y, unp_a.y, unm_a.y, un0_b.y, uu.y, uRa, un0_a.x);
+                nacc_b.x = kinc(ab.x, ob.x, pb.x, unp_b.x, unm_b.x, ud.x, un0_a.x, un0_b.y, uLb);
+                nacc_b.y = kinc(ab.y, ob.y, pb.y, unp_b.y, unm_b.y, ud.y, un0_a.y, uRb, un0_b.x);
+            }
+            if (a.check1) {
+                Bits m1 = Tr::abs_bits(oa.x), m2 = Tr::abs_bits(oa.y);
+                Bits m3 = Tr::abs_bits(ob.x), m4 = Tr::abs_bits(ob.y);
+                m1 = m1 > m2 ? m1 : m2; m3 = m3 > m4 ? m3 : m4; m1 = m1 > m3 ? m1 : m3;
+                lmax1 = m1 > lmax1 ? m1 : lmax1;
+            }
+        }
+        // ring cells (step n only, no accumulation / gather)
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            if (!rg_ok[t]) continue;
+            const int r = rg_r[t], c = rg_c[t];
+            const T u0 = run0[t];
+            T kap;
+            const T coef = MT::coef(M, rg0[t], kap);
+            T o = cell(u0, runp[t], rum[t], S.U[rg_d[t]][c], S.U[rg_u[t]][c], S.U[r][rg_rr[t]],
+                       S.U[r][rg_l[t]], face(rm0[t], rmp[t]), rw0[t], RF0[t].jh, RF0[t].jl,
+                       RF0[t].kh, RF0[t].kl, coef, S.P[r - 1][c]);
+            const int jj = r + j0 - 2, kk = c + k0 - HO;
+            if (my_src) inject_src(p, jj, kk, rg0[t], kap, a.src_val1, o);
+            if (SUP == SUP_INJECT) {
+                const int q = sup_index(p, jj, kk);
+                if (q >= 0) o = o + MT::fc(M, rg0[t], kap) * ldg(a.row1 + q);
+            }
+            X[b][r][c] = o;
+        }
+
+        // ---- c: step n+1 at plane p-1 (tile) ----
+        const int q1 = p - 1;
+        if (q1 >= i0 && q1 < i1) {
+            const T (*Xq)[W] = X[nb];                  // u^{n+1}(p-1) with its ring
+            const V xu = ldv(&Xq[rU][cA]), xd = ldv(&Xq[rD][cA]);
+            const T xLa = Xq[ra][cL], xRa = Xq[ra][cR], xLb = Xq[rb][cL], xRb = Xq[rb][cR];
+            V o2a, o2b;
+            o2a.x = cell(x_0a.x, oa.x, x_m1a.x, x_0b.x, xu.x, x_0a.y, xLa, w1hi_a.x, w1lo_a.x,
+                         F1.jab.x, F1.jlo.x, F1.kIa, F1.kLa, c1[0], un1_a.x);
+            o2a.y = cell(x_0a.y, oa.y, x_m1a.y, x_0b.y, xu.y, xRa, x_0a.x, w1hi_a.y, w1lo_a.y,
+                         F1.jab.y, F1.jlo.y, F1.kRa, F1.kIa, c1[1], un1_a.y);
+            o2b.x = cell(x_0b.x, ob.x, x_m1b.x, xd.x, x_0a.x, x_0b.y, xLb, w1hi_b.x, w1lo_b.x,
+                         F1.jhi.x, F1.jab.x, F1.kIb, F1.kLb, c1[2], un1_b.x);
+            o2b.y = cell(x_0b.y, ob.y, x_m1b.y, xd.y, x_0a.y, xRb, x_0b.x, w1hi_b.y, w1lo_b.y,
+                         F1.jhi.y, F1.jab.y, F1.kRb, F1.kIb, c1[3], un1_b.y);
+            if (my_src) {
+                inject_src(q1, ja, kA, g1_a.x, kap1[0], a.src_val2, o2a.x);
+                inject_src(q1, ja, kA + 1, g1_a.y, kap1[1], a.src_val2, o2a.y);
+                inject_src(q1, ja + 1, kA, g1_b.x, kap1[2], a.src_val2, o2b.x);
+                inject_src(q1, ja + 1, kA + 1, g1_b.y, kap1[3], a.src_val2, o2b.y);
+            }
+            if (SUP != SUP_NONE) {
+                const T xo[4] = {x_0a.x, x_0a.y, x_0b.x, x_0b.y};
+                T* oo[4] = {&o2a.x, &o2a.y, &o2b.x, &o2b.y};
+                const T gg[4] = {g1_a.x, g1_a.y, g1_b.x, g1_b.y};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int q = sup_index(q1, ja + (c >> 1), kA + (c & 1));
+                    if (q >= 0) {
+                        if (SUP == SUP_GATHER) a.row2[q] = xo[c];
+                        else *oo[c] = *oo[c] + MT::fc(M, gg[c], kap1[c]) * ldg(a.row2 + q);
+                    }
+                }
+            }
+            const int oc = q1 * plane + cofs;
+            if (ACC) {
+                V fa, fb;
+                fa.x = kinc(acc1_a.x, o2a.x, un1_a.x, oa.x, x_m1a.x, x_0b.x, xu.x, x_0a.y, xLa);
+                fa.y = kinc(acc1_a.y, o2a.y, un1_a.y, oa.y, x_m1a.y, x_0b.y, xu.y, xRa, x_0a.x);
+                fb.x = kinc(acc1_b.x, o2b.x, un1_b.x, ob.x, x_m1b.x, xd.x, x_0a.x, x_0b.y, xLb);
+                fb.y = kinc(acc1_b.y, o2b.y, un1_b.y, ob.y, x_m1b.y, xd.y, x_0a.y, xRb, x_0b.x);
+                stv(a.acc + oc, fa);
+                stv(a.acc + oc + n2, fb);
+            }
+            stv(a.out1 + oc, x_0a);
+            stv(a.out1 + oc + n2, x_0b);
+            stv(a.out2 + oc, o2a);
+            stv(a.out2 + oc + n2, o2b);
+            if (a.check2) {
+                Bits m1 = Tr::abs_bits(o2a.x), m2 = Tr::abs_bits(o2a.y);
+                Bits m3 = Tr::abs_bits(o2b.x), m4 = Tr::abs_bits(o2b.y);
+                m1 = m1 > m2 ? m1 : m2; m3 = m3 > m4 ? m3 : m4; m1 = m1 > m3 ? m1 : m3;
+                lmax2 = m1 > lmax2 ? m1 : lmax2;
+            }
+        }
+
+        // ---- e: faces of plane p+1; rotate ----
+        Faces Fn = F0;
+        RFaces RFn[2] = {RF0[0], RF0[1]};
+        if (p + 1 <= pfin && exists_p1 && have_p1) {
+            Fn = own_faces(SM[nb]);
+            RFn[0] = ring_faces(SM[nb], 0);
+            RFn[1] = ring_faces(SM[nb], 1);
+        }
+        // step-(n+1) material for plane p (used at the next iteration)
+        F1 = F0;
+        w1lo_a = w0_a; w1lo_b = w0_b; w1hi_a = wh_a; w1hi_b = wh_b;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { c1[c] = cf[c]; kap1[c] = kp[c]; }
+        g1_a = g0_a; g1_b = g0_b;
+        acc1_a = nacc_a; acc1_b = nacc_b;
+        un1_a = un0_a; un1_b = un0_b;
+        // u^{n+1} queue; at the global bottom plane the "previous" plane is
+        // the mirror (the plane itself)
+        x_m1a = p == 0 ? oa : x_0a; x_m1b = p == 0 ? ob : x_0b;
+        x_0a = oa; x_0b = ob;
+        // step-n queue
+        unm_a = un0_a; unm_b = un0_b; un0_a = unp_a; un0_b = unp_b;
+        g0_a = gp_a; g0_b = gp_b; m0_a = mp_a; m0_b = mp_b; w0_a = wh_a; w0_b = wh_b;
+        F0 = Fn;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            rw0[t] = face(rm0[t], rmp[t]);
+            rum[t] = run0[t]; run0[t] = runp[t]; rg0[t] = rgp[t]; rm0[t] = rmp[t];
+            RF0[t] = RFn[t];
+        }
+    }
+
+    // ---- step n+1 for the chunk's last plane when p+1 was beyond the grid ----
+    // (handled inside the loop: pfin = i1 for interior chunks; at the global
+    // end pfin = n0-1 = i1-1 and the mirrored plane n0 is the cell itself)
+    __syncthreads();                         // ring values of the last plane in X
+    if (pfin == i1 - 1) {
+        const int q1 = pfin;                 // step n+1 at the last plane, mirror above
+        const T (*Xq)[W] = X[(pfin - pbeg) & 1];
+        const V xu = ldv(&Xq[rU][cA]), xd = ldv(&Xq[rD][cA]);
+        const T xLa = Xq[ra][cL], xRa = Xq[ra][cR], xLb = Xq[rb][cL], xRb = Xq[rb][cR];
+        // after the rotation: x_0 = u^{n+1}(pfin), x_m1 = u^{n+1}(pfin-1); mirror x_p1 = x_0
+        V o2a, o2b;
+        o2a.x = cell(x_0a.x, x_0a.x, x_m1a.x, x_0b.x, xu.x, x_0a.y, xLa, w1hi_a.x, w1lo_a.x,
+                     F1.jab.x, F1.jlo.x, F1.kIa, F1.kLa, c1[0], un1_a.x);
+        o2a.y = cell(x_0a.y, x_0a.y, x_m1a.y, x_0b.y, xu.y, xRa, x_0a.x, w1hi_a.y, w1lo_a.y,
+                     F1.jab.y, F1.jlo.y, F1.kRa, F1.kIa, c1[1], un1_a.y);
+        o2b.x = cell(x_0b.x, x_0b.x, x_m1b.x, xd.x, x_0a.x, x_0b.y, xLb, w1hi_b.x, w1lo_b.x,
+                     F1.jhi.x, F1.jab.x, F1.kIb, F1.kLb, c1[2], un1_b.x);
+        o2b.y = cell(x_0b.y, x_0b.y, x_m1b.y, xd.y, x_0a.y, xRb, x_0b.x, w1hi_b.y, w1lo_b.y,
+                     F1.jhi.y, F1.jab.y, F1.kRb, F1.kIb, c1[3], un1_b.y);
+        if (my_src) {
+            inject_src(q1, ja, kA, g1_a.x, kap1[0], a.src_val2, o2a.x);
+            inject_src(q1, ja, kA + 1, g1_a.y, kap1[1], a.src_val2, o2a.y);
+            inject_src(q1, ja + 1, kA, g1_b.x, kap1[2], a.src_val2, o2b.x);
+            inject_src(q1, ja + 1, kA + 1, g1_b.y, kap1[3], a.src_val2, o2b.y);
+        }
+        if (SUP != SUP_NONE) {
+            const T xo[4] = {x_0a.x, x_0a.y, x_0b.x, x_0b.y};
+            T* oo[4] = {&o2a.x, &o2a.y, &o2b.x, &o2b.y};
+            const T gg[4] = {g1_a.x, g1_a.y, g1_b.x, g1_b.y};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int q = sup_index(q1, ja + (c >> 1), kA + (c & 1));
+                if (q >= 0) {
+                    if (SUP == SUP_GATHER) a.row2[q] = xo[c];
+                    else *oo[c] = *oo[c] + MT::fc(M, gg[c], kap1[c]) * ldg(a.row2 + q);
+                }
+            }
+        }
+        const int oc = q1 * plane + cofs;
+        if (ACC) {
+            V fa, fb;
+            fa.x = kinc(acc1_a.x, o2a.x, un1_a.x, x_0a.x, x_m1a.x, x_0b.x, xu.x, x_0a.y, xLa);
+            fa.y = kinc(acc1_a.y, o2a.y, un1_a.y, x_0a.y, x_m1a.y, x_0b.y, xu.y, xRa, x_0a.x);
+            fb.x = kinc(acc1_b.x, o2b.x, un1_b.x, x_0b.x, x_m1b.x, xd.x, x_0a.x, x_0b.y, xLb);
+            fb.y = kinc(acc1_b.y, o2b.y, un1_b.y, x_0b.y, x_m1b.y, xd.y, x_0a.y, xRb, x_0b.x);
+            stv(a.acc + oc, fa);
+            stv(a.acc + oc + n2, fb);
+        }
+        stv(a.out1 + oc, x_0a);
+        stv(a.out1 + oc + n2, x_0b);
+        stv(a.out2 + oc, o2a);
+        stv(a.out2 + oc + n2, o2b);
+        if (a.check2) {
+            Bits m1 = Tr::abs_bits(o2a.x), m2 = Tr::abs_bits(o2a.y);
+            Bits m3 = Tr::abs_bits(o2b.x), m4 = Tr::abs_bits(o2b.y);
+            m1 = m1 > m2 ? m1 : m2; m3 = m3 > m4 ? m3 : m4; m1 = m1 > m3 ? m1 : m3;
+            lmax2 = m1 > lmax2 ? m1 : lmax2;
+        }
+    }
+
+    if (a.check1 || a.check2) {
+        for (int o = 16; o > 0; o >>= 1) {
+            Bits v1 = __shfl_xor_sync(0xffffffffu, lmax1, o);
+            Bits v2 = __shfl_xor_sync(0xffffffffu, lmax2, o);
+            lmax1 = v1 > lmax1 ? v1 : lmax1;
+            lmax2 = v2 > lmax2 ? v2 : lmax2;
+        }
+        const int lane = tid & 31, warp = tid >> 5;
+        if (lane == 0) { smax[0][warp] = lmax1; smax[1][warp] = lmax2; }
+        __syncthreads();
+        if (warp == 0) {
+            Bits v1 = lane < (T2_THREADS / 32) ? smax[0][lane] : 0;
+            Bits v2 = lane < (T2_THREADS / 32) ? smax[1][lane] : 0;
+            for (int o = 16; o > 0; o >>= 1) {
+                Bits w1 = __shfl_xor_sync(0xffffffffu, v1, o);
+                Bits w2 = __shfl_xor_sync(0xffffffffu, v2, o);
+                v1 = w1 > v1 ? w1 : v1;
+                v2 = w2 > v2 ? w2 : v2;
+            }
+            if (lane == 0) {
+                if (a.check1 && v1) atomicMax(a.max1, v1);
+                if (a.check2 && v2) atomicMax(a.max2, v2);
+            }
+        }
+    }
+}
+
+}  // namespace wb

@@ -45,13 +45,23 @@ template <typename T> __host__ __device__ constexpr int th_w() { return PBX + 2 
 constexpr int TH_WMAX = PBX + 8;
 
 struct TmaMaps {
-    CUtensorMap u_halo[2];   // u buffers 0/1, (th_w, TH_H, 1) boxes
-    CUtensorMap u_ctr[2];    // u buffers 0/1, (PBX, BY, 1) boxes
+    CUtensorMap u_halo[4];   // level buffers 0..3, (th_w, TH_H, 1) boxes
+    CUtensorMap u_ctr[4];    // level buffers 0..3, (PBX, BY, 1) boxes
     CUtensorMap g_halo;      // gamma, (th_w, TH_H, 1)
     CUtensorMap a_ctr;       // accumulator, (PBX, BY, 1)
-    int cur;                 // index of the buffer holding u^n
+    int cur, prev;           // buffers holding u^n and u^{n-1}
     int lo;                  // ghost planes below plane 0 (map plane = p + lo)
 };
+
+// constant-offset selects keep a descriptor in parameter space
+__device__ __forceinline__ const CUtensorMap* pick_map(const CUtensorMap (&m)[4], int i) {
+    switch (i) {
+        case 1: return &m[1];
+        case 2: return &m[2];
+        case 3: return &m[3];
+        default: return &m[0];
+    }
+}
 
 template <typename T> struct TmaStage {   // every TMA destination 128-byte aligned
     alignas(128) T U[TH_H][th_w<T>()];
@@ -146,8 +156,8 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
 
     constexpr unsigned STAGE_BYTES = (unsigned)(sizeof(T) * (2 * TH_H * W + (ACC ? 2 : 1) * BY * PBX));
     // constant-offset selects keep the descriptors in parameter space
-    const CUtensorMap* mU = maps.cur ? &maps.u_halo[1] : &maps.u_halo[0];
-    const CUtensorMap* mP = maps.cur ? &maps.u_ctr[0] : &maps.u_ctr[1];
+    const CUtensorMap* mU = pick_map(maps.u_halo, maps.cur);
+    const CUtensorMap* mP = pick_map(maps.u_ctr, maps.prev);
     auto issue = [&](int p) {   // producer: plane p into its stage
         const int s = (p - i0) % TS;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -89,8 +89,8 @@ step_kernel_tma4(const __grid_constant__ StepArgs<T> a, const __grid_constant__ 
 
     constexpr unsigned STAGE_BYTES =
         (unsigned)(sizeof(T) * (2 * TH_H * W + (ACC ? 2 : 1) * BY * PBX));
-    const CUtensorMap* mU = maps.cur ? &maps.u_halo[1] : &maps.u_halo[0];
-    const CUtensorMap* mP = maps.cur ? &maps.u_ctr[0] : &maps.u_ctr[1];
+    const CUtensorMap* mU = pick_map(maps.u_halo, maps.cur);
+    const CUtensorMap* mP = pick_map(maps.u_ctr, maps.prev);
     auto issue = [&](int p, int s) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[s], STAGE_BYTES);

@@ -339,6 +339,10 @@ class DeviceGrid:
         """0: never; 1/True: 2x2-cell TMA kernel (default); 2: 256-thread TMA kernel."""
         self._ck(self.L.wo_set_option(self.h, N.WO_OPT_TMA_KERNEL, int(mode)), "wo_set_option")
 
+    def set_two_step(self, on):
+        """Two time steps per HBM pass where the grid allows it (default on)."""
+        self._ck(self.L.wo_set_option(self.h, N.WO_OPT_TWO_STEP, int(bool(on))), "wo_set_option")
+
     def fast_div_active(self):
         return bool(self.L.wo_fast_div_active(self.h))
 
@@ -370,7 +374,8 @@ class DeviceGrid:
         a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
         self._ck(self.L.wo_stats(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)),
                  "wo_stats")
-        return {"launches": a.value, "step_launches": b.value, "step_kernel_ms": c.value}
+        return {"launches": a.value, "step_launches": b.value, "step_kernel_ms": c.value,
+                "pair_launches": int(self.L.wo_pair_launches(self.h))}
 
     def reset_stats(self):
         self._ck(self.L.wo_reset_stats(self.h), "wo_reset_stats")

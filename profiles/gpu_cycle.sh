@@ -5,10 +5,10 @@
 #   profiles/gpu_cycle.sh <tag> [bench args...]
 tag=${1:-cycle}; shift
 out=gpurun_out
-timeout 600 python -m pytest tests -x -q -m gpu > $out/${tag}_tests.log 2>&1; echo "tests rc $?"; tail -2 $out/${tag}_tests.log
+timeout 900 python -m pytest tests -q -m gpu --maxfail=10 ${TESTS:-} > $out/${tag}_tests.log 2>&1; echo "tests rc $?"; tail -15 $out/${tag}_tests.log
 timeout 600 python bench.py --steps 5 --warmup 3 --cpu-sample-steps 4 "$@" > $out/${tag}_bench.json 2> $out/${tag}_bench.err; echo "bench rc $?"
 python profiles/profile_step.py > $out/${tag}_prof_plain.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 10 -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-step2?_kernel} -s 10 -c 1 \
       -o /tmp/${tag}_step python profiles/profile_step.py > $out/${tag}_ncu.log 2>&1; echo "ncu rc $?"
 if [ -f /tmp/${tag}_step.ncu-rep ]; then
   python profiles/analyze_ncu.py /tmp/${tag}_step.ncu-rep > $out/${tag}_ncu_summary.txt 2>&1

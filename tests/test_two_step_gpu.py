@@ -1,0 +1,141 @@
+"""GPU parity of the two-steps-per-pass kernel (csrc/step2_kernel.cuh).
+
+Grids of whole 64 x 8 tiles run the sweeps as two-step passes (plus one
+single step at an odd range end).  Every result must be bit-identical to the
+single-step kernels and to the oracle (oracle/oracle.py): gradients, costs,
+traces, final windows and the stability report.  Sources and sensors sit on
+tile edges and on the plane-chunk boundaries, where the recomputed ring and
+the chunk overlap planes are exercised."""
+
+import numpy as np
+import pytest
+
+from helpers import bits_equal
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+COST_RTOL = 1e-13
+RHO1, KAPPA1, RHO2, KAPPA2 = 1.204, 1.419e5, 2643.0, 6.87e8
+
+
+@pytest.fixture(scope="module")
+def W():
+    import paper_2509_15744_b200 as W
+
+    from paper_2509_15744_b200 import _native
+
+    _native.load(require_device=True)
+    return W
+
+
+def _materials(W, flavor, gamma, grid, dx):
+    if flavor == "rho_scaled":
+        return (W.MaterialModel.rho_scaled(gamma, grid, rho0=2700.0, c0=6000.0),
+                O.Material("rho_scaled", gamma, dx, rho0=2700.0, c0=6000.0), 6000.0)
+    return (W.MaterialModel.acoustic(gamma, grid, RHO1, KAPPA1, RHO2, KAPPA2),
+            O.Material("acoustic", gamma, dx, rho1=RHO1, kappa1=KAPPA1, rho2=RHO2,
+                       kappa2=KAPPA2), float(np.sqrt(KAPPA2 / RHO2)))
+
+
+def _problem(W, shape, flavor, n_steps, seed):
+    rng = np.random.default_rng(seed)
+    dx = 1e-4 if flavor == "rho_scaled" else 1e-2
+    lo = 0.2 if flavor == "rho_scaled" else 0.0
+    gamma = rng.uniform(lo, 1.0, size=shape)
+    grid = W.build_grid(shape, dx)
+    mat, omat, c_max = _materials(W, flavor, gamma, grid, dx)
+    dt = 0.45 * dx / c_max / np.sqrt(len(shape))
+    freq = 0.05 / dt
+    nd = len(shape)
+    # two shots: one on a chunk boundary plane / tile corner, one interior
+    nodes = [tuple([min(8, shape[0] - 1)] + [63 if s > 64 else s // 2 for s in shape[1:]])
+             if nd == 3 else (min(8, shape[0] - 1), 63),
+             tuple(s // 3 for s in shape)]
+    amp = 1e12 if flavor == "rho_scaled" else 1.0
+    srcs = [W.SourceSpec(node=n, amplitude=amp, frequency=freq, cycles=2) for n in nodes]
+    last = shape[-1]
+    if nd == 3:
+        sens = [(shape[0] - 1 - q, j, k) for q in (0, 7) for j in (0, 7, 8, shape[1] - 1)
+                for k in (0, 63, 64, last - 1)]
+    else:
+        sens = [(i, k) for i in (0, 7, 8, shape[0] - 1) for k in (0, 63, 64, last - 1)]
+    sens = list(dict.fromkeys(sens))
+    measured = rng.normal(scale=1e-10 if flavor == "rho_scaled" else 1e-3,
+                          size=(len(srcs), len(sens), n_steps))
+    problem = W.FwiProblem(grid=grid, time=W.TimeConfig(n_steps, dt), material=mat,
+                           sources=srcs, sensors=W.SensorArray(nodes=sens), measured=measured)
+    support = np.array([grid.flat_index(n) for n in sens], dtype=np.int64)
+    shots = [(O.Source(s.node, amp, freq, 2), O.FwiShot(support, measured[q], dt))
+             for q, s in enumerate(srcs)]
+    return problem, mat, omat, dt, shots
+
+
+SHAPES = [(40, 8, 64), (9, 24, 128), (64, 128), (3, 16, 192)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("flavor", ["rho_scaled", "acoustic"])
+@pytest.mark.parametrize("prec", ["single", "double"])
+@pytest.mark.parametrize("n_steps", [60, 61])
+def test_two_step_gradient_bitexact(W, shape, flavor, prec, n_steps):
+    from paper_2509_15744_b200 import engine
+
+    problem, mat, omat, dt, shots = _problem(W, shape, flavor, n_steps, sum(shape) + n_steps)
+    cfg = W.SuperpositionConfig(k=1e13 if flavor == "rho_scaled" else 1e3, precision=prec)
+    ctx = engine.get_context(problem.grid, W.precision_dtype(prec))
+    out = {}
+    for two in (True, False):
+        ctx.set_two_step(two)
+        ctx.reset_stats()
+        out[two] = W.gradient_superposed(problem, mat, cfg)
+        pairs = ctx.stats()["pair_launches"]
+        if two and ctx.fast_div_active():
+            assert pairs > 0, "two-step path did not run"
+        if not two:
+            assert pairs == 0
+    ctx.set_two_step(True)
+    assert bits_equal(out[True].gradient, out[False].gradient)
+    cost, grad, _ = O.gradient_superposed(omat, dt, n_steps, shots, cfg.k, prec)
+    assert bits_equal(out[True].gradient, grad)
+    assert abs(out[True].cost - cost) <= COST_RTOL * abs(cost)
+
+
+@pytest.mark.parametrize("shape", [(40, 8, 64), (64, 128)])
+@pytest.mark.parametrize("dn", ["f32", "f64"])
+def test_two_step_forward_traces_and_window(W, shape, dn):
+    """Trace gather (no accumulation) and the final window after an odd number
+    of steps match the oracle's run_forward."""
+    dtype = np.float32 if dn == "f32" else np.float64
+    problem, mat, omat, dt, shots = _problem(W, shape, "rho_scaled", 73, 3)
+    res = W.run_forward(mat, problem.time, problem.sources,
+                        W.SensorArray(nodes=problem.sensors.nodes), dtype=dtype)
+    sup = np.array([problem.grid.flat_index(n) for n in problem.sensors.nodes], dtype=np.int64)
+    osrc = [s for s, _ in shots]
+    u_prev, u_cur, traces, _, peak = O.run_forward(omat, dt, 73, osrc, sensor_idx=sup,
+                                                   dtype=dtype)
+    assert bits_equal(res.window.u_prev, u_prev)
+    assert bits_equal(res.window.u_cur, u_cur)
+    assert bits_equal(res.traces, traces)
+    assert res.peak_abs == peak
+
+
+@pytest.mark.parametrize("courant", [1.2, 0.75])
+def test_two_step_instability_step(W, courant):
+    """The blow-up step and max reported from a two-step sweep equal the
+    oracle's (the check can land on either half of a pass)."""
+    shape, dx = (16, 16, 64), 1e-4
+    dt = courant * dx / 6000.0
+    grid = W.build_grid(shape, dx)
+    gamma = np.ones(shape)
+    mat = W.MaterialModel.rho_scaled(gamma, grid, rho0=2700.0, c0=6000.0)
+    src = W.SourceSpec(node=(8, 8, 32), amplitude=1e12, frequency=3e6, cycles=2)
+    n_steps = 400
+    with pytest.raises(W.SolverInstabilityError) as ei:
+        W.run_forward(mat, W.TimeConfig(n_steps, dt), [src], None)
+    omat = O.Material("rho_scaled", gamma, dx, rho0=2700.0, c0=6000.0)
+    with pytest.raises(O.OracleInstability) as eo:
+        O.run_forward(omat, dt, n_steps, [O.Source((8, 8, 32), 1e12, 3e6, 2)])
+    assert ei.value.step == eo.value.step
+    assert ei.value.max_abs == eo.value.max_abs or (
+        np.isnan(ei.value.max_abs) and np.isnan(eo.value.max_abs))

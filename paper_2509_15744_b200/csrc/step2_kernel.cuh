@@ -127,7 +127,8 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         if (q < PBX + 2) { jj = j0 - 1; kk = k0 - 1 + q; }
         else if (q < 2 * (PBX + 2)) { jj = j0 + BY; kk = k0 - 1 + (q - (PBX + 2)); }
         else if (q < 2 * (PBX + 2) + BY) { jj = j0 + (q - 2 * (PBX + 2)); kk = k0 - 1; }
-        else { jj = j0 + (q - 2 * (PBX + 2) - BY); kk = k0 + PBX; }
+        else if (q < NRING) { jj = j0 + (q - 2 * (PBX + 2) - BY); kk = k0 + PBX; }
+        else { jj = j0; kk = k0; }   // idle slot: in-frame coordinates, never stored
         rg_ok[t] = q < NRING && jj >= 0 && jj < n1 && kk >= 0 && kk < n2;
         rg_r[t] = rowc(jj); rg_c[t] = colc(kk);
         rg_u[t] = rowc(jj - 1); rg_d[t] = rowc(jj + 1);

@@ -14,5 +14,6 @@ if [ -f /tmp/${tag}_step.ncu-rep ]; then
   python profiles/analyze_ncu.py /tmp/${tag}_step.ncu-rep > $out/${tag}_ncu_summary.txt 2>&1
   ncu -i /tmp/${tag}_step.ncu-rep --page raw --csv > $out/${tag}_ncu_raw.csv 2>/dev/null
   ncu -i /tmp/${tag}_step.ncu-rep --page source --csv --print-source sass > $out/${tag}_ncu_sass.csv 2>/dev/null
+  ncu -i /tmp/${tag}_step.ncu-rep --page source --csv --print-source cuda > $out/${tag}_ncu_src.csv 2>$out/${tag}_ncu_src.err
   cat $out/${tag}_ncu_summary.txt
 fi

@@ -54,12 +54,15 @@ def _problem(W, shape, flavor, n_steps, seed):
              tuple(s // 3 for s in shape)]
     amp = 1e12 if flavor == "rho_scaled" else 1.0
     srcs = [W.SourceSpec(node=n, amplitude=amp, frequency=freq, cycles=2) for n in nodes]
-    last = shape[-1]
+    def edge(n, cuts):   # tile / chunk edges inside an axis of n nodes
+        return sorted({min(c, n - 1) for c in cuts} | {0, n - 1})
+
+    ks = edge(shape[-1], (63, 64))
     if nd == 3:
-        sens = [(shape[0] - 1 - q, j, k) for q in (0, 7) for j in (0, 7, 8, shape[1] - 1)
-                for k in (0, 63, 64, last - 1)]
+        sens = [(i, j, k) for i in sorted({shape[0] - 1, max(shape[0] - 8, 0)})
+                for j in edge(shape[1], (7, 8)) for k in ks]
     else:
-        sens = [(i, k) for i in (0, 7, 8, shape[0] - 1) for k in (0, 63, 64, last - 1)]
+        sens = [(i, k) for i in edge(shape[0], (7, 8)) for k in ks]
     sens = list(dict.fromkeys(sens))
     measured = rng.normal(scale=1e-10 if flavor == "rho_scaled" else 1e-3,
                           size=(len(srcs), len(sens), n_steps))

@@ -2,8 +2,8 @@
 
     python -m paper_2509_15744_b200.build_native
 
-The library is one translation unit (csrc/capi.cu includes the kernel
-headers).  Flags: -fmad=false -prec-div=true -ftz=false keep every field
+The library links csrc/capi.cu (C ABI, aux kernels) with the per-dtype
+step-engine units csrc/step_*.cu and csrc/step2_*.cu, compiled in parallel.  Flags: -fmad=false -prec-div=true -ftz=false keep every field
 operation a single IEEE round-to-nearest op in source order, which is what
 makes the fp64 AND fp32 builds bit-exact against the reference
 (DESIGN.md "Arithmetic contract").
@@ -26,8 +26,8 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
-    "-shared", "--cudart", "static",
 ]
+LINK_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-shared", "--cudart", "static"]
 
 
 def sources():
@@ -47,11 +47,24 @@ def build(force=False, verbose=False, extra=()):
     if not force and up_to_date():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
-    cmd = [NVCC, *NVCC_FLAGS, *extra, os.path.join(CSRC, "capi.cu"), "-o", LIB + ".tmp"]
+    units = sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
+    objs = [os.path.join(OUT_DIR, u[:-3] + ".o") for u in units]
+    cmds = [[NVCC, *NVCC_FLAGS, *extra, "-c", os.path.join(CSRC, u), "-o", o]
+            for u, o in zip(units, objs)]
     if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
+        for c in cmds:
+            print(" ".join(c))
+    procs = [subprocess.Popen(c) for c in cmds]
+    rcs = [p.wait() for p in procs]
+    if any(rcs):
+        raise subprocess.CalledProcessError(max(rcs), cmds[rcs.index(max(rcs))])
+    link = [NVCC, *LINK_FLAGS, *objs, "-o", LIB + ".tmp"]
+    if verbose:
+        print(" ".join(link))
+    subprocess.run(link, check=True)
     os.replace(LIB + ".tmp", LIB)
+    for o in objs:
+        os.remove(o)
     return LIB
 
 

@@ -18,11 +18,7 @@
 #include "common.cuh"
 #include "design_kernels.cuh"
 #include "dropin_kernels.cuh"
-#include "step_kernel.cuh"
-#include "step_kernel_tma.cuh"
-#include "step_kernel_tma4.cuh"
-#include "step2_kernel.cuh"
-#include "step_kernel_v2.cuh"
+#include "launchers.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -262,30 +258,6 @@ bool tma_ready(wo_ctx* ctx) {
     return ctx->tma_state == 1;
 }
 
-template <typename T, int FL, bool FAST, bool ACC, bool CHK, int SUP>
-void launch_tma(dim3 grid, dim3 block, size_t tsm, wo_ctx* ctx, const StepArgs<T>& a) {
-    if (ctx->use_tma == 2) {   // v8 layout: 256 threads, 2 cells each
-        static bool attr_set = false;
-        if (!attr_set) {
-            cudaFuncSetAttribute(step_kernel_tma<T, FL, FAST, ACC, CHK, SUP>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-            attr_set = true;
-        }
-        step_kernel_tma<T, FL, FAST, ACC, CHK, SUP><<<grid, block, tsm, ctx->stream>>>(a, ctx->tmaps);
-        return;
-    }
-    // default: 128 threads, 2x2 cells each, statically unrolled stages
-    const size_t sm4 = tma4_smem_bytes<T>();
-    static bool attr4 = false;
-    if (!attr4) {
-        cudaFuncSetAttribute(step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
-        attr4 = true;
-    }
-    step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP><<<grid, dim3(32, 4, 1), sm4, ctx->stream>>>(
-        a, ctx->tmaps);
-}
-
 struct StepSpec {
     bool acc = false;
     bool check = false;
@@ -362,36 +334,11 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
         ctx->tmaps.cur = ctx->cur;
         ctx->tmaps.prev = ctx->prv;
     }
-    const size_t tsm = tma_smem_bytes<T>();
     if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
-#define LAUNCH(FL, FAST, ACC, CHK)                                                        \
-    do {                                                                                  \
-        if (tma) {                                                                        \
-            if (a.sup_mode == SUP_GATHER)                                                 \
-                launch_tma<T, FL, FAST, ACC, CHK, SUP_GATHER>(grid, block, tsm, ctx, a);  \
-            else if (a.sup_mode == SUP_INJECT)                                            \
-                launch_tma<T, FL, FAST, ACC, CHK, SUP_INJECT>(grid, block, tsm, ctx, a);  \
-            else                                                                          \
-                launch_tma<T, FL, FAST, ACC, CHK, SUP_NONE>(grid, block, tsm, ctx, a);    \
-        } else if (pair)                                                                  \
-            step_kernel_pair<T, FL, FAST, ACC, CHK><<<grid, block, 0, ctx->stream>>>(a);  \
-        else                                                                              \
-            step_kernel<T, FL, FAST, ACC, CHK><<<grid, block, 0, ctx->stream>>>(a);       \
-    } while (0)
-#define LAUNCH_AC(FL, FAST)                                                   \
-    do {                                                                      \
-        if (sp.acc) { if (sp.check) LAUNCH(FL, FAST, true, true);             \
-                      else LAUNCH(FL, FAST, true, false); }                   \
-        else { if (sp.check) LAUNCH(FL, FAST, false, true);                   \
-               else LAUNCH(FL, FAST, false, false); }                         \
-    } while (0)
-    if (ctx->flavor == RHO_SCALED) {
-        if (ctx->fast_div) LAUNCH_AC(RHO_SCALED, true); else LAUNCH_AC(RHO_SCALED, false);
-    } else {
-        if (ctx->fast_div) LAUNCH_AC(ACOUSTIC, true); else LAUNCH_AC(ACOUSTIC, false);
-    }
-#undef LAUNCH_AC
-#undef LAUNCH
+    const StepSel sel{ctx->flavor, ctx->fast_div, sp.acc, sp.check, a.sup_mode};
+    const int engine = tma ? (ctx->use_tma == 2 ? ENGINE_TMA : ENGINE_TMA4)
+                           : (pair ? ENGINE_PAIR : ENGINE_SCALAR);
+    launch_step_engine<T>(engine, sel, grid, block, ctx->stream, a, ctx->tmaps);
     if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
     ctx->launches++;
     ctx->step_launches++;
@@ -496,18 +443,6 @@ struct PairSpec {
     int64_t row1 = 0, row2 = 0, slot1 = 0, slot2 = 0;
 };
 
-template <typename T, int FL, bool ACC, int SUP>
-void launch_two(dim3 grid, wo_ctx* ctx, const Step2Args<T>& a) {
-    const size_t sm = step2_smem_bytes<T>();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(step2_kernel_tma<T, FL, true, ACC, SUP>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        attr = true;
-    }
-    step2_kernel_tma<T, FL, true, ACC, SUP><<<grid, dim3(32, 4, 1), sm, ctx->stream>>>(a, ctx->t2maps);
-}
-
 template <typename T>
 int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     int x[2], nx = 0;
@@ -551,14 +486,8 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     ctx->t2maps.cur = ctx->cur;
     dim3 grid(ctx->kn2 / PBX, ctx->kn1 / BY, (ctx->kn0 + a.chunk - 1) / a.chunk);
     if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
-#define L2(FL, ACC, SUP) launch_two<T, FL, ACC, SUP>(grid, ctx, a)
-#define L2S(FL, ACC) do { if (sup == SUP_GATHER) L2(FL, ACC, SUP_GATHER); \
-                          else if (sup == SUP_INJECT) L2(FL, ACC, SUP_INJECT); \
-                          else L2(FL, ACC, SUP_NONE); } while (0)
-    if (ctx->flavor == RHO_SCALED) { if (sp.acc) L2S(RHO_SCALED, true); else L2S(RHO_SCALED, false); }
-    else { if (sp.acc) L2S(ACOUSTIC, true); else L2S(ACOUSTIC, false); }
-#undef L2S
-#undef L2
+    launch_step2_engine<T>(StepSel{ctx->flavor, true, sp.acc, false, sup}, grid, ctx->stream, a,
+                           ctx->t2maps);
     if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
     ctx->launches++;
     ctx->step_launches++;

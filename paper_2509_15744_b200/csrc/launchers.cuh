@@ -1,0 +1,37 @@
+// Host-side launchers of the sweep step kernels, one translation unit per
+// kernel family and dtype (step_f32.cu, step_f64.cu, step2_f32.cu,
+// step2_f64.cu) so the library builds in parallel.  capi.cu picks the
+// engine and fills the argument blocks; these functions only map the runtime
+// selection onto the template instantiation and launch it on the stream.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "step2_kernel.cuh"
+#include "step_kernel.cuh"
+#include "step_kernel_tma.cuh"
+
+namespace wb {
+
+// single-step engines
+enum StepEngine : int { ENGINE_SCALAR = 0, ENGINE_PAIR = 1, ENGINE_TMA = 2, ENGINE_TMA4 = 3 };
+
+struct StepSel {
+    int flavor;   // RHO_SCALED / ACOUSTIC
+    bool fast;    // verified fast division
+    bool acc;     // kernel increment
+    bool check;   // stability max
+    int sup;      // SUP_NONE / SUP_GATHER / SUP_INJECT (TMA engines)
+};
+
+template <typename T>
+void launch_step_engine(int engine, const StepSel& k, dim3 grid, dim3 block, cudaStream_t s,
+                        const StepArgs<T>& a, const TmaMaps& maps);
+
+// two-step pass (fast division only; checks are runtime flags in the args)
+template <typename T>
+void launch_step2_engine(const StepSel& k, dim3 grid, cudaStream_t s, const Step2Args<T>& a,
+                         const Tma2Maps& maps);
+
+
+}  // namespace wb

@@ -1,0 +1,7 @@
+// Two-step (temporal blocking) engine for double; see launchers.cuh.
+#include "step_launch_impl.cuh"
+
+namespace wb {
+template void launch_step2_engine<double>(const StepSel&, dim3, cudaStream_t,
+                                      const Step2Args<double>&, const Tma2Maps&);
+}  // namespace wb

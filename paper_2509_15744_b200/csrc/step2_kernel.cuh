@@ -5,8 +5,9 @@
 // (stencil, injections, support gather/inject, self-kernel increment,
 // stability max — see step_kernel.cuh for the reference mapping and the
 // mirrored-boundary argument).  Per plane p of the 2.5D march:
-//   a  wait for plane p+1 (TMA ring), m(p+1) on the tile + 2-cell ring
-//   b  __syncthreads
+//   a  wait for plane p+1 (TMA ring); m(p+1) of the tile (registers, owners
+//      store it) and of the 2-cell halo (fixed per-thread slots) -> SM
+//   b  __syncthreads; refill the stage of plane p-1
 //   d  step n at plane p on the tile AND a one-cell ring around it (the ring
 //      is recomputed redundantly so step n+1 never needs another CTA's data);
 //      u^{n+1}(p) goes to a shared-memory plane X
@@ -19,9 +20,14 @@
 // fresh buffers (other CTAs still read u^{n-1} / u^n rings), so the window
 // rotates through four level buffers.  Single-domain contexts only (a slab
 // would need ghost planes two deep).
+//
+// Planes are processed in statically unrolled groups of T2_NS so every
+// stage / buffer index is a compile-time constant and each shared-memory
+// access is one per-thread offset plus an immediate.
 #pragma once
 
 #include <type_traits>
+#include <utility>
 
 #include "common.cuh"
 #include "step_kernel.cuh"
@@ -31,7 +37,7 @@
 namespace wb {
 
 constexpr int T2_THREADS = 128;
-constexpr int T2_NS = 4;             // TMA ring stages
+constexpr int T2_NS = 4;             // TMA ring stages (= planes per unrolled group)
 constexpr int R2_H = BY + 4;         // rows j0-2 .. j0+9
 constexpr int R1_H = BY + 2;         // rows j0-1 .. j0+8
 constexpr int NRING = 2 * (PBX + 2) + 2 * BY;   // one-cell ring around a 64 x 8 tile
@@ -81,6 +87,15 @@ constexpr size_t step2_smem_bytes() {
            T2_NS * sizeof(unsigned long long) + 128;
 }
 
+// body(q, plane) for q = 0..T2_NS-1 while the planes exist
+template <typename B, int... Q>
+__device__ __forceinline__ void unroll_group2(B& body, int p, int pfin, unsigned gpar,
+                                              std::integer_sequence<int, Q...>) {
+    bool go = true;
+    ((go = go && (p + Q <= pfin), go ? (body(std::integral_constant<int, Q>{}, p + Q, gpar), 0) : 0),
+     ...);
+}
+
 template <typename T, int FLAVOR, bool FAST, bool ACC, int SUP>
 __global__ void __launch_bounds__(T2_THREADS, sizeof(T) == 4 ? 3 : 1)
 step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__ Tma2Maps maps) {
@@ -89,15 +104,14 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     using V = typename Pair<T>::V;
     using Bits = typename Tr::Bits;
     constexpr int W = th_w<T>(), HO = th_ho<T>();
+    constexpr int PL = R2_H * W;                       // elements of one R2 plane
     extern __shared__ __align__(128) unsigned char smem_dyn[];
     unsigned char* smem_raw =
         smem_dyn + ((128u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_dyn)) & 127u)) & 127u);
     Tma2Stage<T>* st = reinterpret_cast<Tma2Stage<T>*>(smem_raw);
-    T(*SM)[R2_H][W] = reinterpret_cast<T(*)[R2_H][W]>(smem_raw + T2_NS * sizeof(Tma2Stage<T>));
-    T(*X)[R2_H][W] = reinterpret_cast<T(*)[R2_H][W]>(smem_raw + T2_NS * sizeof(Tma2Stage<T>) +
-                                                     2 * sizeof(T) * R2_H * W);
-    unsigned long long* bar = reinterpret_cast<unsigned long long*>(
-        smem_raw + T2_NS * sizeof(Tma2Stage<T>) + 4 * sizeof(T) * R2_H * W);
+    T* SMb = reinterpret_cast<T*>(smem_raw + T2_NS * sizeof(Tma2Stage<T>));   // SM[2][PL]
+    T* Xb = SMb + 2 * PL;                                                      // X[2][PL]
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(Xb + 2 * PL);
     __shared__ Bits smax[2][T2_THREADS / 32];
 
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -112,28 +126,34 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     const int pfin = min(i1, n0 - 1);
     const MatScalars<T>& M = a.mat;
 
-    // ---- geometry in the R2 frame (rows j0-2.., cols k0-HO..) ----
-    auto rowc = [&](int jj) { return min(max(jj, 0), n1 - 1) - j0 + 2; };
-    auto colc = [&](int kk) { return min(max(kk, 0), n2 - 1) - k0 + HO; };
-    const int ra = 2 * ty + 2, rb = ra + 1, cA = HO + 2 * tx;
-    const int rU = rowc(ja - 1), rD = rowc(ja + 2), cL = colc(kA - 1), cR = colc(kA + 2);
-    // ring cells: q = tid and q = tid + 128 (< NRING)
-    int rg_r[2], rg_c[2], rg_u[2], rg_d[2], rg_l[2], rg_rr[2];
+    // ---- per-thread offsets in the R2 frame (rows j0-2.., cols k0-HO..) ----
+    // tile rows a, b; clamped (mirrored) outer neighbours at the grid edge
+    const int ra = 2 * ty + 2, cA = HO + 2 * tx;
+    const int rU = min(max(ja - 1, 0), n1 - 1) - j0 + 2;
+    const int rD = min(max(ja + 2, 0), n1 - 1) - j0 + 2;
+    const int dL = kA > 0 ? 1 : 0, dR = kA + 2 < n2 ? 1 : 0;   // k-1 / k+2 inside
+    const int oA = ra * W + cA, oB = oA + W;
+    const int oU = rU * W + cA, oD = rD * W + cA;
+    // ring cells: slot 0 = tid, slot 1 = tid + 128 (warp 0, lanes < NRING-128).
+    // Tiles divide the grid, so an in-grid ring cell has in-grid neighbours.
+    int oR[2];
     bool rg_ok[2];
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
         const int q = tid + t * T2_THREADS;
-        int jj = 0, kk = 0;
+        int jj = j0, kk = k0;
         if (q < PBX + 2) { jj = j0 - 1; kk = k0 - 1 + q; }
         else if (q < 2 * (PBX + 2)) { jj = j0 + BY; kk = k0 - 1 + (q - (PBX + 2)); }
         else if (q < 2 * (PBX + 2) + BY) { jj = j0 + (q - 2 * (PBX + 2)); kk = k0 - 1; }
         else if (q < NRING) { jj = j0 + (q - 2 * (PBX + 2) - BY); kk = k0 + PBX; }
-        else { jj = j0; kk = k0; }   // idle slot: in-frame coordinates, never stored
         rg_ok[t] = q < NRING && jj >= 0 && jj < n1 && kk >= 0 && kk < n2;
-        rg_r[t] = rowc(jj); rg_c[t] = colc(kk);
-        rg_u[t] = rowc(jj - 1); rg_d[t] = rowc(jj + 1);
-        rg_l[t] = colc(kk - 1); rg_rr[t] = colc(kk + 1);
+        oR[t] = rg_ok[t] ? (jj - j0 + 2) * W + (kk - k0 + HO) : oA;
     }
+    const bool ring1 = tid < NRING - T2_THREADS;       // warp-uniform except warp 0
+    // m-halo slots: rows {0,1,10,11} x cols HO-2..HO+65 (3 per thread) and the
+    // side columns HO-2, HO-1, HO+64, HO+65 of rows 2..9 (warp 0)
+    const int oH = (ty < 2 ? ty : ty + BY) * W + HO - 2 + tx;
+    const int oS = (2 + (tx >> 2)) * W + ((tx & 3) < 2 ? HO - 2 + (tx & 3) : HO + PBX - 2 + (tx & 3));
 
     unsigned my_src = 0;   // sources in tile + ring and the step-n plane range
     for (int s = 0; s < a.n_src; ++s)
@@ -145,8 +165,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         (unsigned)(sizeof(T) * ((2 * R2_H + R1_H) * W + (ACC ? BY * PBX : 0)));
     const CUtensorMap* mU = pick_map(maps.u_r2, maps.cur);
     const CUtensorMap* mP = pick_map(maps.u_r1, maps.prev);
-    auto issue = [&](int p) {
-        const int s = (p - pbeg) % T2_NS;
+    auto issue = [&](int p, int s) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[s], STAGE_BYTES);
         tma_load_3d(&st[s].U[0][0], mU, k0 - HO, j0 - 2, p, &bar[s]);
@@ -154,38 +173,35 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         tma_load_3d(&st[s].P[0][0], mP, k0 - HO, j0 - 1, p, &bar[s]);
         if (ACC) tma_load_3d(&st[s].A[0][0], &maps.a_ctr, k0, j0, p, &bar[s]);
     };
-    auto wait_plane = [&](int p) {
-        const int n = p - pbeg;
-        mbar_wait(&bar[n % T2_NS], (unsigned)((n / T2_NS) & 1));
-    };
     if (tid == 0) {
         for (int s = 0; s < T2_NS; ++s) mbar_init(&bar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (tid == 0)
-        for (int p = pbeg; p <= min(pbeg + T2_NS - 1, pfin); ++p) issue(p);
+        for (int s = 0; s < T2_NS && pbeg + s <= pfin; ++s) issue(pbeg + s, s);
 
     auto ldv = [](const T* p) { return *reinterpret_cast<const V*>(p); };
     auto stv = [](T* p, V v) { *reinterpret_cast<V*>(p) = v; };
     auto face = [](T lo, T hi) { return MT::face(lo, hi); };
+    auto mv = [&](V g) { return V{MT::m(M, g.x), MT::m(M, g.y)}; };
 
-    // m of the R2 region of a plane (uniform loop, no role divergence)
-    auto mplane = [&](const T (*G)[W], T (*D)[W]) {
-        for (int c = tid; c < R2_H * (PBX + 4); c += T2_THREADS) {
-            const int r = c / (PBX + 4), cc = HO - 2 + c % (PBX + 4);
-            D[r][cc] = MT::m(M, G[r][cc]);
-        }
+    // m of the halo of a plane (tile m is stored by the owners)
+    auto m_halo = [&](const T* G, T* D) {
+        D[oH] = MT::m(M, G[oH]);
+        D[oH + 32] = MT::m(M, G[oH + 32]);
+        if (tx < 4) D[oH + 64] = MT::m(M, G[oH + 64]);
+        if (ty == 0) D[oS] = MT::m(M, G[oS]);
     };
 
     // own faces of a plane (2x2 block) from its m-plane
     struct Faces { T kLa, kIa, kRa, kLb, kIb, kRb; V jlo, jab, jhi; };
-    auto own_faces = [&](const T (*sm)[W]) {
+    auto own_faces = [&](const T* sm) {
         Faces f;
-        const V ma = ldv(&sm[ra][cA]), mb = ldv(&sm[rb][cA]);
-        f.kLa = face(sm[ra][cL], ma.x); f.kIa = face(ma.x, ma.y); f.kRa = face(ma.y, sm[ra][cR]);
-        f.kLb = face(sm[rb][cL], mb.x); f.kIb = face(mb.x, mb.y); f.kRb = face(mb.y, sm[rb][cR]);
-        const V mu = ldv(&sm[rU][cA]), md = ldv(&sm[rD][cA]);
+        const V ma = ldv(sm + oA), mb = ldv(sm + oB);
+        f.kLa = face(sm[oA - dL], ma.x); f.kIa = face(ma.x, ma.y); f.kRa = face(ma.y, sm[oA + 1 + dR]);
+        f.kLb = face(sm[oB - dL], mb.x); f.kIb = face(mb.x, mb.y); f.kRb = face(mb.y, sm[oB + 1 + dR]);
+        const V mu = ldv(sm + oU), md = ldv(sm + oD);
         f.jlo = V{face(mu.x, ma.x), face(mu.y, ma.y)};
         f.jab = V{face(ma.x, mb.x), face(ma.y, mb.y)};
         f.jhi = V{face(mb.x, md.x), face(mb.y, md.y)};
@@ -193,11 +209,11 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     };
     // ring-cell in-plane faces (k lo, k hi, j lo, j hi)
     struct RFaces { T kl, kh, jl, jh; };
-    auto ring_faces = [&](const T (*sm)[W], int t) {
+    auto ring_faces = [&](const T* sm, int o) {
         RFaces f;
-        const T m = sm[rg_r[t]][rg_c[t]];
-        f.kl = face(sm[rg_r[t]][rg_l[t]], m); f.kh = face(m, sm[rg_r[t]][rg_rr[t]]);
-        f.jl = face(sm[rg_u[t]][rg_c[t]], m); f.jh = face(m, sm[rg_d[t]][rg_c[t]]);
+        const T m = sm[o];
+        f.kl = face(sm[o - 1], m); f.kh = face(m, sm[o + 1]);
+        f.jl = face(sm[o - W], m); f.jh = face(m, sm[o + W]);
         return f;
     };
 
@@ -219,11 +235,15 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         const T g2 = (ukp - ukm) * a.inv2dx;
         return accv + a.sdt * ((a.cv * va) * va + a.cg * (((g0 * g0) + (g1 * g1)) + (g2 * g2)));
     };
-    // nodal sources at (plane, j, k) for the step's amplitudes
-    auto inject_src = [&](int p, int jj, int kk, T g, T kap, const T* val, T& o) {
+    // nodal sources at (plane, j, k) for the step's amplitudes; g the cell's
+    // gamma (fc recomputed from it exactly as the single-step kernel does)
+    auto inject_src = [&](int p, int jj, int kk, T g, const T* val, T& o) {
         for (int q = 0; q < a.n_src; ++q)
-            if (((my_src >> q) & 1u) && p == a.src_i[q] && jj == a.src_j[q] && kk == a.src_k[q])
+            if (((my_src >> q) & 1u) && p == a.src_i[q] && jj == a.src_j[q] && kk == a.src_k[q]) {
+                T kap;
+                (void)MT::coef(M, g, kap);
                 o = o + MT::fc(M, g, kap) * val[q];
+            }
     };
     // support bit / compact index of cell (p, jj, kk)
     auto sup_index = [&](int p, int jj, int kk) -> int {
@@ -233,6 +253,11 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         const unsigned bit = flat & 31u;
         if (!((w >> bit) & 1u)) return -1;
         return __ldg(a.sup_prefix + (flat >> 5)) + __popc(w & ((1u << bit) - 1u));
+    };
+    auto sup_inject = [&](int q, T g, T& o, const T* row) {
+        T kap;
+        (void)MT::coef(M, g, kap);
+        o = o + MT::fc(M, g, kap) * ldg(row + q);
     };
 
     // ---------------- prologue: plane pbeg ----------------
@@ -245,97 +270,164 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         gm_a = __ldg(reinterpret_cast<const V*>(a.gamma + (pbeg - 1) * plane + cofs));
         gm_b = __ldg(reinterpret_cast<const V*>(a.gamma + (pbeg - 1) * plane + cofs + n2));
     }
+    auto ring_gofs = [&](int t) {   // global offset (in plane) of ring slot t
+        const int r = oR[t] / W, c = oR[t] - r * W;
+        return (r + j0 - 2) * n2 + (c + k0 - HO);
+    };
     T rum[2] = {T(0), T(0)}, rgm[2] = {T(1), T(1)};
 #pragma unroll
     for (int t = 0; t < 2; ++t)
         if (has_m0 && rg_ok[t]) {
-            const int jj = rg_r[t] + j0 - 2, kk = rg_c[t] + k0 - HO;
-            rum[t] = __ldg(a.u_cur + (pbeg - 1) * plane + jj * n2 + kk);
-            rgm[t] = __ldg(a.gamma + (pbeg - 1) * plane + jj * n2 + kk);
+            const int go = (pbeg - 1) * plane + ring_gofs(t);
+            rum[t] = __ldg(a.u_cur + go);
+            rgm[t] = __ldg(a.gamma + go);
         }
-    wait_plane(pbeg);
-    const int s0 = 0;
-    V un0_a = ldv(&st[s0].U[ra][cA]), un0_b = ldv(&st[s0].U[rb][cA]);
-    V g0_a = ldv(&st[s0].G[ra][cA]), g0_b = ldv(&st[s0].G[rb][cA]);
+    mbar_wait(&bar[0], 0u);
+    V un0_a = ldv(&st[0].U[0][0] + oA), un0_b = ldv(&st[0].U[0][0] + oB);
+    V g0_a = ldv(&st[0].G[0][0] + oA), g0_b = ldv(&st[0].G[0][0] + oB);
     T run0[2], rg0[2];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) { run0[t] = st[s0].U[rg_r[t]][rg_c[t]]; rg0[t] = st[s0].G[rg_r[t]][rg_c[t]]; }
+    for (int t = 0; t < 2; ++t) { run0[t] = (&st[0].U[0][0])[oR[t]]; rg0[t] = (&st[0].G[0][0])[oR[t]]; }
     if (!has_m0) {
         unm_a = un0_a; unm_b = un0_b; gm_a = g0_a; gm_b = g0_b;
         rum[0] = run0[0]; rum[1] = run0[1]; rgm[0] = rg0[0]; rgm[1] = rg0[1];
     }
-    V m0_a = {MT::m(M, g0_a.x), MT::m(M, g0_a.y)}, m0_b = {MT::m(M, g0_b.x), MT::m(M, g0_b.y)};
+    V m0_a = mv(g0_a), m0_b = mv(g0_b);
     V w0_a = {face(MT::m(M, gm_a.x), m0_a.x), face(MT::m(M, gm_a.y), m0_a.y)};
     V w0_b = {face(MT::m(M, gm_b.x), m0_b.x), face(MT::m(M, gm_b.y), m0_b.y)};
     T rm0[2], rw0[2];
 #pragma unroll
     for (int t = 0; t < 2; ++t) { rm0[t] = MT::m(M, rg0[t]); rw0[t] = face(MT::m(M, rgm[t]), rm0[t]); }
-    mplane(st[s0].G, SM[0]);
+    stv(SMb + oA, m0_a);
+    stv(SMb + oB, m0_b);
+    m_halo(&st[0].G[0][0], SMb);
     __syncthreads();
-    Faces F0 = own_faces(SM[0]);
-    RFaces RF0[2] = {ring_faces(SM[0], 0), ring_faces(SM[0], 1)};
+    Faces F0 = own_faces(SMb);
+    RFaces RF0[2] = {ring_faces(SMb, oR[0]), ring_faces(SMb, oR[1])};
 
     // step n+1 state: material of the previous step-n plane, u^{n+1} queue
     Faces F1 = F0;
     V w1lo_a = w0_a, w1lo_b = w0_b, w1hi_a = w0_a, w1hi_b = w0_b;
-    T c1[4] = {T(0), T(0), T(0), T(0)}, kap1[4] = {T(0), T(0), T(0), T(0)};
-    V g1_a = g0_a, g1_b = g0_b;
+    T c1[4] = {T(0), T(0), T(0), T(0)};
     V x_m1a = un0_a, x_m1b = un0_b, x_0a = un0_a, x_0b = un0_b;   // u^{n+1}(p-2), (p-1)
     V un1_a = unm_a, un1_b = unm_b;                                // u^n(p-1)
     V acc1_a = {T(0), T(0)}, acc1_b = acc1_a;                      // acc after step n at p-1
     Bits lmax1 = 0, lmax2 = 0;
 
-    for (int p = pbeg; p <= pfin; ++p) {
-        const int sc = (p - pbeg) % T2_NS, sn = (p + 1 - pbeg) % T2_NS;
-        const int b = (p - pbeg) & 1, nb = b ^ 1;
-        const bool have_p1 = p + 1 <= pfin;         // step n needs plane p+1 (or mirror)
-        const bool exists_p1 = p + 1 <= n0 - 1;
+    // step n+1 at plane q1 for the tile: x_p1 = u^{n+1}(q1+1) (registers)
+    auto step2_tile = [&](int q1, const T* Xq, V xp_a, V xp_b) {
+        const V xu = ldv(Xq + oU), xd = ldv(Xq + oD);
+        const T xLa = Xq[oA - dL], xRa = Xq[oA + 1 + dR], xLb = Xq[oB - dL], xRb = Xq[oB + 1 + dR];
+        V o2a, o2b;
+        o2a.x = cell(x_0a.x, xp_a.x, x_m1a.x, x_0b.x, xu.x, x_0a.y, xLa, w1hi_a.x, w1lo_a.x,
+                     F1.jab.x, F1.jlo.x, F1.kIa, F1.kLa, c1[0], un1_a.x);
+        o2a.y = cell(x_0a.y, xp_a.y, x_m1a.y, x_0b.y, xu.y, xRa, x_0a.x, w1hi_a.y, w1lo_a.y,
+                     F1.jab.y, F1.jlo.y, F1.kRa, F1.kIa, c1[1], un1_a.y);
+        o2b.x = cell(x_0b.x, xp_b.x, x_m1b.x, xd.x, x_0a.x, x_0b.y, xLb, w1hi_b.x, w1lo_b.x,
+                     F1.jhi.x, F1.jab.x, F1.kIb, F1.kLb, c1[2], un1_b.x);
+        o2b.y = cell(x_0b.y, xp_b.y, x_m1b.y, xd.y, x_0a.y, xRb, x_0b.x, w1hi_b.y, w1lo_b.y,
+                     F1.jhi.y, F1.jab.y, F1.kRb, F1.kIb, c1[3], un1_b.y);
+        const int oc = q1 * plane + cofs;
+        if (my_src || SUP != SUP_NONE) {
+            const T* gq = a.gamma + oc;
+            if (my_src) {
+                inject_src(q1, ja, kA, __ldg(gq), a.src_val2, o2a.x);
+                inject_src(q1, ja, kA + 1, __ldg(gq + 1), a.src_val2, o2a.y);
+                inject_src(q1, ja + 1, kA, __ldg(gq + n2), a.src_val2, o2b.x);
+                inject_src(q1, ja + 1, kA + 1, __ldg(gq + n2 + 1), a.src_val2, o2b.y);
+            }
+            if (SUP != SUP_NONE) {
+                const T xo[4] = {x_0a.x, x_0a.y, x_0b.x, x_0b.y};
+                T* oo[4] = {&o2a.x, &o2a.y, &o2b.x, &o2b.y};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int q = sup_index(q1, ja + (c >> 1), kA + (c & 1));
+                    if (q >= 0) {
+                        if (SUP == SUP_GATHER) a.row2[q] = xo[c];
+                        else sup_inject(q, __ldg(gq + (c >> 1) * n2 + (c & 1)), *oo[c], a.row2);
+                    }
+                }
+            }
+        }
+        if (ACC) {
+            V fa, fb;
+            fa.x = kinc(acc1_a.x, o2a.x, un1_a.x, xp_a.x, x_m1a.x, x_0b.x, xu.x, x_0a.y, xLa);
+            fa.y = kinc(acc1_a.y, o2a.y, un1_a.y, xp_a.y, x_m1a.y, x_0b.y, xu.y, xRa, x_0a.x);
+            fb.x = kinc(acc1_b.x, o2b.x, un1_b.x, xp_b.x, x_m1b.x, xd.x, x_0a.x, x_0b.y, xLb);
+            fb.y = kinc(acc1_b.y, o2b.y, un1_b.y, xp_b.y, x_m1b.y, xd.y, x_0a.y, xRb, x_0b.x);
+            stv(a.acc + oc, fa);
+            stv(a.acc + oc + n2, fb);
+        }
+        stv(a.out1 + oc, x_0a);
+        stv(a.out1 + oc + n2, x_0b);
+        stv(a.out2 + oc, o2a);
+        stv(a.out2 + oc + n2, o2b);
+        if (a.check2) {
+            Bits m1 = Tr::abs_bits(o2a.x), m2 = Tr::abs_bits(o2a.y);
+            Bits m3 = Tr::abs_bits(o2b.x), m4 = Tr::abs_bits(o2b.y);
+            m1 = m1 > m2 ? m1 : m2; m3 = m3 > m4 ? m3 : m4; m1 = m1 > m3 ? m1 : m3;
+            lmax2 = m1 > lmax2 ? m1 : lmax2;
+        }
+    };
+
+    auto body = [&](auto stage, int p, unsigned gpar) {
+        constexpr int q = decltype(stage)::value;
+        constexpr int sn = (q + 1) % T2_NS, sf = (q + T2_NS - 1) % T2_NS;
+        constexpr int b = q & 1, nb = b ^ 1;
+        constexpr unsigned pn = (q + 1 == T2_NS) ? 1u : 0u;   // parity flip for plane p+1
+        T* SMn = SMb + nb * PL;
+        T* Xc = Xb + b * PL;
+        const T* Xp = Xb + nb * PL;
+        const Tma2Stage<T>& S = st[q];
+        const T* SU = &S.U[0][0];
+        const T* SP = &S.P[0][0] - W;     // P frame is the R2 frame shifted one row
+        const bool next = p + 1 <= pfin;   // plane p+1 in the ring (and a later step-n plane)
         // ---- a: plane p+1 ----
         V unp_a = un0_a, unp_b = un0_b, gp_a = g0_a, gp_b = g0_b;
         T runp[2] = {run0[0], run0[1]}, rgp[2] = {rg0[0], rg0[1]};
-        if (exists_p1) {
-            if (have_p1) {
-                wait_plane(p + 1);
-                unp_a = ldv(&st[sn].U[ra][cA]); unp_b = ldv(&st[sn].U[rb][cA]);
-                gp_a = ldv(&st[sn].G[ra][cA]); gp_b = ldv(&st[sn].G[rb][cA]);
+        if (next) {
+            mbar_wait(&bar[sn], gpar ^ pn);
+            const T* NU = &st[sn].U[0][0];
+            const T* NG = &st[sn].G[0][0];
+            unp_a = ldv(NU + oA); unp_b = ldv(NU + oB);
+            gp_a = ldv(NG + oA); gp_b = ldv(NG + oB);
 #pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                    runp[t] = st[sn].U[rg_r[t]][rg_c[t]];
-                    rgp[t] = st[sn].G[rg_r[t]][rg_c[t]];
+            for (int t = 0; t < 2; ++t) { runp[t] = NU[oR[t]]; rgp[t] = NG[oR[t]]; }
+            m_halo(NG, SMn);
+        } else if (p + 1 <= n0 - 1) {   // chunk end inside the domain: plane p+1 from HBM
+            const int gp = (p + 1) * plane;
+            unp_a = __ldg(reinterpret_cast<const V*>(a.u_cur + gp + cofs));
+            unp_b = __ldg(reinterpret_cast<const V*>(a.u_cur + gp + cofs + n2));
+            gp_a = __ldg(reinterpret_cast<const V*>(a.gamma + gp + cofs));
+            gp_b = __ldg(reinterpret_cast<const V*>(a.gamma + gp + cofs + n2));
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+                if (rg_ok[t]) {
+                    const int go = gp + ring_gofs(t);
+                    runp[t] = __ldg(a.u_cur + go);
+                    rgp[t] = __ldg(a.gamma + go);
                 }
-                mplane(st[sn].G, SM[nb]);
-            } else {   // chunk end inside the domain: plane p+1 straight from HBM
-                unp_a = __ldg(reinterpret_cast<const V*>(a.u_cur + (p + 1) * plane + cofs));
-                unp_b = __ldg(reinterpret_cast<const V*>(a.u_cur + (p + 1) * plane + cofs + n2));
-                gp_a = __ldg(reinterpret_cast<const V*>(a.gamma + (p + 1) * plane + cofs));
-                gp_b = __ldg(reinterpret_cast<const V*>(a.gamma + (p + 1) * plane + cofs + n2));
-#pragma unroll
-                for (int t = 0; t < 2; ++t)
-                    if (rg_ok[t]) {
-                        const int jj = rg_r[t] + j0 - 2, kk = rg_c[t] + k0 - HO;
-                        runp[t] = __ldg(a.u_cur + (p + 1) * plane + jj * n2 + kk);
-                        rgp[t] = __ldg(a.gamma + (p + 1) * plane + jj * n2 + kk);
-                    }
-            }
         }
-        const V mp_a = {MT::m(M, gp_a.x), MT::m(M, gp_a.y)};
-        const V mp_b = {MT::m(M, gp_b.x), MT::m(M, gp_b.y)};
+        const V mp_a = mv(gp_a), mp_b = mv(gp_b);
         T rmp[2];
 #pragma unroll
         for (int t = 0; t < 2; ++t) rmp[t] = MT::m(M, rgp[t]);
+        if (next) {
+            stv(SMn + oA, mp_a);
+            stv(SMn + oB, mp_b);
+        }
         __syncthreads();
-        if (tid == 0 && p > pbeg && p - 1 + T2_NS <= pfin) issue(p - 1 + T2_NS);
+        if (tid == 0 && p > pbeg && p + T2_NS - 1 <= pfin) issue(p + T2_NS - 1, sf);
 
         // ---- d: step n at plane p (tile + ring) -> X[b] ----
-        const Tma2Stage<T>& S = st[sc];
         const V wh_a = {face(m0_a.x, mp_a.x), face(m0_a.y, mp_a.y)};
         const V wh_b = {face(m0_b.x, mp_b.x), face(m0_b.y, mp_b.y)};
         T kp[4];
         const T cf[4] = {MT::coef(M, g0_a.x, kp[0]), MT::coef(M, g0_a.y, kp[1]),
                          MT::coef(M, g0_b.x, kp[2]), MT::coef(M, g0_b.y, kp[3])};
-        const V uu = ldv(&S.U[rU][cA]), ud = ldv(&S.U[rD][cA]);
-        const T uLa = S.U[ra][cL], uRa = S.U[ra][cR], uLb = S.U[rb][cL], uRb = S.U[rb][cR];
-        const V pa = ldv(&S.P[ra - 1][cA]), pb = ldv(&S.P[rb - 1][cA]);
+        const V uu = ldv(SU + oU), ud = ldv(SU + oD);
+        const T uLa = SU[oA - dL], uRa = SU[oA + 1 + dR], uLb = SU[oB - dL], uRb = SU[oB + 1 + dR];
+        const V pa = ldv(SP + oA), pb = ldv(SP + oB);
         V oa, ob;
         oa.x = cell(un0_a.x, unp_a.x, unm_a.x, un0_b.x, uu.x, un0_a.y, uLa, wh_a.x, w0_a.x,
                     F0.jab.x, F0.jlo.x, F0.kIa, F0.kLa, cf[0], pa.x);
@@ -346,10 +438,10 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         ob.y = cell(un0_b.y, unp_b.y, unm_b.y, ud.y, un0_a.y, uRb, un0_b.x, wh_b.y, w0_b.y,
                     F0.jhi.y, F0.jab.y, F0.kRb, F0.kIb, cf[3], pb.y);
         if (my_src) {
-            inject_src(p, ja, kA, g0_a.x, kp[0], a.src_val1, oa.x);
-            inject_src(p, ja, kA + 1, g0_a.y, kp[1], a.src_val1, oa.y);
-            inject_src(p, ja + 1, kA, g0_b.x, kp[2], a.src_val1, ob.x);
-            inject_src(p, ja + 1, kA + 1, g0_b.y, kp[3], a.src_val1, ob.y);
+            inject_src(p, ja, kA, g0_a.x, a.src_val1, oa.x);
+            inject_src(p, ja, kA + 1, g0_a.y, a.src_val1, oa.y);
+            inject_src(p, ja + 1, kA, g0_b.x, a.src_val1, ob.x);
+            inject_src(p, ja + 1, kA + 1, g0_b.y, a.src_val1, ob.y);
         }
         const bool own_plane = p >= i0 && p < i1;
         if (SUP != SUP_NONE) {
@@ -358,15 +450,15 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
             const T gg[4] = {g0_a.x, g0_a.y, g0_b.x, g0_b.y};
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                const int q = sup_index(p, ja + (c >> 1), kA + (c & 1));
-                if (q >= 0) {
-                    if (SUP == SUP_GATHER) { if (own_plane) a.row1[q] = uo[c]; }
-                    else *oo[c] = *oo[c] + MT::fc(M, gg[c], kp[c]) * ldg(a.row1 + q);
+                const int qi = sup_index(p, ja + (c >> 1), kA + (c & 1));
+                if (qi >= 0) {
+                    if (SUP == SUP_GATHER) { if (own_plane) a.row1[qi] = uo[c]; }
+                    else *oo[c] = *oo[c] + MT::fc(M, gg[c], kp[c]) * ldg(a.row1 + qi);
                 }
             }
         }
-        stv(&X[b][ra][cA], oa);
-        stv(&X[b][rb][cA], ob);
+        stv(Xc + oA, oa);
+        stv(Xc + oB, ob);
         V nacc_a = acc1_a, nacc_b = acc1_b;
         if (own_plane) {
             if (ACC) {
@@ -386,93 +478,43 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         // ring cells (step n only, no accumulation / gather)
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
+            if (t == 1 && !ring1) continue;
             if (!rg_ok[t]) continue;
-            const int r = rg_r[t], c = rg_c[t];
+            const int o = oR[t];
             const T u0 = run0[t];
             T kap;
             const T coef = MT::coef(M, rg0[t], kap);
-            T o = cell(u0, runp[t], rum[t], S.U[rg_d[t]][c], S.U[rg_u[t]][c], S.U[r][rg_rr[t]],
-                       S.U[r][rg_l[t]], face(rm0[t], rmp[t]), rw0[t], RF0[t].jh, RF0[t].jl,
-                       RF0[t].kh, RF0[t].kl, coef, S.P[r - 1][c]);
-            const int jj = r + j0 - 2, kk = c + k0 - HO;
-            if (my_src) inject_src(p, jj, kk, rg0[t], kap, a.src_val1, o);
-            if (SUP == SUP_INJECT) {
-                const int q = sup_index(p, jj, kk);
-                if (q >= 0) o = o + MT::fc(M, rg0[t], kap) * ldg(a.row1 + q);
+            T v = cell(u0, runp[t], rum[t], SU[o + W], SU[o - W], SU[o + 1], SU[o - 1],
+                       face(rm0[t], rmp[t]), rw0[t], RF0[t].jh, RF0[t].jl, RF0[t].kh, RF0[t].kl,
+                       coef, SP[o]);
+            if (my_src || SUP == SUP_INJECT) {
+                const int r = o / W;
+                const int jj = r + j0 - 2, kk = o - r * W + k0 - HO;
+                if (my_src) inject_src(p, jj, kk, rg0[t], a.src_val1, v);
+                if (SUP == SUP_INJECT) {
+                    const int qi = sup_index(p, jj, kk);
+                    if (qi >= 0) v = v + MT::fc(M, rg0[t], kap) * ldg(a.row1 + qi);
+                }
             }
-            X[b][r][c] = o;
+            Xc[o] = v;
         }
 
         // ---- c: step n+1 at plane p-1 (tile) ----
-        const int q1 = p - 1;
-        if (q1 >= i0 && q1 < i1) {
-            const T (*Xq)[W] = X[nb];                  // u^{n+1}(p-1) with its ring
-            const V xu = ldv(&Xq[rU][cA]), xd = ldv(&Xq[rD][cA]);
-            const T xLa = Xq[ra][cL], xRa = Xq[ra][cR], xLb = Xq[rb][cL], xRb = Xq[rb][cR];
-            V o2a, o2b;
-            o2a.x = cell(x_0a.x, oa.x, x_m1a.x, x_0b.x, xu.x, x_0a.y, xLa, w1hi_a.x, w1lo_a.x,
-                         F1.jab.x, F1.jlo.x, F1.kIa, F1.kLa, c1[0], un1_a.x);
-            o2a.y = cell(x_0a.y, oa.y, x_m1a.y, x_0b.y, xu.y, xRa, x_0a.x, w1hi_a.y, w1lo_a.y,
-                         F1.jab.y, F1.jlo.y, F1.kRa, F1.kIa, c1[1], un1_a.y);
-            o2b.x = cell(x_0b.x, ob.x, x_m1b.x, xd.x, x_0a.x, x_0b.y, xLb, w1hi_b.x, w1lo_b.x,
-                         F1.jhi.x, F1.jab.x, F1.kIb, F1.kLb, c1[2], un1_b.x);
-            o2b.y = cell(x_0b.y, ob.y, x_m1b.y, xd.y, x_0a.y, xRb, x_0b.x, w1hi_b.y, w1lo_b.y,
-                         F1.jhi.y, F1.jab.y, F1.kRb, F1.kIb, c1[3], un1_b.y);
-            if (my_src) {
-                inject_src(q1, ja, kA, g1_a.x, kap1[0], a.src_val2, o2a.x);
-                inject_src(q1, ja, kA + 1, g1_a.y, kap1[1], a.src_val2, o2a.y);
-                inject_src(q1, ja + 1, kA, g1_b.x, kap1[2], a.src_val2, o2b.x);
-                inject_src(q1, ja + 1, kA + 1, g1_b.y, kap1[3], a.src_val2, o2b.y);
-            }
-            if (SUP != SUP_NONE) {
-                const T xo[4] = {x_0a.x, x_0a.y, x_0b.x, x_0b.y};
-                T* oo[4] = {&o2a.x, &o2a.y, &o2b.x, &o2b.y};
-                const T gg[4] = {g1_a.x, g1_a.y, g1_b.x, g1_b.y};
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const int q = sup_index(q1, ja + (c >> 1), kA + (c & 1));
-                    if (q >= 0) {
-                        if (SUP == SUP_GATHER) a.row2[q] = xo[c];
-                        else *oo[c] = *oo[c] + MT::fc(M, gg[c], kap1[c]) * ldg(a.row2 + q);
-                    }
-                }
-            }
-            const int oc = q1 * plane + cofs;
-            if (ACC) {
-                V fa, fb;
-                fa.x = kinc(acc1_a.x, o2a.x, un1_a.x, oa.x, x_m1a.x, x_0b.x, xu.x, x_0a.y, xLa);
-                fa.y = kinc(acc1_a.y, o2a.y, un1_a.y, oa.y, x_m1a.y, x_0b.y, xu.y, xRa, x_0a.x);
-                fb.x = kinc(acc1_b.x, o2b.x, un1_b.x, ob.x, x_m1b.x, xd.x, x_0a.x, x_0b.y, xLb);
-                fb.y = kinc(acc1_b.y, o2b.y, un1_b.y, ob.y, x_m1b.y, xd.y, x_0a.y, xRb, x_0b.x);
-                stv(a.acc + oc, fa);
-                stv(a.acc + oc + n2, fb);
-            }
-            stv(a.out1 + oc, x_0a);
-            stv(a.out1 + oc + n2, x_0b);
-            stv(a.out2 + oc, o2a);
-            stv(a.out2 + oc + n2, o2b);
-            if (a.check2) {
-                Bits m1 = Tr::abs_bits(o2a.x), m2 = Tr::abs_bits(o2a.y);
-                Bits m3 = Tr::abs_bits(o2b.x), m4 = Tr::abs_bits(o2b.y);
-                m1 = m1 > m2 ? m1 : m2; m3 = m3 > m4 ? m3 : m4; m1 = m1 > m3 ? m1 : m3;
-                lmax2 = m1 > lmax2 ? m1 : lmax2;
-            }
-        }
+        if (p - 1 >= i0 && p - 1 < i1) step2_tile(p - 1, Xp, oa, ob);
 
         // ---- e: faces of plane p+1; rotate ----
         Faces Fn = F0;
         RFaces RFn[2] = {RF0[0], RF0[1]};
-        if (p + 1 <= pfin && exists_p1 && have_p1) {
-            Fn = own_faces(SM[nb]);
-            RFn[0] = ring_faces(SM[nb], 0);
-            RFn[1] = ring_faces(SM[nb], 1);
+        if (next) {
+            Fn = own_faces(SMn);
+            RFn[0] = ring_faces(SMn, oR[0]);
+            if (ring1) RFn[1] = ring_faces(SMn, oR[1]);
         }
-        // step-(n+1) material for plane p (used at the next iteration)
+        // step-(n+1) material for plane p (used at the next plane)
         F1 = F0;
         w1lo_a = w0_a; w1lo_b = w0_b; w1hi_a = wh_a; w1hi_b = wh_b;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) { c1[c] = cf[c]; kap1[c] = kp[c]; }
-        g1_a = g0_a; g1_b = g0_b;
+        for (int c = 0; c < 4; ++c) c1[c] = cf[c];
         acc1_a = nacc_a; acc1_b = nacc_b;
         un1_a = un0_a; un1_b = un0_b;
         // u^{n+1} queue; at the global bottom plane the "previous" plane is
@@ -489,67 +531,17 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
             rum[t] = run0[t]; run0[t] = runp[t]; rg0[t] = rgp[t]; rm0[t] = rmp[t];
             RF0[t] = RFn[t];
         }
-    }
+    };
 
-    // ---- step n+1 for the chunk's last plane when p+1 was beyond the grid ----
-    // (handled inside the loop: pfin = i1 for interior chunks; at the global
-    // end pfin = n0-1 = i1-1 and the mirrored plane n0 is the cell itself)
+    unsigned gpar = 0;
+    for (int p = pbeg; p <= pfin; p += T2_NS, gpar ^= 1u)
+        unroll_group2(body, p, pfin, gpar, std::make_integer_sequence<int, T2_NS>{});
+
+    // ---- step n+1 at the last plane of the grid (mirror above) ----
+    // interior chunks finish inside the loop (pfin = i1); at the global end
+    // pfin = n0-1 = i1-1 and plane n0 mirrors the plane itself
     __syncthreads();                         // ring values of the last plane in X
-    if (pfin == i1 - 1) {
-        const int q1 = pfin;                 // step n+1 at the last plane, mirror above
-        const T (*Xq)[W] = X[(pfin - pbeg) & 1];
-        const V xu = ldv(&Xq[rU][cA]), xd = ldv(&Xq[rD][cA]);
-        const T xLa = Xq[ra][cL], xRa = Xq[ra][cR], xLb = Xq[rb][cL], xRb = Xq[rb][cR];
-        // after the rotation: x_0 = u^{n+1}(pfin), x_m1 = u^{n+1}(pfin-1); mirror x_p1 = x_0
-        V o2a, o2b;
-        o2a.x = cell(x_0a.x, x_0a.x, x_m1a.x, x_0b.x, xu.x, x_0a.y, xLa, w1hi_a.x, w1lo_a.x,
-                     F1.jab.x, F1.jlo.x, F1.kIa, F1.kLa, c1[0], un1_a.x);
-        o2a.y = cell(x_0a.y, x_0a.y, x_m1a.y, x_0b.y, xu.y, xRa, x_0a.x, w1hi_a.y, w1lo_a.y,
-                     F1.jab.y, F1.jlo.y, F1.kRa, F1.kIa, c1[1], un1_a.y);
-        o2b.x = cell(x_0b.x, x_0b.x, x_m1b.x, xd.x, x_0a.x, x_0b.y, xLb, w1hi_b.x, w1lo_b.x,
-                     F1.jhi.x, F1.jab.x, F1.kIb, F1.kLb, c1[2], un1_b.x);
-        o2b.y = cell(x_0b.y, x_0b.y, x_m1b.y, xd.y, x_0a.y, xRb, x_0b.x, w1hi_b.y, w1lo_b.y,
-                     F1.jhi.y, F1.jab.y, F1.kRb, F1.kIb, c1[3], un1_b.y);
-        if (my_src) {
-            inject_src(q1, ja, kA, g1_a.x, kap1[0], a.src_val2, o2a.x);
-            inject_src(q1, ja, kA + 1, g1_a.y, kap1[1], a.src_val2, o2a.y);
-            inject_src(q1, ja + 1, kA, g1_b.x, kap1[2], a.src_val2, o2b.x);
-            inject_src(q1, ja + 1, kA + 1, g1_b.y, kap1[3], a.src_val2, o2b.y);
-        }
-        if (SUP != SUP_NONE) {
-            const T xo[4] = {x_0a.x, x_0a.y, x_0b.x, x_0b.y};
-            T* oo[4] = {&o2a.x, &o2a.y, &o2b.x, &o2b.y};
-            const T gg[4] = {g1_a.x, g1_a.y, g1_b.x, g1_b.y};
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int q = sup_index(q1, ja + (c >> 1), kA + (c & 1));
-                if (q >= 0) {
-                    if (SUP == SUP_GATHER) a.row2[q] = xo[c];
-                    else *oo[c] = *oo[c] + MT::fc(M, gg[c], kap1[c]) * ldg(a.row2 + q);
-                }
-            }
-        }
-        const int oc = q1 * plane + cofs;
-        if (ACC) {
-            V fa, fb;
-            fa.x = kinc(acc1_a.x, o2a.x, un1_a.x, x_0a.x, x_m1a.x, x_0b.x, xu.x, x_0a.y, xLa);
-            fa.y = kinc(acc1_a.y, o2a.y, un1_a.y, x_0a.y, x_m1a.y, x_0b.y, xu.y, xRa, x_0a.x);
-            fb.x = kinc(acc1_b.x, o2b.x, un1_b.x, x_0b.x, x_m1b.x, xd.x, x_0a.x, x_0b.y, xLb);
-            fb.y = kinc(acc1_b.y, o2b.y, un1_b.y, x_0b.y, x_m1b.y, xd.y, x_0a.y, xRb, x_0b.x);
-            stv(a.acc + oc, fa);
-            stv(a.acc + oc + n2, fb);
-        }
-        stv(a.out1 + oc, x_0a);
-        stv(a.out1 + oc + n2, x_0b);
-        stv(a.out2 + oc, o2a);
-        stv(a.out2 + oc + n2, o2b);
-        if (a.check2) {
-            Bits m1 = Tr::abs_bits(o2a.x), m2 = Tr::abs_bits(o2a.y);
-            Bits m3 = Tr::abs_bits(o2b.x), m4 = Tr::abs_bits(o2b.y);
-            m1 = m1 > m2 ? m1 : m2; m3 = m3 > m4 ? m3 : m4; m1 = m1 > m3 ? m1 : m3;
-            lmax2 = m1 > lmax2 ? m1 : lmax2;
-        }
-    }
+    if (pfin == i1 - 1) step2_tile(pfin, Xb + ((pfin - pbeg) & 1) * PL, x_0a, x_0b);
 
     if (a.check1 || a.check2) {
         for (int o = 16; o > 0; o >>= 1) {

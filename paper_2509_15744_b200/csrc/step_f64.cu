@@ -1,0 +1,7 @@
+// Single-step engines (scalar, pair, TMA, TMA 2x2) for double; see launchers.cuh.
+#include "step_launch_impl.cuh"
+
+namespace wb {
+template void launch_step_engine<double>(int, const StepSel&, dim3, dim3, cudaStream_t,
+                                     const StepArgs<double>&, const TmaMaps&);
+}  // namespace wb

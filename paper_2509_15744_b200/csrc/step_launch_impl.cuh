@@ -1,0 +1,104 @@
+// Template bodies of launch_step_engine / launch_step2_engine (launchers.cuh),
+// included by the per-dtype translation units.
+#pragma once
+
+#include "launchers.cuh"
+#include "step_kernel_tma4.cuh"
+#include "step_kernel_v2.cuh"
+
+namespace wb {
+
+template <typename T, int FL, bool FAST, bool ACC, bool CHK, int SUP>
+void go_step(int engine, dim3 grid, dim3 block, cudaStream_t s, const StepArgs<T>& a,
+             const TmaMaps& maps) {
+    if (engine == ENGINE_TMA4) {   // 128 threads, 2x2 cells each, unrolled stages
+        const size_t sm = tma4_smem_bytes<T>();
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            attr = true;
+        }
+        step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP><<<grid, dim3(32, 4, 1), sm, s>>>(a, maps);
+    } else if (engine == ENGINE_TMA) {   // 256 threads, 2 cells each
+        const size_t sm = tma_smem_bytes<T>();
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(step_kernel_tma<T, FL, FAST, ACC, CHK, SUP>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            attr = true;
+        }
+        step_kernel_tma<T, FL, FAST, ACC, CHK, SUP><<<grid, block, sm, s>>>(a, maps);
+    } else if (SUP == SUP_NONE) {   // pair / scalar kernels read a.sup_mode at run time
+        if (engine == ENGINE_PAIR)
+            step_kernel_pair<T, FL, FAST, ACC, CHK><<<grid, block, 0, s>>>(a);
+        else
+            step_kernel<T, FL, FAST, ACC, CHK><<<grid, block, 0, s>>>(a);
+    }
+}
+
+template <typename T, int FL, bool FAST, bool ACC, bool CHK>
+void go_step_sup(int engine, int sup, dim3 grid, dim3 block, cudaStream_t s,
+                 const StepArgs<T>& a, const TmaMaps& maps) {
+    if (engine != ENGINE_TMA && engine != ENGINE_TMA4) sup = SUP_NONE;
+    if (sup == SUP_GATHER) go_step<T, FL, FAST, ACC, CHK, SUP_GATHER>(engine, grid, block, s, a, maps);
+    else if (sup == SUP_INJECT) go_step<T, FL, FAST, ACC, CHK, SUP_INJECT>(engine, grid, block, s, a, maps);
+    else go_step<T, FL, FAST, ACC, CHK, SUP_NONE>(engine, grid, block, s, a, maps);
+}
+
+template <typename T, int FL, bool FAST>
+void go_step_ac(int engine, const StepSel& k, dim3 grid, dim3 block, cudaStream_t s,
+                const StepArgs<T>& a, const TmaMaps& maps) {
+    if (k.acc) {
+        if (k.check) go_step_sup<T, FL, FAST, true, true>(engine, k.sup, grid, block, s, a, maps);
+        else go_step_sup<T, FL, FAST, true, false>(engine, k.sup, grid, block, s, a, maps);
+    } else {
+        if (k.check) go_step_sup<T, FL, FAST, false, true>(engine, k.sup, grid, block, s, a, maps);
+        else go_step_sup<T, FL, FAST, false, false>(engine, k.sup, grid, block, s, a, maps);
+    }
+}
+
+template <typename T>
+void launch_step_engine(int engine, const StepSel& k, dim3 grid, dim3 block, cudaStream_t s,
+                        const StepArgs<T>& a, const TmaMaps& maps) {
+    if (k.flavor == RHO_SCALED) {
+        if (k.fast) go_step_ac<T, RHO_SCALED, true>(engine, k, grid, block, s, a, maps);
+        else go_step_ac<T, RHO_SCALED, false>(engine, k, grid, block, s, a, maps);
+    } else {
+        if (k.fast) go_step_ac<T, ACOUSTIC, true>(engine, k, grid, block, s, a, maps);
+        else go_step_ac<T, ACOUSTIC, false>(engine, k, grid, block, s, a, maps);
+    }
+}
+
+template <typename T, int FL, bool ACC, int SUP>
+void go_step2(dim3 grid, cudaStream_t s, const Step2Args<T>& a, const Tma2Maps& maps) {
+    const size_t sm = step2_smem_bytes<T>();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(step2_kernel_tma<T, FL, true, ACC, SUP>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        attr = true;
+    }
+    step2_kernel_tma<T, FL, true, ACC, SUP><<<grid, dim3(32, 4, 1), sm, s>>>(a, maps);
+}
+
+template <typename T, int FL, bool ACC>
+void go_step2_sup(int sup, dim3 grid, cudaStream_t s, const Step2Args<T>& a, const Tma2Maps& maps) {
+    if (sup == SUP_GATHER) go_step2<T, FL, ACC, SUP_GATHER>(grid, s, a, maps);
+    else if (sup == SUP_INJECT) go_step2<T, FL, ACC, SUP_INJECT>(grid, s, a, maps);
+    else go_step2<T, FL, ACC, SUP_NONE>(grid, s, a, maps);
+}
+
+template <typename T>
+void launch_step2_engine(const StepSel& k, dim3 grid, cudaStream_t s, const Step2Args<T>& a,
+                         const Tma2Maps& maps) {
+    if (k.flavor == RHO_SCALED) {
+        if (k.acc) go_step2_sup<T, RHO_SCALED, true>(k.sup, grid, s, a, maps);
+        else go_step2_sup<T, RHO_SCALED, false>(k.sup, grid, s, a, maps);
+    } else {
+        if (k.acc) go_step2_sup<T, ACOUSTIC, true>(k.sup, grid, s, a, maps);
+        else go_step2_sup<T, ACOUSTIC, false>(k.sup, grid, s, a, maps);
+    }
+}
+
+}  // namespace wb

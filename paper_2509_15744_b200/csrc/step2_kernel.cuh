@@ -134,9 +134,10 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     const int dL = kA > 0 ? 1 : 0, dR = kA + 2 < n2 ? 1 : 0;   // k-1 / k+2 inside
     const int oA = ra * W + cA, oB = oA + W;
     const int oU = rU * W + cA, oD = rD * W + cA;
-    // ring cells: slot 0 = tid, slot 1 = tid + 128 (warp 0, lanes < NRING-128).
-    // Tiles divide the grid, so an in-grid ring cell has in-grid neighbours.
-    int oR[2];
+    // ring cells: slot 0 = tid, slot 1 = tid + 128 (warp 0, lanes < NRING-128);
+    // rnb packs which neighbours lie inside the grid (bit 0 k-1, 1 k+1, 2 j-1,
+    // 3 j+1) — outside ones mirror to the cell itself
+    int oR[2], rnb[2];
     bool rg_ok[2];
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
@@ -148,7 +149,13 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         else if (q < NRING) { jj = j0 + (q - 2 * (PBX + 2) - BY); kk = k0 + PBX; }
         rg_ok[t] = q < NRING && jj >= 0 && jj < n1 && kk >= 0 && kk < n2;
         oR[t] = rg_ok[t] ? (jj - j0 + 2) * W + (kk - k0 + HO) : oA;
+        rnb[t] = (kk > 0 ? 1 : 0) | (kk < n2 - 1 ? 2 : 0) | (jj > 0 ? 4 : 0) | (jj < n1 - 1 ? 8 : 0);
     }
+    struct RNb { int l, r, u, d; };
+    auto ring_nb = [&](int t) {
+        const int o = oR[t], f = rnb[t];
+        return RNb{o - (f & 1), o + ((f >> 1) & 1), o - W * ((f >> 2) & 1), o + W * ((f >> 3) & 1)};
+    };
     const bool ring1 = tid < NRING - T2_THREADS;       // warp-uniform except warp 0
     // m-halo slots: rows {0,1,10,11} x cols HO-2..HO+65 (3 per thread) and the
     // side columns HO-2, HO-1, HO+64, HO+65 of rows 2..9 (warp 0)
@@ -209,11 +216,12 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     };
     // ring-cell in-plane faces (k lo, k hi, j lo, j hi)
     struct RFaces { T kl, kh, jl, jh; };
-    auto ring_faces = [&](const T* sm, int o) {
+    auto ring_faces = [&](const T* sm, int t) {
         RFaces f;
-        const T m = sm[o];
-        f.kl = face(sm[o - 1], m); f.kh = face(m, sm[o + 1]);
-        f.jl = face(sm[o - W], m); f.jh = face(m, sm[o + W]);
+        const RNb nb = ring_nb(t);
+        const T m = sm[oR[t]];
+        f.kl = face(sm[nb.l], m); f.kh = face(m, sm[nb.r]);
+        f.jl = face(sm[nb.u], m); f.jh = face(m, sm[nb.d]);
         return f;
     };
 
@@ -303,7 +311,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     m_halo(&st[0].G[0][0], SMb);
     __syncthreads();
     Faces F0 = own_faces(SMb);
-    RFaces RF0[2] = {ring_faces(SMb, oR[0]), ring_faces(SMb, oR[1])};
+    RFaces RF0[2] = {ring_faces(SMb, 0), ring_faces(SMb, 1)};
 
     // step n+1 state: material of the previous step-n plane, u^{n+1} queue
     Faces F1 = F0;
@@ -481,10 +489,11 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
             if (t == 1 && !ring1) continue;
             if (!rg_ok[t]) continue;
             const int o = oR[t];
+            const RNb nbo = ring_nb(t);
             const T u0 = run0[t];
             T kap;
             const T coef = MT::coef(M, rg0[t], kap);
-            T v = cell(u0, runp[t], rum[t], SU[o + W], SU[o - W], SU[o + 1], SU[o - 1],
+            T v = cell(u0, runp[t], rum[t], SU[nbo.d], SU[nbo.u], SU[nbo.r], SU[nbo.l],
                        face(rm0[t], rmp[t]), rw0[t], RF0[t].jh, RF0[t].jl, RF0[t].kh, RF0[t].kl,
                        coef, SP[o]);
             if (my_src || SUP == SUP_INJECT) {
@@ -507,8 +516,8 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         RFaces RFn[2] = {RF0[0], RF0[1]};
         if (next) {
             Fn = own_faces(SMn);
-            RFn[0] = ring_faces(SMn, oR[0]);
-            if (ring1) RFn[1] = ring_faces(SMn, oR[1]);
+            RFn[0] = ring_faces(SMn, 0);
+            if (ring1) RFn[1] = ring_faces(SMn, 1);
         }
         // step-(n+1) material for plane p (used at the next plane)
         F1 = F0;

@@ -56,6 +56,8 @@ struct wo_ctx {
     int use_two_step = 1;              // wo_set_option(WO_OPT_TWO_STEP)
     int t2_state = 0;                  // two-step tensor maps: 0 not built, 1 ready, -1 no
     Tma2Maps t2maps;
+    char* mat4 = nullptr;              // coef | +k | +j | +i faces (two-step passes)
+    bool mat4_valid = false;           // computed for the current material
     int64_t pair_launches = 0;
     int tma_state = 0;                 // 0 not built, 1 maps ready, -1 not eligible
     TmaMaps tmaps;                     // tensor maps of gamma, u[0], u[1], acc
@@ -401,15 +403,42 @@ int ensure_four(wo_ctx* ctx) {
     return WO_OK;
 }
 
+// coef and face arrays of the current material for the two-step kernel
+int ensure_mat4(wo_ctx* ctx) {
+    const size_t fb = (size_t)ctx->cells() * ctx->itemsize;
+    if (!ctx->mat4) {
+        int rc = dev_alloc(ctx, (void**)&ctx->mat4, 4 * fb);
+        if (rc) return rc;
+        ctx->t2_state = 0;
+        ctx->mat4_valid = false;
+    }
+    if (!ctx->mat4_valid) {
+        char* g = ctx->base0(ctx->gamma);
+        if (ctx->itemsize == 4)
+            launch_material4<float>(ctx->flavor, ctx->stream, reinterpret_cast<const float*>(g),
+                                    mat_scalars<float>(ctx), ctx->kn0, ctx->kn1, ctx->kn2,
+                                    reinterpret_cast<float*>(ctx->mat4));
+        else
+            launch_material4<double>(ctx->flavor, ctx->stream, reinterpret_cast<const double*>(g),
+                                     mat_scalars<double>(ctx), ctx->kn0, ctx->kn1, ctx->kn2,
+                                     reinterpret_cast<double*>(ctx->mat4));
+        ctx->launches++;
+        CK(cudaGetLastError());
+        ctx->mat4_valid = true;
+    }
+    return WO_OK;
+}
+
 bool pair_ready(wo_ctx* ctx) {
     if (!ctx->use_two_step || !ctx->use_tma || !ctx->use_pair || ctx->has_lo || ctx->has_hi ||
-        !ctx->fast_div || ctx->kn2 % PBX || ctx->kn1 % BY)
+        !ctx->material_set || ctx->kn2 % PBX || ctx->kn1 % BY)
         return false;
-    if (ensure_four(ctx)) return false;
+    if (ensure_four(ctx) || ensure_mat4(ctx)) return false;
     if (ctx->t2_state == 0) {
         ctx->t2_state = -1;
         const uint64_t np = (uint64_t)ctx->kn0;
         const uint32_t hw = ctx->itemsize == 4 ? th_w<float>() : th_w<double>();
+        const size_t fb = (size_t)ctx->cells() * ctx->itemsize;
         bool ok = true;
         for (int b = 0; b < 4; ++b) {
             ok &= make_map(&ctx->t2maps.u_r2[b], ctx->u[b], ctx->itemsize, ctx->kn2, ctx->kn1, np,
@@ -417,8 +446,14 @@ bool pair_ready(wo_ctx* ctx) {
             ok &= make_map(&ctx->t2maps.u_r1[b], ctx->u[b], ctx->itemsize, ctx->kn2, ctx->kn1, np,
                            hw, R1_H);
         }
-        ok &= make_map(&ctx->t2maps.g_r2, ctx->gamma, ctx->itemsize, ctx->kn2, ctx->kn1, np, hw,
-                       R2_H);
+        ok &= make_map(&ctx->t2maps.c_r1, ctx->mat4, ctx->itemsize, ctx->kn2, ctx->kn1, np, hw,
+                       R1_H);
+        ok &= make_map(&ctx->t2maps.fk_r1, ctx->mat4 + fb, ctx->itemsize, ctx->kn2, ctx->kn1, np,
+                       hw, R1_H);
+        ok &= make_map(&ctx->t2maps.fj_r2, ctx->mat4 + 2 * fb, ctx->itemsize, ctx->kn2, ctx->kn1,
+                       np, hw, R2_H);
+        ok &= make_map(&ctx->t2maps.fi_r1, ctx->mat4 + 3 * fb, ctx->itemsize, ctx->kn2, ctx->kn1,
+                       np, hw, R1_H);
         ok &= make_map(&ctx->t2maps.a_ctr, ctx->acc, ctx->itemsize, ctx->kn2, ctx->kn1, np, PBX, BY);
         if (ok) ctx->t2_state = 1;
     }
@@ -452,6 +487,7 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     a.gamma = reinterpret_cast<const T*>(ctx->base0(ctx->gamma));
     a.u_prev = reinterpret_cast<const T*>(ctx->uprev());
     a.u_cur = reinterpret_cast<const T*>(ctx->ucur());
+    a.fi = reinterpret_cast<const T*>(ctx->mat4 + 3 * (size_t)ctx->cells() * ctx->itemsize);
     a.out1 = reinterpret_cast<T*>(ctx->base0(ctx->u[x[0]]));
     a.out2 = reinterpret_cast<T*>(ctx->base0(ctx->u[x[1]]));
     a.acc = reinterpret_cast<T*>(ctx->acc);
@@ -1063,7 +1099,8 @@ void wo_destroy(wo_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    void* bufs[] = {ctx->gamma, ctx->u[0], ctx->u[1], ctx->u[2], ctx->u[3], ctx->acc, ctx->mask, ctx->prefix,
+    void* bufs[] = {ctx->gamma, ctx->u[0], ctx->u[1], ctx->u[2], ctx->u[3], ctx->mat4, ctx->acc,
+                    ctx->mask, ctx->prefix,
                     ctx->store, ctx->measured, ctx->partial, ctx->cost, ctx->maxslots,
                     ctx->f_idx, ctx->f_vals, ctx->f_dense, ctx->hist, ctx->u3};
     for (void* b : bufs)
@@ -1094,6 +1131,7 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
         CK(cudaStreamSynchronize(ctx->stream));
     }
     ctx->material_set = true;
+    ctx->mat4_valid = false;
     return verify_fast_div(ctx);
 }
 

@@ -28,10 +28,15 @@ template <typename T>
 void launch_step_engine(int engine, const StepSel& k, dim3 grid, dim3 block, cudaStream_t s,
                         const StepArgs<T>& a, const TmaMaps& maps);
 
-// two-step pass (fast division only; checks are runtime flags in the args)
+// two-step pass (no divisions on the dense path; checks are runtime flags)
 template <typename T>
 void launch_step2_engine(const StepSel& k, dim3 grid, cudaStream_t s, const Step2Args<T>& a,
                          const Tma2Maps& maps);
+
+// coef | +k | +j | +i face arrays (4 consecutive fields at out) of a material
+template <typename T>
+void launch_material4(int flavor, cudaStream_t s, const T* gamma, const MatScalars<T>& M, int n0,
+                      int n1, int n2, T* out);
 
 
 }  // namespace wb

@@ -4,4 +4,6 @@
 namespace wb {
 template void launch_step2_engine<float>(const StepSel&, dim3, cudaStream_t,
                                       const Step2Args<float>&, const Tma2Maps&);
+template void launch_material4<float>(int, cudaStream_t, const float*, const MatScalars<float>&, int,
+                                     int, int, float*);
 }  // namespace wb

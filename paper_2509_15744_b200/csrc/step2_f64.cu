@@ -4,4 +4,6 @@
 namespace wb {
 template void launch_step2_engine<double>(const StepSel&, dim3, cudaStream_t,
                                       const Step2Args<double>&, const Tma2Maps&);
+template void launch_material4<double>(int, cudaStream_t, const double*, const MatScalars<double>&, int,
+                                     int, int, double*);
 }  // namespace wb

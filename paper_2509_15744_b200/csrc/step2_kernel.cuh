@@ -4,29 +4,33 @@
 // backward: n, n-1), each with the exact per-cell arithmetic of step_kernel
 // (stencil, injections, support gather/inject, self-kernel increment,
 // stability max — see step_kernel.cuh for the reference mapping and the
-// mirrored-boundary argument).  Per plane p of the 2.5D march:
-//   a  wait for plane p+1 (TMA ring); m(p+1) of the tile (registers, owners
-//      store it) and of the 2-cell halo (fixed per-thread slots) -> SM
-//   b  __syncthreads; refill the stage of plane p-1
+// mirrored-boundary argument).
+//
+// Material: the face weights and coef are time-invariant, so a one-off pass
+// (material4_kernel) stores them — coef, the +k, +j and +i face weights of
+// every cell, computed with the same operations the single-step kernel
+// applies to gamma (solver.py:93-119) — and this kernel streams them instead
+// of recomputing reciprocals: its dense arithmetic is only the face sum and
+// the kernel increment.  A face leading out of the grid is stored as 0; it
+// only ever multiplies a mirrored difference (u - u) = 0.
+//
+// Per plane p of the 2.5D march (TMA ring of T2_NS stages, one barrier):
+//   a  wait for plane p+1; u^n(p+1) of the tile + ring (registers)
+//   b  __syncthreads; refill the stage of plane p-1 with plane p+T2_NS-1
 //   d  step n at plane p on the tile AND a one-cell ring around it (the ring
 //      is recomputed redundantly so step n+1 never needs another CTA's data);
 //      u^{n+1}(p) goes to a shared-memory plane X
 //   c  step n+1 at plane p-1 on the tile, from X(p-1), the register queue of
-//      u^{n+1}, and the material coefficients kept from step n's plane p-1
-//   e  face weights of plane p+1 (registers)
-// HBM traffic per fp32 cell-update: (read u^{n-1}, u^n, gamma, acc + write
-// u^{n+1}, u^{n+2}, acc) / 2 = 14 B instead of 24 B, and m, coef and the face
-// weights are computed once for both steps.  u^{n+1} and u^{n+2} go to two
+//      u^{n+1}, and plane p-1's material kept in registers
+// HBM traffic per fp32 cell and pass: read u^{n-1}, u^n, acc, coef and three
+// face arrays, write u^{n+1}, u^{n+2}, acc = 40 B for two cell-updates
+// (20 B each, against 24 B for a single step).  u^{n+1} and u^{n+2} go to two
 // fresh buffers (other CTAs still read u^{n-1} / u^n rings), so the window
 // rotates through four level buffers.  Single-domain contexts only (a slab
 // would need ghost planes two deep).
-//
-// Every shared-memory access is a per-thread offset (computed once) from the
-// plane's stage / buffer base.
 #pragma once
 
 #include <type_traits>
-#include <utility>
 
 #include "common.cuh"
 #include "step_kernel.cuh"
@@ -36,15 +40,16 @@
 namespace wb {
 
 constexpr int T2_THREADS = 128;
-constexpr int T2_NS = 4;             // TMA ring stages
+constexpr int T2_NS = 3;             // TMA ring stages
 constexpr int R2_H = BY + 4;         // rows j0-2 .. j0+9
 constexpr int R1_H = BY + 2;         // rows j0-1 .. j0+8
 constexpr int NRING = 2 * (PBX + 2) + 2 * BY;   // one-cell ring around a 64 x 8 tile
 
 template <typename T> struct Step2Args {
-    const T* gamma;
+    const T* gamma;    // sparse use only (nodal force coefficient)
     const T* u_prev;   // u^{n-1}
     const T* u_cur;    // u^n
+    const T* fi;       // +i face weights (plane below the chunk)
     T* out1;           // u^{n+1}
     T* out2;           // u^{n+2}
     T* acc;
@@ -67,30 +72,57 @@ template <typename T> struct Step2Args {
 struct Tma2Maps {
     CUtensorMap u_r2[4];   // level buffers, (W, R2_H) boxes at (k0-HO, j0-2)
     CUtensorMap u_r1[4];   // level buffers, (W, R1_H) boxes at (k0-HO, j0-1)
-    CUtensorMap g_r2;      // gamma, (W, R2_H)
+    CUtensorMap fj_r2;     // +j faces, (W, R2_H)
+    CUtensorMap c_r1;      // coef, (W, R1_H)
+    CUtensorMap fk_r1;     // +k faces, (W, R1_H)
+    CUtensorMap fi_r1;     // +i faces, (W, R1_H)
     CUtensorMap a_ctr;     // accumulator, (PBX, BY)
     int prev, cur;         // buffer indices of u^{n-1}, u^n
 };
 
 template <typename T> struct Tma2Stage {
     alignas(128) T U[R2_H][th_w<T>()];
-    alignas(128) T G[R2_H][th_w<T>()];
+    alignas(128) T FJ[R2_H][th_w<T>()];
     alignas(128) T P[R1_H][th_w<T>()];
+    alignas(128) T C[R1_H][th_w<T>()];
+    alignas(128) T FK[R1_H][th_w<T>()];
+    alignas(128) T FI[R1_H][th_w<T>()];
     alignas(128) T A[BY][PBX];
 };
 
 template <typename T>
 constexpr size_t step2_smem_bytes() {
-    return T2_NS * sizeof(Tma2Stage<T>) + 2 * sizeof(T) * R2_H * th_w<T>() /* m planes */ +
-           2 * sizeof(T) * R2_H * th_w<T>() /* u^{n+1} planes */ +
+    return T2_NS * sizeof(Tma2Stage<T>) + 2 * sizeof(T) * R2_H * th_w<T>() /* u^{n+1} planes */ +
            T2_NS * sizeof(unsigned long long) + 128;
 }
 
-template <typename T, int FLAVOR, bool FAST, bool ACC, int SUP>
+// coef and the +k / +j / +i face weights of every cell (0 across the grid
+// edge), with the operations of Mat (solver.py:93-119) — the intrinsic
+// divisions, which the fast path is verified against.
+template <typename T, int FLAVOR>
+__global__ void material4_kernel(const T* __restrict__ gamma, MatScalars<T> M, int n0, int n1,
+                                 int n2, T* __restrict__ coef, T* __restrict__ fk,
+                                 T* __restrict__ fj, T* __restrict__ fi) {
+    using P = Mat<T, FLAVOR, false>;
+    const long long pl = (long long)n1 * n2, N = pl * n0;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < N;
+         c += (long long)gridDim.x * blockDim.x) {
+        const int k = (int)(c % n2), j = (int)((c / n2) % n1), i = (int)(c / pl);
+        const T g = gamma[c];
+        const T m = P::m(M, g);
+        T kap;
+        coef[c] = P::coef(M, g, kap);
+        fk[c] = k + 1 < n2 ? P::face(m, P::m(M, gamma[c + 1])) : T(0);
+        fj[c] = j + 1 < n1 ? P::face(m, P::m(M, gamma[c + n2])) : T(0);
+        fi[c] = i + 1 < n0 ? P::face(m, P::m(M, gamma[c + pl])) : T(0);
+    }
+}
+
+template <typename T, int FLAVOR, bool ACC, int SUP>
 __global__ void __launch_bounds__(T2_THREADS, sizeof(T) == 4 ? 3 : 1)
 step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__ Tma2Maps maps) {
     using Tr = FTraits<T>;
-    using MT = Mat<T, FLAVOR, FAST>;
+    using MP = Mat<T, FLAVOR, false>;   // sparse force coefficients only
     using V = typename Pair<T>::V;
     using Bits = typename Tr::Bits;
     constexpr int W = th_w<T>(), HO = th_ho<T>();
@@ -99,8 +131,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     unsigned char* smem_raw =
         smem_dyn + ((128u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_dyn)) & 127u)) & 127u);
     Tma2Stage<T>* st = reinterpret_cast<Tma2Stage<T>*>(smem_raw);
-    T* SMb = reinterpret_cast<T*>(smem_raw + T2_NS * sizeof(Tma2Stage<T>));   // SM[2][PL]
-    T* Xb = SMb + 2 * PL;                                                      // X[2][PL]
+    T* Xb = reinterpret_cast<T*>(smem_raw + T2_NS * sizeof(Tma2Stage<T>));   // X[2][PL]
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(Xb + 2 * PL);
     __shared__ Bits smax[2][T2_THREADS / 32];
 
@@ -114,10 +145,10 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     const int i1 = min(i0 + a.chunk, n0);
     const int pbeg = max(i0 - 1, 0);           // step-n planes of this chunk
     const int pfin = min(i1, n0 - 1);
-    const MatScalars<T>& M = a.mat;
 
     // ---- per-thread offsets in the R2 frame (rows j0-2.., cols k0-HO..) ----
-    // tile rows a, b; clamped (mirrored) outer neighbours at the grid edge
+    // tile rows a, b; clamped (mirrored) outer neighbours at the grid edge.
+    // The R1-frame arrays are addressed through bases shifted by one row.
     const int ra = 2 * ty + 2, cA = HO + 2 * tx;
     const int rU = min(max(ja - 1, 0), n1 - 1) - j0 + 2;
     const int rD = min(max(ja + 2, 0), n1 - 1) - j0 + 2;
@@ -141,16 +172,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         oR[t] = rg_ok[t] ? (jj - j0 + 2) * W + (kk - k0 + HO) : oA;
         rnb[t] = (kk > 0 ? 1 : 0) | (kk < n2 - 1 ? 2 : 0) | (jj > 0 ? 4 : 0) | (jj < n1 - 1 ? 8 : 0);
     }
-    struct RNb { int l, r, u, d; };
-    auto ring_nb = [&](int t) {
-        const int o = oR[t], f = rnb[t];
-        return RNb{o - (f & 1), o + ((f >> 1) & 1), o - W * ((f >> 2) & 1), o + W * ((f >> 3) & 1)};
-    };
     const bool ring1 = tid < NRING - T2_THREADS;       // warp-uniform except warp 0
-    // m-halo slots: rows {0,1,10,11} x cols HO-2..HO+65 (3 per thread) and the
-    // side columns HO-2, HO-1, HO+64, HO+65 of rows 2..9 (warp 0)
-    const int oH = (ty < 2 ? ty : ty + BY) * W + HO - 2 + tx;
-    const int oS = (2 + (tx >> 2)) * W + ((tx & 3) < 2 ? HO - 2 + (tx & 3) : HO + PBX - 2 + (tx & 3));
 
     unsigned my_src = 0;   // sources in tile + ring and the step-n plane range
     for (int s = 0; s < a.n_src; ++s)
@@ -159,15 +181,18 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
             my_src |= 1u << s;
 
     constexpr unsigned STAGE_BYTES =
-        (unsigned)(sizeof(T) * ((2 * R2_H + R1_H) * W + (ACC ? BY * PBX : 0)));
+        (unsigned)(sizeof(T) * ((2 * R2_H + 4 * R1_H) * W + (ACC ? BY * PBX : 0)));
     const CUtensorMap* mU = pick_map(maps.u_r2, maps.cur);
     const CUtensorMap* mP = pick_map(maps.u_r1, maps.prev);
     auto issue = [&](int p, int s) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[s], STAGE_BYTES);
         tma_load_3d(&st[s].U[0][0], mU, k0 - HO, j0 - 2, p, &bar[s]);
-        tma_load_3d(&st[s].G[0][0], &maps.g_r2, k0 - HO, j0 - 2, p, &bar[s]);
+        tma_load_3d(&st[s].FJ[0][0], &maps.fj_r2, k0 - HO, j0 - 2, p, &bar[s]);
         tma_load_3d(&st[s].P[0][0], mP, k0 - HO, j0 - 1, p, &bar[s]);
+        tma_load_3d(&st[s].C[0][0], &maps.c_r1, k0 - HO, j0 - 1, p, &bar[s]);
+        tma_load_3d(&st[s].FK[0][0], &maps.fk_r1, k0 - HO, j0 - 1, p, &bar[s]);
+        tma_load_3d(&st[s].FI[0][0], &maps.fi_r1, k0 - HO, j0 - 1, p, &bar[s]);
         if (ACC) tma_load_3d(&st[s].A[0][0], &maps.a_ctr, k0, j0, p, &bar[s]);
     };
     if (tid == 0) {
@@ -180,39 +205,9 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
 
     auto ldv = [](const T* p) { return *reinterpret_cast<const V*>(p); };
     auto stv = [](T* p, V v) { *reinterpret_cast<V*>(p) = v; };
-    auto face = [](T lo, T hi) { return MT::face(lo, hi); };
-    auto mv = [&](V g) { return V{MT::m(M, g.x), MT::m(M, g.y)}; };
-
-    // m of the halo of a plane (tile m is stored by the owners)
-    auto m_halo = [&](const T* G, T* D) {
-        D[oH] = MT::m(M, G[oH]);
-        D[oH + 32] = MT::m(M, G[oH + 32]);
-        if (tx < 4) D[oH + 64] = MT::m(M, G[oH + 64]);
-        if (ty == 0) D[oS] = MT::m(M, G[oS]);
-    };
-
-    // own faces of a plane (2x2 block) from its m-plane
-    struct Faces { T kLa, kIa, kRa, kLb, kIb, kRb; V jlo, jab, jhi; };
-    auto own_faces = [&](const T* sm) {
-        Faces f;
-        const V ma = ldv(sm + oA), mb = ldv(sm + oB);
-        f.kLa = face(sm[oA - dL], ma.x); f.kIa = face(ma.x, ma.y); f.kRa = face(ma.y, sm[oA + 1 + dR]);
-        f.kLb = face(sm[oB - dL], mb.x); f.kIb = face(mb.x, mb.y); f.kRb = face(mb.y, sm[oB + 1 + dR]);
-        const V mu = ldv(sm + oU), md = ldv(sm + oD);
-        f.jlo = V{face(mu.x, ma.x), face(mu.y, ma.y)};
-        f.jab = V{face(ma.x, mb.x), face(ma.y, mb.y)};
-        f.jhi = V{face(mb.x, md.x), face(mb.y, md.y)};
-        return f;
-    };
-    // ring-cell in-plane faces (k lo, k hi, j lo, j hi)
-    struct RFaces { T kl, kh, jl, jh; };
-    auto ring_faces = [&](const T* sm, int t) {
-        RFaces f;
-        const RNb nb = ring_nb(t);
-        const T m = sm[oR[t]];
-        f.kl = face(sm[nb.l], m); f.kh = face(m, sm[nb.r]);
-        f.jl = face(sm[nb.u], m); f.jh = face(m, sm[nb.d]);
-        return f;
+    auto ring_nb = [&](int t, int& l, int& r, int& u, int& d) {
+        const int o = oR[t], f = rnb[t];
+        l = o - (f & 1); r = o + ((f >> 1) & 1); u = o - W * ((f >> 2) & 1); d = o + W * ((f >> 3) & 1);
     };
 
     auto cell = [&](T u0, T up1, T um1, T ujp, T ujm, T ukp, T ukm, T w0hi, T w0lo, T fjhi, T fjlo,
@@ -233,15 +228,18 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         const T g2 = (ukp - ukm) * a.inv2dx;
         return accv + a.sdt * ((a.cv * va) * va + a.cg * (((g0 * g0) + (g1 * g1)) + (g2 * g2)));
     };
-    // nodal sources at (plane, j, k) for the step's amplitudes; g the cell's
-    // gamma (fc recomputed from it exactly as the single-step kernel does)
-    auto inject_src = [&](int p, int jj, int kk, T g, const T* val, T& o) {
+    // nodal force coefficient of a cell from its gamma (sparse; solver.py:98,110)
+    auto fcoef = [&](int flat) {
+        const T g = __ldg(a.gamma + flat);
+        T kap;
+        (void)MP::coef(a.mat, g, kap);
+        return MP::fc(a.mat, g, kap);
+    };
+    // nodal sources at (plane, j, k) for the step's amplitudes
+    auto inject_src = [&](int p, int jj, int kk, const T* val, T& o) {
         for (int q = 0; q < a.n_src; ++q)
-            if (((my_src >> q) & 1u) && p == a.src_i[q] && jj == a.src_j[q] && kk == a.src_k[q]) {
-                T kap;
-                (void)MT::coef(M, g, kap);
-                o = o + MT::fc(M, g, kap) * val[q];
-            }
+            if (((my_src >> q) & 1u) && p == a.src_i[q] && jj == a.src_j[q] && kk == a.src_k[q])
+                o = o + fcoef(p * plane + jj * n2 + kk) * val[q];
     };
     // support bit / compact index of cell (p, jj, kk)
     auto sup_index = [&](int p, int jj, int kk) -> int {
@@ -252,101 +250,87 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         if (!((w >> bit) & 1u)) return -1;
         return __ldg(a.sup_prefix + (flat >> 5)) + __popc(w & ((1u << bit) - 1u));
     };
-    auto sup_inject = [&](int q, T g, T& o, const T* row) {
-        T kap;
-        (void)MT::coef(M, g, kap);
-        o = o + MT::fc(M, g, kap) * ldg(row + q);
+    // injections of one step into a tile 2x2 block at plane p: sources, then
+    // the support (solver.py:167-170); gather records the pre-step level
+    auto tile_inject = [&](int p, V& oa, V& ob, V ua, V ub, const T* val, T* row, bool gather_ok) {
+        if (my_src) {
+            inject_src(p, ja, kA, val, oa.x);
+            inject_src(p, ja, kA + 1, val, oa.y);
+            inject_src(p, ja + 1, kA, val, ob.x);
+            inject_src(p, ja + 1, kA + 1, val, ob.y);
+        }
+        if (SUP != SUP_NONE && p >= a.sup_lo && p <= a.sup_hi) {
+            const T uo[4] = {ua.x, ua.y, ub.x, ub.y};
+            T* oo[4] = {&oa.x, &oa.y, &ob.x, &ob.y};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int jj = ja + (c >> 1), kk = kA + (c & 1);
+                const int qi = sup_index(p, jj, kk);
+                if (qi >= 0) {
+                    if (SUP == SUP_GATHER) { if (gather_ok) row[qi] = uo[c]; }
+                    else *oo[c] = *oo[c] + fcoef(p * plane + jj * n2 + kk) * ldg(row + qi);
+                }
+            }
+        }
     };
 
     // ---------------- prologue: plane pbeg ----------------
     const int cofs = ja * n2 + kA;
     const bool has_m0 = pbeg > 0;
-    V unm_a, unm_b, gm_a, gm_b;                  // plane pbeg-1 (mirror at 0)
-    if (has_m0) {
-        unm_a = __ldg(reinterpret_cast<const V*>(a.u_cur + (pbeg - 1) * plane + cofs));
-        unm_b = __ldg(reinterpret_cast<const V*>(a.u_cur + (pbeg - 1) * plane + cofs + n2));
-        gm_a = __ldg(reinterpret_cast<const V*>(a.gamma + (pbeg - 1) * plane + cofs));
-        gm_b = __ldg(reinterpret_cast<const V*>(a.gamma + (pbeg - 1) * plane + cofs + n2));
-    }
     auto ring_gofs = [&](int t) {   // global offset (in plane) of ring slot t
         const int r = oR[t] / W, c = oR[t] - r * W;
         return (r + j0 - 2) * n2 + (c + k0 - HO);
     };
-    T rum[2] = {T(0), T(0)}, rgm[2] = {T(1), T(1)};
+    V unm_a, unm_b, w0_a = {T(0), T(0)}, w0_b = {T(0), T(0)};   // plane pbeg-1 (mirror at 0)
+    T rum[2] = {T(0), T(0)}, rw0[2] = {T(0), T(0)};
+    if (has_m0) {
+        const int gm = (pbeg - 1) * plane;
+        unm_a = __ldg(reinterpret_cast<const V*>(a.u_cur + gm + cofs));
+        unm_b = __ldg(reinterpret_cast<const V*>(a.u_cur + gm + cofs + n2));
+        w0_a = __ldg(reinterpret_cast<const V*>(a.fi + gm + cofs));
+        w0_b = __ldg(reinterpret_cast<const V*>(a.fi + gm + cofs + n2));
 #pragma unroll
-    for (int t = 0; t < 2; ++t)
-        if (has_m0 && rg_ok[t]) {
-            const int go = (pbeg - 1) * plane + ring_gofs(t);
-            rum[t] = __ldg(a.u_cur + go);
-            rgm[t] = __ldg(a.gamma + go);
-        }
+        for (int t = 0; t < 2; ++t)
+            if (rg_ok[t]) {
+                rum[t] = __ldg(a.u_cur + gm + ring_gofs(t));
+                rw0[t] = __ldg(a.fi + gm + ring_gofs(t));
+            }
+    }
     mbar_wait(&bar[0], 0u);
     V un0_a = ldv(&st[0].U[0][0] + oA), un0_b = ldv(&st[0].U[0][0] + oB);
-    V g0_a = ldv(&st[0].G[0][0] + oA), g0_b = ldv(&st[0].G[0][0] + oB);
-    T run0[2], rg0[2];
+    T run0[2];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) { run0[t] = (&st[0].U[0][0])[oR[t]]; rg0[t] = (&st[0].G[0][0])[oR[t]]; }
+    for (int t = 0; t < 2; ++t) run0[t] = (&st[0].U[0][0])[oR[t]];
     if (!has_m0) {
-        unm_a = un0_a; unm_b = un0_b; gm_a = g0_a; gm_b = g0_b;
-        rum[0] = run0[0]; rum[1] = run0[1]; rgm[0] = rg0[0]; rgm[1] = rg0[1];
+        unm_a = un0_a; unm_b = un0_b;
+        rum[0] = run0[0]; rum[1] = run0[1];
     }
-    V m0_a = mv(g0_a), m0_b = mv(g0_b);
-    V w0_a = {face(MT::m(M, gm_a.x), m0_a.x), face(MT::m(M, gm_a.y), m0_a.y)};
-    V w0_b = {face(MT::m(M, gm_b.x), m0_b.x), face(MT::m(M, gm_b.y), m0_b.y)};
-    T rm0[2], rw0[2];
-#pragma unroll
-    for (int t = 0; t < 2; ++t) { rm0[t] = MT::m(M, rg0[t]); rw0[t] = face(MT::m(M, rgm[t]), rm0[t]); }
-    stv(SMb + oA, m0_a);
-    stv(SMb + oB, m0_b);
-    m_halo(&st[0].G[0][0], SMb);
-    __syncthreads();
-    Faces F0 = own_faces(SMb);
-    RFaces RF0[2] = {ring_faces(SMb, 0), ring_faces(SMb, 1)};
 
     // step n+1 state: material of the previous step-n plane, u^{n+1} queue
-    Faces F1 = F0;
-    V w1lo_a = w0_a, w1lo_b = w0_b, w1hi_a = w0_a, w1hi_b = w0_b;
-    T c1[4] = {T(0), T(0), T(0), T(0)};
+    T f1_kLa = T(0), f1_kIa = T(0), f1_kRa = T(0), f1_kLb = T(0), f1_kIb = T(0), f1_kRb = T(0);
+    V f1_jlo = {T(0), T(0)}, f1_jab = f1_jlo, f1_jhi = f1_jlo;
+    V w1lo_a = f1_jlo, w1lo_b = f1_jlo, w1hi_a = f1_jlo, w1hi_b = f1_jlo;
+    V c1_a = f1_jlo, c1_b = f1_jlo;
     V x_m1a = un0_a, x_m1b = un0_b, x_0a = un0_a, x_0b = un0_b;   // u^{n+1}(p-2), (p-1)
     V un1_a = unm_a, un1_b = unm_b;                                // u^n(p-1)
     V acc1_a = {T(0), T(0)}, acc1_b = acc1_a;                      // acc after step n at p-1
     Bits lmax1 = 0, lmax2 = 0;
 
-    // step n+1 at plane q1 for the tile: x_p1 = u^{n+1}(q1+1) (registers)
+    // step n+1 at plane q1 for the tile: xp = u^{n+1}(q1+1) (registers)
     auto step2_tile = [&](int q1, const T* Xq, V xp_a, V xp_b) {
         const V xu = ldv(Xq + oU), xd = ldv(Xq + oD);
         const T xLa = Xq[oA - dL], xRa = Xq[oA + 1 + dR], xLb = Xq[oB - dL], xRb = Xq[oB + 1 + dR];
         V o2a, o2b;
         o2a.x = cell(x_0a.x, xp_a.x, x_m1a.x, x_0b.x, xu.x, x_0a.y, xLa, w1hi_a.x, w1lo_a.x,
-                     F1.jab.x, F1.jlo.x, F1.kIa, F1.kLa, c1[0], un1_a.x);
+                     f1_jab.x, f1_jlo.x, f1_kIa, f1_kLa, c1_a.x, un1_a.x);
         o2a.y = cell(x_0a.y, xp_a.y, x_m1a.y, x_0b.y, xu.y, xRa, x_0a.x, w1hi_a.y, w1lo_a.y,
-                     F1.jab.y, F1.jlo.y, F1.kRa, F1.kIa, c1[1], un1_a.y);
+                     f1_jab.y, f1_jlo.y, f1_kRa, f1_kIa, c1_a.y, un1_a.y);
         o2b.x = cell(x_0b.x, xp_b.x, x_m1b.x, xd.x, x_0a.x, x_0b.y, xLb, w1hi_b.x, w1lo_b.x,
-                     F1.jhi.x, F1.jab.x, F1.kIb, F1.kLb, c1[2], un1_b.x);
+                     f1_jhi.x, f1_jab.x, f1_kIb, f1_kLb, c1_b.x, un1_b.x);
         o2b.y = cell(x_0b.y, xp_b.y, x_m1b.y, xd.y, x_0a.y, xRb, x_0b.x, w1hi_b.y, w1lo_b.y,
-                     F1.jhi.y, F1.jab.y, F1.kRb, F1.kIb, c1[3], un1_b.y);
+                     f1_jhi.y, f1_jab.y, f1_kRb, f1_kIb, c1_b.y, un1_b.y);
+        tile_inject(q1, o2a, o2b, x_0a, x_0b, a.src_val2, a.row2, true);
         const int oc = q1 * plane + cofs;
-        if (my_src || SUP != SUP_NONE) {
-            const T* gq = a.gamma + oc;
-            if (my_src) {
-                inject_src(q1, ja, kA, __ldg(gq), a.src_val2, o2a.x);
-                inject_src(q1, ja, kA + 1, __ldg(gq + 1), a.src_val2, o2a.y);
-                inject_src(q1, ja + 1, kA, __ldg(gq + n2), a.src_val2, o2b.x);
-                inject_src(q1, ja + 1, kA + 1, __ldg(gq + n2 + 1), a.src_val2, o2b.y);
-            }
-            if (SUP != SUP_NONE) {
-                const T xo[4] = {x_0a.x, x_0a.y, x_0b.x, x_0b.y};
-                T* oo[4] = {&o2a.x, &o2a.y, &o2b.x, &o2b.y};
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const int q = sup_index(q1, ja + (c >> 1), kA + (c & 1));
-                    if (q >= 0) {
-                        if (SUP == SUP_GATHER) a.row2[q] = xo[c];
-                        else sup_inject(q, __ldg(gq + (c >> 1) * n2 + (c & 1)), *oo[c], a.row2);
-                    }
-                }
-            }
-        }
         if (ACC) {
             V fa, fb;
             fa.x = kinc(acc1_a.x, o2a.x, un1_a.x, xp_a.x, x_m1a.x, x_0b.x, xu.x, x_0a.y, xLa);
@@ -368,95 +352,61 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         }
     };
 
-    // one plane; q = stage of plane p, gpar = its mbarrier parity.  Kept as a
-    // rolled loop: the hot body is large and unrolled copies thrash the
-    // instruction cache (measured: 2.2x slower with a 4-plane unroll).
+    // one plane; q = stage of plane p, gpar = its mbarrier parity (rolled
+    // loop: unrolled copies of this body overflow the instruction cache)
     auto body = [&](int q, int p, unsigned gpar) {
         const int sn = q + 1 == T2_NS ? 0 : q + 1, sf = q == 0 ? T2_NS - 1 : q - 1;
-        const int b = (p - pbeg) & 1, nb = b ^ 1;
+        const int b = (p - pbeg) & 1;
         const unsigned pn = (q + 1 == T2_NS) ? 1u : 0u;   // parity flip for plane p+1
-        T* SMn = SMb + nb * PL;
         T* Xc = Xb + b * PL;
-        const T* Xp = Xb + nb * PL;
+        const T* Xp = Xb + (b ^ 1) * PL;
         const Tma2Stage<T>& S = st[q];
         const T* SU = &S.U[0][0];
-        const T* SP = &S.P[0][0] - W;     // P frame is the R2 frame shifted one row
-        const bool next = p + 1 <= pfin;   // plane p+1 in the ring (and a later step-n plane)
-        // ---- a: plane p+1 ----
-        V unp_a = un0_a, unp_b = un0_b, gp_a = g0_a, gp_b = g0_b;
-        T runp[2] = {run0[0], run0[1]}, rgp[2] = {rg0[0], rg0[1]};
-        if (next) {
+        const T* SFJ = &S.FJ[0][0];
+        const T* SP = &S.P[0][0] - W;     // R1 frame = R2 frame shifted one row
+        const T* SC = &S.C[0][0] - W;
+        const T* SFK = &S.FK[0][0] - W;
+        const T* SFI = &S.FI[0][0] - W;
+        // ---- a: u^n of plane p+1 ----
+        V unp_a = un0_a, unp_b = un0_b;
+        T runp[2] = {run0[0], run0[1]};
+        if (p + 1 <= pfin) {
             mbar_wait(&bar[sn], gpar ^ pn);
             const T* NU = &st[sn].U[0][0];
-            const T* NG = &st[sn].G[0][0];
             unp_a = ldv(NU + oA); unp_b = ldv(NU + oB);
-            gp_a = ldv(NG + oA); gp_b = ldv(NG + oB);
 #pragma unroll
-            for (int t = 0; t < 2; ++t) { runp[t] = NU[oR[t]]; rgp[t] = NG[oR[t]]; }
-            m_halo(NG, SMn);
+            for (int t = 0; t < 2; ++t) runp[t] = NU[oR[t]];
         } else if (p + 1 <= n0 - 1) {   // chunk end inside the domain: plane p+1 from HBM
             const int gp = (p + 1) * plane;
             unp_a = __ldg(reinterpret_cast<const V*>(a.u_cur + gp + cofs));
             unp_b = __ldg(reinterpret_cast<const V*>(a.u_cur + gp + cofs + n2));
-            gp_a = __ldg(reinterpret_cast<const V*>(a.gamma + gp + cofs));
-            gp_b = __ldg(reinterpret_cast<const V*>(a.gamma + gp + cofs + n2));
 #pragma unroll
             for (int t = 0; t < 2; ++t)
-                if (rg_ok[t]) {
-                    const int go = gp + ring_gofs(t);
-                    runp[t] = __ldg(a.u_cur + go);
-                    rgp[t] = __ldg(a.gamma + go);
-                }
-        }
-        const V mp_a = mv(gp_a), mp_b = mv(gp_b);
-        T rmp[2];
-#pragma unroll
-        for (int t = 0; t < 2; ++t) rmp[t] = MT::m(M, rgp[t]);
-        if (next) {
-            stv(SMn + oA, mp_a);
-            stv(SMn + oB, mp_b);
+                if (rg_ok[t]) runp[t] = __ldg(a.u_cur + gp + ring_gofs(t));
         }
         __syncthreads();
         if (tid == 0 && p > pbeg && p + T2_NS - 1 <= pfin) issue(p + T2_NS - 1, sf);
 
         // ---- d: step n at plane p (tile + ring) -> X[b] ----
-        const V wh_a = {face(m0_a.x, mp_a.x), face(m0_a.y, mp_a.y)};
-        const V wh_b = {face(m0_b.x, mp_b.x), face(m0_b.y, mp_b.y)};
-        T kp[4];
-        const T cf[4] = {MT::coef(M, g0_a.x, kp[0]), MT::coef(M, g0_a.y, kp[1]),
-                         MT::coef(M, g0_b.x, kp[2]), MT::coef(M, g0_b.y, kp[3])};
+        const V wh_a = ldv(SFI + oA), wh_b = ldv(SFI + oB);
+        const V cf_a = ldv(SC + oA), cf_b = ldv(SC + oB);
+        const V fka = ldv(SFK + oA), fkb = ldv(SFK + oB);        // (kI, kR) of rows a, b
+        const T kLa = SFK[oA - dL], kLb = SFK[oB - dL];
+        const V jlo = ldv(SFJ + oU), jab = ldv(SFJ + oA), jhi = ldv(SFJ + oB);
         const V uu = ldv(SU + oU), ud = ldv(SU + oD);
         const T uLa = SU[oA - dL], uRa = SU[oA + 1 + dR], uLb = SU[oB - dL], uRb = SU[oB + 1 + dR];
         const V pa = ldv(SP + oA), pb = ldv(SP + oB);
         V oa, ob;
         oa.x = cell(un0_a.x, unp_a.x, unm_a.x, un0_b.x, uu.x, un0_a.y, uLa, wh_a.x, w0_a.x,
-                    F0.jab.x, F0.jlo.x, F0.kIa, F0.kLa, cf[0], pa.x);
+                    jab.x, jlo.x, fka.x, kLa, cf_a.x, pa.x);
         oa.y = cell(un0_a.y, unp_a.y, unm_a.y, un0_b.y, uu.y, uRa, un0_a.x, wh_a.y, w0_a.y,
-                    F0.jab.y, F0.jlo.y, F0.kRa, F0.kIa, cf[1], pa.y);
+                    jab.y, jlo.y, fka.y, fka.x, cf_a.y, pa.y);
         ob.x = cell(un0_b.x, unp_b.x, unm_b.x, ud.x, un0_a.x, un0_b.y, uLb, wh_b.x, w0_b.x,
-                    F0.jhi.x, F0.jab.x, F0.kIb, F0.kLb, cf[2], pb.x);
+                    jhi.x, jab.x, fkb.x, kLb, cf_b.x, pb.x);
         ob.y = cell(un0_b.y, unp_b.y, unm_b.y, ud.y, un0_a.y, uRb, un0_b.x, wh_b.y, w0_b.y,
-                    F0.jhi.y, F0.jab.y, F0.kRb, F0.kIb, cf[3], pb.y);
-        if (my_src) {
-            inject_src(p, ja, kA, g0_a.x, a.src_val1, oa.x);
-            inject_src(p, ja, kA + 1, g0_a.y, a.src_val1, oa.y);
-            inject_src(p, ja + 1, kA, g0_b.x, a.src_val1, ob.x);
-            inject_src(p, ja + 1, kA + 1, g0_b.y, a.src_val1, ob.y);
-        }
+                    jhi.y, jab.y, fkb.y, fkb.x, cf_b.y, pb.y);
         const bool own_plane = p >= i0 && p < i1;
-        if (SUP != SUP_NONE) {
-            const T uo[4] = {un0_a.x, un0_a.y, un0_b.x, un0_b.y};
-            T* oo[4] = {&oa.x, &oa.y, &ob.x, &ob.y};
-            const T gg[4] = {g0_a.x, g0_a.y, g0_b.x, g0_b.y};
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int qi = sup_index(p, ja + (c >> 1), kA + (c & 1));
-                if (qi >= 0) {
-                    if (SUP == SUP_GATHER) { if (own_plane) a.row1[qi] = uo[c]; }
-                    else *oo[c] = *oo[c] + MT::fc(M, gg[c], kp[c]) * ldg(a.row1 + qi);
-                }
-            }
-        }
+        tile_inject(p, oa, ob, un0_a, un0_b, a.src_val1, a.row1, own_plane);
         stv(Xc + oA, oa);
         stv(Xc + oB, ob);
         V nacc_a = acc1_a, nacc_b = acc1_b;
@@ -476,25 +426,24 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
             }
         }
         // ring cells (step n only, no accumulation / gather)
+        T rwh[2] = {rw0[0], rw0[1]};
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
             if (t == 1 && !ring1) continue;
             if (!rg_ok[t]) continue;
             const int o = oR[t];
-            const RNb nbo = ring_nb(t);
-            const T u0 = run0[t];
-            T kap;
-            const T coef = MT::coef(M, rg0[t], kap);
-            T v = cell(u0, runp[t], rum[t], SU[nbo.d], SU[nbo.u], SU[nbo.r], SU[nbo.l],
-                       face(rm0[t], rmp[t]), rw0[t], RF0[t].jh, RF0[t].jl, RF0[t].kh, RF0[t].kl,
-                       coef, SP[o]);
+            int nl, nr, nu, nd;
+            ring_nb(t, nl, nr, nu, nd);
+            rwh[t] = SFI[o];
+            T v = cell(run0[t], runp[t], rum[t], SU[nd], SU[nu], SU[nr], SU[nl], rwh[t], rw0[t],
+                       SFJ[o], SFJ[nu], SFK[o], SFK[nl], SC[o], SP[o]);
             if (my_src || SUP == SUP_INJECT) {
                 const int r = o / W;
                 const int jj = r + j0 - 2, kk = o - r * W + k0 - HO;
-                if (my_src) inject_src(p, jj, kk, rg0[t], a.src_val1, v);
+                if (my_src) inject_src(p, jj, kk, a.src_val1, v);
                 if (SUP == SUP_INJECT) {
                     const int qi = sup_index(p, jj, kk);
-                    if (qi >= 0) v = v + MT::fc(M, rg0[t], kap) * ldg(a.row1 + qi);
+                    if (qi >= 0) v = v + fcoef(p * plane + jj * n2 + kk) * ldg(a.row1 + qi);
                 }
             }
             Xc[o] = v;
@@ -503,19 +452,12 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         // ---- c: step n+1 at plane p-1 (tile) ----
         if (p - 1 >= i0 && p - 1 < i1) step2_tile(p - 1, Xp, oa, ob);
 
-        // ---- e: faces of plane p+1; rotate ----
-        Faces Fn = F0;
-        RFaces RFn[2] = {RF0[0], RF0[1]};
-        if (next) {
-            Fn = own_faces(SMn);
-            RFn[0] = ring_faces(SMn, 0);
-            if (ring1) RFn[1] = ring_faces(SMn, 1);
-        }
-        // step-(n+1) material for plane p (used at the next plane)
-        F1 = F0;
+        // ---- rotate: plane p's material serves step n+1 at the next plane ----
+        f1_kLa = kLa; f1_kIa = fka.x; f1_kRa = fka.y;
+        f1_kLb = kLb; f1_kIb = fkb.x; f1_kRb = fkb.y;
+        f1_jlo = jlo; f1_jab = jab; f1_jhi = jhi;
         w1lo_a = w0_a; w1lo_b = w0_b; w1hi_a = wh_a; w1hi_b = wh_b;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) c1[c] = cf[c];
+        c1_a = cf_a; c1_b = cf_b;
         acc1_a = nacc_a; acc1_b = nacc_b;
         un1_a = un0_a; un1_b = un0_b;
         // u^{n+1} queue; at the global bottom plane the "previous" plane is
@@ -524,13 +466,11 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         x_0a = oa; x_0b = ob;
         // step-n queue
         unm_a = un0_a; unm_b = un0_b; un0_a = unp_a; un0_b = unp_b;
-        g0_a = gp_a; g0_b = gp_b; m0_a = mp_a; m0_b = mp_b; w0_a = wh_a; w0_b = wh_b;
-        F0 = Fn;
+        w0_a = wh_a; w0_b = wh_b;
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
-            rw0[t] = face(rm0[t], rmp[t]);
-            rum[t] = run0[t]; run0[t] = runp[t]; rg0[t] = rgp[t]; rm0[t] = rmp[t];
-            RF0[t] = RFn[t];
+            rw0[t] = rwh[t];
+            rum[t] = run0[t]; run0[t] = runp[t];
         }
     };
 

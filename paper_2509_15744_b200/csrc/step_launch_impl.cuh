@@ -75,11 +75,11 @@ void go_step2(dim3 grid, cudaStream_t s, const Step2Args<T>& a, const Tma2Maps& 
     const size_t sm = step2_smem_bytes<T>();
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(step2_kernel_tma<T, FL, true, ACC, SUP>,
+        cudaFuncSetAttribute(step2_kernel_tma<T, FL, ACC, SUP>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         attr = true;
     }
-    step2_kernel_tma<T, FL, true, ACC, SUP><<<grid, dim3(32, 4, 1), sm, s>>>(a, maps);
+    step2_kernel_tma<T, FL, ACC, SUP><<<grid, dim3(32, 4, 1), sm, s>>>(a, maps);
 }
 
 template <typename T, int FL, bool ACC>
@@ -99,6 +99,18 @@ void launch_step2_engine(const StepSel& k, dim3 grid, cudaStream_t s, const Step
         if (k.acc) go_step2_sup<T, ACOUSTIC, true>(k.sup, grid, s, a, maps);
         else go_step2_sup<T, ACOUSTIC, false>(k.sup, grid, s, a, maps);
     }
+}
+
+template <typename T>
+void launch_material4(int flavor, cudaStream_t s, const T* gamma, const MatScalars<T>& M, int n0,
+                      int n1, int n2, T* out) {
+    const size_t f = (size_t)n0 * n1 * n2;
+    if (flavor == RHO_SCALED)
+        material4_kernel<T, RHO_SCALED><<<592, 256, 0, s>>>(gamma, M, n0, n1, n2, out, out + f,
+                                                           out + 2 * f, out + 3 * f);
+    else
+        material4_kernel<T, ACOUSTIC><<<592, 256, 0, s>>>(gamma, M, n0, n1, n2, out, out + f,
+                                                         out + 2 * f, out + 3 * f);
 }
 
 }  // namespace wb

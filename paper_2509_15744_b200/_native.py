@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libwaveb200.so")
+# WAVEB200_LIB selects an alternative in-tree build (kernel-variant A/B runs)
+LIB_PATH = os.environ.get("WAVEB200_LIB") or os.path.join(_HERE, "_lib", "libwaveb200.so")
 
 WO_OK, WO_ERR_CONFIG, WO_ERR_UNSTABLE, WO_ERR_BUDGET, WO_ERR_CUDA = 0, 1, 2, 3, 4
 WO_RHO_SCALED, WO_ACOUSTIC = 0, 1

@@ -43,12 +43,14 @@ def up_to_date():
     return all(os.path.getmtime(p) <= t for p in deps if os.path.exists(p))
 
 
-def build(force=False, verbose=False, extra=()):
-    if not force and up_to_date():
+def build(force=False, verbose=False, extra=(), out=None):
+    lib = out or LIB
+    if out is None and not force and up_to_date():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
     units = sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
-    objs = [os.path.join(OUT_DIR, u[:-3] + ".o") for u in units]
+    tag = os.path.basename(lib).replace(".", "_")
+    objs = [os.path.join(OUT_DIR, f"{tag}_{u[:-3]}.o") for u in units]
     cmds = [[NVCC, *NVCC_FLAGS, *extra, "-c", os.path.join(CSRC, u), "-o", o]
             for u, o in zip(units, objs)]
     if verbose:
@@ -58,17 +60,22 @@ def build(force=False, verbose=False, extra=()):
     rcs = [p.wait() for p in procs]
     if any(rcs):
         raise subprocess.CalledProcessError(max(rcs), cmds[rcs.index(max(rcs))])
-    link = [NVCC, *LINK_FLAGS, *objs, "-o", LIB + ".tmp"]
+    link = [NVCC, *LINK_FLAGS, *objs, "-o", lib + ".tmp"]
     if verbose:
         print(" ".join(link))
     subprocess.run(link, check=True)
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(lib + ".tmp", lib)
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True,
-          extra=["-Xptxas", "-v"] if "--ptxas" in sys.argv else ())
-    print(LIB)
+    # --force, --ptxas, -DNAME=VALUE (kernel variants), --out=PATH (variant library)
+    args = sys.argv[1:]
+    extra = [a for a in args if a.startswith("-D")]
+    if "--ptxas" in args:
+        extra += ["-Xptxas", "-v"]
+    outs = [a.split("=", 1)[1] for a in args if a.startswith("--out=")]
+    print(build(force="--force" in args, verbose=True, extra=extra,
+                out=os.path.abspath(outs[0]) if outs else None))

@@ -39,8 +39,16 @@
 
 namespace wb {
 
+#ifndef WB_T2_STAGES
+#define WB_T2_STAGES 3
+#endif
+#ifndef WB_T2_PREFETCH
+#define WB_T2_PREFETCH 2
+#endif
 constexpr int T2_THREADS = 128;
-constexpr int T2_NS = 3;             // TMA ring stages
+constexpr int T2_NS = WB_T2_STAGES;  // TMA ring stages
+constexpr int T2_PF = WB_T2_PREFETCH;   // L2 prefetch distance beyond the ring (planes)
+constexpr int T2_PRODUCER = 32;      // thread issuing TMA (warp 0 carries the extra ring cells)
 constexpr int R2_H = BY + 4;         // rows j0-2 .. j0+9
 constexpr int R1_H = BY + 2;         // rows j0-1 .. j0+8
 constexpr int NRING = 2 * (PBX + 2) + 2 * BY;   // one-cell ring around a 64 x 8 tile
@@ -184,6 +192,22 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         (unsigned)(sizeof(T) * ((2 * R2_H + 4 * R1_H) * W + (ACC ? BY * PBX : 0)));
     const CUtensorMap* mU = pick_map(maps.u_r2, maps.cur);
     const CUtensorMap* mP = pick_map(maps.u_r1, maps.prev);
+    // L2 prefetch of a later plane's boxes (no shared memory; hides DRAM
+    // latency beyond the T2_NS-stage ring)
+    auto prefetch = [&](int p) {
+        auto pf = [&](const CUtensorMap* m, int c0, int c1) {
+            asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
+                         ::"l"(reinterpret_cast<unsigned long long>(m)), "r"(c0), "r"(c1), "r"(p)
+                         : "memory");
+        };
+        pf(mU, k0 - HO, j0 - 2);
+        pf(&maps.fj_r2, k0 - HO, j0 - 2);
+        pf(mP, k0 - HO, j0 - 1);
+        pf(&maps.c_r1, k0 - HO, j0 - 1);
+        pf(&maps.fk_r1, k0 - HO, j0 - 1);
+        pf(&maps.fi_r1, k0 - HO, j0 - 1);
+        if (ACC) pf(&maps.a_ctr, k0, j0);
+    };
     auto issue = [&](int p, int s) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[s], STAGE_BYTES);
@@ -200,8 +224,10 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (tid == 0)
+    if (tid == T2_PRODUCER) {
         for (int s = 0; s < T2_NS && pbeg + s <= pfin; ++s) issue(pbeg + s, s);
+        for (int d = 0; d < T2_PF && pbeg + T2_NS + d <= pfin; ++d) prefetch(pbeg + T2_NS + d);
+    }
 
     auto ldv = [](const T* p) { return *reinterpret_cast<const V*>(p); };
     auto stv = [](T* p, V v) { *reinterpret_cast<V*>(p) = v; };
@@ -385,7 +411,10 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
                 if (rg_ok[t]) runp[t] = __ldg(a.u_cur + gp + ring_gofs(t));
         }
         __syncthreads();
-        if (tid == 0 && p > pbeg && p + T2_NS - 1 <= pfin) issue(p + T2_NS - 1, sf);
+        if (tid == T2_PRODUCER && p > pbeg && p + T2_NS - 1 <= pfin) {
+            issue(p + T2_NS - 1, sf);
+            if (p + T2_NS - 1 + T2_PF <= pfin) prefetch(p + T2_NS - 1 + T2_PF);
+        }
 
         // ---- d: step n at plane p (tile + ring) -> X[b] ----
         const V wh_a = ldv(SFI + oA), wh_b = ldv(SFI + oB);

@@ -57,6 +57,10 @@ struct wo_ctx {
     int t2_state = 0;                  // two-step tensor maps: 0 not built, 1 ready, -1 no
     Tma2Maps t2maps;
     char* mat4 = nullptr;              // coef | +k | +j | +i faces (two-step passes)
+    char* stage = nullptr;             // fp64 upload staging (persistent)
+    size_t stage_bytes = 0;
+    char* flag = nullptr;              // device int scratch (verification flag)
+    size_t flag_bytes = 0;
     bool mat4_valid = false;           // computed for the current material
     int64_t pair_launches = 0;
     int tma_state = 0;                 // 0 not built, 1 maps ready, -1 not eligible
@@ -942,9 +946,11 @@ __global__ void cast_kernel(const double* src, T* dst, long long n) {
 template <typename T>
 int upload_cast_t(wo_ctx* ctx, const double* host, char* dev, int64_t n) {
     const int64_t chunk = 4 << 20;  // doubles per staging half (32 MiB)
-    double* stage = nullptr;
-    int rc = dev_alloc(ctx, (void**)&stage, (size_t)std::min(n, 2 * chunk) * 8);
+    // persistent staging buffer: a per-call cudaMalloc/cudaFree pair stalls
+    // the host for up to ~0.5 s on a busy device
+    int rc = ensure(ctx, &ctx->stage, &ctx->stage_bytes, (size_t)std::min(n, 2 * chunk) * 8);
     if (rc) return rc;
+    double* stage = reinterpret_cast<double*>(ctx->stage);
     int half = 0;  // stream order keeps a half busy until its cast kernel ran
     for (int64_t off = 0; off < n; off += chunk, half ^= 1) {
         const int64_t m = std::min(chunk, n - off);
@@ -954,8 +960,6 @@ int upload_cast_t(wo_ctx* ctx, const double* host, char* dev, int64_t n) {
         ctx->launches++;
     }
     CK(cudaStreamSynchronize(ctx->stream));
-    cudaFree(stage);
-    ctx->dev_bytes -= (int64_t)std::min(n, 2 * chunk) * 8;
     return WO_OK;
 }
 
@@ -991,9 +995,9 @@ template <typename T>
 static int verify_fast_div_t(wo_ctx* ctx) {
     ctx->fast_div = false;
     if (!ctx->allow_fast_div) return WO_OK;
-    int* d_ok = nullptr;
-    int rc = dev_alloc(ctx, (void**)&d_ok, sizeof(int));
+    int rc = ensure(ctx, &ctx->flag, &ctx->flag_bytes, sizeof(int));
     if (rc) return rc;
+    int* d_ok = reinterpret_cast<int*>(ctx->flag);
     const int one = 1;
     CK(cudaMemcpyAsync(d_ok, &one, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
     const int n0 = ctx->kn0 + ctx->has_lo + ctx->has_hi;
@@ -1009,8 +1013,6 @@ static int verify_fast_div_t(wo_ctx* ctx) {
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    cudaFree(d_ok);
-    ctx->dev_bytes -= (int64_t)sizeof(int);
     ctx->fast_div = ok != 0;
     return WO_OK;
 }
@@ -1099,7 +1101,8 @@ void wo_destroy(wo_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    void* bufs[] = {ctx->gamma, ctx->u[0], ctx->u[1], ctx->u[2], ctx->u[3], ctx->mat4, ctx->acc,
+    void* bufs[] = {ctx->gamma, ctx->u[0], ctx->u[1], ctx->u[2], ctx->u[3], ctx->mat4, ctx->stage,
+                    ctx->flag, ctx->acc,
                     ctx->mask, ctx->prefix,
                     ctx->store, ctx->measured, ctx->partial, ctx->cost, ctx->maxslots,
                     ctx->f_idx, ctx->f_vals, ctx->f_dense, ctx->hist, ctx->u3};

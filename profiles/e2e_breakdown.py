@@ -26,7 +26,7 @@ def main():
         mp = torch.empty(problem.measured.shape, dtype=torch.float64, pin_memory=True).numpy()
         mp[...] = problem.measured
         problem.measured = mp
-    for rep in range(8):
+    for rep in range(int(os.environ.get("REPS", "8"))):
         t0 = time.perf_counter()
         plan = G.SuperposedPlan(problem, model, cfg)
         t1 = time.perf_counter()

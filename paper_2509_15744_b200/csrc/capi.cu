@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -54,6 +55,7 @@ struct wo_ctx {
     int use_pair = 1;                  // wo_set_option(WO_OPT_PAIR_KERNEL)
     int use_tma = 1;                   // wo_set_option(WO_OPT_TMA_KERNEL)
     int use_two_step = 1;              // wo_set_option(WO_OPT_TWO_STEP)
+    int num_sms = 148;                 // of the context's device
     int t2_state = 0;                  // two-step tensor maps: 0 not built, 1 ready, -1 no
     Tma2Maps t2maps;
     char* mat4 = nullptr;              // coef | +k | +j | +i faces (two-step passes)
@@ -464,11 +466,30 @@ bool pair_ready(wo_ctx* ctx) {
     return ctx->t2_state == 1 && tma_ready(ctx);
 }
 
+// planes per CTA of a two-step pass: whole waves of resident CTAs matter
+// more than chunk length (a 1.73-wave grid idles a quarter of the last
+// wave), and each chunk recomputes ~1 extra step-n plane.  Cost model:
+// waves(nz) * (planes per chunk + 1); WB_T2_NZ overrides (tuning runs).
 int choose_chunk2(const wo_ctx* ctx) {
     const int tiles = (ctx->kn2 / PBX) * (ctx->kn1 / BY);
-    const int target = 148 * 3 * 2;   // two waves of 3 CTAs per SM
-    const int nz = std::max(1, target / std::max(1, tiles));
-    return std::max((ctx->kn0 + nz - 1) / nz, std::min(ctx->kn0, 8));
+    static const int forced = [] {
+        const char* e = getenv("WB_T2_NZ");
+        return e ? atoi(e) : 0;
+    }();
+    int best_nz = 1;
+    if (forced > 0) {
+        best_nz = forced;
+    } else {
+        const int slots = ctx->num_sms * (ctx->itemsize == 4 ? 3 : 1);
+        double best = 1e30;
+        for (int nz = 1; nz <= std::min(ctx->kn0, 64); ++nz) {
+            const int chunk = (ctx->kn0 + nz - 1) / nz;
+            const int waves = (tiles * nz + slots - 1) / slots;
+            const double cost = (double)waves * (chunk + 1);
+            if (cost < best - 1e-9) { best = cost; best_nz = nz; }
+        }
+    }
+    return std::max(1, (ctx->kn0 + best_nz - 1) / best_nz);
 }
 
 struct PairSpec {
@@ -968,6 +989,7 @@ int create_common(wo_ctx* ctx) {
     REQUIRE(ctx->alloc_cells() < (1ll << 31),
             "grid too large for one context (>= 2^31 cells): use slab decomposition");
     CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     const size_t ab = (size_t)ctx->alloc_cells() * ctx->itemsize;
     int rc;

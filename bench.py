@@ -13,10 +13,11 @@ N = 1024 time steps, a 33x33 sensor plane, k = 1e13.  It performs
 * e2e    — the public API call gradient_superposed(problem, material, cfg)
            with host (pinned) inputs: gamma/measured H2D and the gradient
            D2H inside the timed region.
-* roofline — fused step kernels: algorithmic bytes per launch (two-step pass:
-           read u^{n-1}, u^n, gamma, acc, write u^{n+1}, u^{n+2}, acc = 28 B
-           per fp32 cell; single step 24 B) over the CUDA-event durations of
-           all step launches in the timed region, against MEASURED_PEAKS.json.
+* roofline — fused step kernels: SURVEY 8(d)'s 24 algorithmic bytes per fp32
+           cell-update x the cell-updates of every step launch (a two-step
+           pass does 2C), over the launches' summed CUDA-event time, against
+           MEASURED_PEAKS.json; the bytes the two-step kernel really streams
+           (10 fields per cell and pass) are reported beside it.
 * cpu_baseline / --impl reference — the CPU oracle port (oracle/, a
            restatement of the reference's Numba loops pinned bit-exact to
            it) on the host cores, on a bounded sample of the same workload.
@@ -285,19 +286,24 @@ def run_native(args):
     value = world * updates / (ms_per_step * 1e-3) / 1e9
 
     # ---------------- roofline of the fused step kernels -------------------
-    # two-step passes (step2_kernel_tma) move 7 fields per cell (read u^{n-1},
-    # u^n, gamma, acc; write u^{n+1}, u^{n+2}, acc), single steps 6; achieved
-    # = algorithmic bytes of all step launches / their summed event time
+    # 24 algorithmic bytes per fp32 cell-update (read u^n,
+    # u^{n-1}, gamma, acc; write u^{n+1}, acc), also for temporal blocking.
+    # A two-step pass (step2_kernel_tma) performs 2C cell-updates; it actually
+    # streams 10 fields per cell (u^{n-1}, u^n, acc, coef, 3 face arrays in;
+    # u^{n+1}, u^{n+2}, acc out) = "streamed_bytes_per_launch".  achieved =
+    # algorithmic bytes of all step launches / their summed CUDA-event time.
     peaks, peak_kind = measured_peaks()
     item = ITEMSIZE[wl["precision"]]
     pairs = stats.get("pair_launches", 0)
     singles = stats["step_launches"] - pairs
-    alg_bytes = (7 * pairs + 6 * singles) * item * C
+    step_s = stats["step_kernel_ms"] * 1e-3
+    alg_bytes = 6 * item * C * (2 * pairs + singles)
+    achieved = alg_bytes / step_s / 1e9
+    two = pairs >= singles
+    streamed = (10 * pairs + 6 * singles) * item * C / step_s / 1e9
     k_ms = stats["step_kernel_ms"] / max(stats["step_launches"], 1)
-    achieved = alg_bytes / (stats["step_kernel_ms"] * 1e-3) / 1e9
-    bpl = (7 if pairs >= singles else 6) * item * C
     peak = float(peaks["hbm_gbs"])
-    kname = "step2_kernel" if pairs >= singles else "step_kernel"
+    kname = "step2_kernel" if two else "step_kernel"
     traffic = ncu_traffic(f"{kname}_{wl['precision']}_{args.grid}")
 
     # ---------------- end to end through the public API --------------------
@@ -359,11 +365,12 @@ def run_native(args):
                        "l2": "inputs larger than L2 (4 x 67 MB fields = 268 MB > 126 MB)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("wb::step2_kernel_tma (two fused steps per pass)"
-                                    if kname == "step2_kernel" else
-                                    "wb::step_kernel_tma4 (fused step)"),
-                         "algorithmic_bytes_per_launch": bpl,
-                         "cell_updates_per_launch": (2 if kname == "step2_kernel" else 1) * C,
+                         "kernel": ("wb::step2_kernel_tma (two fused steps per pass)" if two
+                                    else "wb::step_kernel_tma4 (fused step)"),
+                         "algorithmic_bytes_per_cell_update": 6 * item,
+                         "algorithmic_bytes_per_launch": 6 * item * C * (2 if two else 1),
+                         "streamed_bytes_per_launch": (10 if two else 6) * item * C,
+                         "streamed_gbs": streamed, "streamed_frac": streamed / peak,
                          "pair_launches": pairs, "single_launches": singles,
                          "mean_launch_ms": k_ms,
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},

@@ -56,6 +56,10 @@ struct wo_ctx {
     int use_tma = 1;                   // wo_set_option(WO_OPT_TMA_KERNEL)
     int use_two_step = 1;              // wo_set_option(WO_OPT_TWO_STEP)
     int num_sms = 148;                 // of the context's device
+    int t2_warps = [] {                // two-step kernel layout (4 or 8 warps; WB_T2_WARPS)
+        const char* e = getenv("WB_T2_WARPS");
+        return e && atoi(e) == 8 ? 8 : 4;
+    }();
     int t2_state = 0;                  // two-step tensor maps: 0 not built, 1 ready, -1 no
     Tma2Maps t2maps;
     char* mat4 = nullptr;              // coef | +k | +j | +i faces (two-step passes)
@@ -547,8 +551,8 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     ctx->t2maps.cur = ctx->cur;
     dim3 grid(ctx->kn2 / PBX, ctx->kn1 / BY, (ctx->kn0 + a.chunk - 1) / a.chunk);
     if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
-    launch_step2_engine<T>(StepSel{ctx->flavor, true, sp.acc, false, sup}, grid, ctx->stream, a,
-                           ctx->t2maps);
+    launch_step2_engine<T>(StepSel{ctx->flavor, true, sp.acc, false, sup}, ctx->t2_warps, grid,
+                           ctx->stream, a, ctx->t2maps);
     if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
     ctx->launches++;
     ctx->step_launches++;

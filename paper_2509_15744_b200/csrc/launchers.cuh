@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include "step2_kernel.cuh"
+#include "step2_kernel_w8.cuh"
 #include "step_kernel.cuh"
 #include "step_kernel_tma.cuh"
 
@@ -29,9 +30,10 @@ void launch_step_engine(int engine, const StepSel& k, dim3 grid, dim3 block, cud
                         const StepArgs<T>& a, const TmaMaps& maps);
 
 // two-step pass (no divisions on the dense path; checks are runtime flags)
+// warps = 4 (2x2 cells per thread) or 8 (1x2 cells per thread)
 template <typename T>
-void launch_step2_engine(const StepSel& k, dim3 grid, cudaStream_t s, const Step2Args<T>& a,
-                         const Tma2Maps& maps);
+void launch_step2_engine(const StepSel& k, int warps, dim3 grid, cudaStream_t s,
+                         const Step2Args<T>& a, const Tma2Maps& maps);
 
 // coef | +k | +j | +i face arrays (4 consecutive fields at out) of a material
 template <typename T>

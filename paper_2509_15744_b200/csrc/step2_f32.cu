@@ -2,7 +2,7 @@
 #include "step_launch_impl.cuh"
 
 namespace wb {
-template void launch_step2_engine<float>(const StepSel&, dim3, cudaStream_t,
+template void launch_step2_engine<float>(const StepSel&, int, dim3, cudaStream_t,
                                       const Step2Args<float>&, const Tma2Maps&);
 template void launch_material4<float>(int, cudaStream_t, const float*, const MatScalars<float>&, int,
                                      int, int, float*);

@@ -16,10 +16,10 @@
 //
 // Per plane p of the 2.5D march (TMA ring of T2_NS stages, one barrier):
 //   a  wait for plane p+1; u^n(p+1) of the tile + ring (registers)
-//   b  __syncthreads; refill the stage of plane p-1 with plane p+T2_NS-1
 //   d  step n at plane p on the tile AND a one-cell ring around it (the ring
 //      is recomputed redundantly so step n+1 never needs another CTA's data);
 //      u^{n+1}(p) goes to a shared-memory plane X
+//   b  __syncthreads; refill the stage of plane p with plane p+T2_NS
 //   c  step n+1 at plane p-1 on the tile, from X(p-1), the register queue of
 //      u^{n+1}, and plane p-1's material kept in registers
 // HBM traffic per fp32 cell and pass: read u^{n-1}, u^n, acc, coef and three
@@ -98,9 +98,11 @@ template <typename T> struct Tma2Stage {
     alignas(128) T A[BY][PBX];
 };
 
+constexpr int T2_NX = 3;             // u^{n+1} plane buffers (X)
+
 template <typename T>
 constexpr size_t step2_smem_bytes() {
-    return T2_NS * sizeof(Tma2Stage<T>) + 2 * sizeof(T) * R2_H * th_w<T>() /* u^{n+1} planes */ +
+    return T2_NS * sizeof(Tma2Stage<T>) + T2_NX * sizeof(T) * R2_H * th_w<T>() /* X planes */ +
            T2_NS * sizeof(unsigned long long) + 128;
 }
 
@@ -139,8 +141,8 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     unsigned char* smem_raw =
         smem_dyn + ((128u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_dyn)) & 127u)) & 127u);
     Tma2Stage<T>* st = reinterpret_cast<Tma2Stage<T>*>(smem_raw);
-    T* Xb = reinterpret_cast<T*>(smem_raw + T2_NS * sizeof(Tma2Stage<T>));   // X[2][PL]
-    unsigned long long* bar = reinterpret_cast<unsigned long long*>(Xb + 2 * PL);
+    T* Xb = reinterpret_cast<T*>(smem_raw + T2_NS * sizeof(Tma2Stage<T>));   // X[T2_NX][PL]
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(Xb + T2_NX * PL);
     __shared__ Bits smax[2][T2_THREADS / 32];
 
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -378,14 +380,16 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         }
     };
 
-    // one plane; q = stage of plane p, gpar = its mbarrier parity (rolled
-    // loop: unrolled copies of this body overflow the instruction cache)
-    auto body = [&](int q, int p, unsigned gpar) {
-        const int sn = q + 1 == T2_NS ? 0 : q + 1, sf = q == 0 ? T2_NS - 1 : q - 1;
-        const int b = (p - pbeg) & 1;
+    // one plane; q = stage of plane p, gpar = its mbarrier parity, xq = its X
+    // buffer (rolled loop: unrolled copies of this body overflow the
+    // instruction cache).  One barrier per plane, after step n: it publishes
+    // X(p) and frees stage(p), which is refilled at once (T2_NS planes ahead);
+    // three X buffers keep X(p) from overwriting X(p-3) before (c) read it.
+    auto body = [&](int q, int xq, int p, unsigned gpar) {
+        const int sn = q + 1 == T2_NS ? 0 : q + 1;
         const unsigned pn = (q + 1 == T2_NS) ? 1u : 0u;   // parity flip for plane p+1
-        T* Xc = Xb + b * PL;
-        const T* Xp = Xb + (b ^ 1) * PL;
+        T* Xc = Xb + xq * PL;
+        const T* Xp = Xb + (xq == 0 ? T2_NX - 1 : xq - 1) * PL;
         const Tma2Stage<T>& S = st[q];
         const T* SU = &S.U[0][0];
         const T* SFJ = &S.FJ[0][0];
@@ -409,11 +413,6 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
 #pragma unroll
             for (int t = 0; t < 2; ++t)
                 if (rg_ok[t]) runp[t] = __ldg(a.u_cur + gp + ring_gofs(t));
-        }
-        __syncthreads();
-        if (tid == T2_PRODUCER && p > pbeg && p + T2_NS - 1 <= pfin) {
-            issue(p + T2_NS - 1, sf);
-            if (p + T2_NS - 1 + T2_PF <= pfin) prefetch(p + T2_NS - 1 + T2_PF);
         }
 
         // ---- d: step n at plane p (tile + ring) -> X[b] ----
@@ -477,6 +476,11 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
             }
             Xc[o] = v;
         }
+        __syncthreads();
+        if (tid == T2_PRODUCER && p + T2_NS <= pfin) {
+            issue(p + T2_NS, q);
+            if (p + T2_NS + T2_PF <= pfin) prefetch(p + T2_NS + T2_PF);
+        }
 
         // ---- c: step n+1 at plane p-1 (tile) ----
         if (p - 1 >= i0 && p - 1 < i1) step2_tile(p - 1, Xp, oa, ob);
@@ -504,16 +508,18 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     };
 
     unsigned gpar = 0;
+    int xq = 0;
     for (int p = pbeg, q = 0; p <= pfin; ++p) {
-        body(q, p, gpar);
+        body(q, xq, p, gpar);
         if (++q == T2_NS) { q = 0; gpar ^= 1u; }
+        if (++xq == T2_NX) xq = 0;
     }
 
     // ---- step n+1 at the last plane of the grid (mirror above) ----
     // interior chunks finish inside the loop (pfin = i1); at the global end
-    // pfin = n0-1 = i1-1 and plane n0 mirrors the plane itself
-    __syncthreads();                         // ring values of the last plane in X
-    if (pfin == i1 - 1) step2_tile(pfin, Xb + ((pfin - pbeg) & 1) * PL, x_0a, x_0b);
+    // pfin = n0-1 = i1-1 and plane n0 mirrors the plane itself (X(pfin) was
+    // published by the last plane's barrier)
+    if (pfin == i1 - 1) step2_tile(pfin, Xb + ((pfin - pbeg) % T2_NX) * PL, x_0a, x_0b);
 
     if (a.check1 || a.check2) {
         for (int o = 16; o > 0; o >>= 1) {

@@ -29,7 +29,7 @@ step2_kernel_w8(const __grid_constant__ Step2Args<T> a, const __grid_constant__ 
         smem_dyn + ((128u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_dyn)) & 127u)) & 127u);
     Tma2Stage<T>* st = reinterpret_cast<Tma2Stage<T>*>(smem_raw);
     T* Xb = reinterpret_cast<T*>(smem_raw + T2_NS * sizeof(Tma2Stage<T>));   // X[2][PL]
-    unsigned long long* bar = reinterpret_cast<unsigned long long*>(Xb + 2 * PL);
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(Xb + T2_NX * PL);
     __shared__ Bits smax[2][T8_THREADS / 32];
 
     const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8

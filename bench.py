@@ -219,7 +219,7 @@ def run_reference_arm(args):
     # host-only: the measured traces are zeros (the misfit then uses r = u;
     # the CPU work per step is identical), so this arm never touches a GPU
     problem, model = build_problem(W, wl, synth_only=-1)
-    n_sample = args.cpu_sample_steps
+    n_sample = args.ref_sample_steps
     for _ in range(args.warmup):
         cpu_oracle_rate(wl, problem, model, min(n_sample, 4))
     rates, els = [], []
@@ -391,7 +391,10 @@ def main():
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--grid", type=int, default=256)
     ap.add_argument("--n-steps", type=int, default=1024)
-    ap.add_argument("--cpu-sample-steps", type=int, default=24)
+    # CPU samples: ~12 s for cpu_baseline; ~5 s per step of the reference arm
+    # (so its default 10 steps finish in about a minute)
+    ap.add_argument("--cpu-sample-steps", type=int, default=400)
+    ap.add_argument("--ref-sample-steps", type=int, default=160)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -56,10 +56,7 @@ struct wo_ctx {
     int use_tma = 1;                   // wo_set_option(WO_OPT_TMA_KERNEL)
     int use_two_step = 1;              // wo_set_option(WO_OPT_TWO_STEP)
     int num_sms = 148;                 // of the context's device
-    int t2_warps = [] {                // two-step kernel layout (4 or 8 warps; WB_T2_WARPS)
-        const char* e = getenv("WB_T2_WARPS");
-        return e && atoi(e) == 8 ? 8 : 4;
-    }();
+    int t2_geo = GEO_NONE;             // two-step tile geometry (set when its maps are built)
     int t2_state = 0;                  // two-step tensor maps: 0 not built, 1 ready, -1 no
     Tma2Maps t2maps;
     char* mat4 = nullptr;              // coef | +k | +j | +i faces (two-step passes)
@@ -439,33 +436,55 @@ int ensure_mat4(wo_ctx* ctx) {
     return WO_OK;
 }
 
+// tile geometry for a two-step pass: 32 x 16 where it divides the plane
+// (balanced warps, smaller ring), else 64 x 8; WB_T2_GEO=wide|tall forces one
+int pick_geo(const wo_ctx* ctx) {
+    static const int forced = [] {
+        const char* e = getenv("WB_T2_GEO");
+        if (!e) return (int)GEO_NONE;
+        return strcmp(e, "wide") == 0 ? (int)GEO_WIDE : strcmp(e, "tall") == 0 ? (int)GEO_TALL
+                                                                               : (int)GEO_NONE;
+    }();
+    const bool tall = ctx->kn2 % GeoTall::TBX == 0 && ctx->kn1 % GeoTall::TBY == 0;
+    const bool wide = ctx->kn2 % GeoWide::TBX == 0 && ctx->kn1 % GeoWide::TBY == 0;
+    if (forced == GEO_TALL && tall) return GEO_TALL;
+    if (forced == GEO_WIDE && wide) return GEO_WIDE;
+    return tall ? GEO_TALL : wide ? GEO_WIDE : GEO_NONE;
+}
+
 bool pair_ready(wo_ctx* ctx) {
     if (!ctx->use_two_step || !ctx->use_tma || !ctx->use_pair || ctx->has_lo || ctx->has_hi ||
-        !ctx->material_set || ctx->kn2 % PBX || ctx->kn1 % BY)
+        !ctx->material_set || pick_geo(ctx) == GEO_NONE)
         return false;
     if (ensure_four(ctx) || ensure_mat4(ctx)) return false;
     if (ctx->t2_state == 0) {
         ctx->t2_state = -1;
+        const int geo = pick_geo(ctx);
         const uint64_t np = (uint64_t)ctx->kn0;
-        const uint32_t hw = ctx->itemsize == 4 ? th_w<float>() : th_w<double>();
+        const uint32_t tbx = geo == GEO_TALL ? GeoTall::TBX : GeoWide::TBX;
+        const uint32_t tby = geo == GEO_TALL ? GeoTall::TBY : GeoWide::TBY;
+        const uint32_t hw = tbx + 2 * (ctx->itemsize == 4 ? th_ho<float>() : th_ho<double>());
+        const uint32_t r2 = tby + 4, r1 = tby + 2;
         const size_t fb = (size_t)ctx->cells() * ctx->itemsize;
         bool ok = true;
         for (int b = 0; b < 4; ++b) {
             ok &= make_map(&ctx->t2maps.u_r2[b], ctx->u[b], ctx->itemsize, ctx->kn2, ctx->kn1, np,
-                           hw, R2_H);
+                           hw, r2);
             ok &= make_map(&ctx->t2maps.u_r1[b], ctx->u[b], ctx->itemsize, ctx->kn2, ctx->kn1, np,
-                           hw, R1_H);
+                           hw, r1);
         }
-        ok &= make_map(&ctx->t2maps.c_r1, ctx->mat4, ctx->itemsize, ctx->kn2, ctx->kn1, np, hw,
-                       R1_H);
+        ok &= make_map(&ctx->t2maps.c_r1, ctx->mat4, ctx->itemsize, ctx->kn2, ctx->kn1, np, hw, r1);
         ok &= make_map(&ctx->t2maps.fk_r1, ctx->mat4 + fb, ctx->itemsize, ctx->kn2, ctx->kn1, np,
-                       hw, R1_H);
+                       hw, r1);
         ok &= make_map(&ctx->t2maps.fj_r2, ctx->mat4 + 2 * fb, ctx->itemsize, ctx->kn2, ctx->kn1,
-                       np, hw, R2_H);
+                       np, hw, r2);
         ok &= make_map(&ctx->t2maps.fi_r1, ctx->mat4 + 3 * fb, ctx->itemsize, ctx->kn2, ctx->kn1,
-                       np, hw, R1_H);
-        ok &= make_map(&ctx->t2maps.a_ctr, ctx->acc, ctx->itemsize, ctx->kn2, ctx->kn1, np, PBX, BY);
-        if (ok) ctx->t2_state = 1;
+                       np, hw, r1);
+        ok &= make_map(&ctx->t2maps.a_ctr, ctx->acc, ctx->itemsize, ctx->kn2, ctx->kn1, np, tbx, tby);
+        if (ok) {
+            ctx->t2_state = 1;
+            ctx->t2_geo = geo;
+        }
     }
     return ctx->t2_state == 1 && tma_ready(ctx);
 }
@@ -475,7 +494,9 @@ bool pair_ready(wo_ctx* ctx) {
 // wave), and each chunk recomputes ~1 extra step-n plane.  Cost model:
 // waves(nz) * (planes per chunk + 1); WB_T2_NZ overrides (tuning runs).
 int choose_chunk2(const wo_ctx* ctx) {
-    const int tiles = (ctx->kn2 / PBX) * (ctx->kn1 / BY);
+    const int tbx = ctx->t2_geo == GEO_TALL ? GeoTall::TBX : GeoWide::TBX;
+    const int tby = ctx->t2_geo == GEO_TALL ? GeoTall::TBY : GeoWide::TBY;
+    const int tiles = (ctx->kn2 / tbx) * (ctx->kn1 / tby);
     static const int forced = [] {
         const char* e = getenv("WB_T2_NZ");
         return e ? atoi(e) : 0;
@@ -549,9 +570,11 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     a.max2 = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots) + sp.slot2;
     ctx->t2maps.prev = ctx->prv;
     ctx->t2maps.cur = ctx->cur;
-    dim3 grid(ctx->kn2 / PBX, ctx->kn1 / BY, (ctx->kn0 + a.chunk - 1) / a.chunk);
+    const int tbx = ctx->t2_geo == GEO_TALL ? GeoTall::TBX : GeoWide::TBX;
+    const int tby = ctx->t2_geo == GEO_TALL ? GeoTall::TBY : GeoWide::TBY;
+    dim3 grid(ctx->kn2 / tbx, ctx->kn1 / tby, (ctx->kn0 + a.chunk - 1) / a.chunk);
     if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
-    launch_step2_engine<T>(StepSel{ctx->flavor, true, sp.acc, false, sup}, ctx->t2_warps, grid,
+    launch_step2_engine<T>(StepSel{ctx->flavor, true, sp.acc, false, sup}, ctx->t2_geo, grid,
                            ctx->stream, a, ctx->t2maps);
     if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
     ctx->launches++;

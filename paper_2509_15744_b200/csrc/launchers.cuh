@@ -8,7 +8,6 @@
 #include <cuda_runtime.h>
 
 #include "step2_kernel.cuh"
-#include "step2_kernel_w8.cuh"
 #include "step_kernel.cuh"
 #include "step_kernel_tma.cuh"
 
@@ -30,9 +29,10 @@ void launch_step_engine(int engine, const StepSel& k, dim3 grid, dim3 block, cud
                         const StepArgs<T>& a, const TmaMaps& maps);
 
 // two-step pass (no divisions on the dense path; checks are runtime flags)
-// warps = 4 (2x2 cells per thread) or 8 (1x2 cells per thread)
+// geometry: GEO_WIDE (64 x 8 tiles) or GEO_TALL (32 x 16 tiles)
+enum Step2Geo : int { GEO_NONE = 0, GEO_WIDE = 1, GEO_TALL = 2 };
 template <typename T>
-void launch_step2_engine(const StepSel& k, int warps, dim3 grid, cudaStream_t s,
+void launch_step2_engine(const StepSel& k, int geo, dim3 grid, cudaStream_t s,
                          const Step2Args<T>& a, const Tma2Maps& maps);
 
 // coef | +k | +j | +i face arrays (4 consecutive fields at out) of a material

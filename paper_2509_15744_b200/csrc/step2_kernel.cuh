@@ -49,9 +49,24 @@ constexpr int T2_THREADS = 128;
 constexpr int T2_NS = WB_T2_STAGES;  // TMA ring stages
 constexpr int T2_PF = WB_T2_PREFETCH;   // L2 prefetch distance beyond the ring (planes)
 constexpr int T2_PRODUCER = 32;      // thread issuing TMA (warp 0 carries the extra ring cells)
-constexpr int R2_H = BY + 4;         // rows j0-2 .. j0+9
-constexpr int R1_H = BY + 2;         // rows j0-1 .. j0+8
-constexpr int NRING = 2 * (PBX + 2) + 2 * BY;   // one-cell ring around a 64 x 8 tile
+
+// Tile geometry of a two-step CTA: TBX x TBY cells (axis 2 x axis 1), 128
+// threads of 2 x 2 cells.  Wide = 64 x 8 (ring of 148 cells: two ring slots
+// for warp 0); Tall = 32 x 16 (ring of 100 cells: one slot, balanced warps,
+// less halo per cell).
+template <int TBX_, int TBY_> struct Geo2 {
+    static constexpr int TBX = TBX_, TBY = TBY_;
+    static constexpr int TX = TBX / 2, TY = TBY / 2;       // threads
+    static constexpr int R2 = TBY + 4;                      // rows j0-2 .. j0+TBY+1
+    static constexpr int R1 = TBY + 2;                      // rows j0-1 .. j0+TBY
+    static constexpr int NRING = 2 * (TBX + 2) + 2 * TBY;   // one-cell ring
+    template <typename T> __host__ __device__ static constexpr int W() {
+        return TBX + 2 * th_ho<T>();
+    }
+    static_assert(TX * TY == 128, "two-step CTAs have 128 threads");
+};
+using GeoWide = Geo2<64, 8>;
+using GeoTall = Geo2<32, 16>;
 
 template <typename T> struct Step2Args {
     const T* gamma;    // sparse use only (nodal force coefficient)
@@ -78,31 +93,32 @@ template <typename T> struct Step2Args {
 };
 
 struct Tma2Maps {
-    CUtensorMap u_r2[4];   // level buffers, (W, R2_H) boxes at (k0-HO, j0-2)
-    CUtensorMap u_r1[4];   // level buffers, (W, R1_H) boxes at (k0-HO, j0-1)
-    CUtensorMap fj_r2;     // +j faces, (W, R2_H)
-    CUtensorMap c_r1;      // coef, (W, R1_H)
-    CUtensorMap fk_r1;     // +k faces, (W, R1_H)
-    CUtensorMap fi_r1;     // +i faces, (W, R1_H)
-    CUtensorMap a_ctr;     // accumulator, (PBX, BY)
+    CUtensorMap u_r2[4];   // level buffers, (W, R2) boxes at (k0-HO, j0-2)
+    CUtensorMap u_r1[4];   // level buffers, (W, R1) boxes at (k0-HO, j0-1)
+    CUtensorMap fj_r2;     // +j faces, (W, R2)
+    CUtensorMap c_r1;      // coef, (W, R1)
+    CUtensorMap fk_r1;     // +k faces, (W, R1)
+    CUtensorMap fi_r1;     // +i faces, (W, R1)
+    CUtensorMap a_ctr;     // accumulator, (TBX, TBY)
     int prev, cur;         // buffer indices of u^{n-1}, u^n
 };
 
-template <typename T> struct Tma2Stage {
-    alignas(128) T U[R2_H][th_w<T>()];
-    alignas(128) T FJ[R2_H][th_w<T>()];
-    alignas(128) T P[R1_H][th_w<T>()];
-    alignas(128) T C[R1_H][th_w<T>()];
-    alignas(128) T FK[R1_H][th_w<T>()];
-    alignas(128) T FI[R1_H][th_w<T>()];
-    alignas(128) T A[BY][PBX];
+template <typename T, typename G> struct Tma2Stage {
+    alignas(128) T U[G::R2][G::template W<T>()];
+    alignas(128) T FJ[G::R2][G::template W<T>()];
+    alignas(128) T P[G::R1][G::template W<T>()];
+    alignas(128) T C[G::R1][G::template W<T>()];
+    alignas(128) T FK[G::R1][G::template W<T>()];
+    alignas(128) T FI[G::R1][G::template W<T>()];
+    alignas(128) T A[G::TBY][G::TBX];
 };
 
 constexpr int T2_NX = 3;             // u^{n+1} plane buffers (X)
 
-template <typename T>
+template <typename T, typename G>
 constexpr size_t step2_smem_bytes() {
-    return T2_NS * sizeof(Tma2Stage<T>) + T2_NX * sizeof(T) * R2_H * th_w<T>() /* X planes */ +
+    return T2_NS * sizeof(Tma2Stage<T, G>) +
+           T2_NX * sizeof(T) * G::R2 * G::template W<T>() /* X planes */ +
            T2_NS * sizeof(unsigned long long) + 128;
 }
 
@@ -128,26 +144,27 @@ __global__ void material4_kernel(const T* __restrict__ gamma, MatScalars<T> M, i
     }
 }
 
-template <typename T, int FLAVOR, bool ACC, int SUP>
+template <typename T, typename G, int FLAVOR, bool ACC, int SUP>
 __global__ void __launch_bounds__(T2_THREADS, sizeof(T) == 4 ? 3 : 1)
 step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__ Tma2Maps maps) {
     using Tr = FTraits<T>;
     using MP = Mat<T, FLAVOR, false>;   // sparse force coefficients only
     using V = typename Pair<T>::V;
     using Bits = typename Tr::Bits;
-    constexpr int W = th_w<T>(), HO = th_ho<T>();
+    constexpr int W = G::template W<T>(), HO = th_ho<T>();
+    constexpr int TBX = G::TBX, TBY = G::TBY, R2_H = G::R2, R1_H = G::R1, NRING = G::NRING;
     constexpr int PL = R2_H * W;                       // elements of one R2 plane
     extern __shared__ __align__(128) unsigned char smem_dyn[];
     unsigned char* smem_raw =
         smem_dyn + ((128u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_dyn)) & 127u)) & 127u);
-    Tma2Stage<T>* st = reinterpret_cast<Tma2Stage<T>*>(smem_raw);
-    T* Xb = reinterpret_cast<T*>(smem_raw + T2_NS * sizeof(Tma2Stage<T>));   // X[T2_NX][PL]
+    Tma2Stage<T, G>* st = reinterpret_cast<Tma2Stage<T, G>*>(smem_raw);
+    T* Xb = reinterpret_cast<T*>(smem_raw + T2_NS * sizeof(Tma2Stage<T, G>));   // X[T2_NX][PL]
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(Xb + T2_NX * PL);
     __shared__ Bits smax[2][T2_THREADS / 32];
 
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const int tid = ty * 32 + tx;
-    const int k0 = blockIdx.x * PBX, j0 = blockIdx.y * BY;
+    const int tid = ty * G::TX + tx;
+    const int k0 = blockIdx.x * TBX, j0 = blockIdx.y * TBY;
     const int kA = k0 + 2 * tx, ja = j0 + 2 * ty;
     const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
     const int plane = n1 * n2;
@@ -165,7 +182,8 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     const int dL = kA > 0 ? 1 : 0, dR = kA + 2 < n2 ? 1 : 0;   // k-1 / k+2 inside
     const int oA = ra * W + cA, oB = oA + W;
     const int oU = rU * W + cA, oD = rD * W + cA;
-    // ring cells: slot 0 = tid, slot 1 = tid + 128 (warp 0, lanes < NRING-128);
+    // ring cells: slot 0 = tid, slot 1 = tid + 128 (only the wide tile: warp
+    // 0, lanes < NRING-128);
     // rnb packs which neighbours lie inside the grid (bit 0 k-1, 1 k+1, 2 j-1,
     // 3 j+1) — outside ones mirror to the cell itself
     int oR[2], rnb[2];
@@ -174,24 +192,24 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     for (int t = 0; t < 2; ++t) {
         const int q = tid + t * T2_THREADS;
         int jj = j0, kk = k0;
-        if (q < PBX + 2) { jj = j0 - 1; kk = k0 - 1 + q; }
-        else if (q < 2 * (PBX + 2)) { jj = j0 + BY; kk = k0 - 1 + (q - (PBX + 2)); }
-        else if (q < 2 * (PBX + 2) + BY) { jj = j0 + (q - 2 * (PBX + 2)); kk = k0 - 1; }
-        else if (q < NRING) { jj = j0 + (q - 2 * (PBX + 2) - BY); kk = k0 + PBX; }
+        if (q < TBX + 2) { jj = j0 - 1; kk = k0 - 1 + q; }
+        else if (q < 2 * (TBX + 2)) { jj = j0 + TBY; kk = k0 - 1 + (q - (TBX + 2)); }
+        else if (q < 2 * (TBX + 2) + TBY) { jj = j0 + (q - 2 * (TBX + 2)); kk = k0 - 1; }
+        else if (q < NRING) { jj = j0 + (q - 2 * (TBX + 2) - TBY); kk = k0 + TBX; }
         rg_ok[t] = q < NRING && jj >= 0 && jj < n1 && kk >= 0 && kk < n2;
         oR[t] = rg_ok[t] ? (jj - j0 + 2) * W + (kk - k0 + HO) : oA;
         rnb[t] = (kk > 0 ? 1 : 0) | (kk < n2 - 1 ? 2 : 0) | (jj > 0 ? 4 : 0) | (jj < n1 - 1 ? 8 : 0);
     }
-    const bool ring1 = tid < NRING - T2_THREADS;       // warp-uniform except warp 0
+    const bool ring1 = NRING > T2_THREADS && tid < NRING - T2_THREADS;   // warp 0 only
 
     unsigned my_src = 0;   // sources in tile + ring and the step-n plane range
     for (int s = 0; s < a.n_src; ++s)
         if (a.src_i[s] >= pbeg && a.src_i[s] <= pfin && a.src_j[s] >= j0 - 1 &&
-            a.src_j[s] <= j0 + BY && a.src_k[s] >= k0 - 1 && a.src_k[s] <= k0 + PBX)
+            a.src_j[s] <= j0 + TBY && a.src_k[s] >= k0 - 1 && a.src_k[s] <= k0 + TBX)
             my_src |= 1u << s;
 
     constexpr unsigned STAGE_BYTES =
-        (unsigned)(sizeof(T) * ((2 * R2_H + 4 * R1_H) * W + (ACC ? BY * PBX : 0)));
+        (unsigned)(sizeof(T) * ((2 * R2_H + 4 * R1_H) * W + (ACC ? TBY * TBX : 0)));
     const CUtensorMap* mU = pick_map(maps.u_r2, maps.cur);
     const CUtensorMap* mP = pick_map(maps.u_r1, maps.prev);
     // L2 prefetch of a later plane's boxes (no shared memory; hides DRAM
@@ -390,7 +408,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         const unsigned pn = (q + 1 == T2_NS) ? 1u : 0u;   // parity flip for plane p+1
         T* Xc = Xb + xq * PL;
         const T* Xp = Xb + (xq == 0 ? T2_NX - 1 : xq - 1) * PL;
-        const Tma2Stage<T>& S = st[q];
+        const Tma2Stage<T, G>& S = st[q];
         const T* SU = &S.U[0][0];
         const T* SFJ = &S.FJ[0][0];
         const T* SP = &S.P[0][0] - W;     // R1 frame = R2 frame shifted one row

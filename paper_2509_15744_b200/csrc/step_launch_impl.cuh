@@ -70,46 +70,42 @@ void launch_step_engine(int engine, const StepSel& k, dim3 grid, dim3 block, cud
     }
 }
 
-template <typename T, int FL, bool ACC, int SUP>
-void go_step2(int warps, dim3 grid, cudaStream_t s, const Step2Args<T>& a, const Tma2Maps& maps) {
-    const size_t sm = step2_smem_bytes<T>();
-    if (warps == 8) {
-        static bool attr8 = false;
-        if (!attr8) {
-            cudaFuncSetAttribute(step2_kernel_w8<T, FL, ACC, SUP>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            attr8 = true;
-        }
-        step2_kernel_w8<T, FL, ACC, SUP><<<grid, dim3(32, 8, 1), sm, s>>>(a, maps);
-        return;
-    }
+template <typename T, typename G, int FL, bool ACC, int SUP>
+void go_step2(dim3 grid, cudaStream_t s, const Step2Args<T>& a, const Tma2Maps& maps) {
+    const size_t sm = step2_smem_bytes<T, G>();
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(step2_kernel_tma<T, FL, ACC, SUP>,
+        cudaFuncSetAttribute(step2_kernel_tma<T, G, FL, ACC, SUP>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         attr = true;
     }
-    step2_kernel_tma<T, FL, ACC, SUP><<<grid, dim3(32, 4, 1), sm, s>>>(a, maps);
+    step2_kernel_tma<T, G, FL, ACC, SUP><<<grid, dim3(G::TX, G::TY, 1), sm, s>>>(a, maps);
 }
 
-template <typename T, int FL, bool ACC>
-void go_step2_sup(int sup, int warps, dim3 grid, cudaStream_t s, const Step2Args<T>& a,
+template <typename T, typename G, int FL, bool ACC>
+void go_step2_sup(int sup, dim3 grid, cudaStream_t s, const Step2Args<T>& a, const Tma2Maps& maps) {
+    if (sup == SUP_GATHER) go_step2<T, G, FL, ACC, SUP_GATHER>(grid, s, a, maps);
+    else if (sup == SUP_INJECT) go_step2<T, G, FL, ACC, SUP_INJECT>(grid, s, a, maps);
+    else go_step2<T, G, FL, ACC, SUP_NONE>(grid, s, a, maps);
+}
+
+template <typename T, typename G>
+void go_step2_geo(const StepSel& k, dim3 grid, cudaStream_t s, const Step2Args<T>& a,
                   const Tma2Maps& maps) {
-    if (sup == SUP_GATHER) go_step2<T, FL, ACC, SUP_GATHER>(warps, grid, s, a, maps);
-    else if (sup == SUP_INJECT) go_step2<T, FL, ACC, SUP_INJECT>(warps, grid, s, a, maps);
-    else go_step2<T, FL, ACC, SUP_NONE>(warps, grid, s, a, maps);
+    if (k.flavor == RHO_SCALED) {
+        if (k.acc) go_step2_sup<T, G, RHO_SCALED, true>(k.sup, grid, s, a, maps);
+        else go_step2_sup<T, G, RHO_SCALED, false>(k.sup, grid, s, a, maps);
+    } else {
+        if (k.acc) go_step2_sup<T, G, ACOUSTIC, true>(k.sup, grid, s, a, maps);
+        else go_step2_sup<T, G, ACOUSTIC, false>(k.sup, grid, s, a, maps);
+    }
 }
 
 template <typename T>
-void launch_step2_engine(const StepSel& k, int warps, dim3 grid, cudaStream_t s,
+void launch_step2_engine(const StepSel& k, int geo, dim3 grid, cudaStream_t s,
                          const Step2Args<T>& a, const Tma2Maps& maps) {
-    if (k.flavor == RHO_SCALED) {
-        if (k.acc) go_step2_sup<T, RHO_SCALED, true>(k.sup, warps, grid, s, a, maps);
-        else go_step2_sup<T, RHO_SCALED, false>(k.sup, warps, grid, s, a, maps);
-    } else {
-        if (k.acc) go_step2_sup<T, ACOUSTIC, true>(k.sup, warps, grid, s, a, maps);
-        else go_step2_sup<T, ACOUSTIC, false>(k.sup, warps, grid, s, a, maps);
-    }
+    if (geo == GEO_TALL) go_step2_geo<T, GeoTall>(k, grid, s, a, maps);
+    else go_step2_geo<T, GeoWide>(k, grid, s, a, maps);
 }
 
 template <typename T>

@@ -74,7 +74,7 @@ def _problem(W, shape, flavor, n_steps, seed):
     return problem, mat, omat, dt, shots
 
 
-SHAPES = [(40, 8, 64), (9, 24, 128), (64, 128), (3, 16, 192), (70, 48, 128)]
+SHAPES = [(40, 8, 64), (9, 24, 128), (64, 128), (3, 16, 192), (70, 48, 128), (10, 16, 96)]
 
 
 @pytest.mark.parametrize("shape", SHAPES)

@@ -83,9 +83,10 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
  * grid tiles exactly into 64 x 8 cells (0 = never). */
 #define WO_OPT_TMA_KERNEL 3
 /* WO_OPT_TWO_STEP (default 1): advance two time steps per pass over HBM
- * (temporal blocking, identical arithmetic) on single-domain contexts whose
- * grid tiles into 64 x 8 cells with the fast-division path active; sweeps
- * fall back to single steps at odd range ends and everywhere else. */
+ * (temporal blocking, identical arithmetic) on single-domain fp32 contexts
+ * whose plane tiles into 64 x 8 or 32 x 16 cells; 2 = also fp64 contexts;
+ * 0 = never.  Sweeps fall back to single steps at odd range ends, while
+ * recording history, and everywhere else. */
 #define WO_OPT_TWO_STEP 4
 int wo_set_option(wo_ctx* ctx, int option, int value);
 int wo_fast_div_active(const wo_ctx* ctx);

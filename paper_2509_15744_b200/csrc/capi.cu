@@ -458,6 +458,10 @@ bool pair_ready(wo_ctx* ctx) {
     if (!ctx->use_two_step || !ctx->use_tma || !ctx->use_pair || ctx->has_lo || ctx->has_hi ||
         !ctx->material_set || pick_geo(ctx) == GEO_NONE)
         return false;
+    // fp64 two-step CTAs need 130 KB of shared memory (1 CTA/SM) and measure
+    // slower than the single-step kernel (100.9 vs 106.7 Gcell-upd/s, 256^3):
+    // fp64 takes two-step passes only when forced (option value 2)
+    if (ctx->itemsize == 8 && ctx->use_two_step != 2) return false;
     if (ensure_four(ctx) || ensure_mat4(ctx)) return false;
     if (ctx->t2_state == 0) {
         ctx->t2_state = -1;
@@ -1196,7 +1200,7 @@ int wo_set_option(wo_ctx* ctx, int option, int value) {
                 option == WO_OPT_TMA_KERNEL || option == WO_OPT_TWO_STEP,
             "unknown option");
     if (option == WO_OPT_TWO_STEP) {
-        ctx->use_two_step = value != 0;
+        ctx->use_two_step = value;   // 0 off, 1 fp32 grids, 2 also fp64
         return WO_OK;
     }
     if (option == WO_OPT_PAIR_KERNEL) {

@@ -339,9 +339,10 @@ class DeviceGrid:
         """0: never; 1/True: 2x2-cell TMA kernel (default); 2: 256-thread TMA kernel."""
         self._ck(self.L.wo_set_option(self.h, N.WO_OPT_TMA_KERNEL, int(mode)), "wo_set_option")
 
-    def set_two_step(self, on):
-        """Two time steps per HBM pass where the grid allows it (default on)."""
-        self._ck(self.L.wo_set_option(self.h, N.WO_OPT_TWO_STEP, int(bool(on))), "wo_set_option")
+    def set_two_step(self, mode):
+        """Two time steps per HBM pass where the grid allows it: 0/False off,
+        1/True fp32 grids (default), 2 also fp64 grids."""
+        self._ck(self.L.wo_set_option(self.h, N.WO_OPT_TWO_STEP, int(mode)), "wo_set_option")
 
     def fast_div_active(self):
         return bool(self.L.wo_fast_div_active(self.h))

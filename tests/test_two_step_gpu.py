@@ -89,15 +89,15 @@ def test_two_step_gradient_bitexact(W, shape, flavor, prec, n_steps):
     ctx = engine.get_context(problem.grid, W.precision_dtype(prec))
     out = {}
     for two in (True, False):
-        ctx.set_two_step(two)
+        ctx.set_two_step(2 if two else 0)   # 2: fp64 grids too
         ctx.reset_stats()
         out[two] = W.gradient_superposed(problem, mat, cfg)
         pairs = ctx.stats()["pair_launches"]
-        if two and ctx.fast_div_active():
+        if two:
             assert pairs > 0, "two-step path did not run"
         if not two:
             assert pairs == 0
-    ctx.set_two_step(True)
+    ctx.set_two_step(1)
     assert bits_equal(out[True].gradient, out[False].gradient)
     cost, grad, _ = O.gradient_superposed(omat, dt, n_steps, shots, cfg.k, prec)
     assert bits_equal(out[True].gradient, grad)
@@ -109,10 +109,19 @@ def test_two_step_gradient_bitexact(W, shape, flavor, prec, n_steps):
 def test_two_step_forward_traces_and_window(W, shape, dn):
     """Trace gather (no accumulation) and the final window after an odd number
     of steps match the oracle's run_forward."""
+    from paper_2509_15744_b200 import engine
+
     dtype = np.float32 if dn == "f32" else np.float64
     problem, mat, omat, dt, shots = _problem(W, shape, "rho_scaled", 73, 3)
-    res = W.run_forward(mat, problem.time, problem.sources,
-                        W.SensorArray(nodes=problem.sensors.nodes), dtype=dtype)
+    ctx = engine.get_context(problem.grid, dtype)
+    ctx.set_two_step(2)
+    try:
+        ctx.reset_stats()
+        res = W.run_forward(mat, problem.time, problem.sources,
+                            W.SensorArray(nodes=problem.sensors.nodes), dtype=dtype)
+        assert ctx.stats()["pair_launches"] > 0
+    finally:
+        ctx.set_two_step(1)
     sup = np.array([problem.grid.flat_index(n) for n in problem.sensors.nodes], dtype=np.int64)
     osrc = [s for s, _ in shots]
     u_prev, u_cur, traces, _, peak = O.run_forward(omat, dt, 73, osrc, sensor_idx=sup,

@@ -61,6 +61,8 @@ struct wo_ctx {
     Tma2Maps t2maps;
     char* mat4 = nullptr;              // coef | +k | +j | +i faces (two-step passes)
     char* stage = nullptr;             // fp64 upload staging (persistent)
+    char* hstage = nullptr;            // pinned host staging for field downloads (2 halves)
+    cudaEvent_t hev[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
     char* flag = nullptr;              // device int scratch (verification flag)
     size_t flag_bytes = 0;
@@ -975,14 +977,43 @@ int misfit_t(wo_ctx* ctx, int64_t N, int kind, const double* measured, double c1
     return WO_OK;
 }
 
+// Device field -> caller's (pageable) host array through a persistent pinned
+// double buffer: the D2H of chunk i+1 overlaps the host copy of chunk i
+// (a plain pageable cudaMemcpy of a 67 MB field ran at ~4.6 GB/s).
+constexpr size_t HSTAGE_HALF = 8u << 20;
+
+int download_field(wo_ctx* ctx, void* out, const char* dev, size_t bytes) {
+    if (!ctx->hstage) {
+        CK(cudaHostAlloc((void**)&ctx->hstage, 2 * HSTAGE_HALF, cudaHostAllocDefault));
+        for (auto& e : ctx->hev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    char* dst = static_cast<char*>(out);
+    size_t prev_off = 0, prev_n = 0;
+    int half = 0;
+    for (size_t off = 0; off < bytes || prev_n; off += HSTAGE_HALF, half ^= 1) {
+        const size_t n = off < bytes ? std::min(HSTAGE_HALF, bytes - off) : 0;
+        if (n) {
+            CK(cudaMemcpyAsync(ctx->hstage + half * HSTAGE_HALF, dev + off, n,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaEventRecord(ctx->hev[half], ctx->stream));
+        }
+        if (prev_n) {
+            CK(cudaEventSynchronize(ctx->hev[half ^ 1]));
+            std::memcpy(dst + prev_off, ctx->hstage + (half ^ 1) * HSTAGE_HALF, prev_n);
+        }
+        prev_off = off;
+        prev_n = n;
+    }
+    return WO_OK;
+}
+
 template <typename T>
 int gradient_t(wo_ctx* ctx, double two_k, void* out) {
     scale_div_kernel<T><<<592, 256, 0, ctx->stream>>>(reinterpret_cast<T*>(ctx->acc), ctx->cells(),
                                                       (T)two_k);
     ctx->launches++;
     CK(cudaGetLastError());
-    if (out)
-        CK(cudaMemcpyAsync(out, ctx->acc, ctx->field_bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+    if (out) return download_field(ctx, out, ctx->acc, ctx->field_bytes());
     CK(cudaStreamSynchronize(ctx->stream));
     return WO_OK;
 }
@@ -1165,6 +1196,9 @@ void wo_destroy(wo_ctx* ctx) {
         if (b) cudaFree(b);
     for (auto e : ctx->marks)
         if (e) cudaEventDestroy(e);
+    for (auto e : ctx->hev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->hstage) cudaFreeHost(ctx->hstage);
     for (auto e : ctx->ev_free) cudaEventDestroy(e);
     for (auto e : ctx->ev_used) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1301,9 +1335,7 @@ int wo_zero_accumulator(wo_ctx* ctx) {
 int wo_get_accumulator(wo_ctx* ctx, void* out) {
     int rc = check_ctx(ctx);
     if (rc) return rc;
-    CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaMemcpy(out, ctx->acc, ctx->field_bytes(), cudaMemcpyDeviceToHost));
-    return WO_OK;
+    return download_field(ctx, out, ctx->acc, ctx->field_bytes());
 }
 
 int wo_set_accumulator(wo_ctx* ctx, const void* in) {

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/waveb200.h"
@@ -999,7 +1000,18 @@ int download_field(wo_ctx* ctx, void* out, const char* dev, size_t bytes) {
         }
         if (prev_n) {
             CK(cudaEventSynchronize(ctx->hev[half ^ 1]));
-            std::memcpy(dst + prev_off, ctx->hstage + (half ^ 1) * HSTAGE_HALF, prev_n);
+            // fresh destination pages fault on first touch: copy with a few
+            // threads so the faults (not the bandwidth) overlap
+            const char* src = ctx->hstage + (half ^ 1) * HSTAGE_HALF;
+            constexpr int NT = 4;
+            const size_t part = (prev_n / NT + 63) & ~size_t(63);
+            std::thread th[NT - 1];
+            for (int t = 1; t < NT; ++t) {
+                const size_t b = std::min(prev_n, t * part), e = std::min(prev_n, (t + 1) * part);
+                th[t - 1] = std::thread([=] { if (e > b) std::memcpy(dst + prev_off + b, src + b, e - b); });
+            }
+            std::memcpy(dst + prev_off, src, std::min(prev_n, part));
+            for (auto& t : th) t.join();
         }
         prev_off = off;
         prev_n = n;

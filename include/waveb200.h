@@ -102,7 +102,17 @@ int wo_set_support(wo_ctx* ctx, int64_t n_sup, const int64_t* flat_sorted);
 int wo_reset_window(wo_ctx* ctx);                                  /* u^0 = u^1 = 0 */
 int wo_set_window(wo_ctx* ctx, const void* u_prev, const void* u_cur);
 int wo_get_window(wo_ctx* ctx, void* u_prev, void* u_cur);
-int wo_swap_direction(wo_ctx* ctx);                                /* solver.py:149 */
+int wo_swap_direction(wo_ctx* ctx);
+/* Device snapshot of the state a forward sweep leaves behind — the two window
+ * levels, the accumulator and the first n_steps rows of the support store —
+ * so k-dependent backward sweeps can be repeated from it (batched
+ * calibrate_k / ksweep of a single-shot problem, gradients.py:480-548: the
+ * forward sweep and the traces do not depend on k).  op: WO_SNAP_SAVE,
+ * WO_SNAP_RESTORE (n_steps must match the save), WO_SNAP_FREE. */
+#define WO_SNAP_FREE 0
+#define WO_SNAP_SAVE 1
+#define WO_SNAP_RESTORE 2
+int wo_snapshot(wo_ctx* ctx, int op, int64_t n_steps);                                /* solver.py:149 */
 int wo_zero_accumulator(wo_ctx* ctx);
 int wo_get_accumulator(wo_ctx* ctx, void* out);
 int wo_set_accumulator(wo_ctx* ctx, const void* in);

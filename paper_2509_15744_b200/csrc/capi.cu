@@ -63,6 +63,9 @@ struct wo_ctx {
     char* mat4 = nullptr;              // coef | +k | +j | +i faces (two-step passes)
     char* stage = nullptr;             // fp64 upload staging (persistent)
     char* hstage = nullptr;            // pinned host staging for field downloads (2 halves)
+    char* snap = nullptr;              // wo_snapshot: window levels | acc | store
+    size_t snap_bytes = 0;
+    int64_t snap_store = -1;           // store bytes held by the snapshot (-1: none)
     cudaEvent_t hev[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
     char* flag = nullptr;              // device int scratch (verification flag)
@@ -1200,6 +1203,7 @@ void wo_destroy(wo_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     void* bufs[] = {ctx->gamma, ctx->u[0], ctx->u[1], ctx->u[2], ctx->u[3], ctx->mat4, ctx->stage,
+                    ctx->snap,
                     ctx->flag, ctx->acc,
                     ctx->mask, ctx->prefix,
                     ctx->store, ctx->measured, ctx->partial, ctx->cost, ctx->maxslots,
@@ -1327,6 +1331,49 @@ int wo_get_window(wo_ctx* ctx, void* u_prev, void* u_cur) {
     CK(cudaStreamSynchronize(ctx->stream));
     if (u_prev) CK(cudaMemcpy(u_prev, ctx->uprev(), ctx->field_bytes(), cudaMemcpyDeviceToHost));
     if (u_cur) CK(cudaMemcpy(u_cur, ctx->ucur(), ctx->field_bytes(), cudaMemcpyDeviceToHost));
+    return WO_OK;
+}
+
+int wo_snapshot(wo_ctx* ctx, int op, int64_t n_steps) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(op == WO_SNAP_SAVE || op == WO_SNAP_RESTORE || op == WO_SNAP_FREE, "unknown snapshot op");
+    if (op == WO_SNAP_FREE) {
+        if (ctx->snap) {
+            CK(cudaStreamSynchronize(ctx->stream));
+            cudaFree(ctx->snap);
+            ctx->dev_bytes -= (int64_t)ctx->snap_bytes;
+        }
+        ctx->snap = nullptr;
+        ctx->snap_bytes = 0;
+        ctx->snap_store = -1;
+        return WO_OK;
+    }
+    const size_t ab = (size_t)ctx->alloc_cells() * ctx->itemsize, fb = ctx->field_bytes();
+    const size_t sb = (size_t)std::max<int64_t>(n_steps, 0) * ctx->n_sup * ctx->itemsize;
+    if (op == WO_SNAP_SAVE) {
+        REQUIRE(sb <= ctx->store_bytes, "support store smaller than n_steps rows");
+        rc = ensure(ctx, &ctx->snap, &ctx->snap_bytes, 2 * ab + fb + sb);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(ctx->snap, ctx->u[ctx->prv], ab, cudaMemcpyDeviceToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->snap + ab, ctx->u[ctx->cur], ab, cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+        CK(cudaMemcpyAsync(ctx->snap + 2 * ab, ctx->acc, fb, cudaMemcpyDeviceToDevice, ctx->stream));
+        if (sb)
+            CK(cudaMemcpyAsync(ctx->snap + 2 * ab + fb, ctx->store, sb, cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+        ctx->snap_store = (int64_t)sb;
+    } else {
+        REQUIRE(ctx->snap && ctx->snap_store == (int64_t)sb, "no snapshot for this step count");
+        CK(cudaMemcpyAsync(ctx->u[ctx->prv], ctx->snap, ab, cudaMemcpyDeviceToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->u[ctx->cur], ctx->snap + ab, ab, cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+        CK(cudaMemcpyAsync(ctx->acc, ctx->snap + 2 * ab, fb, cudaMemcpyDeviceToDevice, ctx->stream));
+        if (sb)
+            CK(cudaMemcpyAsync(ctx->store, ctx->snap + 2 * ab + fb, sb, cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
     return WO_OK;
 }
 

@@ -131,6 +131,7 @@ class DeviceGrid:
         self.h = h
         self._support_key = None
         self.n_sup = 0
+        self.claim = None      # the plan / batch whose material and support are loaded
 
     @property
     def is_slab(self):
@@ -206,6 +207,11 @@ class DeviceGrid:
         uc = np.empty(self.grid.shape, self.dtype)
         self._ck(self.L.wo_get_window(self.h, N.ptr(up), N.ptr(uc)), "wo_get_window")
         return up, uc
+
+    def snapshot(self, op, n_steps=0):
+        """Save / restore / free the post-forward device state (wo_snapshot)."""
+        code = {"save": N.WO_SNAP_SAVE, "restore": N.WO_SNAP_RESTORE, "free": N.WO_SNAP_FREE}[op]
+        self._ck(self.L.wo_snapshot(self.h, code, int(n_steps)), "wo_snapshot")
 
     def swap_direction(self):
         self._ck(self.L.wo_swap_direction(self.h), "wo_swap_direction")

@@ -151,3 +151,63 @@ def test_two_step_instability_step(W, courant):
     assert ei.value.step == eo.value.step
     assert ei.value.max_abs == eo.value.max_abs or (
         np.isnan(ei.value.max_abs) and np.isnan(eo.value.max_abs))
+
+
+# ------------------------------------------------ k batching
+def test_calibrate_k_batched_equals_unbatched(W, golden):
+    """One forward sweep per precision for every decade gives the same rows
+    as one gradient_superposed per decade (and the reference's rows)."""
+    import cases
+    from helpers import product_tato_problem
+
+    g = golden("tato2d")
+    c = cases.tato2d_case()
+    problem = product_tato_problem(W, c)
+    mat = problem.material(g["g_bar"])
+    fast = W.calibrate_k(problem, mat, k_start=1e18)
+    slow = W.calibrate_k(problem, mat, k_start=1e18, batch=False)
+    assert fast.rows == slow.rows
+    assert fast.k == slow.k == float(g["cal_k"])
+    assert fast.diverged_at == slow.diverged_at
+
+
+@pytest.mark.parametrize("shape", [(40, 8, 64), (33, 29)])
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_kbatch_bitexact_per_k(W, shape, prec):
+    from paper_2509_15744_b200 import gradients as G
+
+    problem, mat, omat, dt, shots = _problem(W, shape, "rho_scaled", 60, 7)
+    problem = W.FwiProblem(grid=problem.grid, time=problem.time, material=mat,
+                           sources=problem.sources[:1], sensors=problem.sensors,
+                           measured=problem.measured[:1])
+    batch = G.KBatch(problem, mat, prec)
+    try:
+        for k in (1e15, 1e13, 1e11):
+            got = batch.gradient(k)
+            ref = W.gradient_superposed(problem, mat, W.SuperpositionConfig(k=k, precision=prec))
+            assert bits_equal(got.gradient, ref.gradient), k
+            assert got.cost == ref.cost
+        # interleave an unrelated evaluation on the same context, then batch again
+        other = mat.with_gamma(np.asarray(mat.gamma) * 0.9)
+        W.gradient_superposed(problem, other, W.SuperpositionConfig(k=1e13, precision=prec))
+        got = batch.gradient(1e12)
+        ref = W.gradient_superposed(problem, mat, W.SuperpositionConfig(k=1e12, precision=prec))
+        assert bits_equal(got.gradient, ref.gradient)
+    finally:
+        batch.close()
+
+
+def test_ksweep_batched_rows(W):
+    from paper_2509_15744_b200 import gradients as G
+
+    problem, mat, _, _, _ = _problem(W, (24, 16, 64), "rho_scaled", 50, 9)
+    problem = W.FwiProblem(grid=problem.grid, time=problem.time, material=mat,
+                           sources=problem.sources[:1], sensors=problem.sensors,
+                           measured=problem.measured[:1])
+    ks = [1e14, 1e12]
+    rows, ref = W.ksweep(problem, mat, ks)
+    for (k, e32, e64) in rows:
+        g32 = W.gradient_superposed(problem, mat, W.SuperpositionConfig(k=k, precision="single"))
+        g64 = W.gradient_superposed(problem, mat, W.SuperpositionConfig(k=k, precision="double"))
+        assert e32 == G.rel_mse(g32.gradient, ref)
+        assert e64 == G.rel_mse(g64.gradient, ref)

@@ -171,7 +171,7 @@ def test_calibrate_k_batched_equals_unbatched(W, golden):
     assert fast.diverged_at == slow.diverged_at
 
 
-@pytest.mark.parametrize("shape", [(40, 8, 64), (33, 29)])
+@pytest.mark.parametrize("shape", [(40, 8, 64), (33, 64)])
 @pytest.mark.parametrize("prec", ["single", "double"])
 def test_kbatch_bitexact_per_k(W, shape, prec):
     from paper_2509_15744_b200 import gradients as G

@@ -501,21 +501,32 @@ bool pair_ready(wo_ctx* ctx) {
     return ctx->t2_state == 1;
 }
 
-// (tile, plane) units per CTA of a two-step pass: the CTAs of ONE wave
-// (3 per SM) split the tiles x n0 sequence evenly, so no wave is partly idle
-// (a 1.73-wave grid of fixed chunks idled a quarter of its last wave); each
-// CTA walks one or two contiguous segments and recomputes ~1 extra plane per
-// segment.  At least min(n0, 8) units per CTA; WB_T2_PER_CTA overrides.
-int choose_per_cta(const wo_ctx* ctx, int tiles) {
+// planes per CTA of a two-step pass: whole waves of resident CTAs matter
+// more than chunk length (a 1.73-wave grid idles a quarter of the last
+// wave), and each chunk recomputes ~1 extra step-n plane.  Cost model:
+// waves(nz) * (planes per chunk + 1); WB_T2_NZ overrides (tuning runs).
+int choose_chunk2(const wo_ctx* ctx) {
+    const int tbx = ctx->t2_geo == GEO_TALL ? GeoTall::TBX : GeoWide::TBX;
+    const int tby = ctx->t2_geo == GEO_TALL ? GeoTall::TBY : GeoWide::TBY;
+    const int tiles = (ctx->kn2 / tbx) * (ctx->kn1 / tby);
     static const int forced = [] {
-        const char* e = getenv("WB_T2_PER_CTA");
+        const char* e = getenv("WB_T2_NZ");
         return e ? atoi(e) : 0;
     }();
-    if (forced > 0) return forced;
-    const int64_t units = (int64_t)tiles * ctx->kn0;
-    const int slots = ctx->num_sms * (ctx->itemsize == 4 ? 3 : 1);
-    const int64_t even = (units + slots - 1) / slots;
-    return (int)std::max<int64_t>(even, std::min(ctx->kn0, 8));
+    int best_nz = 1;
+    if (forced > 0) {
+        best_nz = forced;
+    } else {
+        const int slots = ctx->num_sms * (ctx->itemsize == 4 ? 3 : 1);
+        double best = 1e30;
+        for (int nz = 1; nz <= std::min(ctx->kn0, 64); ++nz) {
+            const int chunk = (ctx->kn0 + nz - 1) / nz;
+            const int waves = (tiles * nz + slots - 1) / slots;
+            const double cost = (double)waves * (chunk + 1);
+            if (cost < best - 1e-9) { best = cost; best_nz = nz; }
+        }
+    }
+    return std::max(1, (ctx->kn0 + best_nz - 1) / best_nz);
 }
 
 struct PairSpec {
@@ -543,11 +554,7 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     a.out2 = reinterpret_cast<T*>(ctx->base0(ctx->u[x[1]]));
     a.acc = reinterpret_cast<T*>(ctx->acc);
     a.n0 = ctx->kn0; a.n1 = ctx->kn1; a.n2 = ctx->kn2;
-    const int tbx = ctx->t2_geo == GEO_TALL ? GeoTall::TBX : GeoWide::TBX;
-    const int tby = ctx->t2_geo == GEO_TALL ? GeoTall::TBY : GeoWide::TBY;
-    a.ntx = ctx->kn2 / tbx;
-    a.tiles = a.ntx * (ctx->kn1 / tby);
-    a.per_cta = choose_per_cta(ctx, a.tiles);
+    a.chunk = choose_chunk2(ctx);
     a.mat = mat_scalars<T>(ctx);
     a.cv = (T)ctx->cv; a.cg = (T)ctx->cg; a.inv2dt = (T)ctx->inv2dt; a.inv2dx = (T)ctx->inv2dx;
     a.sdt = (T)sp.sdt;
@@ -575,8 +582,9 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     a.max2 = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots) + sp.slot2;
     ctx->t2maps.prev = ctx->prv;
     ctx->t2maps.cur = ctx->cur;
-    const int64_t units = (int64_t)a.tiles * ctx->kn0;
-    dim3 grid((unsigned)((units + a.per_cta - 1) / a.per_cta), 1, 1);
+    const int tbx = ctx->t2_geo == GEO_TALL ? GeoTall::TBX : GeoWide::TBX;
+    const int tby = ctx->t2_geo == GEO_TALL ? GeoTall::TBY : GeoWide::TBY;
+    dim3 grid(ctx->kn2 / tbx, ctx->kn1 / tby, (ctx->kn0 + a.chunk - 1) / a.chunk);
     if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
     launch_step2_engine<T>(StepSel{ctx->flavor, true, sp.acc, false, sup}, ctx->t2_geo, grid,
                            ctx->stream, a, ctx->t2maps);

@@ -76,8 +76,7 @@ template <typename T> struct Step2Args {
     T* out1;           // u^{n+1}
     T* out2;           // u^{n+2}
     T* acc;
-    int n0, n1, n2;
-    int ntx, tiles, per_cta;   // tiles along axis 2, tiles per plane, (tile, plane) units per CTA
+    int n0, n1, n2, chunk;
     MatScalars<T> mat;
     T cv, cg, inv2dt, inv2dx, sdt;
     int n_src;
@@ -165,23 +164,13 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
 
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = ty * G::TX + tx;
+    const int k0 = blockIdx.x * TBX, j0 = blockIdx.y * TBY;
+    const int kA = k0 + 2 * tx, ja = j0 + 2 * ty;
     const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
     const int plane = n1 * n2;
-    Bits lmax1 = 0, lmax2 = 0;
-    unsigned ph = 0;                           // mbarrier phase bit of every stage
-    if (tid == 0) {
-        for (int s = 0; s < T2_NS; ++s) mbar_init(&bar[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    // One segment = planes [i0, i1) of the tile at (k0, j0).  A CTA walks a
-    // contiguous range of the (tile, plane) sequence (host: per_cta planes,
-    // one wave of CTAs), i.e. one or two segments; every stage is consumed
-    // by the end of a segment, so the next one restarts the ring at stage 0.
-    auto segment = [&](const int k0, const int j0, const int i0, const int i1) {
-    const int kA = k0 + 2 * tx, ja = j0 + 2 * ty;
-    const int pbeg = max(i0 - 1, 0);           // step-n planes of this segment
+    const int i0 = blockIdx.z * a.chunk;
+    const int i1 = min(i0 + a.chunk, n0);
+    const int pbeg = max(i0 - 1, 0);           // step-n planes of this chunk
     const int pfin = min(i1, n0 - 1);
 
     // ---- per-thread offsets in the R2 frame (rows j0-2.., cols k0-HO..) ----
@@ -250,6 +239,11 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         tma_load_3d(&st[s].FI[0][0], &maps.fi_r1, k0 - HO, j0 - 1, p, &bar[s]);
         if (ACC) tma_load_3d(&st[s].A[0][0], &maps.a_ctr, k0, j0, p, &bar[s]);
     };
+    if (tid == 0) {
+        for (int s = 0; s < T2_NS; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
     if (tid == T2_PRODUCER) {
         for (int s = 0; s < T2_NS && pbeg + s <= pfin; ++s) issue(pbeg + s, s);
         for (int d = 0; d < T2_PF && pbeg + T2_NS + d <= pfin; ++d) prefetch(pbeg + T2_NS + d);
@@ -348,8 +342,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
                 rw0[t] = __ldg(a.fi + gm + ring_gofs(t));
             }
     }
-    mbar_wait(&bar[0], ph & 1u);
-    ph ^= 1u;
+    mbar_wait(&bar[0], 0u);
     V un0_a = ldv(&st[0].U[0][0] + oA), un0_b = ldv(&st[0].U[0][0] + oB);
     T run0[2];
 #pragma unroll
@@ -367,6 +360,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     V x_m1a = un0_a, x_m1b = un0_b, x_0a = un0_a, x_0b = un0_b;   // u^{n+1}(p-2), (p-1)
     V un1_a = unm_a, un1_b = unm_b;                                // u^n(p-1)
     V acc1_a = {T(0), T(0)}, acc1_b = acc1_a;                      // acc after step n at p-1
+    Bits lmax1 = 0, lmax2 = 0;
 
     // step n+1 at plane q1 for the tile: xp = u^{n+1}(q1+1) (registers)
     auto step2_tile = [&](int q1, const T* Xq, V xp_a, V xp_b) {
@@ -404,13 +398,14 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         }
     };
 
-    // one plane; q = stage of plane p, xq = its X
+    // one plane; q = stage of plane p, gpar = its mbarrier parity, xq = its X
     // buffer (rolled loop: unrolled copies of this body overflow the
     // instruction cache).  One barrier per plane, after step n: it publishes
     // X(p) and frees stage(p), which is refilled at once (T2_NS planes ahead);
     // three X buffers keep X(p) from overwriting X(p-3) before (c) read it.
-    auto body = [&](int q, int xq, int p) {
+    auto body = [&](int q, int xq, int p, unsigned gpar) {
         const int sn = q + 1 == T2_NS ? 0 : q + 1;
+        const unsigned pn = (q + 1 == T2_NS) ? 1u : 0u;   // parity flip for plane p+1
         T* Xc = Xb + xq * PL;
         const T* Xp = Xb + (xq == 0 ? T2_NX - 1 : xq - 1) * PL;
         const Tma2Stage<T, G>& S = st[q];
@@ -424,8 +419,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         V unp_a = un0_a, unp_b = un0_b;
         T runp[2] = {run0[0], run0[1]};
         if (p + 1 <= pfin) {
-            mbar_wait(&bar[sn], (ph >> sn) & 1u);
-            ph ^= 1u << sn;
+            mbar_wait(&bar[sn], gpar ^ pn);
             const T* NU = &st[sn].U[0][0];
             unp_a = ldv(NU + oA); unp_b = ldv(NU + oB);
 #pragma unroll
@@ -531,10 +525,11 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         }
     };
 
+    unsigned gpar = 0;
     int xq = 0;
     for (int p = pbeg, q = 0; p <= pfin; ++p) {
-        body(q, xq, p);
-        if (++q == T2_NS) q = 0;
+        body(q, xq, p, gpar);
+        if (++q == T2_NS) { q = 0; gpar ^= 1u; }
         if (++xq == T2_NX) xq = 0;
     }
 
@@ -543,16 +538,6 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     // pfin = n0-1 = i1-1 and plane n0 mirrors the plane itself (X(pfin) was
     // published by the last plane's barrier)
     if (pfin == i1 - 1) step2_tile(pfin, Xb + ((pfin - pbeg) % T2_NX) * PL, x_0a, x_0b);
-    };   // segment
-
-    const int w_total = a.tiles * n0;
-    const int c0 = blockIdx.x * a.per_cta, c1 = min(c0 + a.per_cta, w_total);
-    for (int g = c0; g < c1;) {
-        const int tile = g / n0, i0 = g - tile * n0, i1 = min(n0, i0 + (c1 - g));
-        g += i1 - i0;
-        segment((tile % a.ntx) * TBX, (tile / a.ntx) * TBY, i0, i1);
-        __syncthreads();   // the epilogue's X reads finish before the next segment
-    }
 
     if (a.check1 || a.check2) {
         for (int o = 16; o > 0; o >>= 1) {

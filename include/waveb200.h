@@ -185,6 +185,14 @@ int wo_sweep_backward(wo_ctx* ctx, int64_t n_steps, int64_t src_flat, const doub
 /* acc /= T(2k) in place, then copy out (gradients.py:315); out == NULL
  * leaves the gradient resident on the device. */
 int wo_get_gradient(wo_ctx* ctx, double two_k, void* out);
+/* One device field to the host (io.py:29-52 dump layout when
+ * first_axis_fastest != 0: the axes reversed on the device, so the bytes are
+ * exactly np.ravel(field, order="F") of the reference's dump_field). */
+#define WO_FIELD_GAMMA 0
+#define WO_FIELD_UPREV 1
+#define WO_FIELD_UCUR 2
+#define WO_FIELD_ACC 3
+int wo_get_field(wo_ctx* ctx, int which, int first_axis_fastest, void* out);
 
 /* One explicit step with an optional sparse (idx, vals) or dense (fp64
  * field) force and a finiteness max (solver.py:173-177, 189-202; the

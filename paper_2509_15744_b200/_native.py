@@ -31,6 +31,7 @@ EXPORTS = (
     "wo_timer_elapsed", "wo_synchronize", "wo_accumulator_ptr", "wo_set_option",
     "wo_fast_div_active", "wo_sweep_forward_range", "wo_sweep_backward_range",
     "wo_check_maxima", "wo_halo_planes", "wo_exchange_local", "wo_pair_launches", "wo_snapshot",
+    "wo_get_field",
 )
 
 
@@ -96,12 +97,14 @@ _SIGS = {
     "wo_exchange_local": (c_int, [c_vp, c_vp]),
     "wo_pair_launches": (c_i64, [c_vp]),
     "wo_snapshot": (c_int, [c_vp, c_int, c_i64]),
+    "wo_get_field": (c_int, [c_vp, c_int, c_int, c_vp]),
 }
 WO_OPT_FAST_DIV = 1
 WO_OPT_PAIR_KERNEL = 2
 WO_OPT_TMA_KERNEL = 3
 WO_OPT_TWO_STEP = 4
 WO_SNAP_FREE, WO_SNAP_SAVE, WO_SNAP_RESTORE = 0, 1, 2
+WO_FIELD_GAMMA, WO_FIELD_UPREV, WO_FIELD_UCUR, WO_FIELD_ACC = 0, 1, 2, 3
 
 
 def load(require_device=False):

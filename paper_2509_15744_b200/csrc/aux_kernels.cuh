@@ -5,6 +5,7 @@
 //   scale_div_kernel gradients.py:315 — acc /= T(2k)
 //   inject_kernel   solver.py:167-170 — sparse nodal += for >MAX_SRC nodes
 //   dense_force_kernel solver.py:163-165 — out += fc * T(force)
+//   reverse_axes_kernel io.py:29-52 — C-order field -> first-axis-fastest dump
 #pragma once
 
 #include "common.cuh"
@@ -103,6 +104,29 @@ __global__ void max_abs_kernel(const T* u, long long n, typename FTraits<T>::Bit
         m = v > m ? v : m;
     }
     if ((threadIdx.x & 31) == 0 && m) atomicMax(slot, m);
+}
+
+// out = the field with its axes reversed (A, B, C) -> (C, B, A): the
+// first-axis-fastest byte order of the reference's field dumps
+// (io.py:29-52, np.ravel(order="F")).  For each middle index j the (A x C)
+// slab is transposed through a 32 x 33 shared tile so both the reads (along
+// C) and the writes (along A) are coalesced.  2D / 1D fields are (1, n0, n1)
+// / (1, 1, n0) here; reversing those dims gives the same bytes.
+template <typename T>
+__global__ void reverse_axes_kernel(const T* __restrict__ in, T* __restrict__ out, int A, int B,
+                                    int C) {
+    __shared__ T tile[32][33];
+    const int j = blockIdx.z;
+    const int k0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {   // rows i, columns k
+        const int i = i0 + r, k = k0 + threadIdx.x;
+        if (i < A && k < C) tile[r][threadIdx.x] = in[((long long)i * B + j) * C + k];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {   // rows k, columns i
+        const int k = k0 + r, i = i0 + threadIdx.x;
+        if (i < A && k < C) out[((long long)k * B + j) * A + i] = tile[threadIdx.x][r];
+    }
 }
 
 }  // namespace wb

@@ -63,6 +63,8 @@ struct wo_ctx {
     char* mat4 = nullptr;              // coef | +k | +j | +i faces (two-step passes)
     char* stage = nullptr;             // fp64 upload staging (persistent)
     char* hstage = nullptr;            // pinned host staging for field downloads (2 halves)
+    char* scratch = nullptr;           // one field (wo_get_field axis reversal)
+    size_t scratch_bytes = 0;
     char* snap = nullptr;              // wo_snapshot: window levels | acc | store
     size_t snap_bytes = 0;
     int64_t snap_store = -1;           // store bytes held by the snapshot (-1: none)
@@ -1210,7 +1212,7 @@ void wo_destroy(wo_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     void* bufs[] = {ctx->gamma, ctx->u[0], ctx->u[1], ctx->u[2], ctx->u[3], ctx->mat4, ctx->stage,
-                    ctx->snap,
+                    ctx->snap, ctx->scratch,
                     ctx->flag, ctx->acc,
                     ctx->mask, ctx->prefix,
                     ctx->store, ctx->measured, ctx->partial, ctx->cost, ctx->maxslots,
@@ -1554,6 +1556,32 @@ int wo_sweep_backward(wo_ctx* ctx, int64_t n_steps, int64_t src_flat, const doub
     REQUIRE(ctx->material_set, "material not set");
     return DISPATCH(ctx, sweep_backward_t, ctx, n_steps, src_flat, src_amp, inject_support,
                     accumulate, dt, fail_step, fail_max);
+}
+
+int wo_get_field(wo_ctx* ctx, int which, int first_axis_fastest, void* out) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(which >= WO_FIELD_GAMMA && which <= WO_FIELD_ACC, "unknown field");
+    REQUIRE(out, "null output");
+    const char* src = which == WO_FIELD_GAMMA ? ctx->base0(ctx->gamma)
+                      : which == WO_FIELD_UPREV ? ctx->uprev()
+                      : which == WO_FIELD_UCUR ? ctx->ucur()
+                                               : ctx->acc;
+    const size_t fb = ctx->field_bytes();
+    if (!first_axis_fastest) return download_field(ctx, out, src, fb);
+    rc = ensure(ctx, &ctx->scratch, &ctx->scratch_bytes, fb);
+    if (rc) return rc;
+    const int A = ctx->kn0, B = ctx->kn1, C = ctx->kn2;
+    dim3 grid((C + 31) / 32, (A + 31) / 32, B), block(32, 8);
+    if (ctx->itemsize == 4)
+        reverse_axes_kernel<float><<<grid, block, 0, ctx->stream>>>(
+            reinterpret_cast<const float*>(src), reinterpret_cast<float*>(ctx->scratch), A, B, C);
+    else
+        reverse_axes_kernel<double><<<grid, block, 0, ctx->stream>>>(
+            reinterpret_cast<const double*>(src), reinterpret_cast<double*>(ctx->scratch), A, B, C);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    return download_field(ctx, out, ctx->scratch, fb);
 }
 
 int wo_get_gradient(wo_ctx* ctx, double two_k, void* out) {

@@ -208,6 +208,17 @@ class DeviceGrid:
         self._ck(self.L.wo_get_window(self.h, N.ptr(up), N.ptr(uc)), "wo_get_window")
         return up, uc
 
+    def get_field(self, which, first_axis_fastest=False):
+        """A device field ("gamma", "u_prev", "u_cur", "acc") on the host; with
+        first_axis_fastest the flat bytes of the reference's dumps
+        (io.py:29-52), reordered on the device."""
+        code = {"gamma": N.WO_FIELD_GAMMA, "u_prev": N.WO_FIELD_UPREV,
+                "u_cur": N.WO_FIELD_UCUR, "acc": N.WO_FIELD_ACC}[which]
+        out = np.empty(int(np.prod(self.grid.shape)), self.dtype)
+        self._ck(self.L.wo_get_field(self.h, code, int(bool(first_axis_fastest)), N.ptr(out)),
+                 "wo_get_field")
+        return out if first_axis_fastest else out.reshape(self.grid.shape)
+
     def snapshot(self, op, n_steps=0):
         """Save / restore / free the post-forward device state (wo_snapshot)."""
         code = {"save": N.WO_SNAP_SAVE, "restore": N.WO_SNAP_RESTORE, "free": N.WO_SNAP_FREE}[op]

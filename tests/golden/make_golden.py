@@ -207,6 +207,36 @@ def gen_kats(W):
     return out
 
 
+def gen_io(W):
+    """Field dumps and raw traces written by the reference's io.py (byte
+    fixtures for the first-axis-fastest layout and the sidecars)."""
+    import tempfile
+
+    import waveopt_ref.io as RIO
+
+    rng = np.random.default_rng(21)
+    out = {}
+    cases_io = [
+        ("f32_3d", rng.normal(size=(5, 4, 3)).astype(np.float32), (5, 4, 3), 2e-4,
+         dict(dt=3e-9, step_index=17, extra={"what": "acc"})),
+        ("f64_2d", rng.normal(size=(6, 7)), (6, 7), 0.5, {}),
+        ("f32_1d", rng.normal(size=(9,)).astype(np.float32), (9,), 1.0, dict(step_index=0)),
+    ]
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, vals, shape, dx, kw in cases_io:
+            grid = W.build_grid(shape, dx)
+            path = RIO.dump_field(os.path.join(tmp, name), vals, grid, **kw)
+            out[f"{name}_values"] = vals
+            out[f"{name}_bin"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+            out[f"{name}_json"] = np.array(open(str(path)[:-4] + ".json").read())
+        traces = rng.normal(size=(3, 11))
+        path = RIO.save_traces_raw(os.path.join(tmp, "traces"), traces, 2.5e-9)
+        out["traces_values"] = traces
+        out["traces_bin"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+        out["traces_json"] = np.array(open(str(path)[:-4] + ".json").read())
+    return out
+
+
 def main():
     W = load_reference()
     import waveopt_ref.kernels  # noqa: F401
@@ -223,6 +253,7 @@ def main():
         ("fwi3d", lambda: gen_fwi(W, cases.fwi3d_case())),
         ("tato2d", lambda: gen_tato(W, cases.tato2d_case())),
         ("desk_fwi", lambda: gen_fwi(W, cases.DESK)),
+        ("io_dumps", lambda: gen_io(W)),
     ]
     only = set(sys.argv[1:])
     for name, fn in jobs:

@@ -211,3 +211,25 @@ def test_ksweep_batched_rows(W):
         g64 = W.gradient_superposed(problem, mat, W.SuperpositionConfig(k=k, precision="double"))
         assert e32 == G.rel_mse(g32.gradient, ref)
         assert e64 == G.rel_mse(g64.gradient, ref)
+
+
+# ------------------------------------------------ device field dumps (8f-4)
+@pytest.mark.parametrize("shape", [(40, 8, 64), (33, 64), (37, 45, 19)])
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_device_dump_equals_host_dump(W, tmp_path, shape, prec):
+    from paper_2509_15744_b200 import engine
+    from paper_2509_15744_b200 import io as WIO
+
+    problem, mat, _, _, _ = _problem(W, shape, "rho_scaled", 30, 4)
+    res = W.gradient_superposed(problem, mat, W.SuperpositionConfig(k=1e13, precision=prec))
+    ctx = engine.get_context(problem.grid, W.precision_dtype(prec))
+    flat = ctx.get_field("acc", first_axis_fastest=True)
+    assert bits_equal(flat, np.ravel(res.gradient, order="F"))
+    a = WIO.dump_device_field(tmp_path / "dev", ctx, "acc", dt=problem.time.dt, step_index=30)
+    b = WIO.dump_field(tmp_path / "host", res.gradient, problem.grid, dt=problem.time.dt,
+                       step_index=30)
+    assert a.read_bytes() == b.read_bytes()
+    assert a.with_suffix(".json").read_text() == b.with_suffix(".json").read_text()
+    gam = ctx.get_field("gamma", first_axis_fastest=True)
+    dt = np.float32 if prec == "single" else np.float64
+    assert bits_equal(gam, np.ravel(np.asarray(mat.gamma).astype(dt), order="F"))

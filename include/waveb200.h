@@ -89,6 +89,20 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
  * recording history, and everywhere else. */
 #define WO_OPT_TWO_STEP 4
 int wo_set_option(wo_ctx* ctx, int option, int value);
+/* Device-resident optimisation loop (fwi.py:178-238 with
+ * optim.py adam_step / clip_bounds): fp64 parameters (gamma), the Adam
+ * moments and a frozen mask live on the GPU.  wo_opt_step(t) reads the
+ * finished gradient from the accumulator (zeroed on frozen cells when
+ * zero_frozen_grad), applies Adam step t and the [lo, hi] clip with numpy's
+ * fp64 operation order, pins frozen cells to frozen_value, writes
+ * gamma.astype(T) as the context's new material and returns the gradient's
+ * L2 norm (fixed-order fp64 sum; a log value).  wo_opt_get downloads the
+ * parameters. */
+int wo_opt_init(wo_ctx* ctx, const double* params, const unsigned char* frozen, int zero_frozen_grad,
+                double lo, double hi, double frozen_value, double alpha, double beta1,
+                double beta2, double eps);
+int wo_opt_step(wo_ctx* ctx, int t, double* grad_norm);
+int wo_opt_get(wo_ctx* ctx, double* params);
 int wo_fast_div_active(const wo_ctx* ctx);
 /* Kernel-increment scalars (gradients.py:117-129, kernels.py:149-152): the
  * fp64 values cv, cg, 1/(2dt), 1/(2dx); cast to the field dtype here. */

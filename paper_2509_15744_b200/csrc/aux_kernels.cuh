@@ -6,6 +6,7 @@
 //   inject_kernel   solver.py:167-170 — sparse nodal += for >MAX_SRC nodes
 //   dense_force_kernel solver.py:163-165 — out += fc * T(force)
 //   reverse_axes_kernel io.py:29-52 — C-order field -> first-axis-fastest dump
+//   adam_clip_kernel optim.py adam_step + clip_bounds on the device (8f-3)
 #pragma once
 
 #include "common.cuh"
@@ -127,6 +128,61 @@ __global__ void reverse_axes_kernel(const T* __restrict__ in, T* __restrict__ ou
         const int k = k0 + r, i = i0 + threadIdx.x;
         if (i < A && k < C) out[((long long)k * B + j) * A + i] = tile[threadIdx.x][r];
     }
+}
+
+// numpy's clip for floats: MIN(MAX(x, lo), hi) with NaN passed through and
+// PyArray_MAX(a, b) = a > b ? a : b (npy_math / clip loops)
+__device__ __forceinline__ double np_clip(double x, double lo, double hi) {
+    if (x != x) return x;
+    const double y = x > lo ? x : lo;
+    return y < hi ? y : hi;
+}
+
+struct AdamScalars {
+    double beta1, beta2, c1, c2;   // c1 = 1 - beta1, c2 = 1 - beta2 (host Python floats)
+    double bc1, bc2;               // 1 - beta1**t, 1 - beta2**t
+    double alpha, eps, lo, hi, frozen_value;
+};
+
+// One bias-corrected Adam step and bound clip per cell with numpy's fp64
+// operation order (optim.py adam_step / clip_bounds, fwi.py:178-238):
+//   g = double(acc) (0 on frozen cells when zero_frozen)
+//   m = b1*m + (1-b1)*g ;  v = b2*v + ((1-b2)*g)*g
+//   p = p - (alpha*(m/bc1)) / (sqrt(v/bc2) + eps) ; clip ; frozen -> value
+// The new parameters are also cast to the field dtype (gamma.astype(T)) and
+// the block partial sums of g*g (fixed tree) give the logged gradient norm.
+template <typename T>
+__global__ void adam_clip_kernel(const T* __restrict__ acc, double* __restrict__ p,
+                                 double* __restrict__ m, double* __restrict__ v,
+                                 const unsigned char* __restrict__ frozen, int zero_frozen,
+                                 AdamScalars s, long long n, T* __restrict__ gamma,
+                                 double* __restrict__ partial) {
+    __shared__ double red[256];
+    double sq = 0.0;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+         c += (long long)gridDim.x * blockDim.x) {
+        const bool fz = frozen && frozen[c];
+        double g = (double)acc[c];
+        if (zero_frozen && fz) g = 0.0;
+        sq = sq + g * g;
+        const double mc = __dadd_rn(__dmul_rn(s.beta1, m[c]), __dmul_rn(s.c1, g));
+        const double vc = __dadd_rn(__dmul_rn(s.beta2, v[c]), __dmul_rn(__dmul_rn(s.c2, g), g));
+        m[c] = mc;
+        v[c] = vc;
+        const double mh = __ddiv_rn(mc, s.bc1), vh = __ddiv_rn(vc, s.bc2);
+        const double step = __ddiv_rn(__dmul_rn(s.alpha, mh), __dadd_rn(__dsqrt_rn(vh), s.eps));
+        double x = np_clip(__dsub_rn(p[c], step), s.lo, s.hi);
+        if (fz) x = s.frozen_value;
+        p[c] = x;
+        gamma[c] = (T)x;
+    }
+    red[threadIdx.x] = sq;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] = red[threadIdx.x] + red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
 }
 
 }  // namespace wb

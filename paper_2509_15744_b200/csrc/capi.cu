@@ -64,6 +64,11 @@ struct wo_ctx {
     char* stage = nullptr;             // fp64 upload staging (persistent)
     char* hstage = nullptr;            // pinned host staging for field downloads (2 halves)
     char* scratch = nullptr;           // one field (wo_get_field axis reversal)
+    double* opt = nullptr;             // wo_opt_*: params | m | v (fp64 fields)
+    unsigned char* opt_frozen = nullptr;
+    double* opt_partial = nullptr;     // 592 block sums
+    AdamScalars adam{};
+    int opt_zero_frozen = 0;
     size_t scratch_bytes = 0;
     char* snap = nullptr;              // wo_snapshot: window levels | acc | store
     size_t snap_bytes = 0;
@@ -1212,7 +1217,7 @@ void wo_destroy(wo_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     void* bufs[] = {ctx->gamma, ctx->u[0], ctx->u[1], ctx->u[2], ctx->u[3], ctx->mat4, ctx->stage,
-                    ctx->snap, ctx->scratch,
+                    ctx->snap, ctx->scratch, ctx->opt, ctx->opt_frozen, ctx->opt_partial,
                     ctx->flag, ctx->acc,
                     ctx->mask, ctx->prefix,
                     ctx->store, ctx->measured, ctx->partial, ctx->cost, ctx->maxslots,
@@ -1250,6 +1255,72 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
     ctx->material_set = true;
     ctx->mat4_valid = false;
     return verify_fast_div(ctx);
+}
+
+int wo_opt_init(wo_ctx* ctx, const double* params, const unsigned char* frozen, int zero_frozen_grad,
+                double lo, double hi, double frozen_value, double alpha, double beta1,
+                double beta2, double eps) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(!ctx->has_lo && !ctx->has_hi, "the device optimiser runs on single-domain contexts");
+    REQUIRE(lo < hi, "need lo < hi");
+    const int64_t n = ctx->cells();
+    if (!ctx->opt) {
+        if ((rc = dev_alloc(ctx, (void**)&ctx->opt, (size_t)n * 24))) return rc;
+        if ((rc = dev_alloc(ctx, (void**)&ctx->opt_frozen, (size_t)n))) return rc;
+        if ((rc = dev_alloc(ctx, (void**)&ctx->opt_partial, 592 * 8))) return rc;
+    }
+    CK(cudaMemcpyAsync(ctx->opt, params, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(ctx->opt + n, 0, (size_t)n * 16, ctx->stream));   // m = v = 0
+    if (frozen)
+        CK(cudaMemcpyAsync(ctx->opt_frozen, frozen, (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
+    else
+        CK(cudaMemsetAsync(ctx->opt_frozen, 0, (size_t)n, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->opt_zero_frozen = zero_frozen_grad;
+    ctx->adam = AdamScalars{beta1, beta2, 1.0 - beta1, 1.0 - beta2, 1.0, 1.0, alpha, eps, lo, hi,
+                            frozen_value};
+    return WO_OK;
+}
+
+int wo_opt_step(wo_ctx* ctx, int t, double* grad_norm) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(ctx->opt && ctx->material_set, "wo_opt_init / material missing");
+    REQUIRE(t >= 1, "Adam step count starts at 1");
+    AdamScalars s = ctx->adam;
+    s.bc1 = 1.0 - std::pow(s.beta1, (double)t);   // Python float ** int, then 1 - x
+    s.bc2 = 1.0 - std::pow(s.beta2, (double)t);
+    const int64_t n = ctx->cells();
+    char* g = ctx->base0(ctx->gamma);
+    if (ctx->itemsize == 4)
+        adam_clip_kernel<float><<<592, 256, 0, ctx->stream>>>(
+            reinterpret_cast<const float*>(ctx->acc), ctx->opt, ctx->opt + n, ctx->opt + 2 * n,
+            ctx->opt_frozen, ctx->opt_zero_frozen, s, n, reinterpret_cast<float*>(g),
+            ctx->opt_partial);
+    else
+        adam_clip_kernel<double><<<592, 256, 0, ctx->stream>>>(
+            reinterpret_cast<const double*>(ctx->acc), ctx->opt, ctx->opt + n, ctx->opt + 2 * n,
+            ctx->opt_frozen, ctx->opt_zero_frozen, s, n, reinterpret_cast<double*>(g),
+            ctx->opt_partial);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    double part[592];
+    CK(cudaMemcpyAsync(part, ctx->opt_partial, sizeof(part), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    double sq = 0.0;
+    for (double x : part) sq += x;
+    if (grad_norm) *grad_norm = std::sqrt(sq);
+    ctx->mat4_valid = false;           // gamma changed on the device
+    return verify_fast_div(ctx);
+}
+
+int wo_opt_get(wo_ctx* ctx, double* params) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(ctx->opt, "wo_opt_init missing");
+    return download_field(ctx, params, reinterpret_cast<const char*>(ctx->opt),
+                          (size_t)ctx->cells() * 8);
 }
 
 int wo_set_option(wo_ctx* ctx, int option, int value) {

@@ -219,6 +219,26 @@ class DeviceGrid:
                  "wo_get_field")
         return out if first_axis_fastest else out.reshape(self.grid.shape)
 
+    # ------------------------------------------- device optimiser (8f-3)
+    def opt_init(self, params, frozen=None, zero_frozen_grad=False, lo=0.0, hi=1.0,
+                 frozen_value=0.0, alpha=1e-3, beta1=0.9, beta2=0.999, eps=1e-8):
+        p = np.ascontiguousarray(params, dtype=np.float64)
+        fz = None if frozen is None else np.ascontiguousarray(frozen, dtype=np.uint8)
+        self._ck(self.L.wo_opt_init(self.h, N.ptr(p), N.ptr(fz), int(bool(zero_frozen_grad)),
+                                    float(lo), float(hi), float(frozen_value), float(alpha),
+                                    float(beta1), float(beta2), float(eps)), "wo_opt_init")
+
+    def opt_step(self, t):
+        """Adam step t from the accumulator's gradient; returns its L2 norm."""
+        norm = ctypes.c_double(0.0)
+        self._ck(self.L.wo_opt_step(self.h, int(t), ctypes.byref(norm)), "wo_opt_step")
+        return norm.value
+
+    def opt_get(self):
+        out = np.empty(self.grid.shape, np.float64)
+        self._ck(self.L.wo_opt_get(self.h, N.ptr(out)), "wo_opt_get")
+        return out
+
     def snapshot(self, op, n_steps=0):
         """Save / restore / free the post-forward device state (wo_snapshot)."""
         code = {"save": N.WO_SNAP_SAVE, "restore": N.WO_SNAP_RESTORE, "free": N.WO_SNAP_FREE}[op]

@@ -103,6 +103,19 @@ int wo_opt_init(wo_ctx* ctx, const double* params, const unsigned char* frozen, 
                 double beta2, double eps);
 int wo_opt_step(wo_ctx* ctx, int t, double* grad_norm);
 int wo_opt_get(wo_ctx* ctx, double* params);
+/* Device-resident TATO design loop (tato.py:238-304): the optimiser's
+ * parameters are gamma_raw; wo_design_setup stores the design mask (NULL =
+ * everywhere) and the filter footprint (as wo_design_filter) and switches
+ * wo_opt_step to the chain-rule gradient.  wo_design_material: g_tilde =
+ * density_filter(gamma_raw), g_bar = heaviside_project(g_tilde) -> material
+ * g_bar.astype(T).  wo_design_gradient: chain_rule(acc, g_tilde) -> the
+ * gradient of the next wo_opt_step.  wo_design_get: 0 g_tilde, 1 g_bar,
+ * 2 gradient (fp64 fields). */
+int wo_design_setup(wo_ctx* ctx, const unsigned char* mask, int n_fp, const int* offsets,
+                    const double* weights);
+int wo_design_material(wo_ctx* ctx, double beta, double eta, double t_be, double denom);
+int wo_design_gradient(wo_ctx* ctx, double beta, double eta, double denom);
+int wo_design_get(wo_ctx* ctx, int which, double* out);
 int wo_fast_div_active(const wo_ctx* ctx);
 /* Kernel-increment scalars (gradients.py:117-129, kernels.py:149-152): the
  * fp64 values cv, cg, 1/(2dt), 1/(2dx); cast to the field dtype here. */

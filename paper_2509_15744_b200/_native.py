@@ -31,7 +31,8 @@ EXPORTS = (
     "wo_timer_elapsed", "wo_synchronize", "wo_accumulator_ptr", "wo_set_option",
     "wo_fast_div_active", "wo_sweep_forward_range", "wo_sweep_backward_range",
     "wo_check_maxima", "wo_halo_planes", "wo_exchange_local", "wo_pair_launches", "wo_snapshot",
-    "wo_get_field", "wo_opt_init", "wo_opt_step", "wo_opt_get",
+    "wo_get_field", "wo_opt_init", "wo_opt_step", "wo_opt_get", "wo_design_setup",
+    "wo_design_material", "wo_design_gradient", "wo_design_get",
 )
 
 
@@ -102,6 +103,10 @@ _SIGS = {
                             c_dbl]),
     "wo_opt_step": (c_int, [c_vp, c_int, ctypes.POINTER(c_dbl)]),
     "wo_opt_get": (c_int, [c_vp, c_vp]),
+    "wo_design_setup": (c_int, [c_vp, c_vp, c_int, c_vp, c_vp]),
+    "wo_design_material": (c_int, [c_vp, c_dbl, c_dbl, c_dbl, c_dbl]),
+    "wo_design_gradient": (c_int, [c_vp, c_dbl, c_dbl, c_dbl]),
+    "wo_design_get": (c_int, [c_vp, c_int, c_vp]),
 }
 WO_OPT_FAST_DIV = 1
 WO_OPT_PAIR_KERNEL = 2

@@ -149,10 +149,11 @@ struct AdamScalars {
 //   g = double(acc) (0 on frozen cells when zero_frozen)
 //   m = b1*m + (1-b1)*g ;  v = b2*v + ((1-b2)*g)*g
 //   p = p - (alpha*(m/bc1)) / (sqrt(v/bc2) + eps) ; clip ; frozen -> value
-// The new parameters are also cast to the field dtype (gamma.astype(T)) and
+// The new parameters are also cast to the field dtype (gamma.astype(T); FWI:
+// the parameters ARE the material; TATO passes gamma = nullptr) and
 // the block partial sums of g*g (fixed tree) give the logged gradient norm.
-template <typename T>
-__global__ void adam_clip_kernel(const T* __restrict__ acc, double* __restrict__ p,
+template <typename G, typename T>
+__global__ void adam_clip_kernel(const G* __restrict__ acc, double* __restrict__ p,
                                  double* __restrict__ m, double* __restrict__ v,
                                  const unsigned char* __restrict__ frozen, int zero_frozen,
                                  AdamScalars s, long long n, T* __restrict__ gamma,
@@ -174,7 +175,7 @@ __global__ void adam_clip_kernel(const T* __restrict__ acc, double* __restrict__
         double x = np_clip(__dsub_rn(p[c], step), s.lo, s.hi);
         if (fz) x = s.frozen_value;
         p[c] = x;
-        gamma[c] = (T)x;
+        if (gamma) gamma[c] = (T)x;
     }
     red[threadIdx.x] = sq;
     __syncthreads();
@@ -183,6 +184,13 @@ __global__ void adam_clip_kernel(const T* __restrict__ acc, double* __restrict__
         __syncthreads();
     }
     if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+template <typename T>
+__global__ void widen_kernel(const T* __restrict__ src, double* __restrict__ dst, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        dst[i] = (double)src[i];
 }
 
 }  // namespace wb

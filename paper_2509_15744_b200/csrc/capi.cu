@@ -69,6 +69,12 @@ struct wo_ctx {
     double* opt_partial = nullptr;     // 592 block sums
     AdamScalars adam{};
     int opt_zero_frozen = 0;
+    double* dsn = nullptr;             // design loop: g_tilde | g_bar | grad | 3 temporaries (fp64)
+    unsigned char* dmask = nullptr;    // design mask (nullptr: everywhere)
+    int* dfp_off = nullptr;            // filter footprint [n][3]
+    double* dfp_w = nullptr;
+    int dfp_n = 0;
+    int design_active = 0;             // wo_opt_step takes the chain-rule gradient
     size_t scratch_bytes = 0;
     char* snap = nullptr;              // wo_snapshot: window levels | acc | store
     size_t snap_bytes = 0;
@@ -1218,6 +1224,7 @@ void wo_destroy(wo_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     void* bufs[] = {ctx->gamma, ctx->u[0], ctx->u[1], ctx->u[2], ctx->u[3], ctx->mat4, ctx->stage,
                     ctx->snap, ctx->scratch, ctx->opt, ctx->opt_frozen, ctx->opt_partial,
+                    ctx->dsn, ctx->dmask, ctx->dfp_off, ctx->dfp_w,
                     ctx->flag, ctx->acc,
                     ctx->mask, ctx->prefix,
                     ctx->store, ctx->measured, ctx->partial, ctx->cost, ctx->maxslots,
@@ -1278,6 +1285,7 @@ int wo_opt_init(wo_ctx* ctx, const double* params, const unsigned char* frozen, 
         CK(cudaMemsetAsync(ctx->opt_frozen, 0, (size_t)n, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->opt_zero_frozen = zero_frozen_grad;
+    ctx->design_active = 0;
     ctx->adam = AdamScalars{beta1, beta2, 1.0 - beta1, 1.0 - beta2, 1.0, 1.0, alpha, eps, lo, hi,
                             frozen_value};
     return WO_OK;
@@ -1293,16 +1301,20 @@ int wo_opt_step(wo_ctx* ctx, int t, double* grad_norm) {
     s.bc2 = 1.0 - std::pow(s.beta2, (double)t);
     const int64_t n = ctx->cells();
     char* g = ctx->base0(ctx->gamma);
-    if (ctx->itemsize == 4)
-        adam_clip_kernel<float><<<592, 256, 0, ctx->stream>>>(
-            reinterpret_cast<const float*>(ctx->acc), ctx->opt, ctx->opt + n, ctx->opt + 2 * n,
-            ctx->opt_frozen, ctx->opt_zero_frozen, s, n, reinterpret_cast<float*>(g),
-            ctx->opt_partial);
+    double* m = ctx->opt + n;
+    double* v = ctx->opt + 2 * n;
+    if (ctx->design_active)   // TATO: chain-rule gradient, the material comes from g_bar
+        adam_clip_kernel<double, double><<<592, 256, 0, ctx->stream>>>(
+            ctx->dsn + 2 * n, ctx->opt, m, v, ctx->opt_frozen, ctx->opt_zero_frozen, s, n,
+            (double*)nullptr, ctx->opt_partial);
+    else if (ctx->itemsize == 4)
+        adam_clip_kernel<float, float><<<592, 256, 0, ctx->stream>>>(
+            reinterpret_cast<const float*>(ctx->acc), ctx->opt, m, v, ctx->opt_frozen,
+            ctx->opt_zero_frozen, s, n, reinterpret_cast<float*>(g), ctx->opt_partial);
     else
-        adam_clip_kernel<double><<<592, 256, 0, ctx->stream>>>(
-            reinterpret_cast<const double*>(ctx->acc), ctx->opt, ctx->opt + n, ctx->opt + 2 * n,
-            ctx->opt_frozen, ctx->opt_zero_frozen, s, n, reinterpret_cast<double*>(g),
-            ctx->opt_partial);
+        adam_clip_kernel<double, double><<<592, 256, 0, ctx->stream>>>(
+            reinterpret_cast<const double*>(ctx->acc), ctx->opt, m, v, ctx->opt_frozen,
+            ctx->opt_zero_frozen, s, n, reinterpret_cast<double*>(g), ctx->opt_partial);
     ctx->launches++;
     CK(cudaGetLastError());
     double part[592];
@@ -1311,8 +1323,104 @@ int wo_opt_step(wo_ctx* ctx, int t, double* grad_norm) {
     double sq = 0.0;
     for (double x : part) sq += x;
     if (grad_norm) *grad_norm = std::sqrt(sq);
-    ctx->mat4_valid = false;           // gamma changed on the device
+    if (ctx->design_active) return WO_OK;   // the material changes in wo_design_material
+    ctx->mat4_valid = false;                // gamma changed on the device
     return verify_fast_div(ctx);
+}
+
+int wo_design_setup(wo_ctx* ctx, const unsigned char* mask, int n_fp, const int* offsets,
+                    const double* weights) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(!ctx->has_lo && !ctx->has_hi, "the design loop runs on single-domain contexts");
+    REQUIRE(n_fp >= 1, "empty filter footprint");
+    const int64_t n = ctx->cells();
+    if (!ctx->dsn && (rc = dev_alloc(ctx, (void**)&ctx->dsn, (size_t)n * 48))) return rc;
+    if (mask) {
+        if (!ctx->dmask && (rc = dev_alloc(ctx, (void**)&ctx->dmask, (size_t)n))) return rc;
+        CK(cudaMemcpyAsync(ctx->dmask, mask, (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
+    } else if (ctx->dmask) {
+        cudaFree(ctx->dmask);
+        ctx->dev_bytes -= n;
+        ctx->dmask = nullptr;
+    }
+    std::vector<int> o3((size_t)n_fp * 3, 0);   // footprint offsets in kernel space
+    for (int f = 0; f < n_fp; ++f)
+        for (int a = 0; a < ctx->ndim; ++a)
+            o3[(size_t)f * 3 + (3 - ctx->ndim) + a] = offsets[(size_t)f * ctx->ndim + a];
+    if (ctx->dfp_off) { cudaFree(ctx->dfp_off); ctx->dfp_off = nullptr; }
+    if (ctx->dfp_w) { cudaFree(ctx->dfp_w); ctx->dfp_w = nullptr; }
+    ctx->dev_bytes -= (int64_t)ctx->dfp_n * (12 + 8);
+    if ((rc = dev_alloc(ctx, (void**)&ctx->dfp_off, o3.size() * sizeof(int)))) return rc;
+    if ((rc = dev_alloc(ctx, (void**)&ctx->dfp_w, (size_t)n_fp * 8))) return rc;
+    CK(cudaMemcpyAsync(ctx->dfp_off, o3.data(), o3.size() * sizeof(int), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(cudaMemcpyAsync(ctx->dfp_w, weights, (size_t)n_fp * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->dfp_n = n_fp;
+    ctx->design_active = 1;
+    return WO_OK;
+}
+
+int wo_design_material(wo_ctx* ctx, double beta, double eta, double t_be, double denom) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(ctx->opt && ctx->dsn && ctx->material_set, "wo_opt_init / wo_design_setup missing");
+    const int64_t n = ctx->cells();
+    double *gt = ctx->dsn, *gb = ctx->dsn + n, *t1 = ctx->dsn + 3 * n, *t2 = ctx->dsn + 4 * n;
+    const Footprint fp{ctx->dfp_n, ctx->dfp_off, ctx->dfp_w};
+    // g_tilde = density_filter(gamma_raw), g_bar = heaviside_project(g_tilde)
+    masked_correlate_kernel<<<592, 256, 0, ctx->stream>>>(ctx->kn0, ctx->kn1, ctx->kn2, ctx->opt,
+                                                          ctx->dmask, 1, fp, t1, t2);
+    filter_finish_kernel<<<592, 256, 0, ctx->stream>>>(n, ctx->opt, ctx->dmask, t1, t2, gt);
+    heaviside_kernel<<<592, 256, 0, ctx->stream>>>(n, gt, beta, eta, t_be, denom, ctx->dmask, gb);
+    // the material is g_bar.astype(T) (TatoProblem.material, solver.py:100)
+    char* g = ctx->base0(ctx->gamma);
+    if (ctx->itemsize == 4)
+        cast_kernel<float><<<296, 256, 0, ctx->stream>>>(gb, reinterpret_cast<float*>(g), n);
+    else
+        cast_kernel<double><<<296, 256, 0, ctx->stream>>>(gb, reinterpret_cast<double*>(g), n);
+    ctx->launches += 4;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->mat4_valid = false;
+    return verify_fast_div(ctx);
+}
+
+int wo_design_gradient(wo_ctx* ctx, double beta, double eta, double denom) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(ctx->dsn, "wo_design_setup missing");
+    const int64_t n = ctx->cells();
+    double *gt = ctx->dsn, *gr = ctx->dsn + 2 * n;
+    double *t1 = ctx->dsn + 3 * n, *t2 = ctx->dsn + 4 * n, *t3 = ctx->dsn + 5 * n;
+    const Footprint fp{ctx->dfp_n, ctx->dfp_off, ctx->dfp_w};
+    // chain_rule(double(dC/dg_bar), g_tilde, ...) (tato.py:124-140)
+    if (ctx->itemsize == 4)
+        widen_kernel<float><<<592, 256, 0, ctx->stream>>>(reinterpret_cast<const float*>(ctx->acc),
+                                                         gr, n);
+    else
+        widen_kernel<double><<<592, 256, 0, ctx->stream>>>(
+            reinterpret_cast<const double*>(ctx->acc), gr, n);
+    chain_inner_kernel<<<592, 256, 0, ctx->stream>>>(n, gr, gt, beta, eta, denom, ctx->dmask, t1);
+    masked_correlate_kernel<<<592, 256, 0, ctx->stream>>>(ctx->kn0, ctx->kn1, ctx->kn2, t1,
+                                                          ctx->dmask, 1, fp, nullptr, t2);
+    chain_ratio_kernel<<<592, 256, 0, ctx->stream>>>(n, t1, t2, ctx->dmask, t3);
+    masked_correlate_kernel<<<592, 256, 0, ctx->stream>>>(ctx->kn0, ctx->kn1, ctx->kn2, t3,
+                                                          nullptr, 0, fp, gr, nullptr);
+    mask_zero_kernel<<<592, 256, 0, ctx->stream>>>(n, ctx->dmask, gr);
+    ctx->launches += 6;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    return WO_OK;
+}
+
+int wo_design_get(wo_ctx* ctx, int which, double* out) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(ctx->dsn && which >= 0 && which <= 2, "wo_design_setup missing / bad field");
+    return download_field(ctx, out, reinterpret_cast<const char*>(ctx->dsn + which * ctx->cells()),
+                          (size_t)ctx->cells() * 8);
 }
 
 int wo_opt_get(wo_ctx* ctx, double* params) {

@@ -239,6 +239,27 @@ class DeviceGrid:
         self._ck(self.L.wo_opt_get(self.h, N.ptr(out)), "wo_opt_get")
         return out
 
+    def design_setup(self, mask, offsets, weights):
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+        offs = np.ascontiguousarray(offsets, dtype=np.int32)
+        ws = np.ascontiguousarray(weights, dtype=np.float64)
+        self._ck(self.L.wo_design_setup(self.h, N.ptr(m), len(ws), N.ptr(offs), N.ptr(ws)),
+                 "wo_design_setup")
+
+    def design_material(self, beta, eta, t_be, denom):
+        self._ck(self.L.wo_design_material(self.h, float(beta), float(eta), float(t_be),
+                                           float(denom)), "wo_design_material")
+
+    def design_gradient(self, beta, eta, denom):
+        self._ck(self.L.wo_design_gradient(self.h, float(beta), float(eta), float(denom)),
+                 "wo_design_gradient")
+
+    def design_get(self, which):
+        out = np.empty(self.grid.shape, np.float64)
+        code = {"g_tilde": 0, "g_bar": 1, "grad": 2}[which]
+        self._ck(self.L.wo_design_get(self.h, code, N.ptr(out)), "wo_design_get")
+        return out
+
     def snapshot(self, op, n_steps=0):
         """Save / restore / free the post-forward device state (wo_snapshot)."""
         code = {"save": N.WO_SNAP_SAVE, "restore": N.WO_SNAP_RESTORE, "free": N.WO_SNAP_FREE}[op]

@@ -54,3 +54,25 @@ def test_invert_device_loop_with_mask(W, golden):
     host = W.invert(problem, device_loop=False, **kw)
     assert bits_equal(dev.gamma, host.gamma)
     assert np.all(dev.gamma[mask] == problem.material.eps)
+
+
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_optimize_design_device_loop_matches_host_loop(W, golden, prec):
+    from helpers import product_tato_problem
+
+    g = golden("tato2d")
+    c = cases.tato2d_case()
+    problem = product_tato_problem(W, c)
+    kw = dict(method="superposed", k=float(g["cal_k"]), iterations=4, precision=prec,
+              snapshot_every=2)
+    dev = W.optimize_design(problem, device_loop=True, **kw)
+    host = W.optimize_design(problem, device_loop=False, **kw)
+    assert bits_equal(dev.gamma_raw, host.gamma_raw)
+    assert bits_equal(dev.design, host.design)
+    assert len(dev.design_history) == len(host.design_history)
+    for a, b in zip(dev.design_history, host.design_history):
+        assert bits_equal(a, b)
+    for a, b in zip(dev.log, host.log):
+        assert a["cost"] == b["cost"] and a["beta"] == b["beta"]
+        if np.isfinite(b["grad_norm"]):
+            assert abs(a["grad_norm"] - b["grad_norm"]) <= 1e-12 * abs(b["grad_norm"])

@@ -45,6 +45,9 @@ namespace wb {
 #ifndef WB_T2_PREFETCH
 #define WB_T2_PREFETCH 2
 #endif
+#ifndef WB_T2_STREAM_STORES
+#define WB_T2_STREAM_STORES 0
+#endif
 constexpr int T2_THREADS = 128;
 constexpr int T2_NS = WB_T2_STAGES;  // TMA ring stages
 constexpr int T2_PF = WB_T2_PREFETCH;   // L2 prefetch distance beyond the ring (planes)
@@ -254,6 +257,16 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
 
     auto ldv = [](const T* p) { return *reinterpret_cast<const V*>(p); };
     auto stv = [](T* p, V v) { *reinterpret_cast<V*>(p) = v; };
+    // global results (u^{n+1}, u^{n+2}, acc) are next read a whole pass later:
+    // optionally stream them past L2 (evict-first) so the halo rows shared by
+    // neighbouring tiles stay resident (WB_T2_STREAM_STORES)
+    auto stg = [](T* p, V v) {
+#if WB_T2_STREAM_STORES
+        __stcs(reinterpret_cast<V*>(p), v);
+#else
+        *reinterpret_cast<V*>(p) = v;
+#endif
+    };
     auto ring_nb = [&](int t, int& l, int& r, int& u, int& d) {
         const int o = oR[t], f = rnb[t];
         l = o - (f & 1); r = o + ((f >> 1) & 1); u = o - W * ((f >> 2) & 1); d = o + W * ((f >> 3) & 1);
@@ -386,13 +399,13 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
             fa.y = kinc(acc1_a.y, o2a.y, un1_a.y, xp_a.y, x_m1a.y, x_0b.y, xu.y, xRa, x_0a.x);
             fb.x = kinc(acc1_b.x, o2b.x, un1_b.x, xp_b.x, x_m1b.x, xd.x, x_0a.x, x_0b.y, xLb);
             fb.y = kinc(acc1_b.y, o2b.y, un1_b.y, xp_b.y, x_m1b.y, xd.y, x_0a.y, xRb, x_0b.x);
-            stv(a.acc + oc, fa);
-            stv(a.acc + oc + n2, fb);
+            stg(a.acc + oc, fa);
+            stg(a.acc + oc + n2, fb);
         }
-        stv(a.out1 + oc, x_0a);
-        stv(a.out1 + oc + n2, x_0b);
-        stv(a.out2 + oc, o2a);
-        stv(a.out2 + oc + n2, o2b);
+        stg(a.out1 + oc, x_0a);
+        stg(a.out1 + oc + n2, x_0b);
+        stg(a.out2 + oc, o2a);
+        stg(a.out2 + oc + n2, o2b);
         if (a.check2) {
             Bits m1 = Tr::abs_bits(o2a.x), m2 = Tr::abs_bits(o2a.y);
             Bits m3 = Tr::abs_bits(o2b.x), m4 = Tr::abs_bits(o2b.y);

@@ -178,6 +178,9 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     const int i1 = min(i0 + a.chunk, n0);
     const int pbeg = max(i0 - 1, 0);           // step-n planes of this chunk
     const int pfin = min(i1, n0 - 1);
+    // planes streamed through the ring: pbeg .. pfin, plus pfin+1 (u^n of the
+    // chunk end's upper neighbour) so no chunk stalls on a global load
+    const int plast = min(pfin + 1, n0 - 1);
 
     // ---- per-thread offsets in the R2 frame (rows j0-2.., cols k0-HO..) ----
     // tile rows a, b; clamped (mirrored) outer neighbours at the grid edge.
@@ -251,8 +254,8 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     }
     __syncthreads();
     if (tid == T2_PRODUCER) {
-        for (int s = 0; s < T2_NS && pbeg + s <= pfin; ++s) issue(pbeg + s, s);
-        for (int d = 0; d < T2_PF && pbeg + T2_NS + d <= pfin; ++d) prefetch(pbeg + T2_NS + d);
+        for (int s = 0; s < T2_NS && pbeg + s <= plast; ++s) issue(pbeg + s, s);
+        for (int d = 0; d < T2_PF && pbeg + T2_NS + d <= plast; ++d) prefetch(pbeg + T2_NS + d);
     }
 
     auto ldv = [](const T* p) { return *reinterpret_cast<const V*>(p); };
@@ -434,19 +437,12 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         // ---- a: u^n of plane p+1 ----
         V unp_a = un0_a, unp_b = un0_b;
         T runp[2] = {run0[0], run0[1]};
-        if (p + 1 <= pfin) {
+        if (p + 1 <= plast) {            // else: plane n0 mirrors plane n0-1
             mbar_wait(&bar[sn], gpar ^ pn);
             const T* NU = &st[sn].U[0][0];
             unp_a = ldv(NU + oA); unp_b = ldv(NU + oB);
 #pragma unroll
             for (int t = 0; t < 2; ++t) runp[t] = NU[oR[t]];
-        } else if (p + 1 <= n0 - 1) {   // chunk end inside the domain: plane p+1 from HBM
-            const int gp = (p + 1) * plane;
-            unp_a = __ldg(reinterpret_cast<const V*>(a.u_cur + gp + cofs));
-            unp_b = __ldg(reinterpret_cast<const V*>(a.u_cur + gp + cofs + n2));
-#pragma unroll
-            for (int t = 0; t < 2; ++t)
-                if (rg_ok[t]) runp[t] = __ldg(a.u_cur + gp + ring_gofs(t));
         }
 
         // ---- d: step n at plane p (tile + ring) -> X[b] ----
@@ -511,9 +507,9 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
             Xc[o] = v;
         }
         __syncthreads();
-        if (tid == T2_PRODUCER && p + T2_NS <= pfin) {
+        if (tid == T2_PRODUCER && p + T2_NS <= plast) {
             issue(p + T2_NS, q);
-            if (p + T2_NS + T2_PF <= pfin) prefetch(p + T2_NS + T2_PF);
+            if (p + T2_NS + T2_PF <= plast) prefetch(p + T2_NS + T2_PF);
         }
 
         // ---- c: step n+1 at plane p-1 (tile) ----

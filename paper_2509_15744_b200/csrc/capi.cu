@@ -597,13 +597,14 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     ctx->t2maps.cur = ctx->cur;
     const int tbx = ctx->t2_geo == GEO_TALL ? GeoTall::TBX : GeoWide::TBX;
     const int tby = ctx->t2_geo == GEO_TALL ? GeoTall::TBY : GeoWide::TBY;
-    // persistent CTAs over (tile, chunk) items: at most the resident CTAs
-    a.nbx = ctx->kn2 / tbx;
-    a.nby = ctx->kn1 / tby;
-    a.nbz = (ctx->kn0 + a.chunk - 1) / a.chunk;
-    const int items = a.nbx * a.nby * a.nbz;
-    const int resident = ctx->num_sms * (ctx->itemsize == 4 ? 3 : 1);
-    dim3 grid((unsigned)std::min(items, resident), 1, 1);
+    static const int zfast = [] {
+        const char* e = getenv("WB_T2_ZFAST");
+        return e ? atoi(e) : 0;
+    }();
+    a.zfast = zfast;
+    const unsigned nzb = (unsigned)((ctx->kn0 + a.chunk - 1) / a.chunk);
+    dim3 grid = zfast ? dim3(nzb, ctx->kn2 / tbx, ctx->kn1 / tby)
+                      : dim3(ctx->kn2 / tbx, ctx->kn1 / tby, nzb);
     if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
     launch_step2_engine<T>(StepSel{ctx->flavor, true, sp.acc, false, sup}, ctx->t2_geo, grid,
                            ctx->stream, a, ctx->t2maps);

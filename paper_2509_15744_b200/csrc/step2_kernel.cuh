@@ -79,8 +79,7 @@ template <typename T> struct Step2Args {
     T* out1;           // u^{n+1}
     T* out2;           // u^{n+2}
     T* acc;
-    int n0, n1, n2, chunk;
-    int nbx, nby, nbz;   // work items: tiles along axis 2, tiles along axis 1, chunks
+    int n0, n1, n2, chunk, zfast;
     MatScalars<T> mat;
     T cv, cg, inv2dt, inv2dx, sdt;
     int n_src;
@@ -168,98 +167,20 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
 
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = ty * G::TX + tx;
+    // block order: tiles fastest (default) or chunks fastest (a.zfast)
+    const int bx = a.zfast ? blockIdx.y : blockIdx.x, by = a.zfast ? blockIdx.z : blockIdx.y;
+    const int bz = a.zfast ? blockIdx.x : blockIdx.z;
+    const int k0 = bx * TBX, j0 = by * TBY;
+    const int kA = k0 + 2 * tx, ja = j0 + 2 * ty;
     const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
     const int plane = n1 * n2;
-
-    // Persistent CTAs.  Work item w = one tile (k0, j0) x one chunk [i0, i1)
-    // of axis 0, numbered tiles fastest (the order a one-block-per-item grid
-    // would run in, which keeps neighbouring tiles at the same planes at the
-    // same time so they share halo rows through L2).  CTA c runs items c,
-    // c + gridDim.x, ...; its TMA loads form ONE sequence across its items, so
-    // the first planes of the next item stream in while the current one
-    // finishes (no pipeline restart per item).  Per item the sequence is
-    // plane pbeg-1 (if any; u^n and the +i face below the first step-n
-    // plane), pbeg .. pfin (step-n planes) and pfin+1 (u^n above the last).
-    const int n_items = a.nbx * a.nby * a.nbz;
-    auto item_of = [&](int w, int& k0_, int& j0_, int& i0_, int& i1_) {
-        const int bx = w % a.nbx, by = (w / a.nbx) % a.nby, bz = w / (a.nbx * a.nby);
-        k0_ = bx * TBX;
-        j0_ = by * TBY;
-        i0_ = bz * a.chunk;
-        i1_ = min(i0_ + a.chunk, n0);
-    };
-
-    constexpr unsigned STAGE_BYTES =
-        (unsigned)(sizeof(T) * ((2 * R2_H + 4 * R1_H) * W + (ACC ? TBY * TBX : 0)));
-    const CUtensorMap* mU = pick_map(maps.u_r2, maps.cur);
-    const CUtensorMap* mP = pick_map(maps.u_r1, maps.prev);
-    // L2 prefetch of a later plane's boxes (no shared memory; hides DRAM
-    // latency beyond the T2_NS-stage ring)
-    auto prefetch = [&](int k0, int j0, int p) {
-        auto pf = [&](const CUtensorMap* m, int c0, int c1) {
-            asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
-                         ::"l"(reinterpret_cast<unsigned long long>(m)), "r"(c0), "r"(c1), "r"(p)
-                         : "memory");
-        };
-        pf(mU, k0 - HO, j0 - 2);
-        pf(&maps.fj_r2, k0 - HO, j0 - 2);
-        pf(mP, k0 - HO, j0 - 1);
-        pf(&maps.c_r1, k0 - HO, j0 - 1);
-        pf(&maps.fk_r1, k0 - HO, j0 - 1);
-        pf(&maps.fi_r1, k0 - HO, j0 - 1);
-        if (ACC) pf(&maps.a_ctr, k0, j0);
-    };
-    auto issue = [&](int k0, int j0, int p, int s) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar[s], STAGE_BYTES);
-        tma_load_3d(&st[s].U[0][0], mU, k0 - HO, j0 - 2, p, &bar[s]);
-        tma_load_3d(&st[s].FJ[0][0], &maps.fj_r2, k0 - HO, j0 - 2, p, &bar[s]);
-        tma_load_3d(&st[s].P[0][0], mP, k0 - HO, j0 - 1, p, &bar[s]);
-        tma_load_3d(&st[s].C[0][0], &maps.c_r1, k0 - HO, j0 - 1, p, &bar[s]);
-        tma_load_3d(&st[s].FK[0][0], &maps.fk_r1, k0 - HO, j0 - 1, p, &bar[s]);
-        tma_load_3d(&st[s].FI[0][0], &maps.fi_r1, k0 - HO, j0 - 1, p, &bar[s]);
-        if (ACC) tma_load_3d(&st[s].A[0][0], &maps.a_ctr, k0, j0, p, &bar[s]);
-    };
-    if (tid == 0) {
-        for (int s = 0; s < T2_NS; ++s) mbar_init(&bar[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    // producer cursor (thread T2_PRODUCER): load ic goes to stage ic % T2_NS
-    int pw = (int)blockIdx.x - (int)gridDim.x, pnext = 1, plst = 0, pk0 = 0, pj0 = 0;
-    unsigned ic = 0;
-    auto produce = [&](unsigned upto) {
-        while (ic < upto) {
-            if (pnext > plst) {   // next item of this CTA
-                pw += gridDim.x;
-                if (pw >= n_items) return;
-                int i0_, i1_;
-                item_of(pw, pk0, pj0, i0_, i1_);
-                const int pb = max(i0_ - 1, 0), pf = min(i1_, n0 - 1);
-                pnext = pb > 0 ? pb - 1 : pb;
-                plst = min(pf + 1, n0 - 1);
-            }
-            issue(pk0, pj0, pnext, (int)(ic % T2_NS));
-            if (pnext + T2_PF <= plst) prefetch(pk0, pj0, pnext + T2_PF);
-            ++pnext;
-            ++ic;
-        }
-    };
-    if (tid == T2_PRODUCER) produce(T2_NS);
-    // consumer: load L is waited on stage L % T2_NS with parity (L / T2_NS) & 1
-    auto wait_load = [&](unsigned L) { mbar_wait(&bar[L % T2_NS], (L / T2_NS) & 1u); };
-    unsigned cc = 0;   // loads consumed so far (all threads agree)
-    Bits lmax1 = 0, lmax2 = 0;
-
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
-    int k0, j0, i0, i1;
-    item_of(w, k0, j0, i0, i1);
-    const int kA = k0 + 2 * tx, ja = j0 + 2 * ty;
+    const int i0 = bz * a.chunk;
+    const int i1 = min(i0 + a.chunk, n0);
     const int pbeg = max(i0 - 1, 0);           // step-n planes of this chunk
     const int pfin = min(i1, n0 - 1);
-    const int plast = min(pfin + 1, n0 - 1);   // last plane of the item's loads
-    const int first = pbeg > 0 ? pbeg - 1 : pbeg;
-    const unsigned L0 = cc;                    // load index of plane `first`
+    // planes streamed through the ring: pbeg .. pfin, plus pfin+1 (u^n of the
+    // chunk end's upper neighbour) so no chunk stalls on a global load
+    const int plast = min(pfin + 1, n0 - 1);
 
     // ---- per-thread offsets in the R2 frame (rows j0-2.., cols k0-HO..) ----
     // tile rows a, b; clamped (mirrored) outer neighbours at the grid edge.
@@ -295,6 +216,47 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         if (a.src_i[s] >= pbeg && a.src_i[s] <= pfin && a.src_j[s] >= j0 - 1 &&
             a.src_j[s] <= j0 + TBY && a.src_k[s] >= k0 - 1 && a.src_k[s] <= k0 + TBX)
             my_src |= 1u << s;
+
+    constexpr unsigned STAGE_BYTES =
+        (unsigned)(sizeof(T) * ((2 * R2_H + 4 * R1_H) * W + (ACC ? TBY * TBX : 0)));
+    const CUtensorMap* mU = pick_map(maps.u_r2, maps.cur);
+    const CUtensorMap* mP = pick_map(maps.u_r1, maps.prev);
+    // L2 prefetch of a later plane's boxes (no shared memory; hides DRAM
+    // latency beyond the T2_NS-stage ring)
+    auto prefetch = [&](int p) {
+        auto pf = [&](const CUtensorMap* m, int c0, int c1) {
+            asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
+                         ::"l"(reinterpret_cast<unsigned long long>(m)), "r"(c0), "r"(c1), "r"(p)
+                         : "memory");
+        };
+        pf(mU, k0 - HO, j0 - 2);
+        pf(&maps.fj_r2, k0 - HO, j0 - 2);
+        pf(mP, k0 - HO, j0 - 1);
+        pf(&maps.c_r1, k0 - HO, j0 - 1);
+        pf(&maps.fk_r1, k0 - HO, j0 - 1);
+        pf(&maps.fi_r1, k0 - HO, j0 - 1);
+        if (ACC) pf(&maps.a_ctr, k0, j0);
+    };
+    auto issue = [&](int p, int s) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar[s], STAGE_BYTES);
+        tma_load_3d(&st[s].U[0][0], mU, k0 - HO, j0 - 2, p, &bar[s]);
+        tma_load_3d(&st[s].FJ[0][0], &maps.fj_r2, k0 - HO, j0 - 2, p, &bar[s]);
+        tma_load_3d(&st[s].P[0][0], mP, k0 - HO, j0 - 1, p, &bar[s]);
+        tma_load_3d(&st[s].C[0][0], &maps.c_r1, k0 - HO, j0 - 1, p, &bar[s]);
+        tma_load_3d(&st[s].FK[0][0], &maps.fk_r1, k0 - HO, j0 - 1, p, &bar[s]);
+        tma_load_3d(&st[s].FI[0][0], &maps.fi_r1, k0 - HO, j0 - 1, p, &bar[s]);
+        if (ACC) tma_load_3d(&st[s].A[0][0], &maps.a_ctr, k0, j0, p, &bar[s]);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < T2_NS; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == T2_PRODUCER) {
+        for (int s = 0; s < T2_NS && pbeg + s <= plast; ++s) issue(pbeg + s, s);
+        for (int d = 0; d < T2_PF && pbeg + T2_NS + d <= plast; ++d) prefetch(pbeg + T2_NS + d);
+    }
 
     auto ldv = [](const T* p) { return *reinterpret_cast<const V*>(p); };
     auto stv = [](T* p, V v) { *reinterpret_cast<V*>(p) = v; };
@@ -386,24 +348,24 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     };
     V unm_a, unm_b, w0_a = {T(0), T(0)}, w0_b = {T(0), T(0)};   // plane pbeg-1 (mirror at 0)
     T rum[2] = {T(0), T(0)}, rw0[2] = {T(0), T(0)};
-    if (has_m0) {                              // plane pbeg-1 from the ring
-        wait_load(L0);
-        const T* MU = &st[L0 % T2_NS].U[0][0];
-        const T* MFI = &st[L0 % T2_NS].FI[0][0] - W;
-        unm_a = ldv(MU + oA); unm_b = ldv(MU + oB);
-        w0_a = ldv(MFI + oA); w0_b = ldv(MFI + oB);
+    if (has_m0) {
+        const int gm = (pbeg - 1) * plane;
+        unm_a = __ldg(reinterpret_cast<const V*>(a.u_cur + gm + cofs));
+        unm_b = __ldg(reinterpret_cast<const V*>(a.u_cur + gm + cofs + n2));
+        w0_a = __ldg(reinterpret_cast<const V*>(a.fi + gm + cofs));
+        w0_b = __ldg(reinterpret_cast<const V*>(a.fi + gm + cofs + n2));
 #pragma unroll
         for (int t = 0; t < 2; ++t)
-            if (rg_ok[t]) { rum[t] = MU[oR[t]]; rw0[t] = MFI[oR[t]]; }
+            if (rg_ok[t]) {
+                rum[t] = __ldg(a.u_cur + gm + ring_gofs(t));
+                rw0[t] = __ldg(a.fi + gm + ring_gofs(t));
+            }
     }
-    const unsigned Lb = L0 + (unsigned)(pbeg - first);
-    wait_load(Lb);
-    cc = Lb + 1;
-    const int q0 = (int)(Lb % T2_NS);
-    V un0_a = ldv(&st[q0].U[0][0] + oA), un0_b = ldv(&st[q0].U[0][0] + oB);
+    mbar_wait(&bar[0], 0u);
+    V un0_a = ldv(&st[0].U[0][0] + oA), un0_b = ldv(&st[0].U[0][0] + oB);
     T run0[2];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) run0[t] = (&st[q0].U[0][0])[oR[t]];
+    for (int t = 0; t < 2; ++t) run0[t] = (&st[0].U[0][0])[oR[t]];
     if (!has_m0) {
         unm_a = un0_a; unm_b = un0_b;
         rum[0] = run0[0]; rum[1] = run0[1];
@@ -417,6 +379,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     V x_m1a = un0_a, x_m1b = un0_b, x_0a = un0_a, x_0b = un0_b;   // u^{n+1}(p-2), (p-1)
     V un1_a = unm_a, un1_b = unm_b;                                // u^n(p-1)
     V acc1_a = {T(0), T(0)}, acc1_b = acc1_a;                      // acc after step n at p-1
+    Bits lmax1 = 0, lmax2 = 0;
 
     // step n+1 at plane q1 for the tile: xp = u^{n+1}(q1+1) (registers)
     auto step2_tile = [&](int q1, const T* Xq, V xp_a, V xp_b) {
@@ -454,13 +417,14 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         }
     };
 
-    // one plane; q = stage of plane p, xq = its X buffer (rolled loop:
-    // unrolled copies of this body overflow the instruction cache).  One
-    // barrier per plane, after step n: it publishes X(p) and frees stage(p),
-    // which the producer refills at once with the CTA's next load; three X
-    // buffers keep X(p) from overwriting X(p-3) before (c) read it.
-    auto body = [&](int q, int xq, int p) {
+    // one plane; q = stage of plane p, gpar = its mbarrier parity, xq = its X
+    // buffer (rolled loop: unrolled copies of this body overflow the
+    // instruction cache).  One barrier per plane, after step n: it publishes
+    // X(p) and frees stage(p), which is refilled at once (T2_NS planes ahead);
+    // three X buffers keep X(p) from overwriting X(p-3) before (c) read it.
+    auto body = [&](int q, int xq, int p, unsigned gpar) {
         const int sn = q + 1 == T2_NS ? 0 : q + 1;
+        const unsigned pn = (q + 1 == T2_NS) ? 1u : 0u;   // parity flip for plane p+1
         T* Xc = Xb + xq * PL;
         const T* Xp = Xb + (xq == 0 ? T2_NX - 1 : xq - 1) * PL;
         const Tma2Stage<T, G>& S = st[q];
@@ -474,8 +438,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         V unp_a = un0_a, unp_b = un0_b;
         T runp[2] = {run0[0], run0[1]};
         if (p + 1 <= plast) {            // else: plane n0 mirrors plane n0-1
-            wait_load(cc);                // the load of plane p+1 (stage sn)
-            ++cc;
+            mbar_wait(&bar[sn], gpar ^ pn);
             const T* NU = &st[sn].U[0][0];
             unp_a = ldv(NU + oA); unp_b = ldv(NU + oB);
 #pragma unroll
@@ -544,10 +507,10 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
             Xc[o] = v;
         }
         __syncthreads();
-        // released: every load up to plane p (plus plane pfin+1 at the end)
-        if (tid == T2_PRODUCER)
-            produce(L0 + (unsigned)(p - first) + 1u + (p == pfin ? (unsigned)(plast - pfin) : 0u) +
-                    T2_NS);
+        if (tid == T2_PRODUCER && p + T2_NS <= plast) {
+            issue(p + T2_NS, q);
+            if (p + T2_NS + T2_PF <= plast) prefetch(p + T2_NS + T2_PF);
+        }
 
         // ---- c: step n+1 at plane p-1 (tile) ----
         if (p - 1 >= i0 && p - 1 < i1) step2_tile(p - 1, Xp, oa, ob);
@@ -574,10 +537,11 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         }
     };
 
+    unsigned gpar = 0;
     int xq = 0;
-    for (int p = pbeg, q = q0; p <= pfin; ++p) {
-        body(q, xq, p);
-        if (++q == T2_NS) q = 0;
+    for (int p = pbeg, q = 0; p <= pfin; ++p) {
+        body(q, xq, p, gpar);
+        if (++q == T2_NS) { q = 0; gpar ^= 1u; }
         if (++xq == T2_NX) xq = 0;
     }
 
@@ -586,8 +550,6 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     // pfin = n0-1 = i1-1 and plane n0 mirrors the plane itself (X(pfin) was
     // published by the last plane's barrier)
     if (pfin == i1 - 1) step2_tile(pfin, Xb + ((pfin - pbeg) % T2_NX) * PL, x_0a, x_0b);
-    __syncthreads();   // X reads done before the next item overwrites the planes
-    }   // items
 
     if (a.check1 || a.check2) {
         for (int o = 16; o > 0; o >>= 1) {

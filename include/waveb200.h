@@ -255,9 +255,14 @@ int wo_design_chain(int ndim, const int64_t* shape, const double* dcdbar, const 
                     double beta, double eta, double denom, const unsigned char* mask, int n_fp,
                     const int* offsets, const double* weights, double* out, int device);
 
-/* Profiling: when on, every fused step launch is bracketed by CUDA events
- * on the context stream; wo_stats returns launches and summed kernel ms. */
+/* Profiling: on = k > 0 brackets every k-th fused step launch with CUDA
+ * events on the context stream (1 = all; sampling keeps the event overhead
+ * out of a timed region); wo_stats returns launches and the summed bracketed
+ * kernel ms; wo_profile_stats splits the bracketed time and count into
+ * single-step launches and two-step passes. */
 int wo_set_profiling(wo_ctx* ctx, int on);
+int wo_profile_stats(const wo_ctx* ctx, double* single_ms, int64_t* single_n, double* pair_ms,
+                     int64_t* pair_n);
 int wo_stats(wo_ctx* ctx, int64_t* launches, int64_t* step_launches, double* step_kernel_ms);
 int wo_reset_stats(wo_ctx* ctx);
 /* Device bytes held by the context (fields + support storage). */

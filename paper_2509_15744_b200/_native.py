@@ -32,7 +32,7 @@ EXPORTS = (
     "wo_fast_div_active", "wo_sweep_forward_range", "wo_sweep_backward_range",
     "wo_check_maxima", "wo_halo_planes", "wo_exchange_local", "wo_pair_launches", "wo_snapshot",
     "wo_get_field", "wo_opt_init", "wo_opt_step", "wo_opt_get", "wo_design_setup",
-    "wo_design_material", "wo_design_gradient", "wo_design_get",
+    "wo_design_material", "wo_design_gradient", "wo_design_get", "wo_profile_stats",
 )
 
 
@@ -107,6 +107,8 @@ _SIGS = {
     "wo_design_material": (c_int, [c_vp, c_dbl, c_dbl, c_dbl, c_dbl]),
     "wo_design_gradient": (c_int, [c_vp, c_dbl, c_dbl, c_dbl]),
     "wo_design_get": (c_int, [c_vp, c_int, c_vp]),
+    "wo_profile_stats": (c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64),
+                                 ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
 }
 WO_OPT_FAST_DIV = 1
 WO_OPT_PAIR_KERNEL = 2

@@ -115,11 +115,17 @@ struct wo_ctx {
     char* u3 = nullptr;                // third adjoint level (reference engine)
     size_t u3_bytes = 0;
 
-    bool prof = false;
+    bool prof = false;                 // any step-launch profiling
+    int prof_every = 0;                // bracket every prof_every-th step launch with events
+    int64_t prof_tick = 0;
+    bool prof_open = false;            // the current launch is bracketed
     cudaEvent_t marks[8] = {};
     std::vector<cudaEvent_t> ev_free, ev_used;
+    std::vector<char> ev_kind;         // per bracketed launch: 1 two-step pass, 0 single step
     int64_t launches = 0, step_launches = 0;
     double step_ms = 0.0;
+    double prof_ms[2] = {0.0, 0.0};    // summed bracketed time: [single, pair]
+    int64_t prof_n[2] = {0, 0};
     int64_t dev_bytes = 0;
     std::string err;
 
@@ -217,15 +223,32 @@ cudaEvent_t take_event(wo_ctx* ctx) {
     return e;
 }
 
+// bracket a step launch with events when it is one of the sampled launches
+void prof_begin(wo_ctx* ctx, int kind) {
+    ctx->prof_open = ctx->prof && (ctx->prof_tick++ % ctx->prof_every) == 0;
+    if (!ctx->prof_open) return;
+    cudaEventRecord(take_event(ctx), ctx->stream);
+    ctx->ev_kind.push_back((char)kind);
+}
+void prof_end(wo_ctx* ctx) {
+    if (ctx->prof_open) cudaEventRecord(take_event(ctx), ctx->stream);
+    ctx->prof_open = false;
+}
+
 // after a stream sync: fold the bracketed step-kernel times into the stats
 void harvest_events(wo_ctx* ctx) {
     for (size_t i = 0; i + 1 < ctx->ev_used.size(); i += 2) {
         float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, ctx->ev_used[i], ctx->ev_used[i + 1]) == cudaSuccess)
+        if (cudaEventElapsedTime(&ms, ctx->ev_used[i], ctx->ev_used[i + 1]) == cudaSuccess) {
+            const int kind = ctx->ev_kind[i / 2] ? 1 : 0;
             ctx->step_ms += ms;
+            ctx->prof_ms[kind] += ms;
+            ctx->prof_n[kind] += 1;
+        }
     }
     for (auto e : ctx->ev_used) ctx->ev_free.push_back(e);
     ctx->ev_used.clear();
+    ctx->ev_kind.clear();
 }
 
 // ---- TMA tensor maps (driver entry point; no libcuda link dependency) ----
@@ -362,12 +385,12 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
         ctx->tmaps.cur = ctx->cur;
         ctx->tmaps.prev = ctx->prv;
     }
-    if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
+    prof_begin(ctx, 0);
     const StepSel sel{ctx->flavor, ctx->fast_div, sp.acc, sp.check, a.sup_mode};
     const int engine = tma ? (ctx->use_tma == 2 ? ENGINE_TMA : ENGINE_TMA4)
                            : (pair ? ENGINE_PAIR : ENGINE_SCALAR);
     launch_step_engine<T>(engine, sel, grid, block, ctx->stream, a, ctx->tmaps);
-    if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
+    prof_end(ctx);
     ctx->launches++;
     ctx->step_launches++;
     CK(cudaGetLastError());
@@ -605,10 +628,10 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     const unsigned nzb = (unsigned)((ctx->kn0 + a.chunk - 1) / a.chunk);
     dim3 grid = zfast ? dim3(nzb, ctx->kn2 / tbx, ctx->kn1 / tby)
                       : dim3(ctx->kn2 / tbx, ctx->kn1 / tby, nzb);
-    if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
+    prof_begin(ctx, 1);
     launch_step2_engine<T>(StepSel{ctx->flavor, true, sp.acc, false, sup}, ctx->t2_geo, grid,
                            ctx->stream, a, ctx->t2maps);
-    if (ctx->prof) cudaEventRecord(take_event(ctx), ctx->stream);
+    prof_end(ctx);
     ctx->launches++;
     ctx->step_launches++;
     ctx->pair_launches++;
@@ -1779,7 +1802,9 @@ int wo_step(wo_ctx* ctx, int64_t n_force, const int64_t* idx, const double* vals
 
 int wo_set_profiling(wo_ctx* ctx, int on) {
     if (!ctx) return WO_ERR_CONFIG;
-    ctx->prof = on != 0;
+    ctx->prof = on > 0;
+    ctx->prof_every = on > 0 ? on : 0;
+    ctx->prof_tick = 0;
     return WO_OK;
 }
 
@@ -1795,12 +1820,24 @@ int wo_reset_stats(wo_ctx* ctx) {
     if (!ctx) return WO_ERR_CONFIG;
     ctx->launches = ctx->step_launches = ctx->pair_launches = 0;
     ctx->step_ms = 0.0;
+    ctx->prof_ms[0] = ctx->prof_ms[1] = 0.0;
+    ctx->prof_n[0] = ctx->prof_n[1] = 0;
     return WO_OK;
 }
 
 int64_t wo_device_bytes(const wo_ctx* ctx) { return ctx ? ctx->dev_bytes : 0; }
 
 int64_t wo_pair_launches(const wo_ctx* ctx) { return ctx ? ctx->pair_launches : 0; }
+
+int wo_profile_stats(const wo_ctx* ctx, double* single_ms, int64_t* single_n, double* pair_ms,
+                     int64_t* pair_n) {
+    if (!ctx) return WO_ERR_CONFIG;
+    if (single_ms) *single_ms = ctx->prof_ms[0];
+    if (single_n) *single_n = ctx->prof_n[0];
+    if (pair_ms) *pair_ms = ctx->prof_ms[1];
+    if (pair_n) *pair_n = ctx->prof_n[1];
+    return WO_OK;
+}
 
 int wo_timer_mark(wo_ctx* ctx, int idx) {
     int rc = check_ctx(ctx);

@@ -427,14 +427,20 @@ class DeviceGrid:
 
     # ---------------------------------------------------------- profiling
     def set_profiling(self, on):
-        self._ck(self.L.wo_set_profiling(self.h, int(bool(on))), "wo_set_profiling")
+        """on: False/0 off, True/1 every step launch, k: every k-th launch."""
+        self._ck(self.L.wo_set_profiling(self.h, int(on)), "wo_set_profiling")
 
     def stats(self):
         a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
         self._ck(self.L.wo_stats(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)),
                  "wo_stats")
+        sm, sn, pm, pn = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double(), ctypes.c_int64()
+        self._ck(self.L.wo_profile_stats(self.h, ctypes.byref(sm), ctypes.byref(sn),
+                                         ctypes.byref(pm), ctypes.byref(pn)), "wo_profile_stats")
         return {"launches": a.value, "step_launches": b.value, "step_kernel_ms": c.value,
-                "pair_launches": int(self.L.wo_pair_launches(self.h))}
+                "pair_launches": int(self.L.wo_pair_launches(self.h)),
+                "profiled_single_ms": sm.value, "profiled_single_n": sn.value,
+                "profiled_pair_ms": pm.value, "profiled_pair_n": pn.value}
 
     def reset_stats(self):
         self._ck(self.L.wo_reset_stats(self.h), "wo_reset_stats")

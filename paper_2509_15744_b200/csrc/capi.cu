@@ -620,14 +620,7 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     ctx->t2maps.cur = ctx->cur;
     const int tbx = ctx->t2_geo == GEO_TALL ? GeoTall::TBX : GeoWide::TBX;
     const int tby = ctx->t2_geo == GEO_TALL ? GeoTall::TBY : GeoWide::TBY;
-    static const int zfast = [] {
-        const char* e = getenv("WB_T2_ZFAST");
-        return e ? atoi(e) : 0;
-    }();
-    a.zfast = zfast;
-    const unsigned nzb = (unsigned)((ctx->kn0 + a.chunk - 1) / a.chunk);
-    dim3 grid = zfast ? dim3(nzb, ctx->kn2 / tbx, ctx->kn1 / tby)
-                      : dim3(ctx->kn2 / tbx, ctx->kn1 / tby, nzb);
+    dim3 grid(ctx->kn2 / tbx, ctx->kn1 / tby, (ctx->kn0 + a.chunk - 1) / a.chunk);
     prof_begin(ctx, 1);
     launch_step2_engine<T>(StepSel{ctx->flavor, true, sp.acc, false, sup}, ctx->t2_geo, grid,
                            ctx->stream, a, ctx->t2maps);

@@ -79,7 +79,7 @@ template <typename T> struct Step2Args {
     T* out1;           // u^{n+1}
     T* out2;           // u^{n+2}
     T* acc;
-    int n0, n1, n2, chunk, zfast;
+    int n0, n1, n2, chunk;
     MatScalars<T> mat;
     T cv, cg, inv2dt, inv2dx, sdt;
     int n_src;
@@ -167,14 +167,13 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
 
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = ty * G::TX + tx;
-    // block order: tiles fastest (default) or chunks fastest (a.zfast)
-    const int bx = a.zfast ? blockIdx.y : blockIdx.x, by = a.zfast ? blockIdx.z : blockIdx.y;
-    const int bz = a.zfast ? blockIdx.x : blockIdx.z;
-    const int k0 = bx * TBX, j0 = by * TBY;
+    // blocks: tiles fastest, then chunks (a chunk-fastest order measured 4%
+    // slower: neighbouring tiles at the same planes share halos through L2)
+    const int k0 = blockIdx.x * TBX, j0 = blockIdx.y * TBY;
     const int kA = k0 + 2 * tx, ja = j0 + 2 * ty;
     const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
     const int plane = n1 * n2;
-    const int i0 = bz * a.chunk;
+    const int i0 = blockIdx.z * a.chunk;
     const int i1 = min(i0 + a.chunk, n0);
     const int pbeg = max(i0 - 1, 0);           // step-n planes of this chunk
     const int pfin = min(i1, n0 - 1);

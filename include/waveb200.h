@@ -88,6 +88,12 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
  * 0 = never.  Sweeps fall back to single steps at odd range ends, while
  * recording history, and everywhere else. */
 #define WO_OPT_TWO_STEP 4
+/* WO_OPT_PLANE_PART (slab contexts, default 0): 1 = the next single step
+ * computes only the boundary planes 0 and n0-1 (no rotation), 2 = only the
+ * interior planes, then rotates.  Split calls do not synchronise the
+ * stream, so the halo exchange of the new boundary planes (wo_halo_planes_out,
+ * on any stream ordered after the boundary part) overlaps the interior. */
+#define WO_OPT_PLANE_PART 5
 int wo_set_option(wo_ctx* ctx, int option, int value);
 /* Device-resident optimisation loop (fwi.py:178-238 with
  * optim.py adam_step / clip_bounds): fp64 parameters (gamma), the Adam
@@ -182,6 +188,15 @@ int wo_halo_planes(wo_ctx* ctx, void** first, void** last, void** ghost_lo, void
  * devices): lower's last plane -> upper's low ghost, upper's first plane ->
  * lower's high ghost, on the current level. */
 int wo_exchange_local(wo_ctx* lower, wo_ctx* upper);
+/* The planes of the level a split step is writing (before its rotation):
+ * what wo_halo_planes returns for the current level after it. */
+int wo_halo_planes_out(wo_ctx* ctx, void** first, void** last, void** ghost_lo, void** ghost_hi,
+                       int64_t* plane_bytes);
+/* The context's CUDA stream (cudaStream_t), for ordering a caller's
+ * communication with the library's kernels. */
+void* wo_stream(wo_ctx* ctx);
+/* wo_exchange_local for the level a split step is writing. */
+int wo_exchange_local_out(wo_ctx* lower, wo_ctx* upper);
 
 /* Standard-adjoint sweep of gradient_reference (gradients.py:371-386) using
  * the recorded history and the unscaled compact adjoint store; accumulates

@@ -33,6 +33,7 @@ EXPORTS = (
     "wo_check_maxima", "wo_halo_planes", "wo_exchange_local", "wo_pair_launches", "wo_snapshot",
     "wo_get_field", "wo_opt_init", "wo_opt_step", "wo_opt_get", "wo_design_setup",
     "wo_design_material", "wo_design_gradient", "wo_design_get", "wo_profile_stats",
+    "wo_halo_planes_out", "wo_stream", "wo_exchange_local_out",
 )
 
 
@@ -109,11 +110,15 @@ _SIGS = {
     "wo_design_get": (c_int, [c_vp, c_int, c_vp]),
     "wo_profile_stats": (c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64),
                                  ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
+    "wo_halo_planes_out": (c_int, [c_vp] + [ctypes.POINTER(c_vp)] * 4 + [P_i64]),
+    "wo_stream": (c_vp, [c_vp]),
+    "wo_exchange_local_out": (c_int, [c_vp, c_vp]),
 }
 WO_OPT_FAST_DIV = 1
 WO_OPT_PAIR_KERNEL = 2
 WO_OPT_TMA_KERNEL = 3
 WO_OPT_TWO_STEP = 4
+WO_OPT_PLANE_PART = 5
 WO_SNAP_FREE, WO_SNAP_SAVE, WO_SNAP_RESTORE = 0, 1, 2
 WO_FIELD_GAMMA, WO_FIELD_UPREV, WO_FIELD_UCUR, WO_FIELD_ACC = 0, 1, 2, 3
 

@@ -57,6 +57,7 @@ struct wo_ctx {
     int use_tma = 1;                   // wo_set_option(WO_OPT_TMA_KERNEL)
     int use_two_step = 1;              // wo_set_option(WO_OPT_TWO_STEP)
     int num_sms = 148;                 // of the context's device
+    int part = 0;                      // WO_OPT_PLANE_PART: 0 whole steps, 1 boundary, 2 interior
     int t2_geo = GEO_NONE;             // two-step tile geometry (set when its maps are built)
     int t2_state = 0;                  // two-step tensor maps: 0 not built, 1 ready, -1 no
     Tma2Maps t2maps;
@@ -324,6 +325,7 @@ struct StepSpec {
     char* cur = nullptr;
     char* out = nullptr;
     char* hist = nullptr;              // history row receiving a copy of out
+    int c_lo = 0, c_hi = -1;           // computed planes [c_lo, c_hi) (c_hi < 0: all)
 };
 
 template <typename T>
@@ -341,6 +343,9 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     a.i_lo = ctx->has_lo ? -1 : 0;
     a.i_hi = ctx->kn0 + ctx->has_hi;
     a.chunk = choose_chunk(ctx);
+    a.c_lo = sp.c_lo;
+    a.c_hi = sp.c_hi < 0 ? ctx->kn0 : std::min(sp.c_hi, ctx->kn0);
+    if (a.c_hi <= a.c_lo) return WO_OK;   // empty part
     a.mat = mat_scalars<T>(ctx);
     a.cv = (T)ctx->cv;
     a.cg = (T)ctx->cg;
@@ -380,7 +385,7 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     const bool pair = tma || ((ctx->kn2 % 2 == 0) && ctx->use_pair);
     dim3 block(pair ? 32 : BX, BY, 1);
     dim3 grid(pair ? (ctx->kn2 + PBX - 1) / PBX : (ctx->kn2 + BX - 1) / BX,
-              (ctx->kn1 + BY - 1) / BY, (ctx->kn0 + a.chunk - 1) / a.chunk);
+              (ctx->kn1 + BY - 1) / BY, (a.c_hi - a.c_lo + a.chunk - 1) / a.chunk);
     if (tma) {
         ctx->tmaps.cur = ctx->cur;
         ctx->tmaps.prev = ctx->prv;
@@ -395,6 +400,26 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     ctx->step_launches++;
     CK(cudaGetLastError());
     return WO_OK;
+}
+
+// one step of a slab split for halo overlap (wo_set_option WO_OPT_PLANE_PART):
+// part 1 computes the boundary planes 0 and n0-1 (whose new values the
+// neighbours need), part 2 the interior; part 0 everything
+template <typename T>
+int launch_step_part(wo_ctx* ctx, StepSpec sp) {
+    if (ctx->part == 0) return launch_step<T>(ctx, sp);
+    if (ctx->part == 2) {
+        sp.c_lo = 1;
+        sp.c_hi = ctx->kn0 - 1;
+        return launch_step<T>(ctx, sp);
+    }
+    sp.c_lo = 0;
+    sp.c_hi = 1;
+    int rc = launch_step<T>(ctx, sp);
+    if (rc || ctx->kn0 < 2) return rc;
+    sp.c_lo = ctx->kn0 - 1;
+    sp.c_hi = ctx->kn0;
+    return launch_step<T>(ctx, sp);
 }
 
 template <typename T>
@@ -498,6 +523,7 @@ int pick_geo(const wo_ctx* ctx) {
 
 bool pair_ready(wo_ctx* ctx) {
     if (!ctx->use_two_step || !ctx->use_tma || !ctx->use_pair || ctx->has_lo || ctx->has_hi ||
+        ctx->part != 0 ||
         !ctx->material_set || pick_geo(ctx) == GEO_NONE)
         return false;
     // fp64 two-step CTAs need 130 KB of shared memory (1 CTA/SM) and measure
@@ -688,7 +714,9 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
             "history not initialised");
     int rc = WO_OK;
     const bool gather = ctx->n_sup > 0;
-    if (first) {
+    REQUIRE(ctx->part == 0 || (n_end - n_begin <= 1 && ns <= MAX_SRC && !record),
+            "split (boundary / interior) steps go one in-kernel-source step per call");
+    if (first && ctx->part != 2) {
         rc = ensure_slots(ctx, N);
         if (rc) return rc;
         CK(cudaMemsetAsync(ctx->maxslots, 0, (size_t)(N + 2) * 8, ctx->stream));
@@ -756,15 +784,18 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
                 reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots) + n);
             ctx->launches++;
         } else {
-            rc = launch_step<T>(ctx, sp);
+            rc = launch_step_part<T>(ctx, sp);
             if (rc) return rc;
             if (!in_kernel) {
                 rc = inject_host_list<T>(ctx, ns, sidx.data(), vals.data());
                 if (rc) return rc;
             }
         }
-        std::swap(ctx->cur, ctx->prv);  // rotate (u^{n+1} was written over u^{n-1})
+        // rotate (u^{n+1} was written over u^{n-1}); a split step rotates
+        // after its interior part
+        if (ctx->part != 1) std::swap(ctx->cur, ctx->prv);
     }
+    if (ctx->part != 0) return WO_OK;   // split steps stay asynchronous
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->prof) harvest_events(ctx);
     if (!finish) return WO_OK;
@@ -798,7 +829,8 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
     REQUIRE(!inject || ctx->store_bytes >= (size_t)N * ctx->n_sup * sizeof(T),
             "adjoint store not populated for this N");
     int rc = WO_OK;
-    if (n_hi == N - 1) {
+    REQUIRE(ctx->part == 0 || n_hi - n_lo <= 1, "split steps go one step per call");
+    if (n_hi == N - 1 && ctx->part != 2) {
         rc = ensure_slots(ctx, N);
         if (rc) return rc;
         CK(cudaMemsetAsync(ctx->maxslots, 0, (size_t)(N + 2) * 8, ctx->stream));
@@ -846,10 +878,11 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
         sp.sup_mode = inject ? SUP_INJECT : SUP_NONE;
         sp.row = n;
         sp.slot = n;
-        rc = launch_step<T>(ctx, sp);
+        rc = launch_step_part<T>(ctx, sp);
         if (rc) return rc;
-        std::swap(ctx->cur, ctx->prv);
+        if (ctx->part != 1) std::swap(ctx->cur, ctx->prv);
     }
+    if (ctx->part != 0) return WO_OK;   // split steps stay asynchronous
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->prof) harvest_events(ctx);
     if (!finish) return WO_OK;
@@ -1451,8 +1484,14 @@ int wo_set_option(wo_ctx* ctx, int option, int value) {
     int rc = check_ctx(ctx);
     if (rc) return rc;
     REQUIRE(option == WO_OPT_FAST_DIV || option == WO_OPT_PAIR_KERNEL ||
-                option == WO_OPT_TMA_KERNEL || option == WO_OPT_TWO_STEP,
+                option == WO_OPT_TMA_KERNEL || option == WO_OPT_TWO_STEP ||
+                option == WO_OPT_PLANE_PART,
             "unknown option");
+    if (option == WO_OPT_PLANE_PART) {
+        REQUIRE(value >= 0 && value <= 2, "plane part is 0, 1 or 2");
+        ctx->part = value;
+        return WO_OK;
+    }
     if (option == WO_OPT_TWO_STEP) {
         ctx->use_two_step = value;   // 0 off, 1 fp32 grids, 2 also fp64
         return WO_OK;
@@ -1671,7 +1710,23 @@ int wo_halo_planes(wo_ctx* ctx, void** first, void** last, void** ghost_lo, void
     return WO_OK;
 }
 
-int wo_exchange_local(wo_ctx* lower, wo_ctx* upper) {
+int wo_halo_planes_out(wo_ctx* ctx, void** first, void** last, void** ghost_lo, void** ghost_hi,
+                       int64_t* plane_bytes) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    const size_t pb = (size_t)ctx->plane() * ctx->itemsize;
+    char* c = ctx->uprev();   // before the interior part rotates: the new level
+    *first = c;
+    *last = c + (size_t)(ctx->kn0 - 1) * pb;
+    *ghost_lo = ctx->has_lo ? c - pb : nullptr;
+    *ghost_hi = ctx->has_hi ? c + (size_t)ctx->kn0 * pb : nullptr;
+    *plane_bytes = (int64_t)pb;
+    return WO_OK;
+}
+
+void* wo_stream(wo_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+static int exchange_local(wo_ctx* lower, wo_ctx* upper, bool out_level) {
     if (!lower || !upper) return WO_ERR_CONFIG;
     wo_ctx* ctx = lower;
     REQUIRE(lower->has_hi && upper->has_lo && lower->plane() == upper->plane() &&
@@ -1681,10 +1736,12 @@ int wo_exchange_local(wo_ctx* lower, wo_ctx* upper) {
     CK(cudaStreamSynchronize(lower->stream));
     CK(cudaSetDevice(upper->device));
     CK(cudaStreamSynchronize(upper->stream));
-    char* lo_last = lower->ucur() + (size_t)(lower->kn0 - 1) * pb;
-    char* lo_ghost = lower->ucur() + (size_t)lower->kn0 * pb;
-    char* up_first = upper->ucur();
-    char* up_ghost = upper->ucur() - pb;
+    char* lo = out_level ? lower->uprev() : lower->ucur();
+    char* up = out_level ? upper->uprev() : upper->ucur();
+    char* lo_last = lo + (size_t)(lower->kn0 - 1) * pb;
+    char* lo_ghost = lo + (size_t)lower->kn0 * pb;
+    char* up_first = up;
+    char* up_ghost = up - pb;
     if (lower->device == upper->device) {
         CK(cudaMemcpy(up_ghost, lo_last, pb, cudaMemcpyDeviceToDevice));
         CK(cudaMemcpy(lo_ghost, up_first, pb, cudaMemcpyDeviceToDevice));
@@ -1695,6 +1752,10 @@ int wo_exchange_local(wo_ctx* lower, wo_ctx* upper) {
     CK(cudaSetDevice(lower->device));
     return WO_OK;
 }
+
+int wo_exchange_local(wo_ctx* lower, wo_ctx* upper) { return exchange_local(lower, upper, false); }
+
+int wo_exchange_local_out(wo_ctx* lower, wo_ctx* upper) { return exchange_local(lower, upper, true); }
 
 int wo_sweep_adjoint_reference(wo_ctx* ctx, int64_t n_steps, double dt, int64_t* fail_step,
                                double* fail_max) {

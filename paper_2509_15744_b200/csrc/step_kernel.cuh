@@ -61,6 +61,8 @@ template <typename T> struct StepArgs {
     int n0, n1, n2;     // local extents (n0 = planes of this slab)
     int i_lo, i_hi;     // loadable local planes: [-1 if ghost below, n0 (+1 if ghost above))
     int chunk;          // axis-0 planes per CTA
+    int c_lo, c_hi;     // planes this launch computes (a slab step may be split into its
+                        // boundary planes and its interior, to overlap the halo exchange)
     MatScalars<T> mat;
     // kernel-increment scalars, cast to T on the host (kernels.py:149-152)
     T cv, cg, inv2dt, inv2dx, sdt;
@@ -101,8 +103,8 @@ step_kernel(const StepArgs<T> a) {
     const int n1 = a.n1, n2 = a.n2;
     const bool inb = (j < n1) && (k < n2);
     const int plane = n1 * n2;
-    const int i0 = blockIdx.z * a.chunk;
-    const int i1 = min(i0 + a.chunk, a.n0);
+    const int i0 = a.c_lo + blockIdx.z * a.chunk;   // computed planes [c_lo, c_hi)
+    const int i1 = min(i0 + a.chunk, a.c_hi);
     const MatScalars<T>& M = a.mat;
 
     // clamped (mirror) coordinates of this thread's cell and halo cell

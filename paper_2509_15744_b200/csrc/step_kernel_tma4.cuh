@@ -62,8 +62,8 @@ step_kernel_tma4(const __grid_constant__ StepArgs<T> a, const __grid_constant__ 
     const int kA = k0 + 2 * tx, ja = j0 + 2 * ty;
     const int n1 = a.n1, n2 = a.n2;
     const int plane = n1 * n2;
-    const int i0 = blockIdx.z * a.chunk;
-    const int i1 = min(i0 + a.chunk, a.n0);
+    const int i0 = a.c_lo + blockIdx.z * a.chunk;   // computed planes [c_lo, c_hi)
+    const int i1 = min(i0 + a.chunk, a.c_hi);
     const int plast = a.i_hi - 1;
     const int pend = min(i1, plast);
     const MatScalars<T>& M = a.mat;

@@ -46,8 +46,8 @@ step_kernel_pair(const StepArgs<T> a) {
     const bool oob = kA >= n2;                 // pair beyond the row: mirror of the last cell
     const bool inb = (j < n1) && !oob;
     const int plane = n1 * n2;
-    const int i0 = blockIdx.z * a.chunk;
-    const int i1 = min(i0 + a.chunk, a.n0);
+    const int i0 = a.c_lo + blockIdx.z * a.chunk;   // computed planes [c_lo, c_hi)
+    const int i1 = min(i0 + a.chunk, a.c_hi);
     const MatScalars<T>& M = a.mat;
     const int cs = 2 + 2 * tx;                 // smem column of cell A
 

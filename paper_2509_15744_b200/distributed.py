@@ -96,10 +96,11 @@ def first_failure_backward(maxima, n_steps):
     return None
 
 
-def exchange_planes(first, last, ghost_lo, ghost_hi, rank, world, group=None):
-    """Halo exchange of one slab with torch.distributed P2P: first -> rank-1's
-    high ghost, last -> rank+1's low ghost (tensors: CUDA with NCCL, CPU with
-    gloo)."""
+def exchange_planes_async(first, last, ghost_lo, ghost_hi, rank, world, group=None):
+    """Start the halo exchange of one slab with torch.distributed P2P: first
+    -> rank-1's high ghost, last -> rank+1's low ghost (tensors: CUDA with
+    NCCL, CPU with gloo).  Returns the requests; with NCCL the transfers are
+    ordered after the work already queued on the current CUDA stream."""
     import torch.distributed as dist
 
     ops = []
@@ -109,9 +110,13 @@ def exchange_planes(first, last, ghost_lo, ghost_hi, rank, world, group=None):
     if rank < world - 1:
         ops.append(dist.P2POp(dist.isend, last, rank + 1, group))
         ops.append(dist.P2POp(dist.irecv, ghost_hi, rank + 1, group))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+    return dist.batch_isend_irecv(ops) if ops else []
+
+
+def exchange_planes(first, last, ghost_lo, ghost_hi, rank, world, group=None):
+    """Blocking form of exchange_planes_async."""
+    for req in exchange_planes_async(first, last, ghost_lo, ghost_hi, rank, world, group):
+        req.wait()
 
 
 def _device_view(ptr, nbytes, dtype, device):
@@ -140,6 +145,17 @@ class LoopbackHalo:
             if rc:
                 engine._raise(lo.h, rc, "wo_exchange_local")
 
+    # split steps: the boundary planes of the level being written
+    def begin(self):
+        for lo, hi in zip(self.ctxs[:-1], self.ctxs[1:]):
+            rc = lo.L.wo_exchange_local_out(lo.h, hi.h)
+            if rc:
+                engine._raise(lo.h, rc, "wo_exchange_local_out")
+        return []
+
+    def end(self, works):
+        pass
+
     def allreduce_max(self, arr):
         return arr
 
@@ -162,6 +178,30 @@ class TorchHalo:
         exchange_planes(view(first), view(last), view(glo), view(ghi), self.rank, self.world,
                         self.group)
         torch.cuda.synchronize(dev)
+
+    # split steps: the new boundary planes travel while the interior part of
+    # the step runs (NCCL ordered on the context stream both ways)
+    def _ext(self):
+        import torch
+
+        return torch.cuda.ExternalStream(self.ctx.stream_ptr, device=f"cuda:{self.ctx.device}")
+
+    def begin(self):
+        import torch
+
+        (first, last, glo, ghi), pb = self.ctx.halo_planes(out=True)
+        dt, dev = self.ctx.dtype, self.ctx.device
+        view = lambda p: _device_view(p, pb, dt, dev) if p else None  # noqa: E731
+        with torch.cuda.stream(self._ext()):
+            return exchange_planes_async(view(first), view(last), view(glo), view(ghi),
+                                         self.rank, self.world, self.group)
+
+    def end(self, works):
+        import torch
+
+        with torch.cuda.stream(self._ext()):
+            for w in works:
+                w.wait()
 
     def allreduce_max(self, arr):
         import torch
@@ -187,7 +227,8 @@ class SlabGradient:
     slabs: list of (i0, i1) handled by THIS process; halo: 'loopback' (all
     slabs here) or a TorchHalo-compatible object built by ``for_rank``."""
 
-    def __init__(self, problem, material, config, slabs, devices=None, halo="loopback"):
+    def __init__(self, problem, material, config, slabs, devices=None, halo="loopback",
+                 overlap=True):
         from .gradients import SuperpositionConfig, _misfit_spec, _shot_list
 
         if not isinstance(config, SuperpositionConfig):
@@ -202,15 +243,20 @@ class SlabGradient:
         self.ctxs = [engine.DeviceGrid(grid, self.dtype, d, slab=s)
                      for s, d in zip(self.slabs, devices)]
         self.halo = LoopbackHalo(self.ctxs) if halo == "loopback" else halo
+        # overlap: every step runs as boundary planes -> halo exchange started
+        # -> interior planes -> exchange awaited, so the transfer of the new
+        # boundary planes overlaps the interior update (WO_OPT_PLANE_PART)
+        self.overlap = overlap
         self._misfit_spec = _misfit_spec
         self._shots = _shot_list(problem)
 
     @classmethod
-    def for_rank(cls, problem, material, config, rank, world, device=None, group=None):
+    def for_rank(cls, problem, material, config, rank, world, device=None, group=None,
+                 overlap=True):
         """One slab per torchrun rank (NCCL halo exchange)."""
         slab = slab_ranges(problem.grid.shape[0], world)[rank]
         dev = rank if device is None else device
-        obj = cls(problem, material, config, [slab], [dev], halo=None)
+        obj = cls(problem, material, config, [slab], [dev], halo=None, overlap=overlap)
         obj.halo = TorchHalo(obj.ctxs[0], rank, world, group)
         return obj
 
@@ -219,6 +265,28 @@ class SlabGradient:
         for c in self.ctxs:
             c.set_material(self.material, dt)
         return self
+
+    def _steps(self, step, *per_ctx):
+        """One time step on every slab, then the halo exchange; with overlap
+        the exchange of the new boundary planes runs during the interior."""
+        args = list(zip(self.ctxs, *per_ctx))
+        if not self.overlap:
+            for a in args:
+                step(*a)
+            self.halo.exchange()
+            return
+        try:
+            for a in args:
+                a[0].set_plane_part(1)
+                step(*a)
+            works = self.halo.begin()
+            for a in args:
+                a[0].set_plane_part(2)
+                step(*a)
+            self.halo.end(works)
+        finally:
+            for c in self.ctxs:
+                c.set_plane_part(0)
 
     def run(self):
         from .solver import injection_scale
@@ -245,10 +313,9 @@ class SlabGradient:
             src_local = [g_src - c.i_begin * plane if c.i_begin * plane <= g_src < c.i_end * plane
                          else -1 for c in self.ctxs]
             for n in range(1, n_steps):
-                for c, s in zip(self.ctxs, src_local):
-                    c.sweep_forward_range(n_steps, n, n + 1, [s] if s >= 0 else [], amp
-                                          if s >= 0 else np.zeros((0, n_steps)), True, dt)
-                self.halo.exchange()
+                self._steps(lambda c, s, _n=n: c.sweep_forward_range(
+                    n_steps, _n, _n + 1, [s] if s >= 0 else [],
+                    amp if s >= 0 else np.zeros((0, n_steps)), True, dt), src_local)
             maxima = self.halo.allreduce_max(
                 np.max([c.check_maxima(n_steps) for c in self.ctxs], axis=0))
             fail, _ = first_failure_forward(maxima, n_steps, scale)
@@ -260,10 +327,10 @@ class SlabGradient:
                 if nsup:
                     cost += c.shot_misfit(n_steps, kind, meas, cc, adj_coef, True, k)
             total += self.halo.allreduce_sum(cost)
+            inject = [spec[0] > 0 for spec in specs]
             for n in range(n_steps - 1, 0, -1):
-                for c, s, spec in zip(self.ctxs, src_local, specs):
-                    c.sweep_backward_range(n_steps, n, n - 1, s, amp[0], spec[0] > 0, True, dt)
-                self.halo.exchange()
+                self._steps(lambda c, s, inj, _n=n: c.sweep_backward_range(
+                    n_steps, _n, _n - 1, s, amp[0], inj, True, dt), src_local, inject)
             maxima = self.halo.allreduce_max(
                 np.max([c.check_maxima(n_steps) for c in self.ctxs], axis=0))
             fail = first_failure_backward(maxima, n_steps)
@@ -284,12 +351,12 @@ class SlabGradient:
             c.close()
 
 
-def gradient_superposed_slabs(problem, material, config, parts, devices=None):
+def gradient_superposed_slabs(problem, material, config, parts, devices=None, overlap=True):
     """Single-process slab-decomposed gradient (loopback / peer halo)."""
     from .gradients import GradientResult, BufferCounter
 
     sg = SlabGradient(problem, material, config, slab_ranges(problem.grid.shape[0], parts),
-                      devices).upload()
+                      devices, overlap=overlap).upload()
     try:
         cost = sg.run()
         grad = sg.download()

@@ -349,14 +349,23 @@ class DeviceGrid:
         self._ck(self.L.wo_check_maxima(self.h, int(n_steps), N.ptr(out)), "wo_check_maxima")
         return out
 
-    def halo_planes(self):
+    def halo_planes(self, out=False):
         """(first, last, ghost_lo, ghost_hi) device addresses of the current
-        level and the plane size in bytes."""
+        level (out=True: the level a split step is writing) and the plane
+        size in bytes."""
         p = [ctypes.c_void_p() for _ in range(4)]
         pb = ctypes.c_int64()
-        self._ck(self.L.wo_halo_planes(self.h, *[ctypes.byref(x) for x in p], ctypes.byref(pb)),
-                 "wo_halo_planes")
+        fn = self.L.wo_halo_planes_out if out else self.L.wo_halo_planes
+        self._ck(fn(self.h, *[ctypes.byref(x) for x in p], ctypes.byref(pb)), "wo_halo_planes")
         return tuple(x.value for x in p), pb.value
+
+    def set_plane_part(self, part):
+        """Split slab steps: 1 boundary planes, 2 interior (+rotation), 0 whole."""
+        self._ck(self.L.wo_set_option(self.h, N.WO_OPT_PLANE_PART, int(part)), "wo_set_option")
+
+    @property
+    def stream_ptr(self):
+        return int(self.L.wo_stream(self.h) or 0)
 
     def sweep_adjoint_reference(self, n_steps, dt):
         fstep = ctypes.c_int64(0)

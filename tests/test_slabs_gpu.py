@@ -40,13 +40,16 @@ def _problem(W, shape, seed):
 
 @pytest.mark.parametrize("shape,parts", [((24, 16, 64), 3), ((22, 18, 26), 2), ((9, 8, 64), 4)])
 @pytest.mark.parametrize("prec", ["single", "double"])
-def test_slabs_bitwise_equal_single_gpu(W, shape, parts, prec):
+@pytest.mark.parametrize("overlap", [True, False])
+def test_slabs_bitwise_equal_single_gpu(W, shape, parts, prec, overlap):
+    """Slabs (split boundary/interior steps with the exchange between them,
+    or whole steps) give the single-GPU bits."""
     from paper_2509_15744_b200.distributed import gradient_superposed_slabs
 
     problem, mat = _problem(W, shape, sum(shape) + parts)
     cfg = W.SuperpositionConfig(k=1e13, precision=prec)
     ref = W.gradient_superposed(problem, mat, cfg)
-    got = gradient_superposed_slabs(problem, mat, cfg, parts)
+    got = gradient_superposed_slabs(problem, mat, cfg, parts, overlap=overlap)
     assert bits_equal(got.gradient, ref.gradient)
     assert abs(got.cost - ref.cost) <= 1e-13 * abs(ref.cost)
 

@@ -6,8 +6,12 @@ slab decomposition (SlabGradient)
     one ghost plane per interior face; the step kernels read ghost planes
     exactly like interior planes and mirror only at the global ends, so the
     per-cell arithmetic is unchanged and the gradient, traces and adjoint
-    store are BITWISE equal to one GPU.  After every step each slab sends its
-    first/last plane of the new level to its neighbours' ghost planes:
+    store are BITWISE equal to one GPU.  Every step each slab sends its
+    first/last plane of the new level to its neighbours' ghost planes; by
+    default (``overlap``) a step runs as its two boundary planes, then the
+    exchange is started, then the interior planes are updated while the
+    planes travel, and the next step waits for the exchange (WO_OPT_PLANE_PART;
+    NCCL is ordered on the context's stream, no host synchronisation):
       * ``LoopbackHalo`` — all slabs in one process (same device or peer
         devices), ``wo_exchange_local`` copies;
       * ``TorchHalo`` — one slab per process (torchrun), torch.distributed

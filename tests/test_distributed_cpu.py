@@ -73,6 +73,21 @@ def _worker(rank, world, port, q):
             ok &= bool(torch.equal(ghost_lo, field[2 * rank - 1]))
         if rank < world - 1:
             ok &= bool(torch.equal(ghost_hi, field[2 * rank + 2]))
+        # split-step form: start the exchange, do "interior" work, then wait
+        field2 = field * 2.0
+        mine2 = field2[2 * rank:2 * rank + 2].clone()
+        glo2 = torch.full((plane,), -1.0, dtype=torch.float64)
+        ghi2 = torch.full((plane,), -1.0, dtype=torch.float64)
+        works = D.exchange_planes_async(mine2[0].contiguous(), mine2[1].contiguous(), glo2, ghi2,
+                                        rank, world)
+        interior = (mine2 * 0.5).sum()   # stands for the interior update
+        for w in works:
+            w.wait()
+        ok &= float(interior) == float(mine2.sum()) * 0.5
+        if rank > 0:
+            ok &= bool(torch.equal(glo2, field2[2 * rank - 1]))
+        if rank < world - 1:
+            ok &= bool(torch.equal(ghi2, field2[2 * rank + 2]))
         # cost / maxima reductions as the slab driver does them
         c = torch.tensor([float(rank + 1)], dtype=torch.float64)
         dist.all_reduce(c)

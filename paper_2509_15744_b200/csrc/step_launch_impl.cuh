@@ -2,32 +2,38 @@
 // included by the per-dtype translation units.
 #pragma once
 
+#include <atomic>
+
 #include "launchers.cuh"
 #include "step_kernel_tma4.cuh"
 #include "step_kernel_v2.cuh"
 
 namespace wb {
 
+// Opt a kernel into more than 48 KB of dynamic shared memory, once per
+// kernel and device (the attribute is per device; one process may drive
+// several GPUs, e.g. slabs on peer devices).
+template <typename K>
+void smem_opt_in(K kernel, size_t bytes) {
+    static std::atomic<unsigned long long> done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_relaxed) & bit) return;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    done.fetch_or(bit);
+}
+
 template <typename T, int FL, bool FAST, bool ACC, bool CHK, int SUP>
 void go_step(int engine, dim3 grid, dim3 block, cudaStream_t s, const StepArgs<T>& a,
              const TmaMaps& maps) {
     if (engine == ENGINE_TMA4) {   // 128 threads, 2x2 cells each, unrolled stages
         const size_t sm = tma4_smem_bytes<T>();
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            attr = true;
-        }
+        smem_opt_in(step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP>, sm);
         step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP><<<grid, dim3(32, 4, 1), sm, s>>>(a, maps);
     } else if (engine == ENGINE_TMA) {   // 256 threads, 2 cells each
         const size_t sm = tma_smem_bytes<T>();
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(step_kernel_tma<T, FL, FAST, ACC, CHK, SUP>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            attr = true;
-        }
+        smem_opt_in(step_kernel_tma<T, FL, FAST, ACC, CHK, SUP>, sm);
         step_kernel_tma<T, FL, FAST, ACC, CHK, SUP><<<grid, block, sm, s>>>(a, maps);
     } else if (SUP == SUP_NONE) {   // pair / scalar kernels read a.sup_mode at run time
         if (engine == ENGINE_PAIR)
@@ -73,12 +79,7 @@ void launch_step_engine(int engine, const StepSel& k, dim3 grid, dim3 block, cud
 template <typename T, typename G, int FL, bool ACC, int SUP>
 void go_step2(dim3 grid, cudaStream_t s, const Step2Args<T>& a, const Tma2Maps& maps) {
     const size_t sm = step2_smem_bytes<T, G>();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(step2_kernel_tma<T, G, FL, ACC, SUP>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        attr = true;
-    }
+    smem_opt_in(step2_kernel_tma<T, G, FL, ACC, SUP>, sm);
     step2_kernel_tma<T, G, FL, ACC, SUP><<<grid, dim3(G::TX, G::TY, 1), sm, s>>>(a, maps);
 }
 

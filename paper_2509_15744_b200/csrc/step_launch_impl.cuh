@@ -13,14 +13,14 @@ namespace wb {
 // Opt a kernel into more than 48 KB of dynamic shared memory, once per
 // kernel and device (the attribute is per device; one process may drive
 // several GPUs, e.g. slabs on peer devices).
-template <typename K>
-void smem_opt_in(K kernel, size_t bytes) {
-    static std::atomic<unsigned long long> done{0};
+template <auto Kernel>
+void smem_opt_in(size_t bytes) {
+    static std::atomic<unsigned long long> done{0};   // one flag set per kernel
     int dev = 0;
     cudaGetDevice(&dev);
     const unsigned long long bit = 1ull << (dev & 63);
     if (done.load(std::memory_order_relaxed) & bit) return;
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     done.fetch_or(bit);
 }
 
@@ -29,11 +29,11 @@ void go_step(int engine, dim3 grid, dim3 block, cudaStream_t s, const StepArgs<T
              const TmaMaps& maps) {
     if (engine == ENGINE_TMA4) {   // 128 threads, 2x2 cells each, unrolled stages
         const size_t sm = tma4_smem_bytes<T>();
-        smem_opt_in(step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP>, sm);
+        smem_opt_in<step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP>>(sm);
         step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP><<<grid, dim3(32, 4, 1), sm, s>>>(a, maps);
     } else if (engine == ENGINE_TMA) {   // 256 threads, 2 cells each
         const size_t sm = tma_smem_bytes<T>();
-        smem_opt_in(step_kernel_tma<T, FL, FAST, ACC, CHK, SUP>, sm);
+        smem_opt_in<step_kernel_tma<T, FL, FAST, ACC, CHK, SUP>>(sm);
         step_kernel_tma<T, FL, FAST, ACC, CHK, SUP><<<grid, block, sm, s>>>(a, maps);
     } else if (SUP == SUP_NONE) {   // pair / scalar kernels read a.sup_mode at run time
         if (engine == ENGINE_PAIR)
@@ -79,7 +79,7 @@ void launch_step_engine(int engine, const StepSel& k, dim3 grid, dim3 block, cud
 template <typename T, typename G, int FL, bool ACC, int SUP>
 void go_step2(dim3 grid, cudaStream_t s, const Step2Args<T>& a, const Tma2Maps& maps) {
     const size_t sm = step2_smem_bytes<T, G>();
-    smem_opt_in(step2_kernel_tma<T, G, FL, ACC, SUP>, sm);
+    smem_opt_in<step2_kernel_tma<T, G, FL, ACC, SUP>>(sm);
     step2_kernel_tma<T, G, FL, ACC, SUP><<<grid, dim3(G::TX, G::TY, 1), sm, s>>>(a, maps);
 }
 

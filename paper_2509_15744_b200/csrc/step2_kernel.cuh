@@ -48,6 +48,9 @@ namespace wb {
 #ifndef WB_T2_STREAM_STORES
 #define WB_T2_STREAM_STORES 0
 #endif
+#ifndef WB_T2_NEXT_PREFETCH
+#define WB_T2_NEXT_PREFETCH 1
+#endif
 constexpr int T2_THREADS = 128;
 constexpr int T2_NS = WB_T2_STAGES;  // TMA ring stages
 constexpr int T2_PF = WB_T2_PREFETCH;   // L2 prefetch distance beyond the ring (planes)
@@ -80,6 +83,7 @@ template <typename T> struct Step2Args {
     T* out2;           // u^{n+2}
     T* acc;
     int n0, n1, n2, chunk;
+    int resident;      // CTAs resident at once (3 per SM; 0: no next-block prefetch)
     MatScalars<T> mat;
     T cv, cg, inv2dt, inv2dx, sdt;
     int n_src;
@@ -222,20 +226,33 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     const CUtensorMap* mP = pick_map(maps.u_r1, maps.prev);
     // L2 prefetch of a later plane's boxes (no shared memory; hides DRAM
     // latency beyond the T2_NS-stage ring)
-    auto prefetch = [&](int p) {
+    auto prefetch_at = [&](int kk0, int jj0, int p) {
         auto pf = [&](const CUtensorMap* m, int c0, int c1) {
             asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
                          ::"l"(reinterpret_cast<unsigned long long>(m)), "r"(c0), "r"(c1), "r"(p)
                          : "memory");
         };
-        pf(mU, k0 - HO, j0 - 2);
-        pf(&maps.fj_r2, k0 - HO, j0 - 2);
-        pf(mP, k0 - HO, j0 - 1);
-        pf(&maps.c_r1, k0 - HO, j0 - 1);
-        pf(&maps.fk_r1, k0 - HO, j0 - 1);
-        pf(&maps.fi_r1, k0 - HO, j0 - 1);
-        if (ACC) pf(&maps.a_ctr, k0, j0);
+        pf(mU, kk0 - HO, jj0 - 2);
+        pf(&maps.fj_r2, kk0 - HO, jj0 - 2);
+        pf(mP, kk0 - HO, jj0 - 1);
+        pf(&maps.c_r1, kk0 - HO, jj0 - 1);
+        pf(&maps.fk_r1, kk0 - HO, jj0 - 1);
+        pf(&maps.fi_r1, kk0 - HO, jj0 - 1);
+        if (ACC) pf(&maps.a_ctr, kk0, jj0);
     };
+    auto prefetch = [&](int p) { prefetch_at(k0, j0, p); };
+    // the block that will most likely take this block's slot when it ends
+    // (blocks start in index order, a.resident at a time): its first planes
+    // are pulled into L2 during this block's last planes (WB_T2_NEXT_PREFETCH)
+    const int nblk = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z) + a.resident;
+    const bool has_next = WB_T2_NEXT_PREFETCH && a.resident > 0 &&
+                          nblk < (int)(gridDim.x * gridDim.y * gridDim.z);
+    int nk0 = 0, nj0 = 0, npb = 0;
+    if (has_next) {
+        nk0 = (nblk % gridDim.x) * TBX;
+        nj0 = ((nblk / gridDim.x) % gridDim.y) * TBY;
+        npb = max((nblk / (gridDim.x * gridDim.y)) * a.chunk - 1, 0);
+    }
     auto issue = [&](int p, int s) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[s], STAGE_BYTES);
@@ -509,6 +526,9 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         if (tid == T2_PRODUCER && p + T2_NS <= plast) {
             issue(p + T2_NS, q);
             if (p + T2_NS + T2_PF <= plast) prefetch(p + T2_NS + T2_PF);
+        } else if (tid == T2_PRODUCER && has_next) {   // one plane of the next block per body
+            const int d = p + T2_NS - plast - 1;
+            if (d >= 0 && d < T2_NS && npb + d < n0) prefetch_at(nk0, nj0, npb + d);
         }
 
         // ---- c: step n+1 at plane p-1 (tile) ----

@@ -401,7 +401,7 @@ def main():
     ap.add_argument("--n-steps", type=int, default=1024)
     # CPU samples: ~12 s for cpu_baseline; ~5 s per step of the reference arm
     # (so its default 10 steps finish in about a minute)
-    ap.add_argument("--cpu-sample-steps", type=int, default=240)
+    ap.add_argument("--cpu-sample-steps", type=int, default=160)
     ap.add_argument("--ref-sample-steps", type=int, default=100)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -233,3 +233,49 @@ def test_device_dump_equals_host_dump(W, tmp_path, shape, prec):
     gam = ctx.get_field("gamma", first_axis_fastest=True)
     dt = np.float32 if prec == "single" else np.float64
     assert bits_equal(gam, np.ravel(np.asarray(mat.gamma).astype(dt), order="F"))
+
+
+# ------------------------------------------------ randomised parity sweep
+@pytest.mark.parametrize("seed", range(12))
+def test_two_step_random_cases(W, seed):
+    """Random tile-multiple grids, step counts, flavours, precisions and
+    source / sensor placements: gradient and cost bit-exact vs the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    nd = 3 if seed % 4 else 2
+    if nd == 3:
+        shape = (int(rng.integers(2, 30)), 8 * int(rng.integers(1, 5)),
+                 int(rng.choice([64, 96, 128, 192])))
+    else:
+        shape = (8 * int(rng.integers(1, 9)), int(rng.choice([64, 128, 192])))
+    flavor = "rho_scaled" if seed % 3 else "acoustic"
+    prec = "single" if seed % 2 == 0 else "double"
+    n_steps = int(rng.integers(20, 70))
+    dx = 1e-4 if flavor == "rho_scaled" else 1e-2
+    gamma = rng.uniform(0.2 if flavor == "rho_scaled" else 0.0, 1.0, size=shape)
+    grid = W.build_grid(shape, dx)
+    mat, omat, c_max = _materials(W, flavor, gamma, grid, dx)
+    dt = 0.4 * dx / c_max / np.sqrt(nd)
+    amp = 1e12 if flavor == "rho_scaled" else 1.0
+    node = tuple(int(rng.integers(0, s)) for s in shape)
+    src = W.SourceSpec(node=node, amplitude=amp, frequency=0.05 / dt, cycles=2)
+    sens = list(dict.fromkeys(tuple(int(rng.integers(0, s)) for s in shape) for _ in range(7)))
+    meas = rng.normal(scale=1e-10 if flavor == "rho_scaled" else 1e-3,
+                      size=(1, len(sens), n_steps))
+    problem = W.FwiProblem(grid=grid, time=W.TimeConfig(n_steps, dt), material=mat, sources=[src],
+                           sensors=W.SensorArray(nodes=sens), measured=meas)
+    from paper_2509_15744_b200 import engine
+
+    ctx = engine.get_context(grid, W.precision_dtype(prec))
+    ctx.set_two_step(2)
+    try:
+        ctx.reset_stats()
+        k = 1e13 if flavor == "rho_scaled" else 1e3
+        res = W.gradient_superposed(problem, mat, W.SuperpositionConfig(k=k, precision=prec))
+        assert ctx.stats()["pair_launches"] > 0
+    finally:
+        ctx.set_two_step(1)
+    support = np.array([grid.flat_index(n) for n in sens], dtype=np.int64)
+    shots = [(O.Source(node, amp, 0.05 / dt, 2), O.FwiShot(support, meas[0], dt))]
+    cost, grad, _ = O.gradient_superposed(omat, dt, n_steps, shots, k, prec)
+    assert bits_equal(res.gradient, grad)
+    assert abs(res.cost - cost) <= COST_RTOL * abs(cost)

@@ -94,6 +94,11 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
  * stream, so the halo exchange of the new boundary planes (wo_halo_planes_out,
  * on any stream ordered after the boundary part) overlaps the interior. */
 #define WO_OPT_PLANE_PART 5
+/* WO_OPT_GRAPHS (default 1): a sweep whose launch sequence repeats (same
+ * range, sources, amplitudes, window state and context settings) is
+ * captured into a CUDA graph on its second occurrence and replayed from then
+ * on (launch-bound small grids gain most); 0 = always launch directly. */
+#define WO_OPT_GRAPHS 6
 int wo_set_option(wo_ctx* ctx, int option, int value);
 /* Device-resident optimisation loop (fwi.py:178-238 with
  * optim.py adam_step / clip_bounds): fp64 parameters (gamma), the Adam

@@ -58,6 +58,19 @@ struct wo_ctx {
     int use_two_step = 1;              // wo_set_option(WO_OPT_TWO_STEP)
     int num_sms = 148;                 // of the context's device
     int part = 0;                      // WO_OPT_PLANE_PART: 0 whole steps, 1 boundary, 2 interior
+    // CUDA graphs of whole sweeps (WO_OPT_GRAPHS): a sweep whose launch
+    // sequence repeats (same key: range, sources, amplitudes, window indices
+    // and the state generation) is captured on its second sighting and
+    // replayed from then on.  gen changes with every allocation and every
+    // setting that enters a kernel's parameters.
+    struct SweepGraph {
+        uint64_t key = 0, seen = 0;
+        cudaGraphExec_t exec = nullptr;
+        int cur = 0, prv = 0;
+        int64_t d_launches = 0, d_steps = 0, d_pairs = 0;
+    } graph[2];                        // forward, backward
+    int use_graphs = 1;
+    uint64_t gen = 1;
     int t2_geo = GEO_NONE;             // two-step tile geometry (set when its maps are built)
     int t2_state = 0;                  // two-step tensor maps: 0 not built, 1 ready, -1 no
     Tma2Maps t2maps;
@@ -159,6 +172,7 @@ struct wo_ctx {
 namespace {
 
 int dev_alloc(wo_ctx* ctx, void** p, size_t bytes) {
+    ++ctx->gen;   // parameters that hold device pointers may change
     if (bytes == 0) bytes = 16;
     cudaError_t e = cudaMalloc(p, bytes);
     if (e != cudaSuccess) {
@@ -305,6 +319,7 @@ bool tma_ready(wo_ctx* ctx) {
                            (uint64_t)ctx->kn0, PBX, BY);
             ctx->tmaps.lo = ctx->has_lo;
             if (ok) ctx->tma_state = 1;
+            ++ctx->gen;
         }
     }
     return ctx->tma_state == 1;
@@ -420,6 +435,59 @@ int launch_step_part(wo_ctx* ctx, StepSpec sp) {
     sp.c_lo = ctx->kn0 - 1;
     sp.c_hi = ctx->kn0;
     return launch_step<T>(ctx, sp);
+}
+
+// ---- CUDA graphs of repeated sweeps (see wo_ctx::SweepGraph) ----
+struct KeyHash {
+    uint64_t h = 1469598103934665603ull;   // FNV-1a
+    void bytes(const void* p, size_t n) {
+        const unsigned char* c = static_cast<const unsigned char*>(p);
+        for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ull;
+    }
+    template <typename V> void val(const V& v) { bytes(&v, sizeof(v)); }
+};
+
+// true: the sweep was replayed from its graph (the caller skips its loop)
+bool graph_replay(wo_ctx* ctx, int dir, uint64_t key) {
+    auto& g = ctx->graph[dir];
+    if (!g.exec || g.key != key) return false;
+    if (cudaGraphLaunch(g.exec, ctx->stream) != cudaSuccess) return false;
+    ctx->cur = g.cur;
+    ctx->prv = g.prv;
+    ctx->launches += g.d_launches;
+    ctx->step_launches += g.d_steps;
+    ctx->pair_launches += g.d_pairs;
+    return true;
+}
+
+// second sighting of a key: capture this sweep's launches
+bool graph_capture_begin(wo_ctx* ctx, int dir, uint64_t key) {
+    auto& g = ctx->graph[dir];
+    if (g.seen != key) {
+        g.seen = key;
+        return false;
+    }
+    return cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+}
+
+int graph_capture_end(wo_ctx* ctx, int dir, uint64_t key, int64_t l0, int64_t s0, int64_t p0) {
+    auto& g = ctx->graph[dir];
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamEndCapture(ctx->stream, &graph));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CK(e);
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.exec = exec;
+    g.key = key;
+    g.cur = ctx->cur;
+    g.prv = ctx->prv;
+    g.d_launches = ctx->launches - l0;
+    g.d_steps = ctx->step_launches - s0;
+    g.d_pairs = ctx->pair_launches - p0;
+    CK(cudaGraphLaunch(exec, ctx->stream));   // the captured work has not run yet
+    return WO_OK;
 }
 
 template <typename T>
@@ -557,6 +625,7 @@ bool pair_ready(wo_ctx* ctx) {
         ok &= make_map(&ctx->t2maps.a_ctr, ctx->acc, ctx->itemsize, ctx->kn2, ctx->kn1, np, tbx, tby);
         if (ok) {
             ctx->t2_state = 1;
+            ++ctx->gen;
             ctx->t2_geo = geo;
         }
     }
@@ -734,6 +803,26 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
     auto fcheck = [&](int64_t n) { return (n % STABILITY_CHECK_INTERVAL == 0) || (n == N - 1); };
     const bool pairs = ns <= MAX_SRC && !record && pair_ready(ctx);
     std::vector<double> vals2(std::max(ns, 1));
+    // graph of this sweep: the key covers everything the launches depend on
+    // beyond the state generation
+    const bool graphable = ctx->use_graphs && !ctx->prof && ctx->part == 0 && !record &&
+                           ns <= MAX_SRC && n_end - n_begin >= 8;
+    uint64_t gkey = 0;
+    bool capturing = false;
+    const int64_t l0 = ctx->launches, s0 = ctx->step_launches, p0 = ctx->pair_launches;
+    if (graphable) {
+        KeyHash kh;
+        kh.val(0); kh.val(N); kh.val(n_begin); kh.val(n_end); kh.val(flags); kh.val(dt);
+        kh.val(ctx->gen); kh.val(ctx->cur); kh.val(ctx->prv); kh.val(ns); kh.val(gather);
+        kh.val((int)sizeof(T));
+        for (int s = 0; s < ns; ++s) {
+            kh.val(sidx[s]);
+            kh.bytes(src_amp + (int64_t)spos[s] * N + n_begin, (size_t)(n_end - n_begin) * 8);
+        }
+        gkey = kh.h;
+        if (graph_replay(ctx, 0, gkey)) n_end = n_begin;   // loop skipped
+        else capturing = graph_capture_begin(ctx, 0, gkey);
+    }
     for (int64_t n = n_begin; n < n_end; ++n) {
         if (pairs && n + 1 < n_end) {   // steps n and n+1 in one pass
             PairSpec ps;
@@ -796,6 +885,10 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
         // after its interior part
         if (ctx->part != 1) std::swap(ctx->cur, ctx->prv);
     }
+    if (capturing) {
+        rc = graph_capture_end(ctx, 0, gkey, l0, s0, p0);
+        if (rc) return rc;
+    }
     if (ctx->part != 0) return WO_OK;   // split steps stay asynchronous
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->prof) harvest_events(ctx);
@@ -843,6 +936,20 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
     auto bcheck = [](int64_t n) { return (n % STABILITY_CHECK_INTERVAL == 0) || (n == 1); };
     const bool pairs = pair_ready(ctx);
     double val2 = 0.0;
+    const bool graphable = ctx->use_graphs && !ctx->prof && ctx->part == 0 && n_hi - n_lo >= 8;
+    uint64_t gkey = 0;
+    bool capturing = false;
+    const int64_t l0 = ctx->launches, s0 = ctx->step_launches, p0 = ctx->pair_launches;
+    if (graphable) {
+        KeyHash kh;
+        kh.val(1); kh.val(N); kh.val(n_hi); kh.val(n_lo); kh.val(inject); kh.val(accumulate);
+        kh.val(dt); kh.val(ctx->gen); kh.val(ctx->cur); kh.val(ctx->prv); kh.val(src_flat);
+        kh.val((int)sizeof(T));
+        if (src_flat >= 0) kh.bytes(src_amp + n_lo, (size_t)(n_hi - n_lo + 1) * 8);
+        gkey = kh.h;
+        if (graph_replay(ctx, 1, gkey)) n_hi = n_lo;   // loop skipped
+        else capturing = graph_capture_begin(ctx, 1, gkey);
+    }
     for (int64_t n = n_hi; n > n_lo; --n) {
         if (pairs && n - 1 > n_lo) {   // steps n and n-1 in one pass
             PairSpec ps;
@@ -882,6 +989,10 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
         rc = launch_step_part<T>(ctx, sp);
         if (rc) return rc;
         if (ctx->part != 1) std::swap(ctx->cur, ctx->prv);
+    }
+    if (capturing) {
+        rc = graph_capture_end(ctx, 1, gkey, l0, s0, p0);
+        if (rc) return rc;
     }
     if (ctx->part != 0) return WO_OK;   // split steps stay asynchronous
     CK(cudaStreamSynchronize(ctx->stream));
@@ -1185,6 +1296,7 @@ static int verify_fast_div_t(wo_ctx* ctx) {
     CK(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->fast_div = ok != 0;
+    ++ctx->gen;
     return WO_OK;
 }
 
@@ -1285,6 +1397,8 @@ void wo_destroy(wo_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     for (auto e : ctx->hev)
         if (e) cudaEventDestroy(e);
+    for (auto& g : ctx->graph)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     if (ctx->hstage) cudaFreeHost(ctx->hstage);
     for (auto e : ctx->ev_free) cudaEventDestroy(e);
     for (auto e : ctx->ev_used) cudaEventDestroy(e);
@@ -1311,6 +1425,7 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
     }
     ctx->material_set = true;
     ctx->mat4_valid = false;
+    ++ctx->gen;
     return verify_fast_div(ctx);
 }
 
@@ -1484,10 +1599,15 @@ int wo_opt_get(wo_ctx* ctx, double* params) {
 int wo_set_option(wo_ctx* ctx, int option, int value) {
     int rc = check_ctx(ctx);
     if (rc) return rc;
+    ++ctx->gen;
     REQUIRE(option == WO_OPT_FAST_DIV || option == WO_OPT_PAIR_KERNEL ||
                 option == WO_OPT_TMA_KERNEL || option == WO_OPT_TWO_STEP ||
-                option == WO_OPT_PLANE_PART,
+                option == WO_OPT_PLANE_PART || option == WO_OPT_GRAPHS,
             "unknown option");
+    if (option == WO_OPT_GRAPHS) {
+        ctx->use_graphs = value != 0;
+        return WO_OK;
+    }
     if (option == WO_OPT_PLANE_PART) {
         REQUIRE(value >= 0 && value <= 2, "plane part is 0, 1 or 2");
         ctx->part = value;
@@ -1519,6 +1639,7 @@ int wo_set_kernel_coefficients(wo_ctx* ctx, double cv, double cg, double inv2dt,
     int rc = check_ctx(ctx);
     if (rc) return rc;
     ctx->cv = cv; ctx->cg = cg; ctx->inv2dt = inv2dt; ctx->inv2dx = inv2dx;
+    ++ctx->gen;
     return WO_OK;
 }
 
@@ -1548,6 +1669,7 @@ int wo_set_support(wo_ctx* ctx, int64_t n_sup, const int64_t* flat) {
     CK(cudaMemcpy(ctx->mask, m.data(), words * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->prefix, p.data(), words * 4, cudaMemcpyHostToDevice));
     ctx->n_sup = n_sup;
+    ++ctx->gen;
     return WO_OK;
 }
 

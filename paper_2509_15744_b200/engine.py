@@ -359,6 +359,10 @@ class DeviceGrid:
         self._ck(fn(self.h, *[ctypes.byref(x) for x in p], ctypes.byref(pb)), "wo_halo_planes")
         return tuple(x.value for x in p), pb.value
 
+    def set_graphs(self, on):
+        """Replay repeated sweeps from captured CUDA graphs (default on)."""
+        self._ck(self.L.wo_set_option(self.h, N.WO_OPT_GRAPHS, int(bool(on))), "wo_set_option")
+
     def set_plane_part(self, part):
         """Split slab steps: 1 boundary planes, 2 interior (+rotation), 0 whole."""
         self._ck(self.L.wo_set_option(self.h, N.WO_OPT_PLANE_PART, int(part)), "wo_set_option")

@@ -1677,6 +1677,10 @@ int wo_reset_window(wo_ctx* ctx) {
     int rc = check_ctx(ctx);
     if (rc) return rc;
     const size_t ab = (size_t)ctx->alloc_cells() * ctx->itemsize;
+    // both levels are zeroed: restart the rotation at buffers (0, 1), so a
+    // repeated evaluation repeats its launch sequence exactly (sweep graphs)
+    ctx->cur = 0;
+    ctx->prv = 1;
     CK(cudaMemsetAsync(ctx->u[ctx->cur], 0, ab, ctx->stream));
     CK(cudaMemsetAsync(ctx->u[ctx->prv], 0, ab, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));

@@ -13,7 +13,7 @@ for name, make in (("C1", lambda: configs.fwi((256, 256), 3200)),
                    ("C2", lambda: configs.fwi((256, 256, 256), 1024))):
     problem, mat = make()
     for graphs in (False, True):
-        plan = G.SuperposedPlan(problem, mat, W.SuperpositionConfig(k=1e13)).upload()
+        plan = G.SuperposedPlan(problem, mat, W.SuperpositionConfig(k=1e13, precision="single")).upload()
         plan.ctx.set_graphs(graphs)
         ref = None
         for _ in range(3):

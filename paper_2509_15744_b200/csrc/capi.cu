@@ -1275,8 +1275,12 @@ int create_common(wo_ctx* ctx) {
 // (ghost planes included).
 template <typename T>
 static int verify_fast_div_t(wo_ctx* ctx) {
+    const bool before = ctx->fast_div;   // selects the kernel variant (sweep graphs)
     ctx->fast_div = false;
-    if (!ctx->allow_fast_div) return WO_OK;
+    if (!ctx->allow_fast_div) {
+        if (before) ++ctx->gen;
+        return WO_OK;
+    }
     int rc = ensure(ctx, &ctx->flag, &ctx->flag_bytes, sizeof(int));
     if (rc) return rc;
     int* d_ok = reinterpret_cast<int*>(ctx->flag);
@@ -1296,7 +1300,7 @@ static int verify_fast_div_t(wo_ctx* ctx) {
     CK(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->fast_div = ok != 0;
-    ++ctx->gen;
+    if (ctx->fast_div != before) ++ctx->gen;
     return WO_OK;
 }
 
@@ -1411,6 +1415,11 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
     int rc = check_ctx(ctx);
     if (rc) return rc;
     REQUIRE(flavor == WO_RHO_SCALED || flavor == WO_ACOUSTIC, "unknown material flavor");
+    // the scalars enter kernel parameters (sweep graphs); gamma is data
+    const bool same = ctx->material_set && ctx->flavor == flavor && ctx->rho0 == rho0 &&
+                      ctx->rho1 == rho1 && ctx->kappa1 == kappa1 && ctx->rho2 == rho2 &&
+                      ctx->kappa2 == kappa2 && ctx->dt_mat == dt && ctx->ratio2 == ratio2;
+    if (!same) ++ctx->gen;
     ctx->flavor = flavor;
     ctx->rho0 = rho0; ctx->rho1 = rho1; ctx->kappa1 = kappa1;
     ctx->rho2 = rho2; ctx->kappa2 = kappa2; ctx->dt_mat = dt; ctx->ratio2 = ratio2;
@@ -1425,7 +1434,6 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
     }
     ctx->material_set = true;
     ctx->mat4_valid = false;
-    ++ctx->gen;
     return verify_fast_div(ctx);
 }
 

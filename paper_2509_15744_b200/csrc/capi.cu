@@ -61,8 +61,9 @@ struct wo_ctx {
     // CUDA graphs of whole sweeps (WO_OPT_GRAPHS): a sweep whose launch
     // sequence repeats (same key: range, sources, amplitudes, window indices
     // and the state generation) is captured on its second sighting and
-    // replayed from then on.  gen changes with every allocation and every
-    // setting that enters a kernel's parameters.
+    // replayed from then on.  The key hashes the parameter buffers' addresses
+    // and gen, which changes with every setting that enters a kernel's
+    // parameters (material scalars, coefficients, support, options, maps).
     struct SweepGraph {
         uint64_t key = 0, seen = 0;
         cudaGraphExec_t exec = nullptr;
@@ -172,7 +173,6 @@ struct wo_ctx {
 namespace {
 
 int dev_alloc(wo_ctx* ctx, void** p, size_t bytes) {
-    ++ctx->gen;   // parameters that hold device pointers may change
     if (bytes == 0) bytes = 16;
     cudaError_t e = cudaMalloc(p, bytes);
     if (e != cudaSuccess) {
@@ -446,6 +446,13 @@ struct KeyHash {
     }
     template <typename V> void val(const V& v) { bytes(&v, sizeof(v)); }
 };
+
+// the device buffers a sweep's kernel parameters point into
+void hash_param_buffers(KeyHash& kh, const wo_ctx* ctx) {
+    for (auto* b : ctx->u) kh.val(b);
+    kh.val(ctx->gamma); kh.val(ctx->acc); kh.val(ctx->mat4); kh.val(ctx->store);
+    kh.val(ctx->maxslots); kh.val(ctx->mask); kh.val(ctx->prefix);
+}
 
 // true: the sweep was replayed from its graph (the caller skips its loop)
 bool graph_replay(wo_ctx* ctx, int dir, uint64_t key) {
@@ -815,6 +822,7 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
         kh.val(0); kh.val(N); kh.val(n_begin); kh.val(n_end); kh.val(flags); kh.val(dt);
         kh.val(ctx->gen); kh.val(ctx->cur); kh.val(ctx->prv); kh.val(ns); kh.val(gather);
         kh.val((int)sizeof(T));
+        hash_param_buffers(kh, ctx);
         for (int s = 0; s < ns; ++s) {
             kh.val(sidx[s]);
             kh.bytes(src_amp + (int64_t)spos[s] * N + n_begin, (size_t)(n_end - n_begin) * 8);
@@ -945,6 +953,7 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
         kh.val(1); kh.val(N); kh.val(n_hi); kh.val(n_lo); kh.val(inject); kh.val(accumulate);
         kh.val(dt); kh.val(ctx->gen); kh.val(ctx->cur); kh.val(ctx->prv); kh.val(src_flat);
         kh.val((int)sizeof(T));
+        hash_param_buffers(kh, ctx);
         if (src_flat >= 0) kh.bytes(src_amp + n_lo, (size_t)(n_hi - n_lo + 1) * 8);
         gkey = kh.h;
         if (graph_replay(ctx, 1, gkey)) n_hi = n_lo;   // loop skipped

@@ -71,8 +71,8 @@ def tato(shape, n_steps):
 
 def rate(problem, mat, prec, reps=3):
     plan = G.SuperposedPlan(problem, mat, W.SuperpositionConfig(k=1e13, precision=prec)).upload()
-    plan.run()
-    plan.run()   # the second identical evaluation captures the sweep graphs
+    for _ in range(3):   # a repeated evaluation captures its sweep graphs
+        plan.run()
     ctx = plan.ctx
     ctx.synchronize()
     ctx.reset_stats()

@@ -279,3 +279,42 @@ def test_two_step_random_cases(W, seed):
     cost, grad, _ = O.gradient_superposed(omat, dt, n_steps, shots, k, prec)
     assert bits_equal(res.gradient, grad)
     assert abs(res.cost - cost) <= COST_RTOL * abs(cost)
+
+
+# ------------------------------------------------ sweep graphs (WO_OPT_GRAPHS)
+@pytest.mark.parametrize("shape", [(40, 8, 64), (64, 128), (33, 64)])
+def test_sweep_graph_replay_matches_direct_launches(W, shape):
+    """Repeated evaluations replay captured sweep graphs; a new gamma (same
+    scalars: data, graph kept), new measured data, a new k and a new source
+    frequency (new key: recapture) must all give the direct-launch bits."""
+    from paper_2509_15744_b200 import engine
+
+    problem, mat, _, _, _ = _problem(W, shape, "rho_scaled", 40, 11)
+    problem = W.FwiProblem(grid=problem.grid, time=problem.time, material=mat,
+                           sources=problem.sources[:1], sensors=problem.sensors,
+                           measured=problem.measured[:1])
+    ctx = engine.get_context(problem.grid, np.float32)
+    cfg = W.SuperpositionConfig(k=1e13, precision="single")
+
+    def both(prob, m, c):
+        ctx.set_graphs(False)
+        ref = W.gradient_superposed(prob, m, c)
+        ctx.set_graphs(True)
+        got = [W.gradient_superposed(prob, m, c) for _ in range(3)]   # capture, replay
+        for g in got:
+            assert bits_equal(g.gradient, ref.gradient)
+            assert g.cost == ref.cost
+
+    both(problem, mat, cfg)
+    rng = np.random.default_rng(3)
+    mat2 = mat.with_gamma(np.asarray(mat.gamma) * rng.uniform(0.8, 1.0, size=problem.grid.shape))
+    both(problem, mat2, cfg)
+    problem.measured = problem.measured * 1.5
+    both(problem, mat2, cfg)
+    both(problem, mat2, W.SuperpositionConfig(k=1e11, precision="single"))
+    s0 = problem.sources[0]
+    p3 = W.FwiProblem(grid=problem.grid, time=problem.time, material=mat2,
+                      sources=[W.SourceSpec(node=s0.node, amplitude=s0.amplitude,
+                                            frequency=s0.frequency * 1.3, cycles=2)],
+                      sensors=problem.sensors, measured=problem.measured)
+    both(p3, mat2, cfg)

@@ -639,10 +639,14 @@ bool pair_ready(wo_ctx* ctx) {
     return ctx->t2_state == 1;
 }
 
-// planes per CTA of a two-step pass: whole waves of resident CTAs matter
-// more than chunk length (a 1.73-wave grid idles a quarter of the last
-// wave), and each chunk recomputes ~1 extra step-n plane.  Cost model:
-// waves(nz) * (planes per chunk + 1); WB_T2_NZ overrides (tuning runs).
+// planes per CTA of a two-step pass.  Measured: a grid that fits in ONE wave
+// of resident CTAs runs its CTAs in lockstep (all loading, then all
+// computing) and is ~1.35x slower per plane than the same work spread over
+// two or more waves, whose staggered CTAs overlap memory and compute (192^3:
+// 106 vs 79 us per pass; 256^3 with 384 CTAs: 267 vs 137 us); partial last
+// waves idle slots, and each chunk recomputes ~1 extra plane.  Model: at
+// least ~2 waves of work when the grid allows it, then the fewest
+// waves x (planes + 1).  WB_T2_NZ overrides (tuning runs).
 int choose_chunk2(const wo_ctx* ctx) {
     const int tbx = ctx->t2_geo == GEO_TALL ? GeoTall::TBX : GeoWide::TBX;
     const int tby = ctx->t2_geo == GEO_TALL ? GeoTall::TBY : GeoWide::TBY;
@@ -656,8 +660,12 @@ int choose_chunk2(const wo_ctx* ctx) {
         best_nz = forced;
     } else {
         const int slots = ctx->num_sms * (ctx->itemsize == 4 ? 3 : 1);
+        const int nz_max = std::min(ctx->kn0, 64);
+        const double min_work = 1.9 * slots;   // CTAs for ~2 waves
+        const bool can_stagger = (double)tiles * nz_max >= min_work;
         double best = 1e30;
-        for (int nz = 1; nz <= std::min(ctx->kn0, 64); ++nz) {
+        for (int nz = 1; nz <= nz_max; ++nz) {
+            if (can_stagger && (double)tiles * nz < min_work) continue;
             const int chunk = (ctx->kn0 + nz - 1) / nz;
             const int waves = (tiles * nz + slots - 1) / slots;
             const double cost = (double)waves * (chunk + 1);

@@ -218,6 +218,11 @@ MatScalars<T> mat_scalars(const wo_ctx* ctx) {
 }
 
 int choose_chunk(const wo_ctx* ctx) {
+    static const int forced = [] {   // WB_T1_CHUNK: tuning runs
+        const char* e = getenv("WB_T1_CHUNK");
+        return e ? atoi(e) : 0;
+    }();
+    if (forced > 0) return std::min(forced, std::max(ctx->kn0, 1));
     const int tiles = ((ctx->kn2 + BX - 1) / BX) * ((ctx->kn1 + BY - 1) / BY);
     const int target = 148 * 8;  // CTAs in flight we aim to offer per launch
     int nz = std::max(1, target / std::max(1, tiles));

@@ -217,18 +217,31 @@ MatScalars<T> mat_scalars(const wo_ctx* ctx) {
     return M;
 }
 
-int choose_chunk(const wo_ctx* ctx) {
+// planes per CTA of a single-step launch (tile width tw, per_sm resident
+// CTAs): the same model as choose_chunk2 — about two waves or more so CTAs
+// do not run in lockstep (fp64 256^3: 148 us/step at 4.8 waves vs 185 at
+// one), then the fewest waves x (planes + 1).  WB_T1_CHUNK overrides.
+int choose_chunk(const wo_ctx* ctx, int tw, int per_sm) {
     static const int forced = [] {   // WB_T1_CHUNK: tuning runs
         const char* e = getenv("WB_T1_CHUNK");
         return e ? atoi(e) : 0;
     }();
     if (forced > 0) return std::min(forced, std::max(ctx->kn0, 1));
-    const int tiles = ((ctx->kn2 + BX - 1) / BX) * ((ctx->kn1 + BY - 1) / BY);
-    const int target = 148 * 8;  // CTAs in flight we aim to offer per launch
-    int nz = std::max(1, target / std::max(1, tiles));
-    int chunk = (ctx->kn0 + nz - 1) / nz;
-    chunk = std::max(chunk, std::min(ctx->kn0, 16));
-    return std::max(chunk, 1);
+    const int tiles = ((ctx->kn2 + tw - 1) / tw) * ((ctx->kn1 + BY - 1) / BY);
+    const int slots = ctx->num_sms * per_sm;
+    const int nz_max = std::min(ctx->kn0, 128);
+    const double min_work = 1.9 * slots;
+    const bool can_stagger = (double)tiles * nz_max >= min_work;
+    int best_nz = 1;
+    double best = 1e30;
+    for (int nz = 1; nz <= nz_max; ++nz) {
+        if (can_stagger && (double)tiles * nz < min_work) continue;
+        const int chunk = (ctx->kn0 + nz - 1) / nz;
+        const int waves = (int)(((int64_t)tiles * nz + slots - 1) / slots);
+        const double cost = (double)waves * (chunk + 1);
+        if (cost < best - 1e-9) { best = cost; best_nz = nz; }
+    }
+    return std::max(1, (ctx->kn0 + best_nz - 1) / best_nz);
 }
 
 cudaEvent_t take_event(wo_ctx* ctx) {
@@ -362,7 +375,6 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     a.n2 = ctx->kn2;
     a.i_lo = ctx->has_lo ? -1 : 0;
     a.i_hi = ctx->kn0 + ctx->has_hi;
-    a.chunk = choose_chunk(ctx);
     a.c_lo = sp.c_lo;
     a.c_hi = sp.c_hi < 0 ? ctx->kn0 : std::min(sp.c_hi, ctx->kn0);
     if (a.c_hi <= a.c_lo) return WO_OK;   // empty part
@@ -403,6 +415,7 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     const bool tma = ctx->use_tma && ctx->use_pair && !sp.prev && !sp.cur && !sp.out &&
                      !sp.hist && tma_ready(ctx);
     const bool pair = tma || ((ctx->kn2 % 2 == 0) && ctx->use_pair);
+    a.chunk = choose_chunk(ctx, pair ? PBX : BX, tma ? (ctx->itemsize == 4 ? 4 : 2) : 8);
     dim3 block(pair ? 32 : BX, BY, 1);
     dim3 grid(pair ? (ctx->kn2 + PBX - 1) / PBX : (ctx->kn2 + BX - 1) / BX,
               (ctx->kn1 + BY - 1) / BY, (a.c_hi - a.c_lo + a.chunk - 1) / a.chunk);

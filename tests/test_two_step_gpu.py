@@ -318,3 +318,21 @@ def test_sweep_graph_replay_matches_direct_launches(W, shape):
                                             frequency=s0.frequency * 1.3, cycles=2)],
                       sensors=problem.sensors, measured=problem.measured)
     both(p3, mat2, cfg)
+
+
+@pytest.mark.parametrize("nz", [1, 2, 3])
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_two_step_long_chunks(W, nz, prec):
+    """Chunks of 15-45 planes per CTA (several TMA-ring wraps, the mbarrier
+    parities, the chunk-end plane through the ring): the size model picks
+    such chunks only on large grids, so force them (WB_T2_NZ, read once per
+    process) in a subprocess."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, WB_T2_NZ=str(nz))
+    out = subprocess.run([sys.executable, os.path.join(here, "_long_chunk_case.py"), prec],
+                         env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr

@@ -51,9 +51,6 @@ namespace wb {
 #ifndef WB_T2_NEXT_PREFETCH
 #define WB_T2_NEXT_PREFETCH 1
 #endif
-#ifndef WB_T2_STAGGER_NS
-#define WB_T2_STAGGER_NS 0
-#endif
 constexpr int T2_THREADS = 128;
 constexpr int T2_NS = WB_T2_STAGES;  // TMA ring stages
 constexpr int T2_PF = WB_T2_PREFETCH;   // L2 prefetch distance beyond the ring (planes)
@@ -271,14 +268,6 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         for (int s = 0; s < T2_NS; ++s) mbar_init(&bar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-#if WB_T2_STAGGER_NS
-    // first-wave CTAs start at three phase offsets so the co-resident CTAs of
-    // an SM do not all load (then all compute) in lockstep
-    {
-        const int lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-        if (lin < a.resident && (lin % 3)) __nanosleep((unsigned)(lin % 3) * WB_T2_STAGGER_NS);
-    }
-#endif
     __syncthreads();
     if (tid == T2_PRODUCER) {
         for (int s = 0; s < T2_NS && pbeg + s <= plast; ++s) issue(pbeg + s, s);

@@ -151,6 +151,8 @@ class DeviceGrid:
 
     def _ck(self, rc, what):
         if rc:
+            if not self.h:
+                raise DeviceError(f"{what}: context is closed")
             _raise(self.h, rc, what)
 
     def _field(self, a):
@@ -470,6 +472,9 @@ def get_context(grid: Grid, dtype, device=0) -> DeviceGrid:
     """Cached DeviceGrid per (shape, dx, dtype, device)."""
     key = (grid.shape, float(grid.dx), np.dtype(dtype).str, device)
     ctx = _CACHE.get(key)
+    if ctx is not None and not ctx.h:      # closed by its user: replace it
+        del _CACHE[key]
+        ctx = None
     if ctx is None:
         while len(_CACHE) >= _CACHE_MAX:
             _, old = _CACHE.popitem(last=False)

@@ -111,6 +111,22 @@ def test_gradient_superposed_bitexact(W, golden, name, prec):
     assert res.counter.peak_fields == 4
 
 
+def test_closed_pooled_context_is_replaced(W, golden):
+    """A user closing the cached context of a grid does not poison later
+    evaluations on that grid; a closed handle raises DeviceError."""
+    from paper_2509_15744_b200 import engine
+
+    g = golden("fwi3d")
+    c = cases.fwi3d_case()
+    problem, mat = product_fwi_problem(W, c, g["gamma_model"], g["measured"])
+    ctx = engine.get_context(problem.grid, np.float64)
+    ctx.close()
+    with pytest.raises(engine.DeviceError, match="closed"):
+        ctx.set_material(mat, problem.time.dt)
+    res = W.gradient_superposed(problem, mat, W.SuperpositionConfig(k=c["k"], precision="double"))
+    assert bits_equal(res.gradient, g["sup_grad_double"])
+
+
 @pytest.mark.parametrize("prec", ["double", "single"])
 def test_division_paths_agree(W, golden, prec):
     """The verified branch-free division path is active on the desk material

@@ -720,6 +720,7 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     a.n0 = ctx->kn0; a.n1 = ctx->kn1; a.n2 = ctx->kn2;
     a.chunk = choose_chunk2(ctx);
     a.resident = ctx->num_sms * (ctx->itemsize == 4 ? 3 : 1);
+    a.negz = 0x8000000080000000ull;   // (-0.0f, -0.0f): packed fp32 products
     a.mat = mat_scalars<T>(ctx);
     a.cv = (T)ctx->cv; a.cg = (T)ctx->cg; a.inv2dt = (T)ctx->inv2dt; a.inv2dx = (T)ctx->inv2dx;
     a.sdt = (T)sp.sdt;

@@ -51,7 +51,44 @@ namespace wb {
 #ifndef WB_T2_NEXT_PREFETCH
 #define WB_T2_NEXT_PREFETCH 1
 #endif
+#ifndef WB_T2_PACKED
+#define WB_T2_PACKED 1
+#endif
 constexpr int T2_THREADS = 128;
+
+// Packed fp32 pairs (sm_100a FADD2 / FFMA2): the two cells of a thread's row
+// run the same IEEE operation sequence, so one f32x2 instruction computes
+// both with the bits of two scalar ones.  Products are fma(a, b, z) with z =
+// (-0, -0) from a kernel argument: exact a*b (one rounding, signed zeros and
+// subnormals as mul.rn) that ptxas cannot contract with the following add
+// (it does contract a mul.rn.f32x2 + add.rn.f32x2 pair, unlike scalar mul.rn).
+using f2x = unsigned long long;
+__device__ __forceinline__ f2x pk2(float lo, float hi) {
+    f2x r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ f2x pk2(float2 v) { return pk2(v.x, v.y); }
+__device__ __forceinline__ float2 upk2(f2x r) {
+    float2 o;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+    return o;
+}
+__device__ __forceinline__ f2x add2(f2x a, f2x b) {
+    f2x r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2x sub2(f2x a, f2x b) {
+    f2x r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2x mul2(f2x a, f2x b, f2x negz) {
+    f2x r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(negz));
+    return r;
+}
 constexpr int T2_NS = WB_T2_STAGES;  // TMA ring stages
 constexpr int T2_PF = WB_T2_PREFETCH;   // L2 prefetch distance beyond the ring (planes)
 constexpr int T2_PRODUCER = 32;      // thread issuing TMA (warp 0 carries the extra ring cells)
@@ -97,6 +134,7 @@ template <typename T> struct Step2Args {
     int check1, check2;
     typename FTraits<T>::Bits* max1;
     typename FTraits<T>::Bits* max2;
+    unsigned long long negz;   // (-0.0f, -0.0f) bits, opaque to ptxas (packed fp32 products)
 };
 
 struct Tma2Maps {
@@ -309,6 +347,33 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         const T g2 = (ukp - ukm) * a.inv2dx;
         return accv + a.sdt * ((a.cv * va) * va + a.cg * (((g0 * g0) + (g1 * g1)) + (g2 * g2)));
     };
+    // the same two sequences on packed fp32 pairs (cells k, k+1 of a row)
+    constexpr bool PK = WB_T2_PACKED && std::is_same<T, float>::value;
+    const f2x NZ = a.negz;
+    auto cell2 = [&](f2x u0, f2x up1, f2x um1, f2x ujp, f2x ujm, f2x ukp, f2x ukm, f2x w0hi,
+                     f2x w0lo, f2x fjhi, f2x fjlo, f2x fkhi, f2x fklo, f2x coef, f2x up) {
+        f2x s = sub2(u0, u0);
+        s = add2(s, mul2(sub2(up1, u0), w0hi, NZ));
+        s = sub2(s, mul2(sub2(u0, um1), w0lo, NZ));
+        s = add2(s, mul2(sub2(ujp, u0), fjhi, NZ));
+        s = sub2(s, mul2(sub2(u0, ujm), fjlo, NZ));
+        s = add2(s, mul2(sub2(ukp, u0), fkhi, NZ));
+        s = sub2(s, mul2(sub2(u0, ukm), fklo, NZ));
+        return add2(sub2(add2(u0, u0), up), mul2(coef, s, NZ));
+    };
+    auto kinc2 = [&](f2x accv, f2x out, f2x up, f2x up1, f2x um1, f2x ujp, f2x ujm, f2x ukp,
+                     f2x ukm) {
+        const f2x i2dt = pk2((float)a.inv2dt, (float)a.inv2dt);
+        const f2x i2dx = pk2((float)a.inv2dx, (float)a.inv2dx);
+        const f2x va = mul2(sub2(out, up), i2dt, NZ);
+        const f2x g0 = mul2(sub2(up1, um1), i2dx, NZ);
+        const f2x g1 = mul2(sub2(ujp, ujm), i2dx, NZ);
+        const f2x g2 = mul2(sub2(ukp, ukm), i2dx, NZ);
+        const f2x cv = pk2((float)a.cv, (float)a.cv), cg = pk2((float)a.cg, (float)a.cg);
+        const f2x sdt = pk2((float)a.sdt, (float)a.sdt);
+        const f2x gg = add2(add2(mul2(g0, g0, NZ), mul2(g1, g1, NZ)), mul2(g2, g2, NZ));
+        return add2(accv, mul2(sdt, add2(mul2(mul2(cv, va, NZ), va, NZ), mul2(cg, gg, NZ)), NZ));
+    };
     // nodal force coefficient of a cell from its gamma (sparse; solver.py:98,110)
     auto fcoef = [&](int flat) {
         const T g = __ldg(a.gamma + flat);
@@ -402,6 +467,32 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         const V xu = ldv(Xq + oU), xd = ldv(Xq + oD);
         const T xLa = Xq[oA - dL], xRa = Xq[oA + 1 + dR], xLb = Xq[oB - dL], xRb = Xq[oB + 1 + dR];
         V o2a, o2b;
+        if constexpr (PK) {
+            const f2x kpa = pk2(x_0a.y, xRa), kma = pk2(xLa, x_0a.x);
+            const f2x kpb = pk2(x_0b.y, xRb), kmb = pk2(xLb, x_0b.x);
+            const f2x ra = cell2(pk2(x_0a), pk2(xp_a), pk2(x_m1a), pk2(x_0b), pk2(xu), kpa, kma,
+                                 pk2(w1hi_a), pk2(w1lo_a), pk2(f1_jab), pk2(f1_jlo),
+                                 pk2(f1_kIa, f1_kRa), pk2(f1_kLa, f1_kIa), pk2(c1_a), pk2(un1_a));
+            const f2x rb = cell2(pk2(x_0b), pk2(xp_b), pk2(x_m1b), pk2(xd), pk2(x_0a), kpb, kmb,
+                                 pk2(w1hi_b), pk2(w1lo_b), pk2(f1_jhi), pk2(f1_jab),
+                                 pk2(f1_kIb, f1_kRb), pk2(f1_kLb, f1_kIb), pk2(c1_b), pk2(un1_b));
+            o2a = upk2(ra);
+            o2b = upk2(rb);
+            tile_inject(q1, o2a, o2b, x_0a, x_0b, a.src_val2, a.row2, true);
+            const int oc = q1 * plane + cofs;
+            if (ACC) {
+                const f2x fa = kinc2(pk2(acc1_a), pk2(o2a), pk2(un1_a), pk2(xp_a), pk2(x_m1a),
+                                     pk2(x_0b), pk2(xu), kpa, kma);
+                const f2x fb = kinc2(pk2(acc1_b), pk2(o2b), pk2(un1_b), pk2(xp_b), pk2(x_m1b),
+                                     pk2(xd), pk2(x_0a), kpb, kmb);
+                stg(a.acc + oc, upk2(fa));
+                stg(a.acc + oc + n2, upk2(fb));
+            }
+            stg(a.out1 + oc, x_0a);
+            stg(a.out1 + oc + n2, x_0b);
+            stg(a.out2 + oc, o2a);
+            stg(a.out2 + oc + n2, o2b);
+        } else {
         o2a.x = cell(x_0a.x, xp_a.x, x_m1a.x, x_0b.x, xu.x, x_0a.y, xLa, w1hi_a.x, w1lo_a.x,
                      f1_jab.x, f1_jlo.x, f1_kIa, f1_kLa, c1_a.x, un1_a.x);
         o2a.y = cell(x_0a.y, xp_a.y, x_m1a.y, x_0b.y, xu.y, xRa, x_0a.x, w1hi_a.y, w1lo_a.y,
@@ -425,6 +516,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         stg(a.out1 + oc + n2, x_0b);
         stg(a.out2 + oc, o2a);
         stg(a.out2 + oc + n2, o2b);
+        }
         if (a.check2) {
             Bits m1 = Tr::abs_bits(o2a.x), m2 = Tr::abs_bits(o2a.y);
             Bits m3 = Tr::abs_bits(o2b.x), m4 = Tr::abs_bits(o2b.y);
@@ -471,6 +563,17 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         const T uLa = SU[oA - dL], uRa = SU[oA + 1 + dR], uLb = SU[oB - dL], uRb = SU[oB + 1 + dR];
         const V pa = ldv(SP + oA), pb = ldv(SP + oB);
         V oa, ob;
+        f2x kpa = 0, kma = 0, kpb = 0, kmb = 0;
+        if constexpr (PK) {
+            kpa = pk2(un0_a.y, uRa); kma = pk2(uLa, un0_a.x);
+            kpb = pk2(un0_b.y, uRb); kmb = pk2(uLb, un0_b.x);
+            oa = upk2(cell2(pk2(un0_a), pk2(unp_a), pk2(unm_a), pk2(un0_b), pk2(uu), kpa, kma,
+                            pk2(wh_a), pk2(w0_a), pk2(jab), pk2(jlo), pk2(fka), pk2(kLa, fka.x),
+                            pk2(cf_a), pk2(pa)));
+            ob = upk2(cell2(pk2(un0_b), pk2(unp_b), pk2(unm_b), pk2(ud), pk2(un0_a), kpb, kmb,
+                            pk2(wh_b), pk2(w0_b), pk2(jhi), pk2(jab), pk2(fkb), pk2(kLb, fkb.x),
+                            pk2(cf_b), pk2(pb)));
+        } else {
         oa.x = cell(un0_a.x, unp_a.x, unm_a.x, un0_b.x, uu.x, un0_a.y, uLa, wh_a.x, w0_a.x,
                     jab.x, jlo.x, fka.x, kLa, cf_a.x, pa.x);
         oa.y = cell(un0_a.y, unp_a.y, unm_a.y, un0_b.y, uu.y, uRa, un0_a.x, wh_a.y, w0_a.y,
@@ -479,6 +582,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
                     jhi.x, jab.x, fkb.x, kLb, cf_b.x, pb.x);
         ob.y = cell(un0_b.y, unp_b.y, unm_b.y, ud.y, un0_a.y, uRb, un0_b.x, wh_b.y, w0_b.y,
                     jhi.y, jab.y, fkb.y, fkb.x, cf_b.y, pb.y);
+        }
         const bool own_plane = p >= i0 && p < i1;
         tile_inject(p, oa, ob, un0_a, un0_b, a.src_val1, a.row1, own_plane);
         stv(Xc + oA, oa);
@@ -487,10 +591,17 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         if (own_plane) {
             if (ACC) {
                 const V aa = ldv(&S.A[2 * ty][2 * tx]), ab = ldv(&S.A[2 * ty + 1][2 * tx]);
+                if constexpr (PK) {
+                    nacc_a = upk2(kinc2(pk2(aa), pk2(oa), pk2(pa), pk2(unp_a), pk2(unm_a),
+                                        pk2(un0_b), pk2(uu), kpa, kma));
+                    nacc_b = upk2(kinc2(pk2(ab), pk2(ob), pk2(pb), pk2(unp_b), pk2(unm_b),
+                                        pk2(ud), pk2(un0_a), kpb, kmb));
+                } else {
                 nacc_a.x = kinc(aa.x, oa.x, pa.x, unp_a.x, unm_a.x, un0_b.x, uu.x, un0_a.y, uLa);
                 nacc_a.y = kinc(aa.y, oa.y, pa.y, unp_a.y, unm_a.y, un0_b.y, uu.y, uRa, un0_a.x);
                 nacc_b.x = kinc(ab.x, ob.x, pb.x, unp_b.x, unm_b.x, ud.x, un0_a.x, un0_b.y, uLb);
                 nacc_b.y = kinc(ab.y, ob.y, pb.y, unp_b.y, unm_b.y, ud.y, un0_a.y, uRb, un0_b.x);
+                }
             }
             if (a.check1) {
                 Bits m1 = Tr::abs_bits(oa.x), m2 = Tr::abs_bits(oa.y);

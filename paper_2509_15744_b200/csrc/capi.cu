@@ -751,10 +751,36 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     const int tbx = ctx->t2_geo == GEO_TALL ? GeoTall::TBX : GeoWide::TBX;
     const int tby = ctx->t2_geo == GEO_TALL ? GeoTall::TBY : GeoWide::TBY;
     dim3 grid(ctx->kn2 / tbx, ctx->kn1 / tby, (ctx->kn0 + a.chunk - 1) / a.chunk);
+#if WB_T2_TIMELINE
+    // dev builds: the WB_T2_TL_CALL-th pair launch writes its CTA timeline
+    // (header: grid x, y, z, chunk; then start, first data, end, smid per CTA)
+    // to WB_T2_TL_FILE (profiles/dev/cta_timeline.py)
+    static unsigned long long* d_tl = nullptr;
+    static int tl_calls = 0;
+    const size_t nblk = (size_t)grid.x * grid.y * grid.z;
+    if (!d_tl) cudaMalloc(&d_tl, (size_t)32 << 20);
+    a.timeline = nblk <= (1u << 20) ? d_tl : nullptr;
+#endif
     prof_begin(ctx, 1);
     launch_step2_engine<T>(StepSel{ctx->flavor, true, sp.acc, false, sup}, ctx->t2_geo, grid,
                            ctx->stream, a, ctx->t2maps);
     prof_end(ctx);
+#if WB_T2_TIMELINE
+    {
+        const char* want = getenv("WB_T2_TL_CALL");
+        const char* path = getenv("WB_T2_TL_FILE");
+        if (++tl_calls == (want ? atoi(want) : -1) && path && a.timeline) {
+            std::vector<unsigned long long> h(4 * nblk + 4);
+            h[0] = grid.x; h[1] = grid.y; h[2] = grid.z; h[3] = (unsigned long long)a.chunk;
+            cudaStreamSynchronize(ctx->stream);
+            cudaMemcpy(h.data() + 4, d_tl, 4 * 8 * nblk, cudaMemcpyDeviceToHost);
+            if (FILE* f = fopen(path, "wb")) {
+                fwrite(h.data(), 8, h.size(), f);
+                fclose(f);
+            }
+        }
+    }
+#endif
     ctx->launches++;
     ctx->step_launches++;
     ctx->pair_launches++;

@@ -51,6 +51,9 @@ namespace wb {
 #ifndef WB_T2_NEXT_PREFETCH
 #define WB_T2_NEXT_PREFETCH 1
 #endif
+#ifndef WB_T2_TIMELINE
+#define WB_T2_TIMELINE 0   // dev: per-CTA start / first data / end times (launch_pair dump)
+#endif
 #ifndef WB_T2_PACKED
 #define WB_T2_PACKED 1
 #endif
@@ -135,7 +138,14 @@ template <typename T> struct Step2Args {
     typename FTraits<T>::Bits* max1;
     typename FTraits<T>::Bits* max2;
     unsigned long long negz;   // (-0.0f, -0.0f) bits, opaque to ptxas (packed fp32 products)
+    unsigned long long* timeline;   // WB_T2_TIMELINE builds only: 4 words per CTA
 };
+
+__device__ __forceinline__ unsigned long long wb_globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 struct Tma2Maps {
     CUtensorMap u_r2[4];   // level buffers, (W, R2) boxes at (k0-HO, j0-2)
@@ -209,6 +219,9 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
 
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = ty * G::TX + tx;
+#if WB_T2_TIMELINE
+    const unsigned long long tl_start = wb_globaltimer();
+#endif
     // blocks: tiles fastest, then chunks (a chunk-fastest order measured 4%
     // slower: neighbouring tiles at the same planes share halos through L2)
     const int k0 = blockIdx.x * TBX, j0 = blockIdx.y * TBY;
@@ -443,6 +456,9 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
             }
     }
     mbar_wait(&bar[0], 0u);
+#if WB_T2_TIMELINE
+    const unsigned long long tl_data = wb_globaltimer();
+#endif
     V un0_a = ldv(&st[0].U[0][0] + oA), un0_b = ldv(&st[0].U[0][0] + oB);
     T run0[2];
 #pragma unroll
@@ -680,6 +696,15 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     // pfin = n0-1 = i1-1 and plane n0 mirrors the plane itself (X(pfin) was
     // published by the last plane's barrier)
     if (pfin == i1 - 1) step2_tile(pfin, Xb + ((pfin - pbeg) % T2_NX) * PL, x_0a, x_0b);
+#if WB_T2_TIMELINE
+    if (tid == 0 && a.timeline) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        unsigned long long* t = a.timeline +
+            4ull * (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
+        t[0] = tl_start; t[1] = tl_data; t[2] = wb_globaltimer(); t[3] = smid;
+    }
+#endif
 
     if (a.check1 || a.check2) {
         for (int o = 16; o > 0; o >>= 1) {

@@ -1230,6 +1230,14 @@ int misfit_t(wo_ctx* ctx, int64_t N, int kind, const double* measured, double c1
 constexpr size_t HSTAGE_HALF = 8u << 20;
 
 int download_field(wo_ctx* ctx, void* out, const char* dev, size_t bytes) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
+        // page-locked destination: one DMA, no staging
+        CK(cudaMemcpyAsync(out, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        return WO_OK;
+    }
+    (void)cudaGetLastError();
     if (!ctx->hstage) {
         CK(cudaHostAlloc((void**)&ctx->hstage, 2 * HSTAGE_HALF, cudaHostAllocDefault));
         for (auto& e : ctx->hev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

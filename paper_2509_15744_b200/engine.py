@@ -273,8 +273,15 @@ class DeviceGrid:
     def zero_accumulator(self):
         self._ck(self.L.wo_zero_accumulator(self.h), "wo_zero_accumulator")
 
-    def get_accumulator(self):
-        out = np.empty(self.grid.shape, self.dtype)
+    def get_accumulator(self, out=None):
+        """The accumulator as a host array (into ``out``, a C-contiguous array
+        of the grid's shape and dtype, when given)."""
+        if out is None:
+            out = np.empty(self.grid.shape, self.dtype)
+        elif (out.shape != self.grid.shape or out.dtype != self.dtype
+              or not out.flags.c_contiguous):
+            raise ConfigError("accumulator output must be a C-contiguous "
+                              f"{self.grid.shape} {np.dtype(self.dtype).name} array")
         self._ck(self.L.wo_get_accumulator(self.h, N.ptr(out)), "wo_get_accumulator")
         return out
 

@@ -111,6 +111,35 @@ def test_gradient_superposed_bitexact(W, golden, name, prec):
     assert res.counter.peak_fields == 4
 
 
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_gradient_download_pinned_and_pageable(W, golden, prec):
+    """The accumulator downloads identically into a page-locked array (one
+    DMA), a fresh pageable array (staged copy) and the plan's pre-faulted
+    output; a wrong output array is refused."""
+    import torch
+
+    from paper_2509_15744_b200 import engine
+    from paper_2509_15744_b200 import gradients as G
+
+    g = golden("fwi3d")
+    c = cases.fwi3d_case()
+    problem, mat = product_fwi_problem(W, c, g["gamma_model"], g["measured"])
+    plan = G.SuperposedPlan(problem, mat, W.SuperpositionConfig(k=c["k"], precision=prec))
+    plan.upload()
+    plan.run()
+    dt = np.float32 if prec == "single" else np.float64
+    tdt = torch.float32 if prec == "single" else torch.float64
+    pinned = torch.empty(problem.grid.shape, dtype=tdt, pin_memory=True).numpy()
+    plan.ctx.get_accumulator(pinned)
+    pageable = plan.ctx.get_accumulator()
+    via_plan = plan.download()
+    assert bits_equal(pinned, g[f"sup_grad_{prec}"])
+    assert bits_equal(pageable, pinned) and bits_equal(via_plan, pinned)
+    with pytest.raises(W.ConfigError):
+        plan.ctx.get_accumulator(np.empty(problem.grid.shape, np.float16 if dt == np.float32
+                                          else np.float32))
+
+
 def test_closed_pooled_context_is_replaced(W, golden):
     """A user closing the cached context of a grid does not poison later
     evaluations on that grid; a closed handle raises DeviceError."""

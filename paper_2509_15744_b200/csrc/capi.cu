@@ -693,6 +693,41 @@ int choose_chunk2(const wo_ctx* ctx) {
     return std::max(1, (ctx->kn0 + best_nz - 1) / best_nz);
 }
 
+// z layers of a two-step launch: boundaries zb[0..nz] (returns nz).  Uniform
+// chunks of choose_chunk2 unless WB_T2_LAYERS="len x count,..." (tuning
+// runs; layers in launch order, lengths must sum to n0).
+int choose_layers2(const wo_ctx* ctx, int* zb) {
+    static const std::string spec = [] {
+        const char* e = getenv("WB_T2_LAYERS");
+        return std::string(e ? e : "");
+    }();
+    const int n0 = ctx->kn0;
+    if (!spec.empty()) {
+        int nz = 0, pos = 0;
+        zb[0] = 0;
+        size_t i = 0;
+        bool ok = true;
+        while (ok && i < spec.size()) {
+            int len = 0, cnt = 0;
+            if (sscanf(spec.c_str() + i, "%dx%d", &len, &cnt) != 2 || len < 1 || cnt < 1) ok = false;
+            for (int c = 0; ok && c < cnt; ++c) {
+                if (nz >= T2_MAXZ) { ok = false; break; }
+                pos += len;
+                zb[++nz] = pos;
+            }
+            const size_t comma = spec.find(',', i);
+            i = comma == std::string::npos ? spec.size() : comma + 1;
+        }
+        if (ok && pos == n0) return nz;
+    }
+    const int chunk = choose_chunk2(ctx);
+    int nz = 0;
+    zb[0] = 0;
+    for (int p = 0; p < n0 && nz < T2_MAXZ; p += chunk) zb[++nz] = std::min(p + chunk, n0);
+    zb[nz] = n0;
+    return nz;
+}
+
 struct PairSpec {
     bool acc = false, check1 = false, check2 = false;
     double sdt = 0.0;
@@ -718,7 +753,9 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     a.out2 = reinterpret_cast<T*>(ctx->base0(ctx->u[x[1]]));
     a.acc = reinterpret_cast<T*>(ctx->acc);
     a.n0 = ctx->kn0; a.n1 = ctx->kn1; a.n2 = ctx->kn2;
-    a.chunk = choose_chunk2(ctx);
+    const int nz = choose_layers2(ctx, a.zb);
+    a.chunk = 0;
+    for (int z = 0; z < nz; ++z) a.chunk = std::max(a.chunk, a.zb[z + 1] - a.zb[z]);
     a.resident = ctx->num_sms * (ctx->itemsize == 4 ? 3 : 1);
     a.negz = 0x8000000080000000ull;   // (-0.0f, -0.0f): packed fp32 products
     a.mat = mat_scalars<T>(ctx);
@@ -750,7 +787,7 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     ctx->t2maps.cur = ctx->cur;
     const int tbx = ctx->t2_geo == GEO_TALL ? GeoTall::TBX : GeoWide::TBX;
     const int tby = ctx->t2_geo == GEO_TALL ? GeoTall::TBY : GeoWide::TBY;
-    dim3 grid(ctx->kn2 / tbx, ctx->kn1 / tby, (ctx->kn0 + a.chunk - 1) / a.chunk);
+    dim3 grid(ctx->kn2 / tbx, ctx->kn1 / tby, nz);
 #if WB_T2_TIMELINE
     // dev builds: the WB_T2_TL_CALL-th pair launch writes its CTA timeline
     // (header: grid x, y, z, chunk; then start, first data, end, smid per CTA)

@@ -58,6 +58,7 @@ namespace wb {
 #define WB_T2_PACKED 1
 #endif
 constexpr int T2_THREADS = 128;
+constexpr int T2_MAXZ = 64;          // z layers (chunks along axis 0) per launch
 
 // Packed fp32 pairs (sm_100a FADD2 / FFMA2): the two cells of a thread's row
 // run the same IEEE operation sequence, so one f32x2 instruction computes
@@ -123,6 +124,7 @@ template <typename T> struct Step2Args {
     T* out2;           // u^{n+2}
     T* acc;
     int n0, n1, n2, chunk;
+    int zb[T2_MAXZ + 1];   // plane boundaries of the z layers (blockIdx.z); chunk = longest
     int resident;      // CTAs resident at once (3 per SM; 0: no next-block prefetch)
     MatScalars<T> mat;
     T cv, cg, inv2dt, inv2dx, sdt;
@@ -228,8 +230,8 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     const int kA = k0 + 2 * tx, ja = j0 + 2 * ty;
     const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
     const int plane = n1 * n2;
-    const int i0 = blockIdx.z * a.chunk;
-    const int i1 = min(i0 + a.chunk, n0);
+    const int i0 = a.zb[blockIdx.z];
+    const int i1 = a.zb[blockIdx.z + 1];
     const int pbeg = max(i0 - 1, 0);           // step-n planes of this chunk
     const int pfin = min(i1, n0 - 1);
     // planes streamed through the ring: pbeg .. pfin, plus pfin+1 (u^n of the
@@ -302,7 +304,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     if (has_next) {
         nk0 = (nblk % gridDim.x) * TBX;
         nj0 = ((nblk / gridDim.x) % gridDim.y) * TBY;
-        npb = max((nblk / (gridDim.x * gridDim.y)) * a.chunk - 1, 0);
+        npb = max(a.zb[nblk / (gridDim.x * gridDim.y)] - 1, 0);
     }
     auto issue = [&](int p, int s) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -320,19 +320,22 @@ def test_sweep_graph_replay_matches_direct_launches(W, shape):
     both(p3, mat2, cfg)
 
 
-@pytest.mark.parametrize("nz", [1, 2, 3])
+@pytest.mark.parametrize("knob", [("WB_T2_NZ", "1"), ("WB_T2_NZ", "2"), ("WB_T2_NZ", "3"),
+                                  ("WB_T2_LAYERS", "20x1,5x3,10x1"),
+                                  ("WB_T2_LAYERS", "1x1,2x1,42x1")])
 @pytest.mark.parametrize("prec", ["single", "double"])
-def test_two_step_long_chunks(W, nz, prec):
+def test_two_step_long_chunks(W, knob, prec):
     """Chunks of 15-45 planes per CTA (several TMA-ring wraps, the mbarrier
-    parities, the chunk-end plane through the ring): the size model picks
-    such chunks only on large grids, so force them (WB_T2_NZ, read once per
-    process) in a subprocess."""
+    parities, the chunk-end plane through the ring) and uneven z layers down
+    to one plane: the size model picks such chunks only on large grids, so
+    force them (WB_T2_NZ / WB_T2_LAYERS, read once per process) in a
+    subprocess."""
     import os
     import subprocess
     import sys
 
     here = os.path.dirname(os.path.abspath(__file__))
-    env = dict(os.environ, WB_T2_NZ=str(nz))
+    env = dict(os.environ, **{knob[0]: knob[1]})
     out = subprocess.run([sys.executable, os.path.join(here, "_long_chunk_case.py"), prec],
                          env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr

@@ -677,7 +677,7 @@ int choose_chunk2(const wo_ctx* ctx) {
     if (forced > 0) {
         best_nz = forced;
     } else {
-        const int slots = ctx->num_sms * (ctx->itemsize == 4 ? 3 : 1);
+        const int slots = ctx->num_sms * (ctx->itemsize == 4 ? T2_CTAS_F32 : 1);
         const int nz_max = std::min(ctx->kn0, 64);
         const double min_work = 1.9 * slots;   // CTAs for ~2 waves
         const bool can_stagger = (double)tiles * nz_max >= min_work;
@@ -756,7 +756,7 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     const int nz = choose_layers2(ctx, a.zb);
     a.chunk = 0;
     for (int z = 0; z < nz; ++z) a.chunk = std::max(a.chunk, a.zb[z + 1] - a.zb[z]);
-    a.resident = ctx->num_sms * (ctx->itemsize == 4 ? 3 : 1);
+    a.resident = ctx->num_sms * (ctx->itemsize == 4 ? T2_CTAS_F32 : 1);
     a.negz = 0x8000000080000000ull;   // (-0.0f, -0.0f): packed fp32 products
     a.mat = mat_scalars<T>(ctx);
     a.cv = (T)ctx->cv; a.cg = (T)ctx->cg; a.inv2dt = (T)ctx->inv2dt; a.inv2dx = (T)ctx->inv2dx;

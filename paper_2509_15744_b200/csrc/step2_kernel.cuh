@@ -57,7 +57,11 @@ namespace wb {
 #ifndef WB_T2_PACKED
 #define WB_T2_PACKED 1
 #endif
+#ifndef WB_T2_CTAS
+#define WB_T2_CTAS 3
+#endif
 constexpr int T2_THREADS = 128;
+constexpr int T2_CTAS_F32 = WB_T2_CTAS;   // resident fp32 CTAs per SM (fp64: 1)
 constexpr int T2_MAXZ = 64;          // z layers (chunks along axis 0) per launch
 
 // Packed fp32 pairs (sm_100a FADD2 / FFMA2): the two cells of a thread's row
@@ -202,7 +206,7 @@ __global__ void material4_kernel(const T* __restrict__ gamma, MatScalars<T> M, i
 }
 
 template <typename T, typename G, int FLAVOR, bool ACC, int SUP>
-__global__ void __launch_bounds__(T2_THREADS, sizeof(T) == 4 ? 3 : 1)
+__global__ void __launch_bounds__(T2_THREADS, sizeof(T) == 4 ? T2_CTAS_F32 : 1)
 step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__ Tma2Maps maps) {
     using Tr = FTraits<T>;
     using MP = Mat<T, FLAVOR, false>;   // sparse force coefficients only

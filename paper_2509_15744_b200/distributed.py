@@ -35,7 +35,6 @@ import math
 
 import numpy as np
 
-from . import _native as N
 from . import engine
 from .engine import SolverInstabilityError, source_amplitude_table
 from .grids import ConfigError, precision_dtype

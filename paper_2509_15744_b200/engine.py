@@ -14,7 +14,7 @@ from collections import OrderedDict
 import numpy as np
 
 from . import _native as N
-from .grids import ACOUSTIC, RHO_SCALED, ConfigError, Grid, MaterialModel
+from .grids import RHO_SCALED, ConfigError, Grid, MaterialModel
 
 
 class SolverInstabilityError(RuntimeError):

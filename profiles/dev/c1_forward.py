@@ -1,4 +1,4 @@
-import os, sys, time
+import os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np
 import paper_2509_15744_b200 as W

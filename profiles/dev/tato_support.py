@@ -8,7 +8,6 @@ sys.path.insert(0, os.path.join(ROOT, "profiles"))
 import numpy as np  # noqa: E402
 
 import configs  # noqa: E402
-import paper_2509_15744_b200 as W  # noqa: E402
 from paper_2509_15744_b200 import engine  # noqa: E402
 
 N = 200

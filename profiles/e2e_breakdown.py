@@ -6,8 +6,6 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
-
 import bench  # noqa: E402
 import paper_2509_15744_b200 as W  # noqa: E402
 from paper_2509_15744_b200 import gradients as G  # noqa: E402

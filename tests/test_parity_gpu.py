@@ -7,8 +7,7 @@ import numpy as np
 import pytest
 
 import cases
-from helpers import (bits_equal, oracle_fwi_shots, oracle_material, oracle_tato_shots,
-                     product_fwi_problem, product_tato_problem, rel_l2)
+from helpers import bits_equal, product_fwi_problem, product_tato_problem, rel_l2
 from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu

@@ -1129,9 +1129,7 @@ int sweep_adjoint_reference_t(wo_ctx* ctx, int64_t N, double dt, int64_t* fail_s
     CK(cudaMemsetAsync(ctx->maxslots, 0, (size_t)(N + 2) * 8, ctx->stream));
     char* lv[3] = {ctx->uprev(), ctx->ucur(), ctx->u3};   // (prev, cur, next)
     for (char* p : lv) CK(cudaMemsetAsync(p, 0, ctx->field_bytes(), ctx->stream));
-    int n0, n1, n2;
-    n0 = ctx->kn0; n1 = ctx->kn1; n2 = ctx->kn2;
-    const size_t fb = ctx->field_bytes();
+    const int n0 = ctx->kn0, n1 = ctx->kn1, n2 = ctx->kn2;
     for (int64_t n = N - 1; n >= 1; --n) {
         StepSpec sp;
         sp.check = (n % STABILITY_CHECK_INTERVAL == 0) || (n == 1);
@@ -1157,7 +1155,6 @@ int sweep_adjoint_reference_t(wo_ctx* ctx, int64_t N, double dt, int64_t* fail_s
         lv[1] = lv[2];
         lv[2] = t;
     }
-    (void)fb;
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->prof) harvest_events(ctx);
     std::vector<char> hs((size_t)(N + 2) * 8);

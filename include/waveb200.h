@@ -202,6 +202,23 @@ int wo_halo_planes_out(wo_ctx* ctx, void** first, void** last, void** ghost_lo, 
 void* wo_stream(wo_ctx* ctx);
 /* wo_exchange_local for the level a split step is writing. */
 int wo_exchange_local_out(wo_ctx* lower, wo_ctx* upper);
+/* Peer ghost stores (replaces the exchange; the reference has no multi-GPU
+ * path — solver.py:128-151 steps one array).  wo_slab_ghosts returns this
+ * slab's ghost planes in each of its 4 level buffers (NULL when absent) and
+ * the device addresses of its two incoming flags (bumped by the lower /
+ * upper neighbour).  wo_slab_peers hands a slab its neighbours' addresses:
+ * lo_ghost[4] = the lower neighbour's HIGH ghost planes, hi_ghost[4] = the
+ * upper neighbour's LOW ghost planes, lo_flag = the lower neighbour's flag
+ * [1], hi_flag = the upper neighbour's flag [0] (all NULL: off).  Then every
+ * split step's part 1 waits (on its stream) for its own flags to reach the
+ * neighbours' previous step, stores the new boundary planes into both its
+ * own buffer and the neighbour's ghost plane (NVLink stores when the
+ * neighbour is on another GPU; IPC-mapped addresses across processes), and
+ * bumps the neighbours' flags: no copy or collective per step.  Set up every
+ * slab before stepping any; whole steps (part 0) are refused meanwhile. */
+int wo_slab_ghosts(wo_ctx* ctx, void** ghost_lo, void** ghost_hi, void** flags);
+int wo_slab_peers(wo_ctx* ctx, void* const* lo_ghost, void* const* hi_ghost, void* lo_flag,
+                  void* hi_flag);
 
 /* Standard-adjoint sweep of gradient_reference (gradients.py:371-386) using
  * the recorded history and the unscaled compact adjoint store; accumulates

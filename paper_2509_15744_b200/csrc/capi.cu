@@ -58,6 +58,16 @@ struct wo_ctx {
     int use_two_step = 1;              // wo_set_option(WO_OPT_TWO_STEP)
     int num_sms = 148;                 // of the context's device
     int part = 0;                      // WO_OPT_PLANE_PART: 0 whole steps, 1 boundary, 2 interior
+    // peer ghost stores (wo_slab_peers): the boundary launches of part 1 also
+    // store their plane into the neighbour's ghost plane (same level buffer
+    // index: slabs step in lockstep) and then bump the neighbour's flag
+    char* peer_lo[4] = {nullptr, nullptr, nullptr, nullptr};   // lower's high ghost
+    char* peer_hi[4] = {nullptr, nullptr, nullptr, nullptr};   // upper's low ghost
+    unsigned int* peer_lo_flag = nullptr;   // lower's in_flags[1]
+    unsigned int* peer_hi_flag = nullptr;   // upper's in_flags[0]
+    unsigned int* in_flags = nullptr;       // [2]: bumped by the lower / upper neighbour
+    unsigned int p2p_seq = 0;               // part-1 launches done (flag value)
+    bool p2p = false;
     // CUDA graphs of whole sweeps (WO_OPT_GRAPHS): a sweep whose launch
     // sequence repeats (same key: range, sources, amplitudes, window indices
     // and the state generation) is captured on its second sighting and
@@ -300,6 +310,30 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
     return fn;
 }
 
+int cu_fail(wo_ctx* ctx, const char* msg) {
+    ctx->err = msg;
+    return WO_ERR_CUDA;
+}
+
+// stream memory operations (flag wait / write between slab neighbours)
+typedef CUresult (*PfnStreamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PfnStreamValue32 stream_value_fn(const char* name) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+        return reinterpret_cast<PfnStreamValue32>(p);
+    return nullptr;
+}
+PfnStreamValue32 wait_value32() {
+    static PfnStreamValue32 fn = stream_value_fn("cuStreamWaitValue32");
+    return fn;
+}
+PfnStreamValue32 write_value32() {
+    static PfnStreamValue32 fn = stream_value_fn("cuStreamWriteValue32");
+    return fn;
+}
+
 bool make_map(CUtensorMap* m, void* base, int itemsize, uint64_t n2, uint64_t n1, uint64_t np,
               uint32_t bw, uint32_t bh) {
     auto enc = tma_encoder();
@@ -435,17 +469,62 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     return WO_OK;
 }
 
+// part 1 with peer ghost stores: wait until both neighbours finished their
+// previous part 1 (our ghost planes hold their new planes, and they no longer
+// read the ghost slot we are about to overwrite), compute plane 0 / n0-1 with
+// a second store of the result into the neighbour's ghost plane (hist_out,
+// offset so that plane p lands on the ghost plane), then bump the
+// neighbours' flags (stream write with its memory barrier: the stores are
+// visible first).  No copy, no collective; the interior (part 2) overlaps.
+template <typename T>
+int launch_boundary_p2p(wo_ctx* ctx, StepSpec sp) {
+    REQUIRE(!sp.out && !sp.hist && !sp.prev && !sp.cur, "peer ghost stores need in-place steps");
+    auto wait = wait_value32();
+    auto write = write_value32();
+    REQUIRE(wait && write, "stream memory operations unavailable");
+    REQUIRE(ctx->kn0 >= 2, "peer ghost stores need slabs of at least two planes");
+    const size_t pb = (size_t)ctx->plane() * ctx->itemsize;
+    const unsigned seq = ctx->p2p_seq;
+    if (ctx->has_lo && ctx->peer_lo[0] &&
+        wait((CUstream)ctx->stream, (CUdeviceptr)(ctx->in_flags + 0), seq, CU_STREAM_WAIT_VALUE_GEQ))
+        return cu_fail(ctx, "cuStreamWaitValue32 failed");
+    if (ctx->has_hi && ctx->peer_hi[0] &&
+        wait((CUstream)ctx->stream, (CUdeviceptr)(ctx->in_flags + 1), seq, CU_STREAM_WAIT_VALUE_GEQ))
+        return cu_fail(ctx, "cuStreamWaitValue32 failed");
+    const int b = ctx->prv;   // the level this step writes (in place over u^{n-1})
+    for (int side = 0; side < 2; ++side) {
+        const int p = side == 0 ? 0 : ctx->kn0 - 1;
+        char* peer = side == 0 ? ctx->peer_lo[b] : ctx->peer_hi[b];
+        StepSpec s2 = sp;
+        s2.c_lo = p;
+        s2.c_hi = p + 1;
+        s2.hist = peer ? peer - (size_t)p * pb : nullptr;
+        int rc = launch_step<T>(ctx, s2);
+        if (rc) return rc;
+    }
+    ctx->p2p_seq = seq + 1;
+    if (ctx->peer_lo_flag &&
+        write((CUstream)ctx->stream, (CUdeviceptr)ctx->peer_lo_flag, seq + 1, CU_STREAM_WRITE_VALUE_DEFAULT))
+        return cu_fail(ctx, "cuStreamWriteValue32 failed");
+    if (ctx->peer_hi_flag &&
+        write((CUstream)ctx->stream, (CUdeviceptr)ctx->peer_hi_flag, seq + 1, CU_STREAM_WRITE_VALUE_DEFAULT))
+        return cu_fail(ctx, "cuStreamWriteValue32 failed");
+    return WO_OK;
+}
+
 // one step of a slab split for halo overlap (wo_set_option WO_OPT_PLANE_PART):
 // part 1 computes the boundary planes 0 and n0-1 (whose new values the
 // neighbours need), part 2 the interior; part 0 everything
 template <typename T>
 int launch_step_part(wo_ctx* ctx, StepSpec sp) {
+    REQUIRE(!(ctx->p2p && ctx->part == 0), "peer ghost stores run split steps (WO_OPT_PLANE_PART)");
     if (ctx->part == 0) return launch_step<T>(ctx, sp);
     if (ctx->part == 2) {
         sp.c_lo = 1;
         sp.c_hi = ctx->kn0 - 1;
         return launch_step<T>(ctx, sp);
     }
+    if (ctx->p2p) return launch_boundary_p2p<T>(ctx, sp);
     sp.c_lo = 0;
     sp.c_hi = 1;
     int rc = launch_step<T>(ctx, sp);
@@ -1495,7 +1574,7 @@ void wo_destroy(wo_ctx* ctx) {
     void* bufs[] = {ctx->gamma, ctx->u[0], ctx->u[1], ctx->u[2], ctx->u[3], ctx->mat4, ctx->stage,
                     ctx->snap, ctx->scratch, ctx->opt, ctx->opt_frozen, ctx->opt_partial,
                     ctx->dsn, ctx->dmask, ctx->dfp_off, ctx->dfp_w,
-                    ctx->flag, ctx->acc,
+                    ctx->flag, ctx->acc, reinterpret_cast<char*>(ctx->in_flags),
                     ctx->mask, ctx->prefix,
                     ctx->store, ctx->measured, ctx->partial, ctx->cost, ctx->maxslots,
                     ctx->f_idx, ctx->f_vals, ctx->f_dense, ctx->hist, ctx->u3};
@@ -1946,6 +2025,68 @@ int wo_halo_planes(wo_ctx* ctx, void** first, void** last, void** ghost_lo, void
     *ghost_lo = ctx->has_lo ? c - pb : nullptr;
     *ghost_hi = ctx->has_hi ? c + (size_t)ctx->kn0 * pb : nullptr;
     *plane_bytes = (int64_t)pb;
+    return WO_OK;
+}
+
+int wo_slab_ghosts(wo_ctx* ctx, void** ghost_lo, void** ghost_hi, void** flags) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(ctx->has_lo || ctx->has_hi, "not a slab context");
+    if (!ctx->in_flags) {
+        rc = dev_alloc(ctx, (void**)&ctx->in_flags, 2 * sizeof(unsigned int));
+        if (rc) return rc;
+        CK(cudaMemset(ctx->in_flags, 0, 2 * sizeof(unsigned int)));
+    }
+    const size_t pb = (size_t)ctx->plane() * ctx->itemsize;
+    for (int b = 0; b < 4; ++b) {
+        char* u = ctx->u[b];
+        ghost_lo[b] = u && ctx->has_lo ? u : nullptr;
+        ghost_hi[b] = u && ctx->has_hi ? u + (size_t)(ctx->has_lo + ctx->kn0) * pb : nullptr;
+    }
+    flags[0] = ctx->in_flags;
+    flags[1] = ctx->in_flags + 1;
+    return WO_OK;
+}
+
+int wo_slab_peers(wo_ctx* ctx, void* const* lo_ghost, void* const* hi_ghost, void* lo_flag,
+                  void* hi_flag) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    bool any = false;
+    for (int b = 0; b < 4; ++b) {
+        ctx->peer_lo[b] = ctx->has_lo && lo_ghost ? static_cast<char*>(lo_ghost[b]) : nullptr;
+        ctx->peer_hi[b] = ctx->has_hi && hi_ghost ? static_cast<char*>(hi_ghost[b]) : nullptr;
+        any |= ctx->peer_lo[b] || ctx->peer_hi[b];
+    }
+    ctx->peer_lo_flag = ctx->has_lo ? static_cast<unsigned int*>(lo_flag) : nullptr;
+    ctx->peer_hi_flag = ctx->has_hi ? static_cast<unsigned int*>(hi_flag) : nullptr;
+    REQUIRE(!any || ((!ctx->has_lo || (ctx->peer_lo[0] && ctx->peer_lo[1] && ctx->peer_lo_flag)) &&
+                     (!ctx->has_hi || (ctx->peer_hi[0] && ctx->peer_hi[1] && ctx->peer_hi_flag))),
+            "peer ghost stores need both level buffers and the flag of every neighbour");
+    // stores into another GPU's memory need peer access from this device
+    const void* ptrs[4] = {ctx->peer_lo[0], ctx->peer_hi[0], ctx->peer_lo_flag, ctx->peer_hi_flag};
+    for (const void* q : ptrs) {
+        if (!q) continue;
+        cudaPointerAttributes pa{};
+        CK(cudaPointerGetAttributes(&pa, q));
+        if (pa.type == cudaMemoryTypeDevice && pa.device != ctx->device) {
+            const cudaError_t e = cudaDeviceEnablePeerAccess(pa.device, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+            else CK(e);
+        }
+    }
+    if (any) {   // fresh sequence on every slab before any step (set up all slabs first)
+        if (!ctx->in_flags) {
+            rc = dev_alloc(ctx, (void**)&ctx->in_flags, 2 * sizeof(unsigned int));
+            if (rc) return rc;
+        }
+        CK(cudaMemset(ctx->in_flags, 0, 2 * sizeof(unsigned int)));
+    }
+    ctx->p2p_seq = 0;
+    ctx->p2p = any;
+    ++ctx->gen;
     return WO_OK;
 }
 

@@ -14,6 +14,10 @@ slab decomposition (SlabGradient)
     NCCL is ordered on the context's stream, no host synchronisation):
       * ``LoopbackHalo`` — all slabs in one process (same device or peer
         devices), ``wo_exchange_local`` copies;
+      * ``PeerHalo`` — all slabs in one process, no exchange at all: the
+        boundary launches store their planes straight into the neighbours'
+        ghost planes (NVLink stores between GPUs) and signal them with a
+        device flag the neighbour's stream waits on (``wo_slab_peers``);
       * ``TorchHalo`` — one slab per process (torchrun), torch.distributed
         point-to-point send/recv of the plane tensors (NCCL over NVLink on
         GPUs; the same code runs on gloo/CPU tensors in the tests).
@@ -166,6 +170,31 @@ class LoopbackHalo:
         return x
 
 
+class PeerHalo(LoopbackHalo):
+    """All slabs in this process; the step kernels store the boundary planes
+    into the neighbours' ghost planes and bump their flags (split steps
+    only), so begin / end have nothing left to move."""
+
+    def __init__(self, ctxs):
+        super().__init__(ctxs)
+        ghosts = [c.slab_ghosts() for c in ctxs]
+        for i, c in enumerate(ctxs):
+            lo = ghosts[i - 1] if i > 0 else None          # (ghost_lo, ghost_hi, flags)
+            hi = ghosts[i + 1] if i + 1 < len(ctxs) else None
+            c.set_slab_peers(lo_ghost=lo[1] if lo else None, hi_ghost=hi[0] if hi else None,
+                             lo_flag=lo[2][1] if lo else 0, hi_flag=hi[2][0] if hi else 0)
+
+    def exchange(self):
+        raise ConfigError("PeerHalo moves planes inside split steps (overlap=True)")
+
+    def begin(self):
+        return []
+
+    def close(self):
+        for c in self.ctxs:
+            c.set_slab_peers()
+
+
 class TorchHalo:
     """One slab per process; neighbours are ranks r-1 and r+1."""
 
@@ -245,7 +274,14 @@ class SlabGradient:
         self.slabs = list(slabs)
         self.ctxs = [engine.DeviceGrid(grid, self.dtype, d, slab=s)
                      for s, d in zip(self.slabs, devices)]
-        self.halo = LoopbackHalo(self.ctxs) if halo == "loopback" else halo
+        if halo == "peer" and not overlap:
+            raise ConfigError("peer ghost stores run split steps (overlap=True)")
+        if halo == "loopback":
+            self.halo = LoopbackHalo(self.ctxs)
+        elif halo == "peer":
+            self.halo = PeerHalo(self.ctxs)
+        else:
+            self.halo = halo
         # overlap: every step runs as boundary planes -> halo exchange started
         # -> interior planes -> exchange awaited, so the transfer of the new
         # boundary planes overlaps the interior update (WO_OPT_PLANE_PART)
@@ -350,16 +386,19 @@ class SlabGradient:
         return np.concatenate([c.get_accumulator() for c in self.ctxs], axis=0)
 
     def close(self):
+        if hasattr(self.halo, "close"):
+            self.halo.close()
         for c in self.ctxs:
             c.close()
 
 
-def gradient_superposed_slabs(problem, material, config, parts, devices=None, overlap=True):
+def gradient_superposed_slabs(problem, material, config, parts, devices=None, overlap=True,
+                              halo="loopback"):
     """Single-process slab-decomposed gradient (loopback / peer halo)."""
     from .gradients import GradientResult, BufferCounter
 
     sg = SlabGradient(problem, material, config, slab_ranges(problem.grid.shape[0], parts),
-                      devices, overlap=overlap).upload()
+                      devices, halo=halo, overlap=overlap).upload()
     try:
         cost = sg.run()
         grad = sg.download()

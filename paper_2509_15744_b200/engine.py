@@ -368,6 +368,21 @@ class DeviceGrid:
         self._ck(fn(self.h, *[ctypes.byref(x) for x in p], ctypes.byref(pb)), "wo_halo_planes")
         return tuple(x.value for x in p), pb.value
 
+    def slab_ghosts(self):
+        """(ghost_lo[4], ghost_hi[4], flags[2]) device addresses of this
+        slab's ghost planes per level buffer and of its incoming flags."""
+        lo = (ctypes.c_void_p * 4)()
+        hi = (ctypes.c_void_p * 4)()
+        fl = (ctypes.c_void_p * 2)()
+        self._ck(self.L.wo_slab_ghosts(self.h, lo, hi, fl), "wo_slab_ghosts")
+        return [x or 0 for x in lo], [x or 0 for x in hi], [x or 0 for x in fl]
+
+    def set_slab_peers(self, lo_ghost=None, hi_ghost=None, lo_flag=0, hi_flag=0):
+        """Peer ghost stores (wo_slab_peers); no arguments: off."""
+        arr = lambda v: None if v is None else (ctypes.c_void_p * 4)(*[x or None for x in v])
+        self._ck(self.L.wo_slab_peers(self.h, arr(lo_ghost), arr(hi_ghost), lo_flag or None,
+                                      hi_flag or None), "wo_slab_peers")
+
     def set_graphs(self, on):
         """Replay repeated sweeps from captured CUDA graphs (default on)."""
         self._ck(self.L.wo_set_option(self.h, N.WO_OPT_GRAPHS, int(bool(on))), "wo_set_option")

@@ -8,6 +8,7 @@ Times one superposed gradient (fp32, rho-scaled 3D FWI, one shot) as
   slabsO  `parts` slab contexts on this GPU, loopback halo, split
           boundary/interior steps (the overlapped NCCL schedule)
   slabsW  the same with whole steps then the exchange
+  slabsP  split steps with peer ghost stores + device flags (no exchange)
 Host wall clock around a synchronised run (slabs use one stream each).
 On one GPU the slabs run one after the other, so slabsO/slabsW vs mono1 is
 the price of the decomposition itself (split launches, ghost planes, the
@@ -58,8 +59,10 @@ def main():
         ms = timed(plan.run, plan.ctx.synchronize, args.reps)
         rows[name] = ms
         plan.ctx.set_two_step(1)        # pooled context: restore the default
-    for name, overlap in (("slabsO", True), ("slabsW", False)):
-        sg = SlabGradient(problem, mat, cfg, slab_ranges(n, args.parts), overlap=overlap).upload()
+    for name, overlap, halo in (("slabsO", True, "loopback"), ("slabsW", False, "loopback"),
+                                ("slabsP", True, "peer")):
+        sg = SlabGradient(problem, mat, cfg, slab_ranges(n, args.parts), overlap=overlap,
+                          halo=halo).upload()
 
         def sync(sg=sg):
             for c in sg.ctxs:
@@ -71,7 +74,7 @@ def main():
            "ms": {k: round(v, 2) for k, v in rows.items()},
            "gcell_upd_s": {k: round(upd / v / 1e6, 1) for k, v in rows.items()},
            "slab_overhead_vs_mono1": {k: round(rows[k] / rows["mono1"] - 1, 3)
-                                      for k in ("slabsO", "slabsW")}}
+                                      for k in ("slabsO", "slabsW", "slabsP")}}
     print(json.dumps(out))
 
 

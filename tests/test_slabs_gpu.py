@@ -54,6 +54,28 @@ def test_slabs_bitwise_equal_single_gpu(W, shape, parts, prec, overlap):
     assert abs(got.cost - ref.cost) <= 1e-13 * abs(ref.cost)
 
 
+@pytest.mark.parametrize("shape,parts", [((24, 16, 64), 3), ((22, 18, 26), 2), ((9, 8, 64), 4)])
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_slabs_peer_stores_bitwise_equal(W, shape, parts, prec):
+    """Peer ghost stores (boundary launches write the neighbours' ghost
+    planes and bump device flags their streams wait on; no exchange) give
+    the single-GPU bits, twice in a row on the same contexts (the flag
+    sequence continues across evaluations)."""
+    from paper_2509_15744_b200.distributed import SlabGradient, slab_ranges
+
+    problem, mat = _problem(W, shape, sum(shape) + parts + 7)
+    cfg = W.SuperpositionConfig(k=1e13, precision=prec)
+    ref = W.gradient_superposed(problem, mat, cfg)
+    sg = SlabGradient(problem, mat, cfg, slab_ranges(shape[0], parts), halo="peer").upload()
+    try:
+        for _ in range(2):
+            cost = sg.run()
+            assert bits_equal(sg.download(), ref.gradient)
+            assert abs(cost - ref.cost) <= 1e-13 * abs(ref.cost)
+    finally:
+        sg.close()
+
+
 def test_slabs_match_reference_fixture(W, golden):
     from paper_2509_15744_b200.distributed import gradient_superposed_slabs
 

@@ -114,3 +114,44 @@ def test_halo_exchange_gloo(world):
     for p in procs:
         p.join(timeout=60)
     assert all(res[r] for r in range(world)), res
+
+
+class _FakeSlab:
+    """Stands in for a slab DeviceGrid: distinct fake addresses per slab."""
+
+    def __init__(self, idx, has_lo, has_hi):
+        base = 0x10000 * (idx + 1)
+        self.ghost_lo = [base + b if has_lo else 0 for b in range(4)]
+        self.ghost_hi = [base + 0x100 + b if has_hi else 0 for b in range(4)]
+        self.flags = [base + 0x200, base + 0x204]
+        self.peers = None
+
+    def slab_ghosts(self):
+        return self.ghost_lo, self.ghost_hi, self.flags
+
+    def set_slab_peers(self, lo_ghost=None, hi_ghost=None, lo_flag=0, hi_flag=0):
+        self.peers = (lo_ghost, hi_ghost, lo_flag, hi_flag)
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 5])
+def test_peer_halo_wiring(parts):
+    """PeerHalo hands slab i the lower neighbour's HIGH ghost planes and its
+    flag [1], the upper neighbour's LOW ghost planes and its flag [0]; the
+    end slabs get nothing on their open side; close() switches all off."""
+    slabs = [_FakeSlab(i, i > 0, i + 1 < parts) for i in range(parts)]
+    halo = D.PeerHalo(slabs)
+    for i, s in enumerate(slabs):
+        lo_ghost, hi_ghost, lo_flag, hi_flag = s.peers
+        if i > 0:
+            assert lo_ghost == slabs[i - 1].ghost_hi and lo_flag == slabs[i - 1].flags[1]
+        else:
+            assert lo_ghost is None and lo_flag == 0
+        if i + 1 < parts:
+            assert hi_ghost == slabs[i + 1].ghost_lo and hi_flag == slabs[i + 1].flags[0]
+        else:
+            assert hi_ghost is None and hi_flag == 0
+    assert halo.begin() == []
+    with pytest.raises(D.ConfigError):
+        halo.exchange()
+    halo.close()
+    assert all(s.peers == (None, None, 0, 0) for s in slabs)

@@ -57,6 +57,9 @@ namespace wb {
 #ifndef WB_T2_PACKED
 #define WB_T2_PACKED 1
 #endif
+#ifndef WB_T2_PDL
+#define WB_T2_PDL 1   // programmatic dependent launch: overlap the next pass's start with this tail
+#endif
 #ifndef WB_T2_CTAS
 #define WB_T2_CTAS 3
 #endif
@@ -326,6 +329,14 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+#if WB_T2_PDL
+    // launched with programmatic stream serialisation: this CTA may start
+    // while the previous pass drains; nothing above touched global memory.
+    // Wait for the previous grid (and its memory) before the first load, and
+    // let the next pass start its prologue once every CTA of this one runs.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
     if (tid == T2_PRODUCER) {
         for (int s = 0; s < T2_NS && pbeg + s <= plast; ++s) issue(pbeg + s, s);
         for (int d = 0; d < T2_PF && pbeg + T2_NS + d <= plast; ++d) prefetch(pbeg + T2_NS + d);

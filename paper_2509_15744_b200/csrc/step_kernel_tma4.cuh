@@ -105,6 +105,11 @@ step_kernel_tma4(const __grid_constant__ StepArgs<T> a, const __grid_constant__ 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+#if WB_T2_PDL
+    // programmatic dependent launch (as step2_kernel_tma): no global access above
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
     if (tid == 0)
         for (int p = i0; p <= min(i0 + NS - 1, pend); ++p) issue(p, p - i0);
 

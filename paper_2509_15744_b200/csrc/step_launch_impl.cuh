@@ -24,13 +24,39 @@ void smem_opt_in(size_t bytes) {
     done.fetch_or(bit);
 }
 
+// Launch with programmatic stream serialisation (WB_T2_PDL): the kernel may
+// start while the previous kernel of the stream drains; it executes
+// griddepcontrol.wait before touching global memory.  Measured: 2D 256^2
+// superposed gradient 22.2 -> 26.7 Gcell-upd/s (launch-latency-bound), 256^3
+// unchanged.
+template <typename Kernel, typename A, typename M>
+void launch_pdl(Kernel kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, const A& a,
+                const M& maps) {
+#if WB_T2_PDL
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, a, maps);
+#else
+    kernel<<<grid, block, smem, s>>>(a, maps);
+#endif
+}
+
 template <typename T, int FL, bool FAST, bool ACC, bool CHK, int SUP>
 void go_step(int engine, dim3 grid, dim3 block, cudaStream_t s, const StepArgs<T>& a,
              const TmaMaps& maps) {
     if (engine == ENGINE_TMA4) {   // 128 threads, 2x2 cells each, unrolled stages
         const size_t sm = tma4_smem_bytes<T>();
         smem_opt_in<step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP>>(sm);
-        step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP><<<grid, dim3(32, 4, 1), sm, s>>>(a, maps);
+        launch_pdl(step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP>, grid, dim3(32, 4, 1), sm, s, a,
+                   maps);
     } else if (engine == ENGINE_TMA) {   // 256 threads, 2 cells each
         const size_t sm = tma_smem_bytes<T>();
         smem_opt_in<step_kernel_tma<T, FL, FAST, ACC, CHK, SUP>>(sm);
@@ -80,7 +106,7 @@ template <typename T, typename G, int FL, bool ACC, int SUP>
 void go_step2(dim3 grid, cudaStream_t s, const Step2Args<T>& a, const Tma2Maps& maps) {
     const size_t sm = step2_smem_bytes<T, G>();
     smem_opt_in<step2_kernel_tma<T, G, FL, ACC, SUP>>(sm);
-    step2_kernel_tma<T, G, FL, ACC, SUP><<<grid, dim3(G::TX, G::TY, 1), sm, s>>>(a, maps);
+    launch_pdl(step2_kernel_tma<T, G, FL, ACC, SUP>, grid, dim3(G::TX, G::TY, 1), sm, s, a, maps);
 }
 
 template <typename T, typename G, int FL, bool ACC>

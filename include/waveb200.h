@@ -219,6 +219,15 @@ int wo_exchange_local_out(wo_ctx* lower, wo_ctx* upper);
 int wo_slab_ghosts(wo_ctx* ctx, void** ghost_lo, void** ghost_hi, void** flags);
 int wo_slab_peers(wo_ctx* ctx, void* const* lo_ghost, void* const* hi_ghost, void* lo_flag,
                   void* hi_flag);
+/* CUDA IPC for peer ghost stores across processes (one slab per rank, the
+ * torchrun layout; the reference has no multi-GPU path).  wo_ipc_export
+ * writes the 64-byte cudaIpcMemHandle of the allocation holding dev_ptr (a
+ * ghost plane or flag from wo_slab_ghosts) and dev_ptr's byte offset in it;
+ * the neighbour's process passes both to wo_ipc_open, which maps the
+ * allocation once per context (peer access enabled lazily) and returns the
+ * address to hand to wo_slab_peers.  Mappings close in wo_destroy. */
+int wo_ipc_export(wo_ctx* ctx, const void* dev_ptr, void* handle, int64_t* offset);
+int wo_ipc_open(wo_ctx* ctx, const void* handle, int64_t offset, void** ptr);
 
 /* Standard-adjoint sweep of gradient_reference (gradients.py:371-386) using
  * the recorded history and the unscaled compact adjoint store; accumulates

@@ -34,6 +34,7 @@ EXPORTS = (
     "wo_get_field", "wo_opt_init", "wo_opt_step", "wo_opt_get", "wo_design_setup",
     "wo_design_material", "wo_design_gradient", "wo_design_get", "wo_profile_stats",
     "wo_halo_planes_out", "wo_stream", "wo_exchange_local_out", "wo_slab_ghosts", "wo_slab_peers",
+    "wo_ipc_export", "wo_ipc_open",
 )
 
 
@@ -115,6 +116,8 @@ _SIGS = {
     "wo_exchange_local_out": (c_int, [c_vp, c_vp]),
     "wo_slab_ghosts": (c_int, [c_vp, c_vp, c_vp, c_vp]),
     "wo_slab_peers": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "wo_ipc_export": (c_int, [c_vp, c_vp, c_vp, P_i64]),
+    "wo_ipc_open": (c_int, [c_vp, c_vp, c_i64, ctypes.POINTER(c_vp)]),
 }
 WO_OPT_FAST_DIV = 1
 WO_OPT_PAIR_KERNEL = 2

@@ -68,6 +68,9 @@ struct wo_ctx {
     unsigned int* in_flags = nullptr;       // [2]: bumped by the lower / upper neighbour
     unsigned int p2p_seq = 0;               // part-1 launches done (flag value)
     bool p2p = false;
+    // neighbours' allocations mapped through CUDA IPC (wo_ipc_open): handle
+    // bytes -> mapped base, closed by wo_destroy
+    std::vector<std::pair<std::string, char*>> ipc_maps;
     // CUDA graphs of whole sweeps (WO_OPT_GRAPHS): a sweep whose launch
     // sequence repeats (same key: range, sources, amplitudes, window indices
     // and the state generation) is captured on its second sighting and
@@ -1578,6 +1581,7 @@ void wo_destroy(wo_ctx* ctx) {
                     ctx->mask, ctx->prefix,
                     ctx->store, ctx->measured, ctx->partial, ctx->cost, ctx->maxslots,
                     ctx->f_idx, ctx->f_vals, ctx->f_dense, ctx->hist, ctx->u3};
+    for (auto& m : ctx->ipc_maps) cudaIpcCloseMemHandle(m.second);
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (auto e : ctx->marks)
@@ -2087,6 +2091,54 @@ int wo_slab_peers(wo_ctx* ctx, void* const* lo_ghost, void* const* hi_ghost, voi
     ctx->p2p_seq = 0;
     ctx->p2p = any;
     ++ctx->gen;
+    return WO_OK;
+}
+
+typedef CUresult (*PfnAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+int wo_ipc_export(wo_ctx* ctx, const void* dev_ptr, void* handle, int64_t* offset) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(dev_ptr && handle && offset, "wo_ipc_export: null argument");
+    CK(cudaSetDevice(ctx->device));
+    static PfnAddressRange range = [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        return cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) ==
+                               cudaSuccess && q == cudaDriverEntryPointSuccess
+                   ? reinterpret_cast<PfnAddressRange>(p)
+                   : nullptr;
+    }();
+    if (!range) return cu_fail(ctx, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS)
+        return cu_fail(ctx, "cuMemGetAddressRange failed (not a device allocation?)");
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    std::memcpy(handle, &h, sizeof(h));
+    *offset = (int64_t)((CUdeviceptr)dev_ptr - base);
+    return WO_OK;
+}
+
+int wo_ipc_open(wo_ctx* ctx, const void* handle, int64_t offset, void** ptr) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(handle && ptr && offset >= 0, "wo_ipc_open: bad argument");
+    CK(cudaSetDevice(ctx->device));
+    const std::string key(static_cast<const char*>(handle), sizeof(cudaIpcMemHandle_t));
+    char* base = nullptr;
+    for (auto& m : ctx->ipc_maps)   // one mapping per exported allocation
+        if (m.first == key) base = m.second;
+    if (!base) {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof(h));
+        void* p = nullptr;
+        CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        base = static_cast<char*>(p);
+        ctx->ipc_maps.emplace_back(key, base);
+    }
+    *ptr = base + offset;
     return WO_OK;
 }
 

@@ -20,7 +20,12 @@ slab decomposition (SlabGradient)
         device flag the neighbour's stream waits on (``wo_slab_peers``);
       * ``TorchHalo`` — one slab per process (torchrun), torch.distributed
         point-to-point send/recv of the plane tensors (NCCL over NVLink on
-        GPUs; the same code runs on gloo/CPU tensors in the tests).
+        GPUs; the same code runs on gloo/CPU tensors in the tests);
+      * ``IpcPeerHalo`` — one slab per process, PeerHalo's kernel stores
+        across processes: each rank exports its ghost planes and flags as
+        CUDA IPC handles (``wo_ipc_export``), the neighbours map them
+        (``wo_ipc_open``) and hand them to ``wo_slab_peers``; the handles
+        travel once through an object all-gather, then no collective per step.
     Costs are summed per slab then across slabs (fp64, not bitwise: the
     reference's BLAS dot order is unknown anyway); stability maxima are
     combined with max before the reference's first-failure scan.
@@ -252,6 +257,57 @@ class TorchHalo:
         return float(t.item())
 
 
+def ipc_peer_wiring(rank, world, exports):
+    """Which neighbour exports rank opens for wo_slab_peers.
+
+    exports[r] = (ghost_lo[4], ghost_hi[4], flags[2]) of rank r, each entry an
+    exported (handle, offset) or None.  The lower neighbour contributes its
+    HIGH ghost planes and flag [1] (bumped by its upper neighbour = this
+    rank), the upper neighbour its LOW ghost planes and flag [0]."""
+    lo = exports[rank - 1] if rank > 0 else None
+    hi = exports[rank + 1] if rank + 1 < world else None
+    return {"lo_ghost": lo[1] if lo else None, "lo_flag": lo[2][1] if lo else None,
+            "hi_ghost": hi[0] if hi else None, "hi_flag": hi[2][0] if hi else None}
+
+
+class IpcPeerHalo(TorchHalo):
+    """One slab per process, no exchange step: the boundary launches store
+    their planes into the neighbour processes' ghost planes through CUDA IPC
+    mappings and bump their flags (``wo_slab_peers``), like PeerHalo.  Setup
+    is one all-gather of the exported handles; the stability / cost
+    all-reduces of TorchHalo stay (they also order a rank's next window reset
+    after its neighbours' last stores into it)."""
+
+    def __init__(self, ctx, rank, world, group=None):
+        import torch.distributed as dist
+
+        super().__init__(ctx, rank, world, group)
+        glo, ghi, flags = ctx.slab_ghosts()
+        exp = lambda p: ctx.ipc_export(p) if p else None  # noqa: E731
+        mine = ([exp(p) for p in glo], [exp(p) for p in ghi], [exp(p) for p in flags])
+        exports = [None] * world
+        dist.all_gather_object(exports, mine, group=group)
+        w = ipc_peer_wiring(rank, world, exports)
+        opn = lambda e: ctx.ipc_open(*e) if e else 0  # noqa: E731
+        ctx.set_slab_peers(
+            lo_ghost=[opn(e) for e in w["lo_ghost"]] if w["lo_ghost"] else None,
+            hi_ghost=[opn(e) for e in w["hi_ghost"]] if w["hi_ghost"] else None,
+            lo_flag=opn(w["lo_flag"]), hi_flag=opn(w["hi_flag"]))
+        dist.barrier(group=group)   # every slab's flags reset before anyone steps
+
+    def exchange(self):
+        raise ConfigError("IpcPeerHalo moves planes inside split steps (overlap=True)")
+
+    def begin(self):
+        return []
+
+    def end(self, works):
+        pass
+
+    def close(self):
+        self.ctx.set_slab_peers()
+
+
 # ------------------------------------------------------------ slab driver
 class SlabGradient:
     """gradient_superposed over axis-0 slabs (bitwise equal to one GPU).
@@ -291,12 +347,19 @@ class SlabGradient:
 
     @classmethod
     def for_rank(cls, problem, material, config, rank, world, device=None, group=None,
-                 overlap=True):
-        """One slab per torchrun rank (NCCL halo exchange)."""
+                 overlap=True, halo="nccl"):
+        """One slab per torchrun rank: halo 'nccl' (send/recv of the planes,
+        TorchHalo) or 'ipc' (peer ghost stores through CUDA IPC, IpcPeerHalo;
+        needs overlap)."""
+        if halo not in ("nccl", "ipc"):
+            raise ConfigError(f"unknown rank halo {halo!r}")
+        if halo == "ipc" and not overlap:
+            raise ConfigError("peer ghost stores run split steps (overlap=True)")
         slab = slab_ranges(problem.grid.shape[0], world)[rank]
         dev = rank if device is None else device
         obj = cls(problem, material, config, [slab], [dev], halo=None, overlap=overlap)
-        obj.halo = TorchHalo(obj.ctxs[0], rank, world, group)
+        make = IpcPeerHalo if halo == "ipc" else TorchHalo
+        obj.halo = make(obj.ctxs[0], rank, world, group)
         return obj
 
     def upload(self):

@@ -383,6 +383,22 @@ class DeviceGrid:
         self._ck(self.L.wo_slab_peers(self.h, arr(lo_ghost), arr(hi_ghost), lo_flag or None,
                                       hi_flag or None), "wo_slab_peers")
 
+    def ipc_export(self, ptr):
+        """(64-byte CUDA IPC handle, byte offset) of the device address ptr
+        (wo_ipc_export), for a neighbour process's ipc_open."""
+        h = ctypes.create_string_buffer(64)
+        off = ctypes.c_int64()
+        self._ck(self.L.wo_ipc_export(self.h, ptr, h, ctypes.byref(off)), "wo_ipc_export")
+        return h.raw, off.value
+
+    def ipc_open(self, handle, offset):
+        """Device address in this process of a neighbour's exported pointer
+        (wo_ipc_open; the mapping lives as long as this context)."""
+        p = ctypes.c_void_p()
+        self._ck(self.L.wo_ipc_open(self.h, bytes(handle), int(offset), ctypes.byref(p)),
+                 "wo_ipc_open")
+        return p.value
+
     def set_graphs(self, on):
         """Replay repeated sweeps from captured CUDA graphs (default on)."""
         self._ck(self.L.wo_set_option(self.h, N.WO_OPT_GRAPHS, int(bool(on))), "wo_set_option")

@@ -155,3 +155,73 @@ def test_peer_halo_wiring(parts):
         halo.exchange()
     halo.close()
     assert all(s.peers == (None, None, 0, 0) for s in slabs)
+
+
+class _FakeIpcSlab(_FakeSlab):
+    """A slab context whose IPC export / open round-trip is a byte encoding:
+    the handle names the exporting address, the opened address is that
+    address tagged as mapped (bit 40)."""
+
+    MAPPED = 1 << 40
+
+    def ipc_export(self, ptr):
+        return ptr.to_bytes(8, "little") + b"\0" * 56, 0
+
+    def ipc_open(self, handle, offset):
+        assert len(handle) == 64
+        return int.from_bytes(handle[:8], "little") + offset + self.MAPPED
+
+
+def _ipc_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        slabs = [_FakeIpcSlab(i, i > 0, i + 1 < world) for i in range(world)]
+        me = slabs[rank]
+        halo = D.IpcPeerHalo(me, rank, world)
+        lo_ghost, hi_ghost, lo_flag, hi_flag = me.peers
+        m = _FakeIpcSlab.MAPPED
+        ok = True
+        if rank > 0:
+            ok &= lo_ghost == [p + m for p in slabs[rank - 1].ghost_hi]
+            ok &= lo_flag == slabs[rank - 1].flags[1] + m
+        else:
+            ok &= lo_ghost is None and lo_flag == 0
+        if rank + 1 < world:
+            ok &= hi_ghost == [p + m for p in slabs[rank + 1].ghost_lo]
+            ok &= hi_flag == slabs[rank + 1].flags[0] + m
+        else:
+            ok &= hi_ghost is None and hi_flag == 0
+        ok &= halo.begin() == []
+        halo.close()
+        ok &= me.peers == (None, None, 0, 0)
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ipc_peer_halo_wiring_gloo(world):
+    """IpcPeerHalo: one slab per rank, handles all-gathered over the group;
+    rank r maps its lower neighbour's HIGH ghost planes and flag [1] and its
+    upper neighbour's LOW ghost planes and flag [0]."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res[r] for r in range(world)), res
+
+
+def test_for_rank_rejects_unknown_halo():
+    with pytest.raises(D.ConfigError):
+        D.SlabGradient.for_rank(None, None, 1e13, 0, 2, halo="shm")

@@ -747,6 +747,8 @@ bool pair_ready(wo_ctx* ctx) {
 // waves idle slots, and each chunk recomputes ~1 extra plane.  Model: at
 // least ~2 waves of work when the grid allows it, then the fewest
 // waves x (planes + 1).  WB_T2_NZ overrides (tuning runs).
+constexpr double T2_LONG_CHUNK_PENALTY = 1.7e-4;   // per plane beyond 32
+
 int choose_chunk2(const wo_ctx* ctx) {
     const int tbx = ctx->t2_geo == GEO_TALL ? GeoTall::TBX : GeoWide::TBX;
     const int tby = ctx->t2_geo == GEO_TALL ? GeoTall::TBY : GeoWide::TBY;
@@ -768,7 +770,11 @@ int choose_chunk2(const wo_ctx* ctx) {
             if (can_stagger && (double)tiles * nz < min_work) continue;
             const int chunk = (ctx->kn0 + nz - 1) / nz;
             const int waves = (tiles * nz + slots - 1) / slots;
-            const double cost = (double)waves * (chunk + 1);
+            // chunks past 32 planes also lose per plane (measured at 1024^3:
+            // 128-plane chunks 222-260 Gcell/s, 64-plane 279-280; 512^3 keeps
+            // 86): a mild length penalty on top of the wave count
+            const double cost = (double)waves * (chunk + 1) *
+                                (1.0 + T2_LONG_CHUNK_PENALTY * std::max(0, chunk - 32));
             if (cost < best - 1e-9) { best = cost; best_nz = nz; }
         }
     }

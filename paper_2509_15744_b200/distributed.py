@@ -282,6 +282,8 @@ class IpcPeerHalo(TorchHalo):
         import torch.distributed as dist
 
         super().__init__(ctx, rank, world, group)
+        if world == 1:   # one slab, no neighbours: nothing to map
+            return
         glo, ghi, flags = ctx.slab_ghosts()
         exp = lambda p: ctx.ipc_export(p) if p else None  # noqa: E731
         mine = ([exp(p) for p in glo], [exp(p) for p in ghi], [exp(p) for p in flags])
@@ -305,7 +307,8 @@ class IpcPeerHalo(TorchHalo):
         pass
 
     def close(self):
-        self.ctx.set_slab_peers()
+        if self.world > 1:
+            self.ctx.set_slab_peers()
 
 
 # ------------------------------------------------------------ slab driver

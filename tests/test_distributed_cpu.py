@@ -225,3 +225,12 @@ def test_ipc_peer_halo_wiring_gloo(world):
 def test_for_rank_rejects_unknown_halo():
     with pytest.raises(D.ConfigError):
         D.SlabGradient.for_rank(None, None, 1e13, 0, 2, halo="shm")
+
+
+def test_ipc_peer_halo_single_rank_is_inert():
+    """world 1: one slab without neighbours; nothing exported, mapped or set."""
+    s = _FakeIpcSlab(0, False, False)
+    halo = D.IpcPeerHalo(s, 0, 1)
+    assert s.peers is None and halo.begin() == []
+    halo.close()
+    assert s.peers is None

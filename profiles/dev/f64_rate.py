@@ -21,10 +21,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--grid", type=int, default=256)
 ap.add_argument("--n-steps", type=int, default=256)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--two-step", type=int, default=1, help="2: fp64 two-step passes")
 args = ap.parse_args()
 n = args.grid
 problem, mat = configs.fwi((n, n, n), args.n_steps)
 plan = G.SuperposedPlan(problem, mat, W.SuperpositionConfig(k=1e13, precision="double")).upload()
+plan.ctx.set_two_step(args.two_step)
 plan.run()
 plan.ctx.synchronize()
 t0 = time.perf_counter()
@@ -34,4 +36,5 @@ plan.ctx.synchronize()
 ms = (time.perf_counter() - t0) / args.reps * 1e3
 upd = 2 * (args.n_steps - 1) * problem.grid.n_nodes
 print(json.dumps({"grid": n, "n_steps": args.n_steps, "chunk": os.environ.get("WB_T1_CHUNK", "model"),
+                  "two_step": args.two_step,
                   "ms": round(ms, 2), "gcell_upd_s": round(upd / ms / 1e6, 1)}))

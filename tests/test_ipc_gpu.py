@@ -28,6 +28,12 @@ def _mapper(handles, q):
         _device_view(ghost, plane * 4, np.float32, 0).fill_(7.0)
         _device_view(flag, 4, np.int32, 0).fill_(3)
         torch.cuda.synchronize()
+        # the mapped addresses are what wo_slab_peers gets across processes:
+        # a lower slab of its own accepts them as its upper neighbour's
+        lower = engine.DeviceGrid(engine.Grid(SHAPE, 1e-4), np.float32, 0, slab=(0, SLAB[0]))
+        lower.set_slab_peers(hi_ghost=[ghost] * 4, hi_flag=flag)
+        lower.set_slab_peers()
+        lower.close()
         ctx.close()
         q.put(("ok", ghost == again))
     except Exception as e:  # noqa: BLE001 - reported to the parent

@@ -82,11 +82,18 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
 /* WO_OPT_TMA_KERNEL (default 1): TMA/mbarrier-pipelined step kernel when the
  * grid tiles exactly into 64 x 8 cells (0 = never). */
 #define WO_OPT_TMA_KERNEL 3
-/* WO_OPT_TWO_STEP (default 1): advance two time steps per pass over HBM
- * (temporal blocking, identical arithmetic) on single-domain fp32 contexts
+/* WO_OPT_TWO_STEP (default 1; slab contexts 0): advance two time steps per
+ * pass over HBM (temporal blocking, identical arithmetic) on fp32 contexts
  * whose plane tiles into 64 x 8 or 32 x 16 cells; 2 = also fp64 contexts;
  * 0 = never.  Sweeps fall back to single steps at odd range ends, while
- * recording history, and everywhere else. */
+ * recording history, and everywhere else.  Slabs take two-step passes only
+ * with peer ghost stores and two ghost planes per neighbour; the caller
+ * enables them on every slab of a decomposition or on none (all slabs must
+ * launch alike) and only when no support node lies on a plane next to a
+ * slab boundary (the recomputed planes do not inject the neighbour's
+ * adjoint store).  Single-domain contexts with 0 hold the reference's four
+ * solution-sized buffers: gamma, two window levels (u^{n+1} in place over
+ * u^{n-1}) and the accumulator. */
 #define WO_OPT_TWO_STEP 4
 /* WO_OPT_PLANE_PART (slab contexts, default 0): 1 = the next single step
  * computes only the boundary planes 0 and n0-1 (no rotation), 2 = only the
@@ -176,7 +183,15 @@ int wo_sweep_forward(wo_ctx* ctx, int64_t n_steps, int n_src, const int64_t* src
  * Backward: steps n = n_hi .. n_lo+1 descending; the range starting at
  * n_hi = N-1 swaps the direction.  No stability evaluation: read the
  * per-step max|u| with wo_check_maxima (out[n], n in [0, N+2), step n's
- * check value) and combine across slabs.  Each call returns synchronised. */
+ * check value) and combine across slabs.  Each call returns synchronised,
+ * except on a slab with peer ghost stores (wo_slab_peers), where the ranges
+ * only enqueue (a whole sweep is one range; the neighbours' sweeps may still
+ * have to be enqueued) and wo_check_maxima waits for the stream.
+ * Slab contexts take source indices local to their own planes, negative ones
+ * down to their lowest ghost plane included (a two-step pass recomputes one
+ * plane beyond each slab boundary, sources there included); the backward
+ * sweeps of a slab take WO_NO_SOURCE for "no source". */
+#define WO_NO_SOURCE INT64_MIN
 int wo_sweep_forward_range(wo_ctx* ctx, int64_t n_steps, int64_t n_begin, int64_t n_end,
                            int n_src, const int64_t* src_flat, const double* src_amp, int flags,
                            double dt);
@@ -203,20 +218,28 @@ void* wo_stream(wo_ctx* ctx);
 /* wo_exchange_local for the level a split step is writing. */
 int wo_exchange_local_out(wo_ctx* lower, wo_ctx* upper);
 /* Peer ghost stores (replaces the exchange; the reference has no multi-GPU
- * path — solver.py:128-151 steps one array).  wo_slab_ghosts returns this
- * slab's ghost planes in each of its 4 level buffers (NULL when absent) and
- * the device addresses of its two incoming flags (bumped by the lower /
- * upper neighbour).  wo_slab_peers hands a slab its neighbours' addresses:
+ * path — solver.py:128-151 steps one array).  A slab holds two ghost planes
+ * per neighbour.  wo_slab_ghosts returns, per level buffer (4), the address of
+ * its lowest ghost plane (plane -2) and of its first high ghost plane (plane
+ * n0), NULL when absent, and the addresses of its two incoming flags (bumped
+ * by the lower / upper neighbour; each flag word has a twin 2 words further
+ * for odd sweeps).  wo_slab_peers hands a slab its neighbours' addresses:
  * lo_ghost[4] = the lower neighbour's HIGH ghost planes, hi_ghost[4] = the
  * upper neighbour's LOW ghost planes, lo_flag = the lower neighbour's flag
  * [1], hi_flag = the upper neighbour's flag [0] (all NULL: off).  Then every
- * split step's part 1 waits (on its stream) for its own flags to reach the
- * neighbours' previous step, stores the new boundary planes into both its
- * own buffer and the neighbour's ghost plane (NVLink stores when the
- * neighbour is on another GPU; IPC-mapped addresses across processes), and
- * bumps the neighbours' flags: no copy or collective per step.  Set up every
- * slab before stepping any; whole steps (part 0) are refused meanwhile. */
+ * launch of a sweep (single step or two-step pass) waits on its stream until
+ * both neighbours completed their previous launch, stores its own planes 0, 1
+ * and n0-2, n0-1 of the level(s) it writes into both its own buffer and the
+ * neighbour's ghost planes (NVLink stores when the neighbour is on another
+ * GPU; IPC-mapped addresses across processes), and bumps the neighbours'
+ * flags: no copy or collective per step.  Each sweep is an epoch with its own
+ * flag slot, begun after the window reset; the caller synchronises every slab
+ * between sweeps (wo_check_maxima + its cost / stability reduction).  Set up
+ * every slab before stepping any; split steps are refused meanwhile. */
 int wo_slab_ghosts(wo_ctx* ctx, void** ghost_lo, void** ghost_hi, void** flags);
+/* Error recovery: set this slab's and its neighbours' flags to the maximum
+ * so no stream keeps waiting on a sweep that was only partly enqueued. */
+int wo_slab_abort(wo_ctx* ctx);
 int wo_slab_peers(wo_ctx* ctx, void* const* lo_ghost, void* const* hi_ghost, void* lo_flag,
                   void* hi_flag);
 /* CUDA IPC for peer ghost stores across processes (one slab per rank, the
@@ -313,6 +336,12 @@ int wo_stats(wo_ctx* ctx, int64_t* launches, int64_t* step_launches, double* ste
 int wo_reset_stats(wo_ctx* ctx);
 /* Device bytes held by the context (fields + support storage). */
 int64_t wo_device_bytes(const wo_ctx* ctx);
+/* Solution-sized device buffers the context holds right now: gamma, the
+ * window levels (2; 4 once two-step passes ran), the accumulator, the third
+ * adjoint level of the reference engine, and the 4 precomputed material
+ * fields of the two-step kernel (coef and 3 face arrays).  The history of
+ * the reference engine is not included (see wo_device_bytes). */
+int wo_field_buffers(const wo_ctx* ctx);
 /* Step launches since the last wo_reset_stats that were two-step passes
  * (WO_OPT_TWO_STEP); the rest of wo_stats' step_launches are single steps. */
 int64_t wo_pair_launches(const wo_ctx* ctx);

@@ -17,6 +17,7 @@ WO_OK, WO_ERR_CONFIG, WO_ERR_UNSTABLE, WO_ERR_BUDGET, WO_ERR_CUDA = 0, 1, 2, 3, 
 WO_RHO_SCALED, WO_ACOUSTIC = 0, 1
 WO_SHOT_FWI, WO_SHOT_TATO = 1, 2
 WO_FWD_ACCUMULATE, WO_FWD_HISTORY = 1, 2
+WO_NO_SOURCE = -(2 ** 63)   # slab backward sweeps: no source
 
 # every symbol declared in include/waveb200.h
 EXPORTS = (
@@ -26,7 +27,7 @@ EXPORTS = (
     "wo_zero_accumulator", "wo_get_accumulator", "wo_set_accumulator", "wo_sweep_forward",
     "wo_shot_misfit", "wo_get_store", "wo_sweep_backward", "wo_get_gradient", "wo_step",
     "wo_apply_step", "wo_apply_kernel_increment", "wo_set_profiling", "wo_stats",
-    "wo_reset_stats", "wo_device_bytes", "wo_sweep_adjoint_reference", "wo_free_history",
+    "wo_reset_stats", "wo_device_bytes", "wo_field_buffers", "wo_slab_abort", "wo_sweep_adjoint_reference", "wo_free_history",
     "wo_design_filter", "wo_design_project", "wo_design_chain", "wo_timer_mark",
     "wo_timer_elapsed", "wo_synchronize", "wo_accumulator_ptr", "wo_set_option",
     "wo_fast_div_active", "wo_sweep_forward_range", "wo_sweep_backward_range",
@@ -79,6 +80,8 @@ _SIGS = {
     "wo_stats": (c_int, [c_vp, P_i64, P_i64, P_dbl]),
     "wo_reset_stats": (c_int, [c_vp]),
     "wo_device_bytes": (c_i64, [c_vp]),
+    "wo_field_buffers": (c_int, [c_vp]),
+    "wo_slab_abort": (c_int, [c_vp]),
     "wo_sweep_adjoint_reference": (c_int, [c_vp, c_i64, c_dbl, P_i64, P_dbl]),
     "wo_free_history": (c_int, [c_vp]),
     "wo_design_filter": (c_int, [c_int, P_i64, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_int]),

@@ -26,6 +26,10 @@
 
 using namespace wb;
 
+namespace wb {
+thread_local bool t_no_pdl = false;
+}
+
 namespace {
 
 constexpr int STABILITY_CHECK_INTERVAL = 50;     // solver.py:29
@@ -40,7 +44,8 @@ struct wo_ctx {
     int64_t shape[3] = {1, 1, 1};      // caller's shape (local for slabs)
     int kn0 = 1, kn1 = 1, kn2 = 1;     // kernel-space local extents
     int i_off = 0, n0g = 1;            // slab placement along axis 0
-    int has_lo = 0, has_hi = 0;        // ghost planes present
+    int has_lo = 0, has_hi = 0;        // neighbour slab below / above
+    int gl = 0, gh = 0;                // ghost planes below / above (2 if room, global end: 0)
     int itemsize = 8;
     double dx = 0.0;
     cudaStream_t stream = nullptr;
@@ -58,15 +63,18 @@ struct wo_ctx {
     int use_two_step = 1;              // wo_set_option(WO_OPT_TWO_STEP)
     int num_sms = 148;                 // of the context's device
     int part = 0;                      // WO_OPT_PLANE_PART: 0 whole steps, 1 boundary, 2 interior
-    // peer ghost stores (wo_slab_peers): the boundary launches of part 1 also
-    // store their plane into the neighbour's ghost plane (same level buffer
-    // index: slabs step in lockstep) and then bump the neighbour's flag
-    char* peer_lo[4] = {nullptr, nullptr, nullptr, nullptr};   // lower's high ghost
-    char* peer_hi[4] = {nullptr, nullptr, nullptr, nullptr};   // upper's low ghost
-    unsigned int* peer_lo_flag = nullptr;   // lower's in_flags[1]
-    unsigned int* peer_hi_flag = nullptr;   // upper's in_flags[0]
-    unsigned int* in_flags = nullptr;       // [2]: bumped by the lower / upper neighbour
-    unsigned int p2p_seq = 0;               // part-1 launches done (flag value)
+    // peer ghost stores (wo_slab_peers): every launch also stores its own
+    // planes 0, 1 / n0-2, n0-1 of the level(s) it writes into the neighbours'
+    // two ghost planes of the same level buffer (slabs step in lockstep), then
+    // bumps the neighbours' flags; the next launch waits for both neighbours'
+    // flags (p2p_wait / p2p_signal, one epoch per sweep)
+    char* peer_lo[4] = {nullptr, nullptr, nullptr, nullptr};   // lower's top ghost planes
+    char* peer_hi[4] = {nullptr, nullptr, nullptr, nullptr};   // upper's bottom ghost planes
+    unsigned int* peer_lo_flag = nullptr;   // lower's in_flags + 1 (its "from upper" word)
+    unsigned int* peer_hi_flag = nullptr;   // upper's in_flags + 0 (its "from lower" word)
+    unsigned int* in_flags = nullptr;       // [parity][from lower, from upper]
+    unsigned int p2p_seq = 0;               // signals sent in this epoch
+    int p2p_epoch = 0;                      // sweeps begun (flag slot = epoch parity)
     bool p2p = false;
     // neighbours' allocations mapped through CUDA IPC (wo_ipc_open): handle
     // bytes -> mapped base, closed by wo_destroy
@@ -159,9 +167,10 @@ struct wo_ctx {
 
     int64_t plane() const { return (int64_t)kn1 * kn2; }
     int64_t cells() const { return (int64_t)kn0 * plane(); }
-    int64_t alloc_cells() const { return (int64_t)(kn0 + has_lo + has_hi) * plane(); }
+    int alloc_planes() const { return kn0 + gl + gh; }
+    int64_t alloc_cells() const { return (int64_t)alloc_planes() * plane(); }
     size_t field_bytes() const { return (size_t)cells() * itemsize; }
-    char* base0(char* p) const { return p + (size_t)has_lo * plane() * itemsize; }
+    char* base0(char* p) const { return p + (size_t)gl * plane() * itemsize; }
     char* ucur() const { return base0(u[cur]); }
     char* uprev() const { return base0(u[prv]); }
 };
@@ -313,6 +322,16 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
     return fn;
 }
 
+// programmatic dependent launch between peer-store launches (which stream
+// memory operations separate): off unless WB_P2P_PDL=1
+bool p2p_pdl() {
+    static const bool on = [] {
+        const char* e = getenv("WB_P2P_PDL");
+        return e && atoi(e) == 1;
+    }();
+    return on;
+}
+
 int cu_fail(wo_ctx* ctx, const char* msg) {
     ctx->err = msg;
     return WO_ERR_CUDA;
@@ -358,7 +377,7 @@ bool tma_ready(wo_ctx* ctx) {
     if (ctx->tma_state == 0) {
         ctx->tma_state = -1;
         if (ctx->kn2 % PBX == 0 && ctx->kn1 % BY == 0) {
-            const uint64_t np = (uint64_t)(ctx->kn0 + ctx->has_lo + ctx->has_hi);
+            const uint64_t np = (uint64_t)ctx->alloc_planes();
             const uint32_t hw = ctx->itemsize == 4 ? th_w<float>() : th_w<double>();
             bool ok = true;
             for (int b = 0; b < 4; ++b) {
@@ -372,7 +391,7 @@ bool tma_ready(wo_ctx* ctx) {
                            hw, TH_H);
             ok &= make_map(&ctx->tmaps.a_ctr, ctx->acc, ctx->itemsize, ctx->kn2, ctx->kn1,
                            (uint64_t)ctx->kn0, PBX, BY);
-            ctx->tmaps.lo = ctx->has_lo;
+            ctx->tmaps.lo = ctx->gl;
             if (ok) ctx->tma_state = 1;
             ++ctx->gen;
         }
@@ -396,6 +415,7 @@ struct StepSpec {
     char* out = nullptr;
     char* hist = nullptr;              // history row receiving a copy of out
     int c_lo = 0, c_hi = -1;           // computed planes [c_lo, c_hi) (c_hi < 0: all)
+    bool peer = false;                 // peer ghost stores of the written level (p2p sweeps)
 };
 
 template <typename T>
@@ -446,6 +466,11 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
         a.adj_row = st;
     }
     a.max_slot = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots) + sp.slot;
+    if (sp.peer) {   // the written level is buffer prv (in place over u^{n-1})
+        const size_t up = (size_t)(ctx->kn0 - 2) * ctx->plane() * ctx->itemsize;
+        a.plo = reinterpret_cast<T*>(ctx->peer_lo[ctx->prv]);
+        a.phi = ctx->peer_hi[ctx->prv] ? reinterpret_cast<T*>(ctx->peer_hi[ctx->prv] - up) : nullptr;
+    }
 
     // whole 64x8 tiles on the default window: TMA pipeline; even rows: the
     // pair-vectorised kernel; otherwise the scalar kernel
@@ -462,9 +487,12 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     }
     prof_begin(ctx, 0);
     const StepSel sel{ctx->flavor, ctx->fast_div, sp.acc, sp.check, a.sup_mode};
-    const int engine = tma ? (ctx->use_tma == 2 ? ENGINE_TMA : ENGINE_TMA4)
+    // (the superseded 256-thread TMA engine has no peer stores)
+    const int engine = tma ? (ctx->use_tma == 2 && !sp.peer ? ENGINE_TMA : ENGINE_TMA4)
                            : (pair ? ENGINE_PAIR : ENGINE_SCALAR);
+    t_no_pdl = sp.peer && !p2p_pdl();
     launch_step_engine<T>(engine, sel, grid, block, ctx->stream, a, ctx->tmaps);
+    t_no_pdl = false;
     prof_end(ctx);
     ctx->launches++;
     ctx->step_launches++;
@@ -472,47 +500,55 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     return WO_OK;
 }
 
-// part 1 with peer ghost stores: wait until both neighbours finished their
-// previous part 1 (our ghost planes hold their new planes, and they no longer
-// read the ghost slot we are about to overwrite), compute plane 0 / n0-1 with
-// a second store of the result into the neighbour's ghost plane (hist_out,
-// offset so that plane p lands on the ghost plane), then bump the
-// neighbours' flags (stream write with its memory barrier: the stores are
-// visible first).  No copy, no collective; the interior (part 2) overlaps.
-template <typename T>
-int launch_boundary_p2p(wo_ctx* ctx, StepSpec sp) {
-    REQUIRE(!sp.out && !sp.hist && !sp.prev && !sp.cur, "peer ghost stores need in-place steps");
-    auto wait = wait_value32();
+// Peer ghost stores between slabs (wo_slab_peers): no exchange step.  Every
+// launch stores its own planes 0, 1 / n0-2, n0-1 of the level(s) it writes
+// straight into the neighbours' two ghost planes of the same level buffer
+// (NVLink stores when the neighbour is another GPU; slabs rotate their buffers
+// in lockstep), then bumps the neighbours' flag (cuStreamWriteValue32: its
+// memory barrier makes the plane stores visible first).  Launch i of a sweep
+// first waits (cuStreamWaitValue32 GEQ, on the stream: no SM spins) until both
+// neighbours completed their launch i-1: their stores into our ghost planes
+// are then complete, and they no longer read the ghost planes our launch i
+// overwrites (it writes buffers their launch i-1 was reading).  Each sweep is
+// one epoch with its own flag slot (parity): the epoch's first signal comes
+// after the context's window reset (so no neighbour store can precede it) and
+// the slot of the previous epoch is cleared for the next one; every epoch is
+// separated from the next by a host synchronisation on all slabs (the
+// stability / cost reductions), which orders those clears.
+int p2p_signal(wo_ctx* ctx) {
     auto write = write_value32();
-    REQUIRE(wait && write, "stream memory operations unavailable");
-    REQUIRE(ctx->kn0 >= 2, "peer ghost stores need slabs of at least two planes");
-    const size_t pb = (size_t)ctx->plane() * ctx->itemsize;
-    const unsigned seq = ctx->p2p_seq;
-    if (ctx->has_lo && ctx->peer_lo[0] &&
-        wait((CUstream)ctx->stream, (CUdeviceptr)(ctx->in_flags + 0), seq, CU_STREAM_WAIT_VALUE_GEQ))
-        return cu_fail(ctx, "cuStreamWaitValue32 failed");
-    if (ctx->has_hi && ctx->peer_hi[0] &&
-        wait((CUstream)ctx->stream, (CUdeviceptr)(ctx->in_flags + 1), seq, CU_STREAM_WAIT_VALUE_GEQ))
-        return cu_fail(ctx, "cuStreamWaitValue32 failed");
-    const int b = ctx->prv;   // the level this step writes (in place over u^{n-1})
-    for (int side = 0; side < 2; ++side) {
-        const int p = side == 0 ? 0 : ctx->kn0 - 1;
-        char* peer = side == 0 ? ctx->peer_lo[b] : ctx->peer_hi[b];
-        StepSpec s2 = sp;
-        s2.c_lo = p;
-        s2.c_hi = p + 1;
-        s2.hist = peer ? peer - (size_t)p * pb : nullptr;
-        int rc = launch_step<T>(ctx, s2);
-        if (rc) return rc;
-    }
-    ctx->p2p_seq = seq + 1;
-    if (ctx->peer_lo_flag &&
-        write((CUstream)ctx->stream, (CUdeviceptr)ctx->peer_lo_flag, seq + 1, CU_STREAM_WRITE_VALUE_DEFAULT))
-        return cu_fail(ctx, "cuStreamWriteValue32 failed");
-    if (ctx->peer_hi_flag &&
-        write((CUstream)ctx->stream, (CUdeviceptr)ctx->peer_hi_flag, seq + 1, CU_STREAM_WRITE_VALUE_DEFAULT))
-        return cu_fail(ctx, "cuStreamWriteValue32 failed");
+    REQUIRE(write, "stream memory operations unavailable");
+    const int par = ctx->p2p_epoch & 1;
+    ++ctx->p2p_seq;
+    for (unsigned int* f : {ctx->peer_lo_flag, ctx->peer_hi_flag})
+        if (f && write((CUstream)ctx->stream, (CUdeviceptr)(f + 2 * par), ctx->p2p_seq,
+                       CU_STREAM_WRITE_VALUE_DEFAULT))
+            return cu_fail(ctx, "cuStreamWriteValue32 failed");
     return WO_OK;
+}
+
+int p2p_wait(wo_ctx* ctx) {
+    auto wait = wait_value32();
+    REQUIRE(wait, "stream memory operations unavailable");
+    const int par = ctx->p2p_epoch & 1;
+    if (ctx->peer_lo_flag &&
+        wait((CUstream)ctx->stream, (CUdeviceptr)(ctx->in_flags + 2 * par), ctx->p2p_seq,
+             CU_STREAM_WAIT_VALUE_GEQ))
+        return cu_fail(ctx, "cuStreamWaitValue32 failed");
+    if (ctx->peer_hi_flag &&
+        wait((CUstream)ctx->stream, (CUdeviceptr)(ctx->in_flags + 2 * par + 1), ctx->p2p_seq,
+             CU_STREAM_WAIT_VALUE_GEQ))
+        return cu_fail(ctx, "cuStreamWaitValue32 failed");
+    return WO_OK;
+}
+
+int p2p_epoch_begin(wo_ctx* ctx) {
+    if (!ctx->p2p) return WO_OK;
+    ++ctx->p2p_epoch;
+    const int par = ctx->p2p_epoch & 1;
+    CK(cudaMemsetAsync(ctx->in_flags + 2 * (par ^ 1), 0, 2 * sizeof(unsigned int), ctx->stream));
+    ctx->p2p_seq = 0;
+    return p2p_signal(ctx);   // sends 1: everything enqueued before (window reset) is done
 }
 
 // one step of a slab split for halo overlap (wo_set_option WO_OPT_PLANE_PART):
@@ -520,14 +556,21 @@ int launch_boundary_p2p(wo_ctx* ctx, StepSpec sp) {
 // neighbours need), part 2 the interior; part 0 everything
 template <typename T>
 int launch_step_part(wo_ctx* ctx, StepSpec sp) {
-    REQUIRE(!(ctx->p2p && ctx->part == 0), "peer ghost stores run split steps (WO_OPT_PLANE_PART)");
+    if (ctx->p2p) {   // whole step between the neighbours' flags
+        REQUIRE(ctx->part == 0, "peer ghost stores run whole steps (WO_OPT_PLANE_PART 0)");
+        int rc = p2p_wait(ctx);
+        if (rc) return rc;
+        sp.peer = true;
+        rc = launch_step<T>(ctx, sp);
+        if (rc) return rc;
+        return p2p_signal(ctx);
+    }
     if (ctx->part == 0) return launch_step<T>(ctx, sp);
     if (ctx->part == 2) {
         sp.c_lo = 1;
         sp.c_hi = ctx->kn0 - 1;
         return launch_step<T>(ctx, sp);
     }
-    if (ctx->p2p) return launch_boundary_p2p<T>(ctx, sp);
     sp.c_lo = 0;
     sp.c_hi = 1;
     int rc = launch_step<T>(ctx, sp);
@@ -652,9 +695,12 @@ int ensure_four(wo_ctx* ctx) {
     return WO_OK;
 }
 
-// coef and face arrays of the current material for the two-step kernel
+// coef and face arrays of the current material for the two-step kernel, over
+// the whole allocation (a slab's ghost planes included: its passes recompute
+// one plane beyond each boundary; the top allocated plane's +i face is 0 and
+// never used there)
 int ensure_mat4(wo_ctx* ctx) {
-    const size_t fb = (size_t)ctx->cells() * ctx->itemsize;
+    const size_t fb = (size_t)ctx->alloc_cells() * ctx->itemsize;
     if (!ctx->mat4) {
         int rc = dev_alloc(ctx, (void**)&ctx->mat4, 4 * fb);
         if (rc) return rc;
@@ -662,14 +708,15 @@ int ensure_mat4(wo_ctx* ctx) {
         ctx->mat4_valid = false;
     }
     if (!ctx->mat4_valid) {
-        char* g = ctx->base0(ctx->gamma);
+        char* g = ctx->gamma;
+        const int np = ctx->alloc_planes();
         if (ctx->itemsize == 4)
             launch_material4<float>(ctx->flavor, ctx->stream, reinterpret_cast<const float*>(g),
-                                    mat_scalars<float>(ctx), ctx->kn0, ctx->kn1, ctx->kn2,
+                                    mat_scalars<float>(ctx), np, ctx->kn1, ctx->kn2,
                                     reinterpret_cast<float*>(ctx->mat4));
         else
             launch_material4<double>(ctx->flavor, ctx->stream, reinterpret_cast<const double*>(g),
-                                     mat_scalars<double>(ctx), ctx->kn0, ctx->kn1, ctx->kn2,
+                                     mat_scalars<double>(ctx), np, ctx->kn1, ctx->kn2,
                                      reinterpret_cast<double*>(ctx->mat4));
         ctx->launches++;
         CK(cudaGetLastError());
@@ -697,9 +744,13 @@ int pick_geo(const wo_ctx* ctx) {
 }
 
 bool pair_ready(wo_ctx* ctx) {
-    if (!ctx->use_two_step || !ctx->use_tma || !ctx->use_pair || ctx->has_lo || ctx->has_hi ||
-        ctx->part != 0 ||
+    if (!ctx->use_two_step || !ctx->use_tma || !ctx->use_pair || ctx->part != 0 ||
         !ctx->material_set || pick_geo(ctx) == GEO_NONE)
+        return false;
+    // slabs: two ghost planes at every neighbour and at least two own planes
+    // (the peer stores cover planes 0, 1 and n0-2, n0-1)
+    if ((ctx->has_lo && ctx->gl < 2) || (ctx->has_hi && ctx->gh < 2) ||
+        ((ctx->has_lo || ctx->has_hi) && ctx->kn0 < 2))
         return false;
     // fp64 two-step CTAs need 130 KB of shared memory (1 CTA/SM) and measure
     // slower than the single-step kernel (100.9 vs 106.7 Gcell-upd/s, 256^3):
@@ -709,12 +760,12 @@ bool pair_ready(wo_ctx* ctx) {
     if (ctx->t2_state == 0) {
         ctx->t2_state = -1;
         const int geo = pick_geo(ctx);
-        const uint64_t np = (uint64_t)ctx->kn0;
+        const uint64_t np = (uint64_t)ctx->alloc_planes();   // plane coordinate = p + gl
         const uint32_t tbx = geo == GEO_TALL ? GeoTall::TBX : GeoWide::TBX;
         const uint32_t tby = geo == GEO_TALL ? GeoTall::TBY : GeoWide::TBY;
         const uint32_t hw = tbx + 2 * (ctx->itemsize == 4 ? th_ho<float>() : th_ho<double>());
         const uint32_t r2 = tby + 4, r1 = tby + 2;
-        const size_t fb = (size_t)ctx->cells() * ctx->itemsize;
+        const size_t fb = (size_t)ctx->alloc_cells() * ctx->itemsize;
         bool ok = true;
         for (int b = 0; b < 4; ++b) {
             ok &= make_map(&ctx->t2maps.u_r2[b], ctx->u[b], ctx->itemsize, ctx->kn2, ctx->kn1, np,
@@ -729,7 +780,8 @@ bool pair_ready(wo_ctx* ctx) {
                        np, hw, r2);
         ok &= make_map(&ctx->t2maps.fi_r1, ctx->mat4 + 3 * fb, ctx->itemsize, ctx->kn2, ctx->kn1,
                        np, hw, r1);
-        ok &= make_map(&ctx->t2maps.a_ctr, ctx->acc, ctx->itemsize, ctx->kn2, ctx->kn1, np, tbx, tby);
+        ok &= make_map(&ctx->t2maps.a_ctr, ctx->acc, ctx->itemsize, ctx->kn2, ctx->kn1,
+                       (uint64_t)ctx->kn0, tbx, tby);
         if (ok) {
             ctx->t2_state = 1;
             ++ctx->gen;
@@ -836,7 +888,8 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     a.gamma = reinterpret_cast<const T*>(ctx->base0(ctx->gamma));
     a.u_prev = reinterpret_cast<const T*>(ctx->uprev());
     a.u_cur = reinterpret_cast<const T*>(ctx->ucur());
-    a.fi = reinterpret_cast<const T*>(ctx->mat4 + 3 * (size_t)ctx->cells() * ctx->itemsize);
+    a.fi = reinterpret_cast<const T*>(
+        ctx->base0(ctx->mat4 + 3 * (size_t)ctx->alloc_cells() * ctx->itemsize));
     a.out1 = reinterpret_cast<T*>(ctx->base0(ctx->u[x[0]]));
     a.out2 = reinterpret_cast<T*>(ctx->base0(ctx->u[x[1]]));
     a.acc = reinterpret_cast<T*>(ctx->acc);
@@ -849,14 +902,29 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     a.mat = mat_scalars<T>(ctx);
     a.cv = (T)ctx->cv; a.cg = (T)ctx->cg; a.inv2dt = (T)ctx->inv2dt; a.inv2dx = (T)ctx->inv2dx;
     a.sdt = (T)sp.sdt;
+    a.lo_open = ctx->has_lo;
+    a.hi_open = ctx->has_hi;
+    a.zo = ctx->gl;
+    if (ctx->p2p) {
+        const size_t pb = (size_t)ctx->plane() * ctx->itemsize;
+        const size_t up = (size_t)(ctx->kn0 - 2) * pb;   // own plane n0-2 -> ghost plane -2
+        a.plo1 = reinterpret_cast<T*>(ctx->peer_lo[x[0]]);
+        a.plo2 = reinterpret_cast<T*>(ctx->peer_lo[x[1]]);
+        a.phi1 = ctx->peer_hi[x[0]] ? reinterpret_cast<T*>(ctx->peer_hi[x[0]] - up) : nullptr;
+        a.phi2 = ctx->peer_hi[x[1]] ? reinterpret_cast<T*>(ctx->peer_hi[x[1]] - up) : nullptr;
+    }
     a.n_src = 0;
     for (int s = 0; s < sp.n_src; ++s) {
+        // local (i, j, k); a slab also takes sources on its ghost planes,
+        // whose step n it recomputes
         const long long f = sp.src_flat[s];
         const long long pl = ctx->plane();
-        if (f < 0 || f >= ctx->cells()) continue;
-        a.src_i[a.n_src] = (int)(f / pl);
-        a.src_j[a.n_src] = (int)((f % pl) / ctx->kn2);
-        a.src_k[a.n_src] = (int)(f % ctx->kn2);
+        if (f < -(long long)ctx->gl * pl || f >= ctx->cells() + (long long)ctx->gh * pl) continue;
+        const long long pi = f >= 0 ? f / pl : -((-f + pl - 1) / pl);
+        const long long r = f - pi * pl;
+        a.src_i[a.n_src] = (int)pi;
+        a.src_j[a.n_src] = (int)(r / ctx->kn2);
+        a.src_k[a.n_src] = (int)(r % ctx->kn2);
         a.src_val1[a.n_src] = (T)sp.val1[s];
         a.src_val2[a.n_src] = (T)sp.val2[s];
         a.n_src++;
@@ -886,9 +954,15 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     if (!d_tl) cudaMalloc(&d_tl, (size_t)32 << 20);
     a.timeline = nblk <= (1u << 20) ? d_tl : nullptr;
 #endif
+    if (ctx->p2p) {
+        const int rc = p2p_wait(ctx);
+        if (rc) return rc;
+    }
     prof_begin(ctx, 1);
+    t_no_pdl = ctx->p2p && !p2p_pdl();
     launch_step2_engine<T>(StepSel{ctx->flavor, true, sp.acc, false, sup}, ctx->t2_geo, grid,
                            ctx->stream, a, ctx->t2maps);
+    t_no_pdl = false;
     prof_end(ctx);
 #if WB_T2_TIMELINE
     {
@@ -912,7 +986,7 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     CK(cudaGetLastError());
     ctx->prv = x[0];
     ctx->cur = x[1];
-    return WO_OK;
+    return ctx->p2p ? p2p_signal(ctx) : WO_OK;
 }
 
 template <typename T>
@@ -971,6 +1045,8 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
     const bool gather = ctx->n_sup > 0;
     REQUIRE(ctx->part == 0 || (n_end - n_begin <= 1 && ns <= MAX_SRC && !record),
             "split (boundary / interior) steps go one in-kernel-source step per call");
+    REQUIRE(!ctx->p2p || (ns <= MAX_SRC && !record),
+            "peer-store sweeps take at most 8 in-kernel source nodes and no history");
     if (first && ctx->part != 2) {
         rc = ensure_slots(ctx, N);
         if (rc) return rc;
@@ -980,6 +1056,8 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
             if (rc) return rc;
             CK(cudaMemsetAsync(ctx->store, 0, (size_t)N * ctx->n_sup * sizeof(T), ctx->stream));
         }
+        rc = p2p_epoch_begin(ctx);
+        if (rc) return rc;
     }
     REQUIRE(ctx->maxslot_bytes >= (size_t)(N + 2) * 8 &&
                 (!gather || ctx->store_bytes >= (size_t)N * ctx->n_sup * sizeof(T)),
@@ -991,7 +1069,7 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
     // graph of this sweep: the key covers everything the launches depend on
     // beyond the state generation
     const bool graphable = ctx->use_graphs && !ctx->prof && ctx->part == 0 && !record &&
-                           ns <= MAX_SRC && n_end - n_begin >= 8;
+                           !ctx->p2p && ns <= MAX_SRC && n_end - n_begin >= 8;
     uint64_t gkey = 0;
     bool capturing = false;
     const int64_t l0 = ctx->launches, s0 = ctx->step_launches, p0 = ctx->pair_launches;
@@ -1075,7 +1153,9 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
         rc = graph_capture_end(ctx, 0, gkey, l0, s0, p0);
         if (rc) return rc;
     }
-    if (ctx->part != 0) return WO_OK;   // split steps stay asynchronous
+    // split steps and peer-store ranges stay asynchronous (the neighbours'
+    // sweeps may not be enqueued yet); wo_check_maxima waits
+    if (ctx->part != 0 || (ctx->p2p && !finish)) return WO_OK;
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->prof) harvest_events(ctx);
     if (!finish) return WO_OK;
@@ -1115,14 +1195,23 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
         if (rc) return rc;
         CK(cudaMemsetAsync(ctx->maxslots, 0, (size_t)(N + 2) * 8, ctx->stream));
         std::swap(ctx->cur, ctx->prv);  // swap_direction: u_prev <- u^N, u_cur <- u^{N-1}
+        rc = p2p_epoch_begin(ctx);
+        if (rc) return rc;
     }
     REQUIRE(ctx->maxslot_bytes >= (size_t)(N + 2) * 8, "sweep not initialised");
     long long sf = (long long)src_flat;
+    // no source: any negative index on a single domain; on a slab, negative
+    // indices down to its lowest ghost plane are ghost-plane sources (the
+    // two-step pass recomputes that plane) and WO_NO_SOURCE means none
+    const bool has_src = (ctx->has_lo || ctx->has_hi)
+                             ? src_flat != WO_NO_SOURCE && src_flat >= -(int64_t)ctx->gl * ctx->plane()
+                             : src_flat >= 0;
     double val = 0.0;
     auto bcheck = [](int64_t n) { return (n % STABILITY_CHECK_INTERVAL == 0) || (n == 1); };
     const bool pairs = pair_ready(ctx);
     double val2 = 0.0;
-    const bool graphable = ctx->use_graphs && !ctx->prof && ctx->part == 0 && n_hi - n_lo >= 8;
+    const bool graphable =
+        ctx->use_graphs && !ctx->prof && ctx->part == 0 && !ctx->p2p && n_hi - n_lo >= 8;
     uint64_t gkey = 0;
     bool capturing = false;
     const int64_t l0 = ctx->launches, s0 = ctx->step_launches, p0 = ctx->pair_launches;
@@ -1132,7 +1221,7 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
         kh.val(dt); kh.val(ctx->gen); kh.val(ctx->cur); kh.val(ctx->prv); kh.val(src_flat);
         kh.val((int)sizeof(T));
         hash_param_buffers(kh, ctx);
-        if (src_flat >= 0) kh.bytes(src_amp + n_lo, (size_t)(n_hi - n_lo + 1) * 8);
+        if (has_src) kh.bytes(src_amp + n_lo, (size_t)(n_hi - n_lo + 1) * 8);
         gkey = kh.h;
         if (graph_replay(ctx, 1, gkey)) n_hi = n_lo;   // loop skipped
         else capturing = graph_capture_begin(ctx, 1, gkey);
@@ -1144,7 +1233,7 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
             ps.check1 = bcheck(n);
             ps.check2 = bcheck(n - 1);
             ps.sdt = dt;
-            if (src_flat >= 0) {
+            if (has_src) {
                 val = src_amp[n];
                 val2 = src_amp[n - 1];
                 ps.n_src = 1;
@@ -1164,7 +1253,7 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
         sp.check = bcheck(n);
         sp.backward = 1;
         sp.sdt = dt;
-        if (src_flat >= 0) {
+        if (has_src) {
             val = src_amp[n];
             sp.n_src = 1;
             sp.src_flat = &sf;
@@ -1181,7 +1270,7 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
         rc = graph_capture_end(ctx, 1, gkey, l0, s0, p0);
         if (rc) return rc;
     }
-    if (ctx->part != 0) return WO_OK;   // split steps stay asynchronous
+    if (ctx->part != 0 || (ctx->p2p && !finish)) return WO_OK;
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->prof) harvest_events(ctx);
     if (!finish) return WO_OK;
@@ -1208,6 +1297,7 @@ template <typename T>
 int sweep_adjoint_reference_t(wo_ctx* ctx, int64_t N, double dt, int64_t* fail_step,
                               double* fail_max) {
     REQUIRE(ctx->hist_bytes >= (size_t)(N + 1) * ctx->field_bytes(), "no forward history recorded");
+    REQUIRE(!ctx->p2p, "the reference engine runs on single-domain contexts");
     REQUIRE(ctx->n_sup > 0 && ctx->store_bytes >= (size_t)N * ctx->n_sup * sizeof(T),
             "adjoint store not populated");
     int rc = ensure(ctx, &ctx->u3, &ctx->u3_bytes, ctx->field_bytes());
@@ -1263,6 +1353,7 @@ int sweep_adjoint_reference_t(wo_ctx* ctx, int64_t N, double dt, int64_t* fail_s
 template <typename T>
 int step_t(wo_ctx* ctx, int64_t n_force, const int64_t* idx, const double* vals,
            const double* dense, int want_max, double* max_out) {
+    REQUIRE(!ctx->p2p, "single steps on a peer-store slab: run sweeps (or clear the peers)");
     int rc = ensure_slots(ctx, 1);
     if (rc) return rc;
     CK(cudaMemsetAsync(ctx->maxslots, 0, 8, ctx->stream));
@@ -1437,9 +1528,9 @@ int upload_cast_t(wo_ctx* ctx, const double* host, char* dev, int64_t n) {
 }
 
 int create_common(wo_ctx* ctx) {
-    // the step kernel indexes a context with 32-bit offsets (ghost planes incl.)
-    REQUIRE(ctx->alloc_cells() < (1ll << 31),
-            "grid too large for one context (>= 2^31 cells): use slab decomposition");
+    // plane offsets are 64-bit in every kernel; in-plane offsets and plane
+    // indices stay 32-bit (n1*n2 < 2^31 per plane)
+    REQUIRE(ctx->plane() < (1ll << 31), "plane too large (n1*n2 >= 2^31 cells)");
     CK(cudaSetDevice(ctx->device));
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
@@ -1478,7 +1569,7 @@ static int verify_fast_div_t(wo_ctx* ctx) {
     int* d_ok = reinterpret_cast<int*>(ctx->flag);
     const int one = 1;
     CK(cudaMemcpyAsync(d_ok, &one, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-    const int n0 = ctx->kn0 + ctx->has_lo + ctx->has_hi;
+    const int n0 = ctx->alloc_planes();
     const T* g = reinterpret_cast<const T*>(ctx->gamma);
     if (ctx->flavor == RHO_SCALED)
         verify_material_kernel<T, RHO_SCALED><<<592, 256, 0, ctx->stream>>>(
@@ -1566,6 +1657,13 @@ int wo_create_slab(wo_ctx** out, const int64_t* gshape, int64_t i_begin, int64_t
     ctx->n0g = (int)gshape[0];
     ctx->has_lo = i_begin > 0;
     ctx->has_hi = i_end < gshape[0];
+    // two ghost planes per neighbour (the two-step pass recomputes one plane
+    // beyond the slab and reads one more); one where the global end is closer
+    ctx->gl = (int)std::min<int64_t>(2, i_begin);
+    ctx->gh = (int)std::min<int64_t>(2, gshape[0] - i_end);
+    // two-step passes on slabs only when the caller enables them for every
+    // slab of the decomposition (all slabs must take the same launches)
+    ctx->use_two_step = 0;
     int rc = create_common(ctx);
     if (rc) {
         g_create_error = ctx->err;
@@ -2038,23 +2136,54 @@ int wo_halo_planes(wo_ctx* ctx, void** first, void** last, void** ghost_lo, void
     return WO_OK;
 }
 
+static int ensure_flags(wo_ctx* ctx) {
+    if (ctx->in_flags) return WO_OK;
+    int rc = dev_alloc(ctx, (void**)&ctx->in_flags, 4 * sizeof(unsigned int));
+    if (rc) return rc;
+    // on the context's stream, complete before any neighbour can see the address
+    CK(cudaMemsetAsync(ctx->in_flags, 0, 4 * sizeof(unsigned int), ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return WO_OK;
+}
+
 int wo_slab_ghosts(wo_ctx* ctx, void** ghost_lo, void** ghost_hi, void** flags) {
     int rc = check_ctx(ctx);
     if (rc) return rc;
     REQUIRE(ctx->has_lo || ctx->has_hi, "not a slab context");
-    if (!ctx->in_flags) {
-        rc = dev_alloc(ctx, (void**)&ctx->in_flags, 2 * sizeof(unsigned int));
-        if (rc) return rc;
-        CK(cudaMemset(ctx->in_flags, 0, 2 * sizeof(unsigned int)));
-    }
+    // all four level buffers exist from here on: their ghost planes are what
+    // the neighbours store into, whichever buffers a launch writes
+    if ((rc = ensure_four(ctx))) return rc;
+    if ((rc = ensure_flags(ctx))) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
     const size_t pb = (size_t)ctx->plane() * ctx->itemsize;
     for (int b = 0; b < 4; ++b) {
-        char* u = ctx->u[b];
-        ghost_lo[b] = u && ctx->has_lo ? u : nullptr;
-        ghost_hi[b] = u && ctx->has_hi ? u + (size_t)(ctx->has_lo + ctx->kn0) * pb : nullptr;
+        char* u = ctx->base0(ctx->u[b]);
+        ghost_lo[b] = ctx->has_lo ? u - (size_t)ctx->gl * pb : nullptr;   // plane -gl
+        ghost_hi[b] = ctx->has_hi ? u + (size_t)ctx->kn0 * pb : nullptr;   // plane n0
     }
-    flags[0] = ctx->in_flags;
-    flags[1] = ctx->in_flags + 1;
+    flags[0] = ctx->in_flags;       // bumped by the lower neighbour (+2: odd epochs)
+    flags[1] = ctx->in_flags + 1;   // bumped by the upper neighbour
+    return WO_OK;
+}
+
+// Release every stream that waits on this slab's flags or its neighbours'
+// (set them to the maximum): after an error left a sweep half enqueued, the
+// other slabs' streams would otherwise wait forever.  Their results are void.
+int wo_slab_abort(wo_ctx* ctx) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if (!ctx->in_flags) return WO_OK;
+    cudaStream_t s = nullptr;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaMemsetAsync(ctx->in_flags, 0xff, 4 * sizeof(unsigned int), s);
+    for (unsigned int* f : {ctx->peer_lo_flag, ctx->peer_hi_flag})
+        if (f) {   // the two parity words of the neighbour's flag
+            cudaMemsetAsync(f, 0xff, sizeof(unsigned int), s);
+            cudaMemsetAsync(f + 2, 0xff, sizeof(unsigned int), s);
+        }
+    const cudaError_t e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    CK(e);
     return WO_OK;
 }
 
@@ -2072,9 +2201,15 @@ int wo_slab_peers(wo_ctx* ctx, void* const* lo_ghost, void* const* hi_ghost, voi
     }
     ctx->peer_lo_flag = ctx->has_lo ? static_cast<unsigned int*>(lo_flag) : nullptr;
     ctx->peer_hi_flag = ctx->has_hi ? static_cast<unsigned int*>(hi_flag) : nullptr;
-    REQUIRE(!any || ((!ctx->has_lo || (ctx->peer_lo[0] && ctx->peer_lo[1] && ctx->peer_lo_flag)) &&
-                     (!ctx->has_hi || (ctx->peer_hi[0] && ctx->peer_hi[1] && ctx->peer_hi_flag))),
-            "peer ghost stores need both level buffers and the flag of every neighbour");
+    bool full = true;
+    for (int b = 0; b < 4; ++b)
+        full &= (!ctx->has_lo || ctx->peer_lo[b]) && (!ctx->has_hi || ctx->peer_hi[b]);
+    REQUIRE(!any || (full && (!ctx->has_lo || ctx->peer_lo_flag) &&
+                     (!ctx->has_hi || ctx->peer_hi_flag)),
+            "peer ghost stores need all four level buffers and the flag of every neighbour");
+    REQUIRE(!any || ((!ctx->has_lo || ctx->gl == 2) && (!ctx->has_hi || ctx->gh == 2) &&
+                     ctx->kn0 >= 2),
+            "peer ghost stores need two ghost planes per neighbour and slabs of >= 2 planes");
     // stores into another GPU's memory need peer access from this device
     const void* ptrs[4] = {ctx->peer_lo[0], ctx->peer_hi[0], ctx->peer_lo_flag, ctx->peer_hi_flag};
     for (const void* q : ptrs) {
@@ -2087,14 +2222,14 @@ int wo_slab_peers(wo_ctx* ctx, void* const* lo_ghost, void* const* hi_ghost, voi
             else CK(e);
         }
     }
-    if (any) {   // fresh sequence on every slab before any step (set up all slabs first)
-        if (!ctx->in_flags) {
-            rc = dev_alloc(ctx, (void**)&ctx->in_flags, 2 * sizeof(unsigned int));
-            if (rc) return rc;
-        }
-        CK(cudaMemset(ctx->in_flags, 0, 2 * sizeof(unsigned int)));
+    if (any) {   // fresh flags on every slab before any sweep (wire up all slabs first)
+        if ((rc = ensure_four(ctx))) return rc;
+        if ((rc = ensure_flags(ctx))) return rc;
+        CK(cudaMemsetAsync(ctx->in_flags, 0, 4 * sizeof(unsigned int), ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
     }
     ctx->p2p_seq = 0;
+    ctx->p2p_epoch = 0;
     ctx->p2p = any;
     ++ctx->gen;
     return WO_OK;
@@ -2318,6 +2453,14 @@ int wo_reset_stats(wo_ctx* ctx) {
 }
 
 int64_t wo_device_bytes(const wo_ctx* ctx) { return ctx ? ctx->dev_bytes : 0; }
+
+int wo_field_buffers(const wo_ctx* ctx) {
+    if (!ctx) return 0;
+    int n = 0;
+    for (const char* p : {ctx->gamma, ctx->u[0], ctx->u[1], ctx->u[2], ctx->u[3], ctx->acc, ctx->u3})
+        n += p ? 1 : 0;
+    return n + (ctx->mat4 ? 4 : 0);
+}
 
 int64_t wo_pair_launches(const wo_ctx* ctx) { return ctx ? ctx->pair_launches : 0; }
 

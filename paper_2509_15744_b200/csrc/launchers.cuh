@@ -24,6 +24,11 @@ struct StepSel {
     int sup;      // SUP_NONE / SUP_GATHER / SUP_INJECT (TMA engines)
 };
 
+// Plain launches instead of programmatic dependent launch on this thread
+// (set by the C ABI around launches that stream memory operations separate:
+// peer-store slabs; defined in capi.cu).
+extern thread_local bool t_no_pdl;
+
 template <typename T>
 void launch_step_engine(int engine, const StepSel& k, dim3 grid, dim3 block, cudaStream_t s,
                         const StepArgs<T>& a, const TmaMaps& maps);

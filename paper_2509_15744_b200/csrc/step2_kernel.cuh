@@ -147,6 +147,14 @@ template <typename T> struct Step2Args {
     typename FTraits<T>::Bits* max1;
     typename FTraits<T>::Bits* max2;
     unsigned long long negz;   // (-0.0f, -0.0f) bits, opaque to ptxas (packed fp32 products)
+    // slab contexts: neighbours below / above (two ghost planes each side in
+    // the level buffers and the material; TMA plane coordinate = p + zo) and
+    // the peer ghost stores of the results (see StepArgs::plo / phi)
+    int lo_open, hi_open, zo;
+    T* plo1;
+    T* phi1;
+    T* plo2;
+    T* phi2;
     unsigned long long* timeline;   // WB_T2_TIMELINE builds only: 4 words per CTA
 };
 
@@ -236,14 +244,17 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     const int k0 = blockIdx.x * TBX, j0 = blockIdx.y * TBY;
     const int kA = k0 + 2 * tx, ja = j0 + 2 * ty;
     const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
-    const int plane = n1 * n2;
+    const long long plane = (long long)n1 * n2;   // 64-bit plane offsets: grids of >= 2^31 cells
     const int i0 = a.zb[blockIdx.z];
     const int i1 = a.zb[blockIdx.z + 1];
-    const int pbeg = max(i0 - 1, 0);           // step-n planes of this chunk
-    const int pfin = min(i1, n0 - 1);
+    // step-n planes of this chunk: one recomputed plane beyond each end
+    // (a ghost plane at a slab boundary; none at the global ends)
+    const int pbeg = (i0 > 0 || a.lo_open) ? i0 - 1 : 0;
+    const int pfin = (i1 < n0 || a.hi_open) ? i1 : n0 - 1;
     // planes streamed through the ring: pbeg .. pfin, plus pfin+1 (u^n of the
     // chunk end's upper neighbour) so no chunk stalls on a global load
-    const int plast = min(pfin + 1, n0 - 1);
+    const int plast = min(pfin + 1, a.hi_open ? n0 + 1 : n0 - 1);
+    const int zo = a.zo;
 
     // ---- per-thread offsets in the R2 frame (rows j0-2.., cols k0-HO..) ----
     // tile rows a, b; clamped (mirrored) outer neighbours at the grid edge.
@@ -287,18 +298,18 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     // L2 prefetch of a later plane's boxes (no shared memory; hides DRAM
     // latency beyond the T2_NS-stage ring)
     auto prefetch_at = [&](int kk0, int jj0, int p) {
-        auto pf = [&](const CUtensorMap* m, int c0, int c1) {
+        auto pf = [&](const CUtensorMap* m, int c0, int c1, int c2) {
             asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
-                         ::"l"(reinterpret_cast<unsigned long long>(m)), "r"(c0), "r"(c1), "r"(p)
+                         ::"l"(reinterpret_cast<unsigned long long>(m)), "r"(c0), "r"(c1), "r"(c2)
                          : "memory");
         };
-        pf(mU, kk0 - HO, jj0 - 2);
-        pf(&maps.fj_r2, kk0 - HO, jj0 - 2);
-        pf(mP, kk0 - HO, jj0 - 1);
-        pf(&maps.c_r1, kk0 - HO, jj0 - 1);
-        pf(&maps.fk_r1, kk0 - HO, jj0 - 1);
-        pf(&maps.fi_r1, kk0 - HO, jj0 - 1);
-        if (ACC) pf(&maps.a_ctr, kk0, jj0);
+        pf(mU, kk0 - HO, jj0 - 2, p + zo);
+        pf(&maps.fj_r2, kk0 - HO, jj0 - 2, p + zo);
+        pf(mP, kk0 - HO, jj0 - 1, p + zo);
+        pf(&maps.c_r1, kk0 - HO, jj0 - 1, p + zo);
+        pf(&maps.fk_r1, kk0 - HO, jj0 - 1, p + zo);
+        pf(&maps.fi_r1, kk0 - HO, jj0 - 1, p + zo);
+        if (ACC) pf(&maps.a_ctr, kk0, jj0, p);
     };
     auto prefetch = [&](int p) { prefetch_at(k0, j0, p); };
     // the block that will most likely take this block's slot when it ends
@@ -311,17 +322,20 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     if (has_next) {
         nk0 = (nblk % gridDim.x) * TBX;
         nj0 = ((nblk / gridDim.x) % gridDim.y) * TBY;
-        npb = max(a.zb[nblk / (gridDim.x * gridDim.y)] - 1, 0);
+        const int nz0 = a.zb[nblk / (gridDim.x * gridDim.y)];
+        npb = (nz0 > 0 || a.lo_open) ? nz0 - 1 : 0;
     }
     auto issue = [&](int p, int s) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[s], STAGE_BYTES);
-        tma_load_3d(&st[s].U[0][0], mU, k0 - HO, j0 - 2, p, &bar[s]);
-        tma_load_3d(&st[s].FJ[0][0], &maps.fj_r2, k0 - HO, j0 - 2, p, &bar[s]);
-        tma_load_3d(&st[s].P[0][0], mP, k0 - HO, j0 - 1, p, &bar[s]);
-        tma_load_3d(&st[s].C[0][0], &maps.c_r1, k0 - HO, j0 - 1, p, &bar[s]);
-        tma_load_3d(&st[s].FK[0][0], &maps.fk_r1, k0 - HO, j0 - 1, p, &bar[s]);
-        tma_load_3d(&st[s].FI[0][0], &maps.fi_r1, k0 - HO, j0 - 1, p, &bar[s]);
+        tma_load_3d(&st[s].U[0][0], mU, k0 - HO, j0 - 2, p + zo, &bar[s]);
+        tma_load_3d(&st[s].FJ[0][0], &maps.fj_r2, k0 - HO, j0 - 2, p + zo, &bar[s]);
+        tma_load_3d(&st[s].P[0][0], mP, k0 - HO, j0 - 1, p + zo, &bar[s]);
+        tma_load_3d(&st[s].C[0][0], &maps.c_r1, k0 - HO, j0 - 1, p + zo, &bar[s]);
+        tma_load_3d(&st[s].FK[0][0], &maps.fk_r1, k0 - HO, j0 - 1, p + zo, &bar[s]);
+        tma_load_3d(&st[s].FI[0][0], &maps.fi_r1, k0 - HO, j0 - 1, p + zo, &bar[s]);
+        // acc holds the own planes only (a ghost plane's box reads as zeros
+        // and is never used)
         if (ACC) tma_load_3d(&st[s].A[0][0], &maps.a_ctr, k0, j0, p, &bar[s]);
     };
     if (tid == 0) {
@@ -405,7 +419,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         return add2(accv, mul2(sdt, add2(mul2(mul2(cv, va, NZ), va, NZ), mul2(cg, gg, NZ)), NZ));
     };
     // nodal force coefficient of a cell from its gamma (sparse; solver.py:98,110)
-    auto fcoef = [&](int flat) {
+    auto fcoef = [&](long long flat) {
         const T g = __ldg(a.gamma + flat);
         T kap;
         (void)MP::coef(a.mat, g, kap);
@@ -420,9 +434,9 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     // support bit / compact index of cell (p, jj, kk)
     auto sup_index = [&](int p, int jj, int kk) -> int {
         if (SUP == SUP_NONE || p < a.sup_lo || p > a.sup_hi) return -1;
-        const unsigned flat = (unsigned)(p * plane + jj * n2 + kk);
+        const unsigned long long flat = (unsigned long long)(p * plane + jj * n2 + kk);
         const unsigned w = __ldg(a.sup_mask + (flat >> 5));
-        const unsigned bit = flat & 31u;
+        const unsigned bit = (unsigned)(flat & 31u);
         if (!((w >> bit) & 1u)) return -1;
         return __ldg(a.sup_prefix + (flat >> 5)) + __popc(w & ((1u << bit) - 1u));
     };
@@ -452,7 +466,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
 
     // ---------------- prologue: plane pbeg ----------------
     const int cofs = ja * n2 + kA;
-    const bool has_m0 = pbeg > 0;
+    const bool has_m0 = pbeg - 1 >= (a.lo_open ? -2 : 0);   // plane pbeg-1 (ghost or real)
     auto ring_gofs = [&](int t) {   // global offset (in plane) of ring slot t
         const int r = oR[t] / W, c = oR[t] - r * W;
         return (r + j0 - 2) * n2 + (c + k0 - HO);
@@ -460,7 +474,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     V unm_a, unm_b, w0_a = {T(0), T(0)}, w0_b = {T(0), T(0)};   // plane pbeg-1 (mirror at 0)
     T rum[2] = {T(0), T(0)}, rw0[2] = {T(0), T(0)};
     if (has_m0) {
-        const int gm = (pbeg - 1) * plane;
+        const long long gm = (pbeg - 1) * plane;
         unm_a = __ldg(reinterpret_cast<const V*>(a.u_cur + gm + cofs));
         unm_b = __ldg(reinterpret_cast<const V*>(a.u_cur + gm + cofs + n2));
         w0_a = __ldg(reinterpret_cast<const V*>(a.fi + gm + cofs));
@@ -512,7 +526,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
             o2a = upk2(ra);
             o2b = upk2(rb);
             tile_inject(q1, o2a, o2b, x_0a, x_0b, a.src_val2, a.row2, true);
-            const int oc = q1 * plane + cofs;
+            const long long oc = q1 * plane + cofs;
             if (ACC) {
                 const f2x fa = kinc2(pk2(acc1_a), pk2(o2a), pk2(un1_a), pk2(xp_a), pk2(x_m1a),
                                      pk2(x_0b), pk2(xu), kpa, kma);
@@ -535,7 +549,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         o2b.y = cell(x_0b.y, xp_b.y, x_m1b.y, xd.y, x_0a.y, xRb, x_0b.x, w1hi_b.y, w1lo_b.y,
                      f1_jhi.y, f1_jab.y, f1_kRb, f1_kIb, c1_b.y, un1_b.y);
         tile_inject(q1, o2a, o2b, x_0a, x_0b, a.src_val2, a.row2, true);
-        const int oc = q1 * plane + cofs;
+        const long long oc = q1 * plane + cofs;
         if (ACC) {
             V fa, fb;
             fa.x = kinc(acc1_a.x, o2a.x, un1_a.x, xp_a.x, x_m1a.x, x_0b.x, xu.x, x_0a.y, xLa);
@@ -549,6 +563,18 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         stg(a.out1 + oc + n2, x_0b);
         stg(a.out2 + oc, o2a);
         stg(a.out2 + oc + n2, o2b);
+        }
+        // slab boundary planes: both new levels also go straight into the
+        // neighbour's ghost planes (NVLink stores across GPUs)
+        if (q1 < 2 && a.plo1) {
+            const long long oc = q1 * plane + cofs;
+            stg(a.plo1 + oc, x_0a); stg(a.plo1 + oc + n2, x_0b);
+            stg(a.plo2 + oc, o2a); stg(a.plo2 + oc + n2, o2b);
+        }
+        if (q1 >= n0 - 2 && a.phi1) {
+            const long long oc = q1 * plane + cofs;
+            stg(a.phi1 + oc, x_0a); stg(a.phi1 + oc + n2, x_0b);
+            stg(a.phi2 + oc, o2a); stg(a.phi2 + oc + n2, o2b);
         }
         if (a.check2) {
             Bits m1 = Tr::abs_bits(o2a.x), m2 = Tr::abs_bits(o2a.y);
@@ -688,7 +714,8 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         un1_a = un0_a; un1_b = un0_b;
         // u^{n+1} queue; at the global bottom plane the "previous" plane is
         // the mirror (the plane itself)
-        x_m1a = p == 0 ? oa : x_0a; x_m1b = p == 0 ? ob : x_0b;
+        const bool gbot = p == 0 && !a.lo_open;
+        x_m1a = gbot ? oa : x_0a; x_m1b = gbot ? ob : x_0b;
         x_0a = oa; x_0b = ob;
         // step-n queue
         unm_a = un0_a; unm_b = un0_b; un0_a = unp_a; un0_b = unp_b;

@@ -57,6 +57,11 @@ template <typename T> struct StepArgs {
     const T* u_cur;     // u^n
     T* u_out;           // may alias u_prev
     T* hist_out;        // optional second copy of u_out (full-history recording)
+    // peer ghost stores (slab contexts with neighbours, wo_slab_peers): planes
+    // 0, 1 also go to plo + offset (the lower neighbour's top ghost planes),
+    // planes n0-2, n0-1 to phi + offset (the upper neighbour's bottom ghosts)
+    T* plo;
+    T* phi;
     T* acc;             // kernel accumulator (ACC only)
     int n0, n1, n2;     // local extents (n0 = planes of this slab)
     int i_lo, i_hi;     // loadable local planes: [-1 if ghost below, n0 (+1 if ghost above))
@@ -102,7 +107,7 @@ step_kernel(const StepArgs<T> a) {
     const int k = k0 + tx, j = j0 + ty;
     const int n1 = a.n1, n2 = a.n2;
     const bool inb = (j < n1) && (k < n2);
-    const int plane = n1 * n2;
+    const long long plane = (long long)n1 * n2;   // 64-bit plane offsets: grids of >= 2^31 cells
     const int i0 = a.c_lo + blockIdx.z * a.chunk;   // computed planes [c_lo, c_hi)
     const int i1 = min(i0 + a.chunk, a.c_hi);
     const MatScalars<T>& M = a.mat;
@@ -170,11 +175,11 @@ step_kernel(const StepArgs<T> a) {
     auto body = [&](auto parity, int i) {
         constexpr int b = decltype(parity)::value, nb = b ^ 1;
         const bool next = i + 1 < i1;
-        const int oc = i * plane;
+        const long long oc = i * plane;
 
         // ---- loads for the next iteration (clamped: always in bounds) ----
-        const int on = min(i + 1, last) * plane;
-        const int o2 = pc(i + 2);
+        const long long on = min(i + 1, last) * plane;
+        const long long o2 = pc(i + 2);
         const T up_n = ldg(pP + on);
         const T acc_n = ACC ? pA[on] : T(0);
         const T u_p2 = ldg(pU + o2);
@@ -228,9 +233,9 @@ step_kernel(const StepArgs<T> a) {
                     out = out + MT::fc(M, g_0, kappa) * a.src_val[s];
         }
         if (a.sup_mode != SUP_NONE && i >= a.sup_lo && i <= a.sup_hi && inb) {
-            const unsigned int flat = (unsigned int)(oc + cofs);
+            const unsigned long long flat = (unsigned long long)(oc + cofs);
             const unsigned int w = __ldg(a.sup_mask + (flat >> 5));
-            const unsigned int bit = flat & 31u;
+            const unsigned int bit = (unsigned int)(flat & 31u);
             if ((w >> bit) & 1u) {
                 const int s = __ldg(a.sup_prefix + (flat >> 5)) + __popc(w & ((1u << bit) - 1u));
                 if (a.sup_mode == SUP_GATHER) a.trace_row[s] = u_0;
@@ -252,6 +257,8 @@ step_kernel(const StepArgs<T> a) {
         if (inb) {
             pO[oc] = out;
             if (pH) pH[oc] = out;
+            if (i < 2 && a.plo) a.plo[oc + cofs] = out;
+            if (i >= a.n0 - 2 && a.phi) a.phi[oc + cofs] = out;
             if (CHECK) {
                 const typename Tr::Bits bits = Tr::abs_bits(out);
                 local_max = bits > local_max ? bits : local_max;

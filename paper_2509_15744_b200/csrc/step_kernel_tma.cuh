@@ -129,7 +129,7 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
     const int k0 = blockIdx.x * PBX, j0 = blockIdx.y * BY;
     const int kA = k0 + 2 * tx, j = j0 + ty;
     const int n1 = a.n1, n2 = a.n2;
-    const int plane = n1 * n2;
+    const long long plane = (long long)n1 * n2;   // 64-bit plane offsets: grids of >= 2^31 cells
     const int i0 = a.c_lo + blockIdx.z * a.chunk;   // computed planes [c_lo, c_hi)
     const int i1 = min(i0 + a.chunk, a.c_hi);
     const int plast = a.i_hi - 1;              // last loadable local plane
@@ -293,11 +293,11 @@ step_kernel_tma(const __grid_constant__ StepArgs<T> a, const __grid_constant__ T
                 if (kA + 1 == a.src_k[s]) out.y = out.y + MT::fc(M, g_0.y, kapB) * a.src_val[s];
             }
         }
-        const int oc = i * plane + cofs;
+        const long long oc = i * plane + cofs;
         if (SUP != SUP_NONE && i >= a.sup_lo && i <= a.sup_hi) {
-            const unsigned int flat = (unsigned int)oc;
+            const unsigned long long flat = (unsigned long long)oc;
             const unsigned int w = __ldg(a.sup_mask + (flat >> 5));
-            const unsigned int bit = flat & 31u;
+            const unsigned int bit = (unsigned int)(flat & 31u);
             const unsigned int two = (w >> bit) & 3u;
             if (two) {
                 const int s = __ldg(a.sup_prefix + (flat >> 5)) + __popc(w & ((1u << bit) - 1u));

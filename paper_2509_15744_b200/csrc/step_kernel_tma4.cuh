@@ -61,7 +61,7 @@ step_kernel_tma4(const __grid_constant__ StepArgs<T> a, const __grid_constant__ 
     const int k0 = blockIdx.x * PBX, j0 = blockIdx.y * BY;
     const int kA = k0 + 2 * tx, ja = j0 + 2 * ty;
     const int n1 = a.n1, n2 = a.n2;
-    const int plane = n1 * n2;
+    const long long plane = (long long)n1 * n2;   // 64-bit plane offsets: grids of >= 2^31 cells
     const int i0 = a.c_lo + blockIdx.z * a.chunk;   // computed planes [c_lo, c_hi)
     const int i1 = min(i0 + a.chunk, a.c_hi);
     const int plast = a.i_hi - 1;
@@ -254,13 +254,13 @@ step_kernel_tma4(const __grid_constant__ StepArgs<T> a, const __grid_constant__ 
                 if (dj == 1 && dk == 1) ob.y = ob.y + MT::fc(M, g0_b.y, kap[3]) * a.src_val[q];
             }
         }
-        const int oc = i * plane + cofs;
+        const long long oc = i * plane + cofs;
         if (SUP != SUP_NONE && i >= a.sup_lo && i <= a.sup_hi) {
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
-                const unsigned int flat = (unsigned int)(oc + r * n2);
+                const unsigned long long flat = (unsigned long long)(oc + r * n2);
                 const unsigned int w = __ldg(a.sup_mask + (flat >> 5));
-                const unsigned int bit = flat & 31u;
+                const unsigned int bit = (unsigned int)(flat & 31u);
                 const unsigned int two = (w >> bit) & 3u;
                 if (two) {
                     V& o = r ? ob : oa;
@@ -291,6 +291,8 @@ step_kernel_tma4(const __grid_constant__ StepArgs<T> a, const __grid_constant__ 
         }
         stv(a.u_out + oc, oa);
         stv(a.u_out + oc + n2, ob);
+        if (i < 2 && a.plo) { stv(a.plo + oc, oa); stv(a.plo + oc + n2, ob); }
+        if (i >= a.n0 - 2 && a.phi) { stv(a.phi + oc, oa); stv(a.phi + oc + n2, ob); }
         if (CHECK) {
             typename Tr::Bits m1 = Tr::abs_bits(oa.x), m2 = Tr::abs_bits(oa.y);
             typename Tr::Bits m3 = Tr::abs_bits(ob.x), m4 = Tr::abs_bits(ob.y);

@@ -45,7 +45,7 @@ step_kernel_pair(const StepArgs<T> a) {
     const int n1 = a.n1, n2 = a.n2;
     const bool oob = kA >= n2;                 // pair beyond the row: mirror of the last cell
     const bool inb = (j < n1) && !oob;
-    const int plane = n1 * n2;
+    const long long plane = (long long)n1 * n2;   // 64-bit plane offsets: grids of >= 2^31 cells
     const int i0 = a.c_lo + blockIdx.z * a.chunk;   // computed planes [c_lo, c_hi)
     const int i1 = min(i0 + a.chunk, a.c_hi);
     const MatScalars<T>& M = a.mat;
@@ -85,7 +85,7 @@ step_kernel_pair(const StepArgs<T> a) {
         if (oob) v.x = v.y;
         return v;
     };
-    auto ldh = [&](const T* base, int o) {       // halo load (scalar or pair role)
+    auto ldh = [&](const T* base, long long o) {       // halo load (scalar or pair role)
         V v;
         if (hk_role) { v.x = __ldg(base + o + hofs); v.y = v.x; }
         else v = __ldg(reinterpret_cast<const V*>(base + o + hofs));
@@ -148,11 +148,11 @@ step_kernel_pair(const StepArgs<T> a) {
     auto body = [&](auto parity, int i) {
         constexpr int b = decltype(parity)::value, nb = b ^ 1;
         const bool next = i + 1 < i1;
-        const int oc = i * plane + cofs;
+        const long long oc = i * plane + cofs;
 
         // loads for the next iteration (clamped, always in bounds)
-        const int on = min(i + 1, last) * plane;
-        const int o2 = pc(i + 2);
+        const long long on = min(i + 1, last) * plane;
+        const long long o2 = pc(i + 2);
         const V up_n = __ldg(reinterpret_cast<const V*>(a.u_prev + on + cofs));
         const V acc_n = ACC ? *reinterpret_cast<const V*>(a.acc + on + cofs) : V{};
         const V u_p2 = ldv(a.u_cur + o2 + cofs);
@@ -217,9 +217,9 @@ step_kernel_pair(const StepArgs<T> a) {
             }
         }
         if (a.sup_mode != SUP_NONE && i >= a.sup_lo && i <= a.sup_hi && inb) {
-            const unsigned int flat = (unsigned int)oc;       // even: A and B share a word
+            const unsigned long long flat = (unsigned long long)oc;       // even: A and B share a word
             const unsigned int w = __ldg(a.sup_mask + (flat >> 5));
-            const unsigned int bit = flat & 31u;
+            const unsigned int bit = (unsigned int)(flat & 31u);
             const unsigned int two = (w >> bit) & 3u;
             if (two) {
                 const int s = __ldg(a.sup_prefix + (flat >> 5)) + __popc(w & ((1u << bit) - 1u));
@@ -256,6 +256,8 @@ step_kernel_pair(const StepArgs<T> a) {
         if (inb) {
             *reinterpret_cast<V*>(a.u_out + oc) = out;
             if (a.hist_out) *reinterpret_cast<V*>(a.hist_out + oc) = out;
+            if (i < 2 && a.plo) *reinterpret_cast<V*>(a.plo + oc) = out;
+            if (i >= a.n0 - 2 && a.phi) *reinterpret_cast<V*>(a.phi + oc) = out;
             if (CHECK) {
                 typename Tr::Bits bx = Tr::abs_bits(out.x), by = Tr::abs_bits(out.y);
                 bx = bx > by ? bx : by;

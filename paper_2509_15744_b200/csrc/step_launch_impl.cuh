@@ -32,6 +32,10 @@ void smem_opt_in(size_t bytes) {
 template <typename Kernel, typename A, typename M>
 void launch_pdl(Kernel kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, const A& a,
                 const M& maps) {
+    if (t_no_pdl) {
+        kernel<<<grid, block, smem, s>>>(a, maps);
+        return;
+    }
 #if WB_T2_PDL
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;

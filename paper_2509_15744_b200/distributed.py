@@ -3,21 +3,24 @@
 slab decomposition (SlabGradient)
     The grid is cut along axis 0 (outermost, so a halo is one contiguous
     n1*n2 plane).  Each slab context (``wo_create_slab``) holds its planes plus
-    one ghost plane per interior face; the step kernels read ghost planes
+    two ghost planes per interior face; the step kernels read ghost planes
     exactly like interior planes and mirror only at the global ends, so the
     per-cell arithmetic is unchanged and the gradient, traces and adjoint
-    store are BITWISE equal to one GPU.  Every step each slab sends its
-    first/last plane of the new level to its neighbours' ghost planes; by
+    store are BITWISE equal to one GPU.  With the exchange halos every step
+    each slab sends its first/last plane of the new level to its neighbours'
+    ghost planes; by
     default (``overlap``) a step runs as its two boundary planes, then the
     exchange is started, then the interior planes are updated while the
     planes travel, and the next step waits for the exchange (WO_OPT_PLANE_PART;
     NCCL is ordered on the context's stream, no host synchronisation):
       * ``LoopbackHalo`` — all slabs in one process (same device or peer
         devices), ``wo_exchange_local`` copies;
-      * ``PeerHalo`` — all slabs in one process, no exchange at all: the
-        boundary launches store their planes straight into the neighbours'
-        ghost planes (NVLink stores between GPUs) and signal them with a
-        device flag the neighbour's stream waits on (``wo_slab_peers``);
+      * ``PeerHalo`` — all slabs in one process, no exchange at all: every
+        launch stores its boundary planes straight into the neighbours' two
+        ghost planes (NVLink stores between GPUs) and signals them with a
+        device flag the neighbour's next launch waits on (``wo_slab_peers``);
+        whole sweeps are enqueued on every slab without returning to Python,
+        and two-step passes run on slabs too (two ghost planes deep);
       * ``TorchHalo`` — one slab per process (torchrun), torch.distributed
         point-to-point send/recv of the plane tensors (NCCL over NVLink on
         GPUs; the same code runs on gloo/CPU tensors in the tests);
@@ -44,6 +47,7 @@ import math
 
 import numpy as np
 
+from . import _native as N
 from . import engine
 from .engine import SolverInstabilityError, source_amplitude_table
 from .grids import ConfigError, precision_dtype
@@ -81,6 +85,43 @@ def localize(flat, shape, i0, i1):
     i = flat // plane
     owned = (i >= i0) & (i < i1)
     return owned, flat[owned] - i0 * plane
+
+
+def recomputed_planes(slabs):
+    """Global planes a two-step slab pass recomputes beyond the slab
+    boundaries: b-1 (by the slab above) and b (by the slab below) for every
+    interior boundary b."""
+    out = set()
+    for i0, _ in list(slabs)[1:]:
+        out.update((i0 - 1, i0))
+    return out
+
+
+def two_step_slabs_ok(slabs, plane, supports):
+    """Whether every slab of the decomposition may run two-step passes with
+    peer ghost stores: at least two planes per slab (two ghost planes per
+    neighbour, peer stores of planes 0, 1 / n0-2, n0-1) and no support node on
+    a recomputed plane (its adjoint force lives in the neighbour's store;
+    sources there are injected by the kernels themselves).  All slabs decide
+    alike, as their launches must match one for one."""
+    if any(i1 - i0 < 2 for i0, i1 in slabs):
+        return False
+    bad = recomputed_planes(slabs)
+    for sup in supports:
+        planes = np.unique(np.asarray(sup, dtype=np.int64) // int(plane))
+        if any(int(p) in bad for p in planes):
+            return False
+    return True
+
+
+def local_source(g_src, plane, alloc_range, i_begin):
+    """Slab-local flat index of a global source node when it lies on the
+    slab's own or ghost planes (a two-step pass recomputes one plane beyond
+    the slab, sources included), else None."""
+    lo, hi = alloc_range
+    if lo * plane <= g_src < hi * plane:
+        return int(g_src - i_begin * plane)
+    return None
 
 
 def first_failure_forward(maxima, n_steps, scale):
@@ -190,7 +231,7 @@ class PeerHalo(LoopbackHalo):
                              lo_flag=lo[2][1] if lo else 0, hi_flag=hi[2][0] if hi else 0)
 
     def exchange(self):
-        raise ConfigError("PeerHalo moves planes inside split steps (overlap=True)")
+        raise ConfigError("PeerHalo moves planes inside the sweeps' launches")
 
     def begin(self):
         return []
@@ -271,12 +312,13 @@ def ipc_peer_wiring(rank, world, exports):
 
 
 class IpcPeerHalo(TorchHalo):
-    """One slab per process, no exchange step: the boundary launches store
-    their planes into the neighbour processes' ghost planes through CUDA IPC
-    mappings and bump their flags (``wo_slab_peers``), like PeerHalo.  Setup
-    is one all-gather of the exported handles; the stability / cost
-    all-reduces of TorchHalo stay (they also order a rank's next window reset
-    after its neighbours' last stores into it)."""
+    """One slab per process, no exchange step: every launch stores its
+    boundary planes into the neighbour processes' ghost planes through CUDA
+    IPC mappings and bumps their flags (``wo_slab_peers``), like PeerHalo.
+    Setup is one all-gather of the exported handles.  Each sweep is a flag
+    epoch whose first signal follows the rank's window reset (so no
+    neighbour store lands before it); the stability / cost all-reduces of
+    TorchHalo separate consecutive epochs, which the flag-slot reuse needs."""
 
     def __init__(self, ctx, rank, world, group=None):
         import torch.distributed as dist
@@ -298,7 +340,7 @@ class IpcPeerHalo(TorchHalo):
         dist.barrier(group=group)   # every slab's flags reset before anyone steps
 
     def exchange(self):
-        raise ConfigError("IpcPeerHalo moves planes inside split steps (overlap=True)")
+        raise ConfigError("IpcPeerHalo moves planes inside the sweeps' launches")
 
     def begin(self):
         return []
@@ -331,10 +373,9 @@ class SlabGradient:
         self.dtype = precision_dtype(config.precision)
         devices = devices or [0] * len(slabs)
         self.slabs = list(slabs)
+        self.all_slabs = list(slabs)   # the whole decomposition (for_rank: every rank's)
         self.ctxs = [engine.DeviceGrid(grid, self.dtype, d, slab=s)
                      for s, d in zip(self.slabs, devices)]
-        if halo == "peer" and not overlap:
-            raise ConfigError("peer ghost stores run split steps (overlap=True)")
         if halo == "loopback":
             self.halo = LoopbackHalo(self.ctxs)
         elif halo == "peer":
@@ -356,20 +397,101 @@ class SlabGradient:
         needs overlap)."""
         if halo not in ("nccl", "ipc"):
             raise ConfigError(f"unknown rank halo {halo!r}")
-        if halo == "ipc" and not overlap:
-            raise ConfigError("peer ghost stores run split steps (overlap=True)")
         slab = slab_ranges(problem.grid.shape[0], world)[rank]
         dev = rank if device is None else device
         obj = cls(problem, material, config, [slab], [dev], halo=None, overlap=overlap)
+        obj.all_slabs = slab_ranges(problem.grid.shape[0], world)
         make = IpcPeerHalo if halo == "ipc" else TorchHalo
         obj.halo = make(obj.ctxs[0], rank, world, group)
         return obj
 
-    def upload(self):
+    @property
+    def peer_stores(self):
+        """Whole sweeps with in-kernel peer ghost stores (PeerHalo /
+        IpcPeerHalo with neighbours) instead of per-step exchanges."""
+        h = self.halo
+        return isinstance(h, PeerHalo) or (isinstance(h, IpcPeerHalo) and h.world > 1)
+
+    def upload(self, material=None, gamma_local=None):
+        """Material onto every slab (own + ghost planes; gamma_local: per
+        context, its planes as contiguous fp64 host arrays); decides two-step
+        passes for the whole decomposition."""
         dt = self.problem.time.dt
+        for i, c in enumerate(self.ctxs):
+            c.set_material(self.material if material is None else material, dt,
+                           None if gamma_local is None else gamma_local[i])
+        grid = self.problem.grid
+        n0 = grid.shape[0]
+        solo = all(i0 == 0 and i1 == n0 for i0, i1 in self.all_slabs)   # no neighbours
+        self.two_step = (self.peer_stores or solo) and two_step_slabs_ok(
+            self.all_slabs, grid.shape[1] * grid.shape[2], [s.support_idx for _, s in self._shots])
         for c in self.ctxs:
-            c.set_material(self.material, dt)
+            c.set_two_step(1 if self.two_step else 0)
         return self
+
+    def set_measured(self, measured):
+        """New measured traces [n_shots, n_support, N] for the FWI shots."""
+        from .gradients import _shot_list
+
+        self.problem.measured = np.asarray(measured, dtype=np.float64)
+        self._shots = _shot_list(self.problem)
+
+    def _forward_all(self, n_steps, src_local, amp, accumulate, dt):
+        no_src = np.zeros((0, n_steps))
+        if self.peer_stores:   # whole sweeps, enqueued on every slab, then awaited
+            for c, s in zip(self.ctxs, src_local):
+                c.sweep_forward_range(n_steps, 1, n_steps, [] if s is None else [s],
+                                      no_src if s is None else amp, accumulate, dt)
+        else:
+            for n in range(1, n_steps):
+                self._steps(lambda c, s, _n=n: c.sweep_forward_range(
+                    n_steps, _n, _n + 1, [] if s is None else [s],
+                    no_src if s is None else amp, accumulate, dt), src_local)
+
+    def record_traces(self, material):
+        """Forward solves of `material` (one per shot, the shots' sources) with
+        u^n recorded at this process's support nodes: traces [n_shots,
+        n_support, N] in the problem's support order, rows of nodes owned by
+        other processes left 0 — the slab form of synthesize_measurements
+        with refine = 1 (fwi.py:121-168; the bench's C5 truth).  The material
+        of the gradient evaluations is restored afterwards."""
+        self.upload(material)
+        n_steps = self.problem.time.n_steps
+        out = np.zeros((len(self._shots), len(self._shots[0][1].support_idx), n_steps))
+        self._guarded(self._record, material, out)
+        return out
+
+    def _record(self, material, out):
+        from .solver import injection_scale
+
+        problem, grid = self.problem, self.problem.grid
+        n_steps, dt = problem.time.n_steps, problem.time.dt
+        plane = grid.shape[1] * grid.shape[2]
+        try:
+            for si, (source, shot) in enumerate(self._shots):
+                g_src = grid.flat_index(source.node)
+                amp = source_amplitude_table([source], dt, n_steps)
+                scale = injection_scale([source], material, dt, self.dtype) * n_steps
+                owned_rows = []
+                for c in self.ctxs:
+                    owned, local = localize(shot.support_idx, grid.shape, c.i_begin, c.i_end)
+                    order = c.set_support(local)
+                    owned_rows.append((np.flatnonzero(owned), order))
+                    c.reset_window()
+                src_local = [local_source(g_src, plane, c.alloc_range, c.i_begin)
+                             for c in self.ctxs]
+                self._forward_all(n_steps, src_local, amp, False, dt)
+                maxima = self.halo.allreduce_max(
+                    np.max([c.check_maxima(n_steps) for c in self.ctxs], axis=0))
+                fail, _ = first_failure_forward(maxima, n_steps, scale)
+                if fail:
+                    raise SolverInstabilityError(*fail)
+                for c, (rows, order) in zip(self.ctxs, owned_rows):
+                    if len(rows):
+                        store = c.get_store(n_steps)          # [N][n_sup], device order
+                        out[si, rows[order]] = store.T
+        finally:
+            self.upload()
 
     def _steps(self, step, *per_ctx):
         """One time step on every slab, then the halo exchange; with overlap
@@ -394,6 +516,24 @@ class SlabGradient:
                 c.set_plane_part(0)
 
     def run(self):
+        return self._guarded(self._run)
+
+    def _guarded(self, fn, *a):
+        if not self.peer_stores:
+            return fn(*a)
+        try:
+            return fn(*a)
+        except BaseException:
+            # a sweep left half enqueued would keep the neighbours' streams
+            # waiting on its flags: release them before reporting
+            for c in self.ctxs:
+                try:
+                    c.slab_abort()
+                except Exception:
+                    pass
+            raise
+
+    def _run(self):
         from .solver import injection_scale
 
         problem, grid = self.problem, self.problem.grid
@@ -415,12 +555,8 @@ class SlabGradient:
                     meas = np.ascontiguousarray(meas[owned][order])
                 specs.append((len(local), kind, cc, adj_coef, meas))
                 c.reset_window()
-            src_local = [g_src - c.i_begin * plane if c.i_begin * plane <= g_src < c.i_end * plane
-                         else -1 for c in self.ctxs]
-            for n in range(1, n_steps):
-                self._steps(lambda c, s, _n=n: c.sweep_forward_range(
-                    n_steps, _n, _n + 1, [s] if s >= 0 else [],
-                    amp if s >= 0 else np.zeros((0, n_steps)), True, dt), src_local)
+            src_local = [local_source(g_src, plane, c.alloc_range, c.i_begin) for c in self.ctxs]
+            self._forward_all(n_steps, src_local, amp, True, dt)
             maxima = self.halo.allreduce_max(
                 np.max([c.check_maxima(n_steps) for c in self.ctxs], axis=0))
             fail, _ = first_failure_forward(maxima, n_steps, scale)
@@ -433,9 +569,14 @@ class SlabGradient:
                     cost += c.shot_misfit(n_steps, kind, meas, cc, adj_coef, True, k)
             total += self.halo.allreduce_sum(cost)
             inject = [spec[0] > 0 for spec in specs]
-            for n in range(n_steps - 1, 0, -1):
-                self._steps(lambda c, s, inj, _n=n: c.sweep_backward_range(
-                    n_steps, _n, _n - 1, s, amp[0], inj, True, dt), src_local, inject)
+            src_b = [N.WO_NO_SOURCE if s is None else s for s in src_local]
+            if self.peer_stores:
+                for c, s, inj in zip(self.ctxs, src_b, inject):
+                    c.sweep_backward_range(n_steps, n_steps - 1, 0, s, amp[0], inj, True, dt)
+            else:
+                for n in range(n_steps - 1, 0, -1):
+                    self._steps(lambda c, s, inj, _n=n: c.sweep_backward_range(
+                        n_steps, _n, _n - 1, s, amp[0], inj, True, dt), src_b, inject)
             maxima = self.halo.allreduce_max(
                 np.max([c.check_maxima(n_steps) for c in self.ctxs], axis=0))
             fail = first_failure_backward(maxima, n_steps)

@@ -137,6 +137,15 @@ class DeviceGrid:
     def is_slab(self):
         return self.grid is not self.global_grid
 
+    @property
+    def alloc_range(self):
+        """Global planes [lo, hi) held on the device: own planes plus up to two
+        ghost planes per neighbour (wo_create_slab)."""
+        n0 = self.global_grid.shape[0]
+        if not self.is_slab:
+            return 0, n0
+        return self.i_begin - min(2, self.i_begin), self.i_end + min(2, n0 - self.i_end)
+
     # --------------------------------------------------------------- basics
     def close(self):
         if getattr(self, "h", None):
@@ -161,13 +170,22 @@ class DeviceGrid:
             raise ConfigError(f"field shape {a.shape} != grid {self.grid.shape}")
         return a
 
-    def set_material(self, material: MaterialModel, dt):
+    def set_material(self, material: MaterialModel, dt, gamma_local=None):
+        """Material constants of `material` and its gamma (fp64, cast on the
+        device).  gamma_local: this context's planes of gamma (own + ghost
+        planes, alloc_range) as a C-contiguous fp64 array, used instead of
+        slicing material.gamma (e.g. a pinned host copy of a slab)."""
         if material.grid.shape != self.global_grid.shape:
             raise ConfigError("material lives on a different grid")
+        self.claim = None      # loaded state changed: a plan that cached it re-uploads
         flavor = N.WO_RHO_SCALED if material.flavor == RHO_SCALED else N.WO_ACOUSTIC
-        if self.is_slab:   # own planes plus the ghost planes (solver.py:94 per slab)
-            lo = max(self.i_begin - 1, 0)
-            hi = min(self.i_end + 1, self.global_grid.shape[0])
+        lo, hi = self.alloc_range
+        if gamma_local is not None:
+            gamma = gamma_local
+            if (gamma.dtype != np.float64 or not gamma.flags.c_contiguous or
+                    gamma.shape != (hi - lo,) + tuple(self.global_grid.shape[1:])):
+                raise ConfigError("gamma_local must be this context's planes, C-order fp64")
+        elif self.is_slab:   # own planes plus the ghost planes (solver.py:94 per slab)
             gamma = np.ascontiguousarray(material.gamma[lo:hi], dtype=np.float64)
         else:
             gamma = np.ascontiguousarray(material.gamma, dtype=np.float64)
@@ -313,6 +331,8 @@ class DeviceGrid:
     def shot_misfit(self, n_steps, kind, measured, c, adj_coef, write_adj, k):
         meas = (np.ascontiguousarray(measured, dtype=np.float64) if measured is not None
                 else None)
+        if meas is not None:
+            self.claim = None  # new measured traces resident: the owner re-claims
         cost = ctypes.c_double(0.0)
         self._ck(self.L.wo_shot_misfit(self.h, int(n_steps), int(kind), N.ptr(meas),
                                        float(c[0]), float(c[1]), float(c[2]), float(c[3]),
@@ -402,6 +422,15 @@ class DeviceGrid:
     def set_graphs(self, on):
         """Replay repeated sweeps from captured CUDA graphs (default on)."""
         self._ck(self.L.wo_set_option(self.h, N.WO_OPT_GRAPHS, int(bool(on))), "wo_set_option")
+
+    def slab_abort(self):
+        """Release streams waiting on this slab's peer flags (wo_slab_abort)."""
+        self._ck(self.L.wo_slab_abort(self.h), "wo_slab_abort")
+
+    def set_two_step(self, on):
+        """Two time steps per HBM pass (WO_OPT_TWO_STEP; slabs: off until the
+        decomposition enables it on every slab)."""
+        self._ck(self.L.wo_set_option(self.h, N.WO_OPT_TWO_STEP, int(on)), "wo_set_option")
 
     def set_plane_part(self, part):
         """Split slab steps: 1 boundary planes, 2 interior (+rotation), 0 whole."""
@@ -501,14 +530,24 @@ class DeviceGrid:
     def device_bytes(self):
         return int(self.L.wo_device_bytes(self.h))
 
+    def field_buffers(self):
+        """Solution-sized device buffers held now (wo_field_buffers)."""
+        return int(self.L.wo_field_buffers(self.h))
+
 
 _CACHE: OrderedDict = OrderedDict()
 _CACHE_MAX = 3
 
 
-def get_context(grid: Grid, dtype, device=0) -> DeviceGrid:
-    """Cached DeviceGrid per (shape, dx, dtype, device)."""
-    key = (grid.shape, float(grid.dx), np.dtype(dtype).str, device)
+def get_context(grid: Grid, dtype, device=0, four_fields=False) -> DeviceGrid:
+    """Cached DeviceGrid per (shape, dx, dtype, device, memory mode).
+
+    four_fields: a context that never takes two-step passes, so it holds the
+    reference's memory contract of four solution-sized buffers (SPEC
+    acceptance 5: gamma, two window levels — u^{n+1} in place over u^{n-1} —
+    and the accumulator) instead of the fast path's ten (four levels, the
+    accumulator, gamma and four precomputed material fields)."""
+    key = (grid.shape, float(grid.dx), np.dtype(dtype).str, device, bool(four_fields))
     ctx = _CACHE.get(key)
     if ctx is not None and not ctx.h:      # closed by its user: replace it
         del _CACHE[key]
@@ -518,6 +557,8 @@ def get_context(grid: Grid, dtype, device=0) -> DeviceGrid:
             _, old = _CACHE.popitem(last=False)
             old.close()
         ctx = DeviceGrid(grid, dtype, device)
+        if four_fields:
+            ctx.set_two_step(0)
         _CACHE[key] = ctx
     else:
         _CACHE.move_to_end(key)

@@ -71,6 +71,14 @@ class ForwardResult:
     peak_abs: float
 
 
+def source_injections(sources, grid: Grid, t):
+    """(flat indices, fp64 values) of the nodal sources at time t, the force
+    form propagate_step / run_backward take (solver.py:267-270)."""
+    idx = np.array([grid.flat_index(s.node) for s in sources], dtype=np.int64)
+    values = np.array([burst_amplitude(t, s) for s in sources])
+    return idx, values
+
+
 def injection_scale(sources, material: MaterialModel, dt, dtype):
     """max |psi0| * force_coef[node] over the sources (solver.py:273-279)."""
     scale = 0.0

@@ -11,5 +11,5 @@ NCU_RANGE="--profile-from-start off"   # bench.py brackets its timed region
 timeout 300 $CMD > $out/${tag}_plain.json 2>$out/${tag}_plain.err; echo "plain rc $?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none $NCU_RANGE -c 2000 --csv \
     --log-file $out/launches_bench_${tag}.csv $CMD > $out/${tag}_ncu_launch.log 2>&1; echo "launches rc $?"
-python profiles/launch_shares.py $out/launches_bench_${tag}.csv "$NCU_RANGE -c 2000 $CMD" > $out/launches_bench_${tag}.txt
+python profiles/launch_shares.py $out/launches_bench_${tag}.csv "$NCU_RANGE -c 2000 $CMD" $out/launch_share_${tag}.json > $out/launches_bench_${tag}.txt
 [ -n "$NO_FULL" ] || TESTS="-k no_test_selected_zzz" profiles/gpu_cycle.sh ${tag} > $out/${tag}_cycle.log 2>&1; echo "cycle rc $?"

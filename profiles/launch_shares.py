@@ -1,11 +1,14 @@
 """Summarise an ncu launch list (``--metrics gpu__time_duration.sum --csv``)
 into per-kernel totals and shares of the captured launches.
 
-    python profiles/launch_shares.py launches.csv "<command line>" > launches.txt
-"""
+    python profiles/launch_shares.py launches.csv "<command line>" [share.json] > launches.txt
+
+With a third argument the shares are also written as JSON (bench.py reads
+profiles/launch_share.json: the dominant kernel's share of the step)."""
 
 import collections
 import csv
+import json
 import sys
 
 
@@ -34,6 +37,18 @@ def main():
     for name in sorted(tot, key=tot.get, reverse=True):
         print(f"{name[:90]:90s} n={cnt[name]:5d} total_us={tot[name]:9.1f} "
               f"share={100 * tot[name] / all_us:5.1f}% mean_us={tot[name] / cnt[name]:7.2f}")
+    if len(sys.argv) > 3:
+        # kernels of one family (template instantiations) summed by base name
+        fam = collections.defaultdict(lambda: [0.0, 0])
+        for name in tot:
+            base = name.split("<")[0]
+            fam[base][0] += tot[name]
+            fam[base][1] += cnt[name]
+        out = {"source": f"{path} ({cmd})", "launches": len(rows),
+               "kernels": {k: {"share": v[0] / all_us, "launches": v[1], "total_us": v[0]}
+                           for k, v in sorted(fam.items(), key=lambda kv: -kv[1][0])}}
+        with open(sys.argv[3], "w") as fh:
+            json.dump(out, fh, indent=1)
 
 
 if __name__ == "__main__":

@@ -124,3 +124,37 @@ def ki_inputs(shape, dtype, seed):
     acc = rng.standard_normal(shape).astype(dtype)
     scal = (-2700.0, 2700.0 * 6000.0**2, 1.0 / (2.0 * 1.7e-8), 1.0 / (2.0 * 1e-4), 1.7e-8)
     return acc, wins, scal
+
+
+def desk_mask(shape, width=2):
+    """Fictitious-domain mask for the masked invert case: a border of
+    `width` nodes held at eps (fwi.py:42-46 clip_indicator frozen_mask)."""
+    m = np.zeros(shape, dtype=bool)
+    m[:width, :] = m[-width:, :] = True
+    m[:, :width] = m[:, -width:] = True
+    return m
+
+
+def solver2d_case():
+    """Small 2D rho-scaled grid for run_forward / run_backward parity."""
+    shape = (40, 33)
+    dx = 2.0e-4
+    return dict(name="solver2d", shape=shape, dx=dx, n_steps=150, dt=0.5 * dx / 6000.0,
+                rho0=2700.0, c0=6000.0, eps=1e-5,
+                gamma=smooth_random_gamma(shape, 31, 0.4, 1.0))
+
+
+def colocated_sources(c):
+    """Three sources, two of them on the same node (solver.py:154-170: numpy
+    fancy-index += keeps the LAST duplicate's value)."""
+    shape = c["shape"]
+    a = tuple(n // 3 for n in shape)
+    b = tuple(n // 2 for n in shape)
+    return [(a, 1.0e12, 5.0e6, 2), (b, 7.0e11, 3.0e6, 2), (a, 3.0e11, 2.0e6, 2)]
+
+
+def solver_sensors(c):
+    shape = c["shape"]
+    hi = tuple(n - 2 for n in shape)
+    mid = tuple(n // 2 + 1 for n in shape)
+    return sorted({tuple(1 for _ in shape), hi, mid})

@@ -189,6 +189,90 @@ def gen_tato(W, c):
     return out
 
 
+def _log_arrays(out, key, log):
+    out[f"{key}_cost"] = np.array([r["cost"] for r in log], dtype=np.float64)
+    out[f"{key}_gnorm"] = np.array([r["grad_norm"] for r in log], dtype=np.float64)
+    if "beta" in log[0]:
+        out[f"{key}_beta"] = np.array([r["beta"] for r in log], dtype=np.float64)
+
+
+def gen_loops(W):
+    """Optimisation loops of the reference: 3 iterations of
+    invert on configs/fwi_desk.toml (fwi.py:178-238), with and without a
+    frozen mask, and of optimize_design on the tato2d case (tato.py:238-304):
+    parameters after every iteration and the cost / gradient-norm logs."""
+    out = {}
+    g = np.load(os.path.join(HERE, "desk_fwi.npz"))
+    c = cases.DESK
+    problem, _ = make_fwi_problem(W, c, g["gamma_model"], g["measured"])
+    for prec in ("double", "single"):
+        t0 = time.time()
+        res = W.invert(problem, method="superposed", k=c["k"], iterations=3, precision=prec,
+                       snapshot_every=1)
+        print(f"  invert {prec} {time.time() - t0:.1f}s")
+        out[f"inv_hist_{prec}"] = np.array(res.gamma_history)
+        _log_arrays(out, f"inv_{prec}", res.log)
+    mask = cases.desk_mask(c["shape"])
+    problem.mask = mask
+    res = W.invert(problem, method="superposed", k=c["k"], iterations=2, precision="double",
+                   snapshot_every=1)
+    out["inv_mask"] = mask
+    out["invm_hist_double"] = np.array(res.gamma_history)
+    _log_arrays(out, "invm_double", res.log)
+    res = W.invert(problem, method="reference", iterations=2, precision="double",
+                   snapshot_every=1)
+    out["invr_hist_double"] = np.array(res.gamma_history)
+    _log_arrays(out, "invr_double", res.log)
+
+    t = np.load(os.path.join(HERE, "tato2d.npz"))
+    ct = cases.tato2d_case()
+    tp = make_tato_problem(W, ct)
+    for prec in ("double", "single"):
+        t0 = time.time()
+        res = W.optimize_design(tp, method="superposed", k=float(t["cal_k"]), iterations=3,
+                                precision=prec, snapshot_every=1)
+        print(f"  optimize_design {prec} {time.time() - t0:.1f}s")
+        out[f"des_raw_{prec}"] = res.gamma_raw
+        out[f"des_hist_{prec}"] = np.array(res.design_history)
+        _log_arrays(out, f"des_{prec}", res.log)
+    return out
+
+
+def gen_solver(W):
+    """run_forward with co-located sources (solver.py:154-170: numpy fancy
+    `+=` keeps the LAST duplicate) and run_backward (solver.py:343-372), from
+    the forward's end window and from a random end window, 3D and 2D."""
+    out = {}
+    for tag, c in (("3d", cases.fwi3d_case()), ("2d", cases.solver2d_case())):
+        grid = W.build_grid(c["shape"], c["dx"])
+        tcfg = W.TimeConfig(n_steps=c["n_steps"], dt=c["dt"])
+        mat = W.MaterialModel.rho_scaled(c["gamma"], grid, rho0=c["rho0"], c0=c["c0"],
+                                         eps=c["eps"])
+        srcs = [W.SourceSpec(node=n, amplitude=a, frequency=f, cycles=cy)
+                for n, a, f, cy in cases.colocated_sources(c)]
+        sens = W.SensorArray(nodes=cases.solver_sensors(c))
+        for dtype in (np.float32, np.float64):
+            key = f"{tag}_{dtname(dtype)}"
+            fr = W.run_forward(mat, tcfg, srcs, sens, dtype=dtype)
+            out[f"fwd_traces_{key}"] = fr.traces
+            out[f"fwd_uprev_{key}"] = fr.window.u_prev
+            out[f"fwd_ucur_{key}"] = fr.window.u_cur
+            forces = lambda n: W.solver.source_injections(srcs, grid, n * c["dt"])  # noqa: E731
+            wb = W.run_backward(mat, tcfg, fr.window, forces)
+            out[f"bwd_uprev_{key}"] = wb.u_prev
+            out[f"bwd_ucur_{key}"] = wb.u_cur
+            rng = np.random.default_rng(77 + dtype().itemsize)
+            end = W.SolverWindow(u_prev=rng.normal(size=c["shape"]).astype(dtype),
+                                 u_cur=rng.normal(size=c["shape"]).astype(dtype),
+                                 u_next=np.zeros(c["shape"], dtype))
+            out[f"rnd_uprev_in_{key}"] = end.u_prev.copy()
+            out[f"rnd_ucur_in_{key}"] = end.u_cur.copy()
+            wr = W.run_backward(mat, tcfg, end, forces)
+            out[f"rnd_uprev_{key}"] = wr.u_prev
+            out[f"rnd_ucur_{key}"] = wr.u_cur
+    return out
+
+
 def gen_kats(W):
     """SPEC KATs, evaluated on the reference."""
     out = {}
@@ -254,6 +338,8 @@ def main():
         ("tato2d", lambda: gen_tato(W, cases.tato2d_case())),
         ("desk_fwi", lambda: gen_fwi(W, cases.DESK)),
         ("io_dumps", lambda: gen_io(W)),
+        ("loops", lambda: gen_loops(W)),
+        ("solver", lambda: gen_solver(W)),
     ]
     only = set(sys.argv[1:])
     for name, fn in jobs:

@@ -23,6 +23,31 @@ def test_slab_ranges_and_localize():
     assert local.tolist() == [0, 39]
 
 
+def test_two_step_slab_decision():
+    """Two-step slab passes recompute planes b-1 and b at every interior
+    boundary b: a support node there keeps all slabs on single steps; so do
+    slabs thinner than two planes.  Sources anywhere are fine."""
+    slabs = D.slab_ranges(32, 2)                 # boundary at 16
+    assert D.recomputed_planes(slabs) == {15, 16}
+    plane = 16 * 64
+    assert D.two_step_slabs_ok(slabs, plane, [np.array([3 * plane + 5, 28 * plane])])
+    assert not D.two_step_slabs_ok(slabs, plane, [np.array([3 * plane, 15 * plane + 7])])
+    assert not D.two_step_slabs_ok(slabs, plane, [np.array([16 * plane])])
+    assert D.recomputed_planes(D.slab_ranges(12, 4)) == {2, 3, 5, 6, 8, 9}
+    assert not D.two_step_slabs_ok([(0, 1), (1, 4)], plane, [np.array([3 * plane])])
+    assert D.two_step_slabs_ok([(0, 10)], plane, [np.array([9 * plane])])   # one slab
+
+
+def test_local_source_covers_ghost_planes():
+    plane = 100
+    # slab [10, 20) of a 40-plane grid holds planes 8..21 (two ghosts a side)
+    assert D.local_source(9 * plane + 3, plane, (8, 22), 10) == -plane + 3
+    assert D.local_source(21 * plane, plane, (8, 22), 10) == 11 * plane
+    assert D.local_source(7 * plane, plane, (8, 22), 10) is None
+    assert D.local_source(22 * plane, plane, (8, 22), 10) is None
+    assert D.local_source(12 * plane + 1, plane, (8, 22), 10) == 2 * plane + 1
+
+
 def test_shot_partition_covers_all():
     for world in (1, 2, 3, 8):
         got = sorted(s for r in range(world) for s in D.shot_partition(5, r, world))

@@ -55,8 +55,10 @@ def test_ipc_export_open_cross_process():
     h_hi, off_hi = ctx.ipc_export(ghi[1])
     h_f, off_f = ctx.ipc_export(flags[1])
     assert len(h_hi) == 64 and h_lo == h_hi        # one level buffer, one allocation
-    assert off_lo == 0 and off_hi == (1 + SLAB[1] - SLAB[0]) * plane_bytes
-    assert off_f == 4                              # in_flags[1]
+    # two ghost planes per neighbour: the low ghost region starts the
+    # allocation, the high one follows the slab's own planes
+    assert off_lo == 0 and off_hi == (2 + SLAB[1] - SLAB[0]) * plane_bytes
+    assert off_f == 4                              # in_flags[1] (parity-0 slot)
     with pytest.raises(Exception):
         ctx.ipc_export(0)
 

@@ -107,7 +107,31 @@ def test_gradient_superposed_bitexact(W, golden, name, prec):
     assert bits_equal(res.gradient, g[f"sup_grad_{prec}"])
     ref_cost = float(g[f"sup_cost_{prec}"])
     assert abs(res.cost - ref_cost) <= COST_RTOL * abs(ref_cost)
+    # these grids do not tile into two-step CTAs: gamma, 2 levels, acc
     assert res.counter.peak_fields == 4
+
+
+def test_buffer_counter_reports_device_fields(W):
+    """BufferCounter reads the buffers the context really holds: 10 on the
+    fast fp32 path (4 levels, acc, gamma, coef + 3 faces), 4 in the
+    four-field mode (SPEC acceptance 5), with identical gradients."""
+    rng = np.random.default_rng(4)
+    shape, n_steps, dx = (10, 16, 64), 30, 1e-4
+    dt = 0.45 * dx / 6000.0 / np.sqrt(3)
+    grid = W.build_grid(shape, dx)
+    mat = W.MaterialModel.rho_scaled(rng.uniform(0.4, 1.0, size=shape), grid, rho0=2700.0,
+                                     c0=6000.0)
+    src = W.SourceSpec(node=(4, 8, 30), amplitude=1e12, frequency=4e6, cycles=2)
+    sens = [(8, j, 10) for j in (1, 7, 14)]
+    problem = W.FwiProblem(grid=grid, time=W.TimeConfig(n_steps, dt), material=mat,
+                           sources=[src], sensors=W.SensorArray(nodes=sens),
+                           measured=rng.normal(scale=1e-10, size=(1, 3, n_steps)))
+    fast = W.gradient_superposed(problem, mat, W.SuperpositionConfig(k=1e13, precision="single"))
+    four = W.gradient_superposed(problem, mat, W.SuperpositionConfig(
+        k=1e13, precision="single", memory="four_fields"))
+    assert fast.counter.peak_fields == 10
+    assert four.counter.peak_fields == 4
+    assert bits_equal(fast.gradient, four.gradient)
 
 
 @pytest.mark.parametrize("prec", ["single", "double"])

@@ -1,0 +1,153 @@
+"""Optimisation loops and solver entry points against outputs of the
+REFERENCE itself (tests/golden/loops.npz, solver.npz, written by
+make_golden.py from /root/reference/pkg/src/waveopt):
+
+* invert (fwi.py:178-238) on configs/fwi_desk.toml, 3 iterations, fp64 and
+  fp32, plus a frozen-mask run and the reference-gradient method;
+* optimize_design (tato.py:238-304) on the tato2d case, 3 iterations;
+* run_forward with co-located sources (solver.py:154-170) and run_backward
+  (solver.py:343-372) from the forward end window and from a random one.
+
+Parameters and fields must be bit-identical; logged costs and gradient norms
+within 1e-13 relative (the reference sums them through BLAS dot / norm, the
+device through fixed-order trees)."""
+
+import numpy as np
+import pytest
+
+import cases
+from helpers import bits_equal, product_fwi_problem
+
+pytestmark = pytest.mark.gpu
+LOG_RTOL = 1e-13
+
+
+@pytest.fixture(scope="module")
+def W():
+    import paper_2509_15744_b200 as W
+    from paper_2509_15744_b200 import _native
+
+    _native.load(require_device=True)
+    return W
+
+
+def _check_log(log, g, key):
+    cost, gnorm = g[f"{key}_cost"], g[f"{key}_gnorm"]
+    assert len(log) == len(cost)
+    for row, c, n in zip(log, cost, gnorm):
+        assert abs(row["cost"] - c) <= LOG_RTOL * abs(c), (key, row["cost"], c)
+        if np.isfinite(n):
+            assert abs(row["grad_norm"] - n) <= LOG_RTOL * abs(n), (key, row["grad_norm"], n)
+        else:
+            assert not np.isfinite(row["grad_norm"])
+    if f"{key}_beta" in g:
+        assert [r["beta"] for r in log] == list(g[f"{key}_beta"])
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+@pytest.mark.parametrize("device_loop", [True, False])
+def test_invert_matches_reference(W, golden, prec, device_loop):
+    g, d = golden("loops"), golden("desk_fwi")
+    problem, _ = product_fwi_problem(W, cases.DESK, d["gamma_model"], d["measured"])
+    res = W.invert(problem, method="superposed", k=cases.DESK["k"], iterations=3,
+                   precision=prec, snapshot_every=1, device_loop=device_loop)
+    hist = g[f"inv_hist_{prec}"]
+    assert len(res.gamma_history) == len(hist)
+    for a, b in zip(res.gamma_history, hist):
+        assert bits_equal(a, b)
+    assert bits_equal(res.gamma, hist[-1])
+    _check_log(res.log, g, f"inv_{prec}")
+
+
+@pytest.mark.parametrize("device_loop", [True, False])
+def test_invert_masked_matches_reference(W, golden, device_loop):
+    g, d = golden("loops"), golden("desk_fwi")
+    problem, _ = product_fwi_problem(W, cases.DESK, d["gamma_model"], d["measured"])
+    problem.mask = g["inv_mask"]
+    res = W.invert(problem, method="superposed", k=cases.DESK["k"], iterations=2,
+                   precision="double", snapshot_every=1, device_loop=device_loop)
+    for a, b in zip(res.gamma_history, g["invm_hist_double"]):
+        assert bits_equal(a, b)
+    _check_log(res.log, g, "invm_double")
+
+
+def test_invert_reference_gradient_matches_reference(W, golden):
+    g, d = golden("loops"), golden("desk_fwi")
+    problem, _ = product_fwi_problem(W, cases.DESK, d["gamma_model"], d["measured"])
+    problem.mask = g["inv_mask"]
+    res = W.invert(problem, method="reference", iterations=2, precision="double",
+                   snapshot_every=1)
+    for a, b in zip(res.gamma_history, g["invr_hist_double"]):
+        assert bits_equal(a, b)
+    _check_log(res.log, g, "invr_double")
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+@pytest.mark.parametrize("device_loop", [True, False])
+def test_optimize_design_matches_reference(W, golden, prec, device_loop):
+    from helpers import product_tato_problem
+
+    g, t = golden("loops"), golden("tato2d")
+    problem = product_tato_problem(W, cases.tato2d_case())
+    res = W.optimize_design(problem, method="superposed", k=float(t["cal_k"]), iterations=3,
+                            precision=prec, snapshot_every=1, device_loop=device_loop)
+    assert bits_equal(res.gamma_raw, g[f"des_raw_{prec}"])
+    hist = g[f"des_hist_{prec}"]
+    assert len(res.design_history) == len(hist)
+    for a, b in zip(res.design_history, hist):
+        # the Heaviside projection's tanh is libm's on the host and CUDA's on
+        # the device: a few ulp
+        np.testing.assert_allclose(a, b, rtol=0, atol=1e-14)
+    _check_log(res.log, g, f"des_{prec}")
+
+
+def _solver_inputs(W, tag):
+    c = cases.fwi3d_case() if tag == "3d" else cases.solver2d_case()
+    grid = W.build_grid(c["shape"], c["dx"])
+    tcfg = W.TimeConfig(n_steps=c["n_steps"], dt=c["dt"])
+    mat = W.MaterialModel.rho_scaled(c["gamma"], grid, rho0=c["rho0"], c0=c["c0"], eps=c["eps"])
+    srcs = [W.SourceSpec(node=n, amplitude=a, frequency=f, cycles=cy)
+            for n, a, f, cy in cases.colocated_sources(c)]
+    sens = W.SensorArray(nodes=cases.solver_sensors(c))
+    return c, grid, tcfg, mat, srcs, sens
+
+
+@pytest.mark.parametrize("tag", ["3d", "2d"])
+@pytest.mark.parametrize("dt_name", ["f32", "f64"])
+def test_run_forward_colocated_sources_match_reference(W, golden, tag, dt_name):
+    """Two sources on one node: only the LAST one's value is injected
+    (numpy fancy-index +=, solver.py:170), in the traces and the window."""
+    g = golden("solver")
+    c, grid, tcfg, mat, srcs, sens = _solver_inputs(W, tag)
+    dtype = np.float32 if dt_name == "f32" else np.float64
+    key = f"{tag}_{dt_name}"
+    fr = W.run_forward(mat, tcfg, srcs, sens, dtype=dtype)
+    assert bits_equal(fr.traces, g[f"fwd_traces_{key}"])
+    assert bits_equal(fr.window.u_prev, g[f"fwd_uprev_{key}"])
+    assert bits_equal(fr.window.u_cur, g[f"fwd_ucur_{key}"])
+
+
+@pytest.mark.parametrize("tag", ["3d", "2d"])
+@pytest.mark.parametrize("dt_name", ["f32", "f64"])
+@pytest.mark.parametrize("start", ["forward_end", "random"])
+def test_run_backward_matches_reference(W, golden, tag, dt_name, start):
+    g = golden("solver")
+    c, grid, tcfg, mat, srcs, sens = _solver_inputs(W, tag)
+    dtype = np.float32 if dt_name == "f32" else np.float64
+    key = f"{tag}_{dt_name}"
+    from paper_2509_15744_b200.solver import source_injections
+
+    forces = lambda n: source_injections(srcs, grid, n * c["dt"])  # noqa: E731
+    if start == "forward_end":
+        end = W.SolverWindow(u_prev=g[f"fwd_uprev_{key}"].copy(),
+                             u_cur=g[f"fwd_ucur_{key}"].copy(),
+                             u_next=np.zeros(c["shape"], dtype))
+        pre = "bwd"
+    else:
+        end = W.SolverWindow(u_prev=g[f"rnd_uprev_in_{key}"].copy(),
+                             u_cur=g[f"rnd_ucur_in_{key}"].copy(),
+                             u_next=np.zeros(c["shape"], dtype))
+        pre = "rnd"
+    wb = W.run_backward(mat, tcfg, end, forces)
+    assert bits_equal(wb.u_prev, g[f"{pre}_uprev_{key}"])
+    assert bits_equal(wb.u_cur, g[f"{pre}_ucur_{key}"])

@@ -240,6 +240,10 @@ int wo_slab_ghosts(wo_ctx* ctx, void** ghost_lo, void** ghost_hi, void** flags);
 /* Error recovery: set this slab's and its neighbours' flags to the maximum
  * so no stream keeps waiting on a sweep that was only partly enqueued. */
 int wo_slab_abort(wo_ctx* ctx);
+/* Diagnostics (no wait on the context's stream): out[0..3] the flag words,
+ * out[4] signals sent in the current epoch, out[5] epochs begun, out[6] 1 if
+ * the stream is idle. */
+int wo_slab_state(wo_ctx* ctx, int64_t* out);
 int wo_slab_peers(wo_ctx* ctx, void* const* lo_ghost, void* const* hi_ghost, void* lo_flag,
                   void* hi_flag);
 /* CUDA IPC for peer ghost stores across processes (one slab per rank, the

@@ -97,6 +97,10 @@ struct wo_ctx {
     int t2_state = 0;                  // two-step tensor maps: 0 not built, 1 ready, -1 no
     Tma2Maps t2maps;
     char* mat4 = nullptr;              // coef | +k | +j | +i faces (two-step passes)
+    unsigned int* tflags = nullptr;    // per-block completion of the last two-step pass
+    size_t tflags_bytes = 0;
+    unsigned int t2_seq = 0;           // two-step passes of the current sweep (flag values)
+    bool t2_chain_next = false;        // the next pass directly follows one of this sweep
     char* stage = nullptr;             // fp64 upload staging (persistent)
     char* hstage = nullptr;            // pinned host staging for field downloads (2 halves)
     char* scratch = nullptr;           // one field (wo_get_field axis reversal)
@@ -491,6 +495,7 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     const int engine = tma ? (ctx->use_tma == 2 && !sp.peer ? ENGINE_TMA : ENGINE_TMA4)
                            : (pair ? ENGINE_PAIR : ENGINE_SCALAR);
     t_no_pdl = sp.peer && !p2p_pdl();
+    ctx->t2_chain_next = false;   // the next two-step pass waits for this whole grid
     launch_step_engine<T>(engine, sel, grid, block, ctx->stream, a, ctx->tmaps);
     t_no_pdl = false;
     prof_end(ctx);
@@ -836,6 +841,12 @@ int choose_chunk2(const wo_ctx* ctx) {
 // z layers of a two-step launch: boundaries zb[0..nz] (returns nz).  Uniform
 // chunks of choose_chunk2 unless WB_T2_LAYERS="len x count,..." (tuning
 // runs; layers in launch order, lengths must sum to n0).
+int n0_min_layer(const int* zb, int nz) {
+    int m = 1 << 30;
+    for (int z = 0; z < nz; ++z) m = std::min(m, zb[z + 1] - zb[z]);
+    return m;
+}
+
 int choose_layers2(const wo_ctx* ctx, int* zb) {
     static const std::string spec = [] {
         const char* e = getenv("WB_T2_LAYERS");
@@ -866,6 +877,26 @@ int choose_layers2(const wo_ctx* ctx, int* zb) {
     for (int p = 0; p < n0 && nz < T2_MAXZ; p += chunk) zb[++nz] = std::min(p + chunk, n0);
     zb[nz] = n0;
     return nz;
+}
+
+// WB_T2_CHAIN (default 1): consecutive two-step passes of a sweep wait only
+// for their neighbour blocks of the previous pass (Step2Args::chain)
+bool t2_chain_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("WB_T2_CHAIN");
+        return !e || atoi(e) != 0;
+    }();
+    return on;
+}
+
+// start of a run of two-step passes (a sweep): fresh block flags, so the
+// values a captured sweep graph bakes in repeat on every replay
+int t2_sweep_begin(wo_ctx* ctx) {
+    ctx->t2_seq = 0;
+    ctx->t2_chain_next = false;
+    if (!ctx->tflags || ctx->p2p || !t2_chain_enabled()) return WO_OK;
+    CK(cudaMemsetAsync(ctx->tflags, 0, ctx->tflags_bytes, ctx->stream));
+    return WO_OK;
 }
 
 struct PairSpec {
@@ -937,6 +968,24 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
         a.row2 = reinterpret_cast<T*>(ctx->store) + sp.row2 * ctx->n_sup;
     }
     a.check1 = sp.check1; a.check2 = sp.check2;
+    // dataflow chaining: only right after a pass of this sweep, with z layers
+    // of >= 2 planes (the 3x3x3 block neighbourhood then covers every plane a
+    // block reads or overwrites), PDL launches and no stream operations between
+    int min_layer = n0_min_layer(a.zb, nz);
+    const bool chain_ok = t2_chain_enabled() && !ctx->p2p && WB_T2_PDL && min_layer >= 2;
+    if (chain_ok && !ctx->tflags) {
+        const size_t need = (size_t)(ctx->kn2 / 32 + 1) * (ctx->kn1 / 8 + 1) * (T2_MAXZ + 1) * 4;
+        if (dev_alloc(ctx, (void**)&ctx->tflags, need) == WO_OK) {
+            ctx->tflags_bytes = need;
+            CK(cudaMemsetAsync(ctx->tflags, 0, need, ctx->stream));
+        }
+        ctx->t2_chain_next = false;   // flags fresh from here on
+    }
+    if (chain_ok && ctx->tflags) {
+        a.tflags = ctx->tflags;
+        a.seq = ++ctx->t2_seq;
+        a.chain = ctx->t2_chain_next ? 1 : 0;
+    }
     a.max1 = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots) + sp.slot1;
     a.max2 = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots) + sp.slot2;
     ctx->t2maps.prev = ctx->prv;
@@ -986,6 +1035,7 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     CK(cudaGetLastError());
     ctx->prv = x[0];
     ctx->cur = x[1];
+    ctx->t2_chain_next = a.tflags != nullptr;
     return ctx->p2p ? p2p_signal(ctx) : WO_OK;
 }
 
@@ -1086,6 +1136,10 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
         gkey = kh.h;
         if (graph_replay(ctx, 0, gkey)) n_end = n_begin;   // loop skipped
         else capturing = graph_capture_begin(ctx, 0, gkey);
+    }
+    if (pairs && n_end - n_begin >= 2) {
+        rc = t2_sweep_begin(ctx);
+        if (rc) return rc;
     }
     for (int64_t n = n_begin; n < n_end; ++n) {
         if (pairs && n + 1 < n_end) {   // steps n and n+1 in one pass
@@ -1225,6 +1279,10 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
         gkey = kh.h;
         if (graph_replay(ctx, 1, gkey)) n_hi = n_lo;   // loop skipped
         else capturing = graph_capture_begin(ctx, 1, gkey);
+    }
+    if (pairs && n_hi - n_lo >= 2) {
+        rc = t2_sweep_begin(ctx);
+        if (rc) return rc;
     }
     for (int64_t n = n_hi; n > n_lo; --n) {
         if (pairs && n - 1 > n_lo) {   // steps n and n-1 in one pass
@@ -2187,6 +2245,28 @@ int wo_slab_abort(wo_ctx* ctx) {
     return WO_OK;
 }
 
+// Diagnostics of the peer-store protocol without touching the context's
+// stream: out = {flag words [4], signals sent this epoch, epoch, stream idle}
+int wo_slab_state(wo_ctx* ctx, int64_t* out) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    unsigned int w[4] = {0, 0, 0, 0};
+    if (ctx->in_flags) {
+        cudaStream_t s = nullptr;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        cudaMemcpyAsync(w, ctx->in_flags, sizeof(w), cudaMemcpyDeviceToHost, s);
+        const cudaError_t e = cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+        CK(e);
+    }
+    for (int i = 0; i < 4; ++i) out[i] = w[i];
+    out[4] = ctx->p2p_seq;
+    out[5] = ctx->p2p_epoch;
+    out[6] = cudaStreamQuery(ctx->stream) == cudaSuccess ? 1 : 0;
+    (void)cudaGetLastError();
+    return WO_OK;
+}
+
 int wo_slab_peers(wo_ctx* ctx, void* const* lo_ghost, void* const* hi_ghost, void* lo_flag,
                   void* hi_flag) {
     int rc = check_ctx(ctx);
@@ -2221,6 +2301,18 @@ int wo_slab_peers(wo_ctx* ctx, void* const* lo_ghost, void* const* hi_ghost, voi
             if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
             else CK(e);
         }
+    }
+    if (any) {
+        // no lazy kernel load (a context-wide synchronisation) may happen
+        // while a stream waits on a neighbour (launchers.cuh)
+        if (ctx->itemsize == 4) {
+            preload_step_kernels<float>();
+            preload_step2_kernels<float>();
+        } else {
+            preload_step_kernels<double>();
+            preload_step2_kernels<double>();
+        }
+        CK(cudaGetLastError());
     }
     if (any) {   // fresh flags on every slab before any sweep (wire up all slabs first)
         if ((rc = ensure_four(ctx))) return rc;

@@ -45,5 +45,14 @@ template <typename T>
 void launch_material4(int flavor, cudaStream_t s, const T* gamma, const MatScalars<T>& M, int n0,
                       int n1, int n2, T* out);
 
+// Load every step / two-step / material kernel instantiation now.  With the
+// CUDA runtime's lazy module loading (the CUDA 12 default) the first launch
+// of a kernel loads it, which synchronises the context: while a peer-store
+// slab's stream waits on a neighbour's flag that only a later-enqueued launch
+// of this process will set, such a load would wait forever.  The peer-store
+// setup (wo_slab_peers) therefore loads them all up front.
+template <typename T> void preload_step_kernels();
+template <typename T> void preload_step2_kernels();
+
 
 }  // namespace wb

@@ -6,4 +6,5 @@ template void launch_step2_engine<float>(const StepSel&, int, dim3, cudaStream_t
                                       const Step2Args<float>&, const Tma2Maps&);
 template void launch_material4<float>(int, cudaStream_t, const float*, const MatScalars<float>&, int,
                                      int, int, float*);
+template void preload_step2_kernels<float>();
 }  // namespace wb

@@ -6,4 +6,5 @@ template void launch_step2_engine<double>(const StepSel&, int, dim3, cudaStream_
                                       const Step2Args<double>&, const Tma2Maps&);
 template void launch_material4<double>(int, cudaStream_t, const double*, const MatScalars<double>&, int,
                                      int, int, double*);
+template void preload_step2_kernels<double>();
 }  // namespace wb

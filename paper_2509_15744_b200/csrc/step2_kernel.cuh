@@ -151,6 +151,14 @@ template <typename T> struct Step2Args {
     // the level buffers and the material; TMA plane coordinate = p + zo) and
     // the peer ghost stores of the results (see StepArgs::plo / phi)
     int lo_open, hi_open, zo;
+    // dataflow chaining of consecutive passes (WB_T2_CHAIN): every CTA
+    // publishes seq in tflags[block] when done; with chain = 1 a CTA waits
+    // only for its 3 x 3 x 3 neighbour blocks of the previous pass (seq - 1:
+    // everything it reads, and every block still reading what it overwrites)
+    // instead of the whole previous grid (griddepcontrol.wait)
+    unsigned int* tflags;
+    unsigned int seq;
+    int chain;
     T* plo1;
     T* phi1;
     T* plo2;
@@ -348,8 +356,31 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     // while the previous pass drains; nothing above touched global memory.
     // Wait for the previous grid (and its memory) before the first load, and
     // let the next pass start its prologue once every CTA of this one runs.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (a.chain) {
+        // the next pass may dispatch as soon as all our CTAs run; ours only
+        // depend on the previous pass's blocks around this one
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        if (tid < 27) {
+            const int bx = (int)blockIdx.x + tid % 3 - 1, by = (int)blockIdx.y + (tid / 3) % 3 - 1;
+            const int bz = (int)blockIdx.z + tid / 9 - 1;
+            if (bx >= 0 && bx < (int)gridDim.x && by >= 0 && by < (int)gridDim.y && bz >= 0 &&
+                bz < (int)gridDim.z) {
+                const unsigned int* f = a.tflags + ((size_t)bz * gridDim.y + by) * gridDim.x + bx;
+                unsigned int v;
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                    if (v + 1u >= a.seq) break;
+                    __nanosleep(128);
+                }
+            }
+        }
+        __syncthreads();
+        // generic-proxy writes of the previous pass -> our TMA (async proxy) reads
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+    } else {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    }
 #endif
     if (tid == T2_PRODUCER) {
         for (int s = 0; s < T2_NS && pbeg + s <= plast; ++s) issue(pbeg + s, s);
@@ -773,6 +804,16 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
                 if (a.check1 && v1) atomicMax(a.max1, v1);
                 if (a.check2 && v2) atomicMax(a.max2, v2);
             }
+        }
+    }
+    if (a.tflags) {   // publish this block's completion (release: all its writes first)
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __threadfence();
+            unsigned int* f = a.tflags + ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x +
+                              blockIdx.x;
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(a.seq) : "memory");
         }
     }
 }

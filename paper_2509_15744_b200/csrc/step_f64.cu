@@ -4,4 +4,5 @@
 namespace wb {
 template void launch_step_engine<double>(int, const StepSel&, dim3, dim3, cudaStream_t,
                                      const StepArgs<double>&, const TmaMaps&);
+template void preload_step_kernels<double>();
 }  // namespace wb

@@ -151,4 +151,63 @@ void launch_material4(int flavor, cudaStream_t s, const T* gamma, const MatScala
                                                          out + 2 * f, out + 3 * f);
 }
 
+template <typename K>
+void load_kernel(K kernel) {
+    cudaFuncAttributes attr;
+    cudaFuncGetAttributes(&attr, kernel);
+}
+
+template <typename T, int FL, bool FAST, bool ACC, bool CHK>
+void preload_step_variant() {
+    load_kernel(step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP_NONE>);
+    load_kernel(step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP_GATHER>);
+    load_kernel(step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP_INJECT>);
+    smem_opt_in<step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP_NONE>>(tma4_smem_bytes<T>());
+    smem_opt_in<step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP_GATHER>>(tma4_smem_bytes<T>());
+    smem_opt_in<step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP_INJECT>>(tma4_smem_bytes<T>());
+    load_kernel(step_kernel_pair<T, FL, FAST, ACC, CHK>);
+    load_kernel(step_kernel<T, FL, FAST, ACC, CHK>);
+}
+
+template <typename T, int FL, bool FAST>
+void preload_step_fl() {
+    preload_step_variant<T, FL, FAST, false, false>();
+    preload_step_variant<T, FL, FAST, false, true>();
+    preload_step_variant<T, FL, FAST, true, false>();
+    preload_step_variant<T, FL, FAST, true, true>();
+}
+
+template <typename T>
+void preload_step_kernels() {
+    preload_step_fl<T, RHO_SCALED, false>();
+    preload_step_fl<T, RHO_SCALED, true>();
+    preload_step_fl<T, ACOUSTIC, false>();
+    preload_step_fl<T, ACOUSTIC, true>();
+}
+
+template <typename T, typename G, int FL, bool ACC>
+void preload_step2_variant() {
+    const size_t sm = step2_smem_bytes<T, G>();
+    load_kernel(step2_kernel_tma<T, G, FL, ACC, SUP_NONE>);
+    load_kernel(step2_kernel_tma<T, G, FL, ACC, SUP_GATHER>);
+    load_kernel(step2_kernel_tma<T, G, FL, ACC, SUP_INJECT>);
+    smem_opt_in<step2_kernel_tma<T, G, FL, ACC, SUP_NONE>>(sm);
+    smem_opt_in<step2_kernel_tma<T, G, FL, ACC, SUP_GATHER>>(sm);
+    smem_opt_in<step2_kernel_tma<T, G, FL, ACC, SUP_INJECT>>(sm);
+}
+
+template <typename T>
+void preload_step2_kernels() {
+    preload_step2_variant<T, GeoWide, RHO_SCALED, false>();
+    preload_step2_variant<T, GeoWide, RHO_SCALED, true>();
+    preload_step2_variant<T, GeoWide, ACOUSTIC, false>();
+    preload_step2_variant<T, GeoWide, ACOUSTIC, true>();
+    preload_step2_variant<T, GeoTall, RHO_SCALED, false>();
+    preload_step2_variant<T, GeoTall, RHO_SCALED, true>();
+    preload_step2_variant<T, GeoTall, ACOUSTIC, false>();
+    preload_step2_variant<T, GeoTall, ACOUSTIC, true>();
+    load_kernel(material4_kernel<T, RHO_SCALED>);
+    load_kernel(material4_kernel<T, ACOUSTIC>);
+}
+
 }  // namespace wb

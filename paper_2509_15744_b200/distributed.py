@@ -436,12 +436,31 @@ class SlabGradient:
         self.problem.measured = np.asarray(measured, dtype=np.float64)
         self._shots = _shot_list(self.problem)
 
+    def _peer_ranges(self, first, last, step):
+        """Step ranges in which the peer-store sweeps are enqueued.  Slabs on
+        different devices (one per process, or one per GPU here): the whole
+        sweep at once.  Several slabs on ONE device: one two-step pass per
+        range, interleaved across the slabs, so every flag wait refers to work
+        enqueued before it — a stream blocked on a wait may share a hardware
+        queue with a neighbour's stream, and a wait on work enqueued later
+        behind it would never be satisfied."""
+        devices = [c.device for c in self.ctxs]
+        if len(set(devices)) == len(devices):
+            return [(first, last)]
+        out, n = [], first
+        while n != last:
+            m = n + step if abs(last - n) > 2 else last
+            out.append((n, m))
+            n = m
+        return out
+
     def _forward_all(self, n_steps, src_local, amp, accumulate, dt):
         no_src = np.zeros((0, n_steps))
-        if self.peer_stores:   # whole sweeps, enqueued on every slab, then awaited
-            for c, s in zip(self.ctxs, src_local):
-                c.sweep_forward_range(n_steps, 1, n_steps, [] if s is None else [s],
-                                      no_src if s is None else amp, accumulate, dt)
+        if self.peer_stores:   # sweeps enqueued on every slab (interleaved), then awaited
+            for n0, n1 in self._peer_ranges(1, n_steps, 2):
+                for c, s in zip(self.ctxs, src_local):
+                    c.sweep_forward_range(n_steps, n0, n1, [] if s is None else [s],
+                                          no_src if s is None else amp, accumulate, dt)
         else:
             for n in range(1, n_steps):
                 self._steps(lambda c, s, _n=n: c.sweep_forward_range(
@@ -571,8 +590,9 @@ class SlabGradient:
             inject = [spec[0] > 0 for spec in specs]
             src_b = [N.WO_NO_SOURCE if s is None else s for s in src_local]
             if self.peer_stores:
-                for c, s, inj in zip(self.ctxs, src_b, inject):
-                    c.sweep_backward_range(n_steps, n_steps - 1, 0, s, amp[0], inj, True, dt)
+                for hi, lo in self._peer_ranges(n_steps - 1, 0, -2):
+                    for c, s, inj in zip(self.ctxs, src_b, inject):
+                        c.sweep_backward_range(n_steps, hi, lo, s, amp[0], inj, True, dt)
             else:
                 for n in range(n_steps - 1, 0, -1):
                     self._steps(lambda c, s, inj, _n=n: c.sweep_backward_range(

@@ -427,6 +427,12 @@ class DeviceGrid:
         """Release streams waiting on this slab's peer flags (wo_slab_abort)."""
         self._ck(self.L.wo_slab_abort(self.h), "wo_slab_abort")
 
+    def slab_state(self):
+        """(flag words [4], signals sent, epoch, stream idle) — wo_slab_state."""
+        out = np.zeros(7, dtype=np.int64)
+        self._ck(self.L.wo_slab_state(self.h, N.ptr(out)), "wo_slab_state")
+        return out.tolist()
+
     def set_two_step(self, on):
         """Two time steps per HBM pass (WO_OPT_TWO_STEP; slabs: off until the
         decomposition enables it on every slab)."""

@@ -20,6 +20,7 @@ from helpers import bits_equal, product_fwi_problem
 
 pytestmark = pytest.mark.gpu
 LOG_RTOL = 1e-13
+DESIGN_RTOL = 1e-8   # TATO loop (projection tanh differs by ulps; see the test)
 
 
 @pytest.fixture(scope="module")
@@ -31,13 +32,13 @@ def W():
     return W
 
 
-def _check_log(log, g, key):
+def _check_log(log, g, key, rtol=LOG_RTOL):
     cost, gnorm = g[f"{key}_cost"], g[f"{key}_gnorm"]
     assert len(log) == len(cost)
     for row, c, n in zip(log, cost, gnorm):
-        assert abs(row["cost"] - c) <= LOG_RTOL * abs(c), (key, row["cost"], c)
+        assert abs(row["cost"] - c) <= rtol * abs(c), (key, row["cost"], c)
         if np.isfinite(n):
-            assert abs(row["grad_norm"] - n) <= LOG_RTOL * abs(n), (key, row["grad_norm"], n)
+            assert abs(row["grad_norm"] - n) <= rtol * abs(n), (key, row["grad_norm"], n)
         else:
             assert not np.isfinite(row["grad_norm"])
     if f"{key}_beta" in g:
@@ -91,14 +92,21 @@ def test_optimize_design_matches_reference(W, golden, prec, device_loop):
     problem = product_tato_problem(W, cases.tato2d_case())
     res = W.optimize_design(problem, method="superposed", k=float(t["cal_k"]), iterations=3,
                             precision=prec, snapshot_every=1, device_loop=device_loop)
-    assert bits_equal(res.gamma_raw, g[f"des_raw_{prec}"])
+    # The Heaviside projection's tanh is numpy's (vectorised libm) in the
+    # reference and CUDA's here: g_bar differs by a few ulp (<= 1e-14, DESIGN.md
+    # §4), so the design loop is compared with tolerances: the projected
+    # designs to 1e-14 absolute, the Adam parameters and logs relatively
+    # (the superposed sensitivity is a difference of two large kernels, which
+    # amplifies the ulp differences of the material).
     hist = g[f"des_hist_{prec}"]
     assert len(res.design_history) == len(hist)
     for a, b in zip(res.design_history, hist):
-        # the Heaviside projection's tanh is libm's on the host and CUDA's on
-        # the device: a few ulp
         np.testing.assert_allclose(a, b, rtol=0, atol=1e-14)
-    _check_log(res.log, g, f"des_{prec}")
+    ref_raw = g[f"des_raw_{prec}"]
+    err = np.max(np.abs(res.gamma_raw - ref_raw)) / np.max(np.abs(ref_raw))
+    assert err <= DESIGN_RTOL, err
+    assert np.array_equal(res.gamma_raw == 0, ref_raw == 0)      # frozen / clipped cells
+    _check_log(res.log, g, f"des_{prec}", rtol=DESIGN_RTOL)
 
 
 def _solver_inputs(W, tag):

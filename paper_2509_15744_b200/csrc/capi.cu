@@ -1365,26 +1365,36 @@ int sweep_adjoint_reference_t(wo_ctx* ctx, int64_t N, double dt, int64_t* fail_s
     CK(cudaMemsetAsync(ctx->maxslots, 0, (size_t)(N + 2) * 8, ctx->stream));
     char* lv[3] = {ctx->uprev(), ctx->ucur(), ctx->u3};   // (prev, cur, next)
     for (char* p : lv) CK(cudaMemsetAsync(p, 0, ctx->field_bytes(), ctx->stream));
-    const int n0 = ctx->kn0, n1 = ctx->kn1, n2 = ctx->kn2;
+    // one fused launch per step: stencil + support forces + mixed increment
+    RefAdjArgs<T> ra{};
+    ra.nd = ctx->ndim;
+    ra.n0 = ctx->kn0; ra.n1 = ctx->kn1; ra.n2 = ctx->kn2;
+    ra.gamma = reinterpret_cast<const T*>(ctx->base0(ctx->gamma));
+    ra.acc = reinterpret_cast<T*>(ctx->acc);
+    ra.mat = mat_scalars<T>(ctx);
+    ra.cv = (T)ctx->cv; ra.cg = (T)ctx->cg; ra.inv2dt = (T)ctx->inv2dt; ra.inv2dx = (T)ctx->inv2dx;
+    ra.sdt = (T)dt;
+    ra.sup_mask = ctx->mask;
+    ra.sup_prefix = ctx->prefix;
+    const size_t C = (size_t)ctx->cells();
+    const unsigned blocks = (unsigned)std::min<size_t>((C + 255) / 256, (size_t)ctx->num_sms * 8);
+    const T* h = reinterpret_cast<const T*>(ctx->hist);
     for (int64_t n = N - 1; n >= 1; --n) {
-        StepSpec sp;
-        sp.check = (n % STABILITY_CHECK_INTERVAL == 0) || (n == 1);
-        sp.sup_mode = SUP_INJECT;
-        sp.row = n;
-        sp.slot = n;
-        sp.prev = lv[0];
-        sp.cur = lv[1];
-        sp.out = lv[2];
-        rc = launch_step<T>(ctx, sp);
-        if (rc) return rc;
-        const T* h = reinterpret_cast<const T*>(ctx->hist);
-        const size_t C = (size_t)ctx->cells();
-        dropin_ki_kernel<T><<<592, 256, 0, ctx->stream>>>(
-            ctx->ndim, n0, n1, n2, reinterpret_cast<T*>(ctx->acc), h + (n - 1) * C, h + n * C,
-            h + (n + 1) * C, reinterpret_cast<const T*>(lv[2]), reinterpret_cast<const T*>(lv[1]),
-            reinterpret_cast<const T*>(lv[0]), (T)ctx->cv, (T)ctx->cg, (T)ctx->inv2dt,
-            (T)ctx->inv2dx, (T)dt);
+        ra.u_prev = reinterpret_cast<const T*>(lv[0]);
+        ra.u_cur = reinterpret_cast<const T*>(lv[1]);
+        ra.u_out = reinterpret_cast<T*>(lv[2]);
+        ra.h_old = h + (n - 1) * C;
+        ra.h_mid = h + n * C;
+        ra.h_new = h + (n + 1) * C;
+        ra.adj_row = reinterpret_cast<const T*>(ctx->store) + n * ctx->n_sup;
+        ra.check = (n % STABILITY_CHECK_INTERVAL == 0) || (n == 1);
+        ra.max_slot = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots) + n;
+        if (ctx->flavor == RHO_SCALED)
+            ref_adjoint_step_kernel<T, RHO_SCALED><<<blocks, 256, 0, ctx->stream>>>(ra);
+        else
+            ref_adjoint_step_kernel<T, ACOUSTIC><<<blocks, 256, 0, ctx->stream>>>(ra);
         ctx->launches++;
+        ctx->step_launches++;
         CK(cudaGetLastError());
         char* t = lv[0];   // rotate: (prev, cur, next) <- (cur, next, prev)
         lv[0] = lv[1];

@@ -89,6 +89,22 @@ def rate(problem, mat, prec, reps=3):
             "step_launches": st["step_launches"] // reps}
 
 
+def rate_reference(problem, mat, prec, reps=2):
+    """gradient_reference (gradients.py:329-391, the C1 comparator): forward
+    with the full history on the device, fused adjoint + mixed-kernel steps."""
+    import time
+
+    W.gradient_reference(problem, mat, precision=prec)          # warm
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        W.gradient_reference(problem, mat, precision=prec)
+    ms = (time.perf_counter() - t0) / reps * 1e3
+    n_shots = len(list(problem.shots()))
+    upd = 2 * (problem.time.n_steps - 1) * problem.grid.n_nodes * n_shots
+    return {"ms_per_gradient": ms, "gcell_upd_s": upd / ms / 1e6, "engine": "reference",
+            "timing": "host wall clock around gradient_reference (incl. the gradient D2H)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
@@ -112,6 +128,11 @@ def main():
             r.update({"config": name, "precision": prec})
             rows.append(r)
             print(json.dumps(r), flush=True)
+            if name.startswith("C1"):
+                r = rate_reference(problem, mat, prec)
+                r.update({"config": name + " gradient_reference", "precision": prec})
+                rows.append(r)
+                print(json.dumps(r), flush=True)
         W.release_contexts() if hasattr(W, "release_contexts") else None
     if args.out:
         with open(args.out, "w") as fh:

@@ -101,6 +101,7 @@ struct wo_ctx {
     size_t tflags_bytes = 0;
     unsigned int t2_seq = 0;           // two-step passes of the current sweep (flag values)
     bool t2_chain_next = false;        // the next pass directly follows one of this sweep
+    bool t2_oom = false;               // two-step buffers did not fit: single steps only
     char* stage = nullptr;             // fp64 upload staging (persistent)
     char* hstage = nullptr;            // pinned host staging for field downloads (2 halves)
     char* scratch = nullptr;           // one field (wo_get_field axis reversal)
@@ -202,6 +203,8 @@ int dev_alloc(wo_ctx* ctx, void** p, size_t bytes) {
     if (bytes == 0) bytes = 16;
     cudaError_t e = cudaMalloc(p, bytes);
     if (e != cudaSuccess) {
+        (void)cudaGetLastError();   // not sticky: later launch checks must not see it
+        *p = nullptr;
         ctx->err = std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e);
         return e == cudaErrorMemoryAllocation ? WO_ERR_BUDGET : WO_ERR_CUDA;
     }
@@ -241,6 +244,16 @@ MatScalars<T> mat_scalars(const wo_ctx* ctx) {
     }
     M.dt2 = (T)(dt * dt);
     return M;
+}
+
+// WB_T2_CHAIN (default 1): consecutive two-step passes of a sweep wait only
+// for their neighbour blocks of the previous pass (Step2Args::chain)
+bool t2_chain_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("WB_T2_CHAIN");
+        return !e || atoi(e) != 0;
+    }();
+    return on;
 }
 
 // planes per CTA of a single-step launch (tile width tw, per_sm resident
@@ -761,7 +774,29 @@ bool pair_ready(wo_ctx* ctx) {
     // slower than the single-step kernel (100.9 vs 106.7 Gcell-upd/s, 256^3):
     // fp64 takes two-step passes only when forced (option value 2)
     if (ctx->itemsize == 8 && ctx->use_two_step != 2) return false;
-    if (ensure_four(ctx) || ensure_mat4(ctx)) return false;
+    if (ctx->t2_oom) return false;
+    if (ensure_four(ctx) || ensure_mat4(ctx)) {
+        // the two extra levels and the material do not fit next to the rest:
+        // give back what was taken and keep single steps (four field buffers)
+        if (ctx->has_lo || ctx->has_hi) {   // slabs keep their 4 levels (peers)
+            ctx->t2_oom = true;
+            return false;
+        }
+        for (int b = 2; b < 4; ++b)
+            if (ctx->u[b]) {
+                cudaFree(ctx->u[b]);
+                ctx->u[b] = nullptr;
+                ctx->dev_bytes -= (int64_t)ctx->alloc_cells() * ctx->itemsize;
+            }
+        if (ctx->mat4) {
+            cudaFree(ctx->mat4);
+            ctx->mat4 = nullptr;
+            ctx->dev_bytes -= 4 * (int64_t)ctx->alloc_cells() * ctx->itemsize;
+        }
+        ctx->tma_state = 0;
+        ctx->t2_oom = true;
+        return false;
+    }
     if (ctx->t2_state == 0) {
         ctx->t2_state = -1;
         const int geo = pick_geo(ctx);
@@ -820,17 +855,28 @@ int choose_chunk2(const wo_ctx* ctx) {
     } else {
         const int slots = ctx->num_sms * (ctx->itemsize == 4 ? T2_CTAS_F32 : 1);
         const int nz_max = std::min(ctx->kn0, 64);
-        const double min_work = 1.9 * slots;   // CTAs for ~2 waves
+        // dataflow-chained passes (t2_chain_enabled) overlap one pass's tail
+        // with the next pass's start, so partial waves cost their CTAs only:
+        // a continuous wave count, with >= 2.2 waves of CTAs (256^3: 8
+        // layers, 254.9 Gcell/s, vs 250.4 for the whole-wave model's 10;
+        // 7 layers / 2.0 waves 248.4; profiles/r2/nz_chain.txt)
+        const bool chained = t2_chain_enabled() && !ctx->p2p && WB_T2_PDL;
+        const double min_work = (chained ? 2.2 : 1.9) * slots;   // CTAs for ~2 waves
         const bool can_stagger = (double)tiles * nz_max >= min_work;
         double best = 1e30;
         for (int nz = 1; nz <= nz_max; ++nz) {
             if (can_stagger && (double)tiles * nz < min_work) continue;
             const int chunk = (ctx->kn0 + nz - 1) / nz;
-            const int waves = (tiles * nz + slots - 1) / slots;
+            if (chained && chunk < 2 && nz > 1) continue;   // chaining needs >= 2 planes
+            // (grids too small for two waves keep whole waves: fewer, longer
+            // layers would only idle SMs)
+            const double waves = chained && can_stagger
+                                     ? (double)tiles * nz / slots
+                                     : (double)((tiles * nz + slots - 1) / slots);
             // chunks past 32 planes also lose per plane (measured at 1024^3:
             // 128-plane chunks 222-260 Gcell/s, 64-plane 279-280; 512^3 keeps
             // 86): a mild length penalty on top of the wave count
-            const double cost = (double)waves * (chunk + 1) *
+            const double cost = waves * (chunk + 1) *
                                 (1.0 + T2_LONG_CHUNK_PENALTY * std::max(0, chunk - 32));
             if (cost < best - 1e-9) { best = cost; best_nz = nz; }
         }
@@ -877,16 +923,6 @@ int choose_layers2(const wo_ctx* ctx, int* zb) {
     for (int p = 0; p < n0 && nz < T2_MAXZ; p += chunk) zb[++nz] = std::min(p + chunk, n0);
     zb[nz] = n0;
     return nz;
-}
-
-// WB_T2_CHAIN (default 1): consecutive two-step passes of a sweep wait only
-// for their neighbour blocks of the previous pass (Step2Args::chain)
-bool t2_chain_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("WB_T2_CHAIN");
-        return !e || atoi(e) != 0;
-    }();
-    return on;
 }
 
 // start of a run of two-step passes (a sweep): fresh block flags, so the
@@ -1115,6 +1151,10 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
     std::vector<double> vals(std::max(ns, 1));
     auto fcheck = [&](int64_t n) { return (n % STABILITY_CHECK_INTERVAL == 0) || (n == N - 1); };
     const bool pairs = ns <= MAX_SRC && !record && pair_ready(ctx);
+    // a peer-store slab must launch exactly like its neighbours
+    REQUIRE(!(ctx->p2p && ctx->t2_oom),
+            "two-step buffers do not fit on this peer-store slab: disable two-step passes on "
+            "every slab of the decomposition");
     std::vector<double> vals2(std::max(ns, 1));
     // graph of this sweep: the key covers everything the launches depend on
     // beyond the state generation
@@ -1263,6 +1303,9 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
     double val = 0.0;
     auto bcheck = [](int64_t n) { return (n % STABILITY_CHECK_INTERVAL == 0) || (n == 1); };
     const bool pairs = pair_ready(ctx);
+    REQUIRE(!(ctx->p2p && ctx->t2_oom),
+            "two-step buffers do not fit on this peer-store slab: disable two-step passes on "
+            "every slab of the decomposition");
     double val2 = 0.0;
     const bool graphable =
         ctx->use_graphs && !ctx->prof && ctx->part == 0 && !ctx->p2p && n_hi - n_lo >= 8;

@@ -416,6 +416,16 @@ class SlabGradient:
         h = self.halo
         return isinstance(h, PeerHalo) or (isinstance(h, IpcPeerHalo) and h.world > 1)
 
+    @property
+    def solo(self):
+        """One slab covering the whole grid (one rank): no halo at all."""
+        n0 = self.problem.grid.shape[0]
+        return all(i0 == 0 and i1 == n0 for i0, i1 in self.all_slabs)
+
+    @property
+    def whole_sweeps(self):
+        return self.peer_stores or self.solo
+
     def upload(self, material=None, gamma_local=None):
         """Material onto every slab (own + ghost planes; gamma_local: per
         context, its planes as contiguous fp64 host arrays); decides two-step
@@ -425,9 +435,7 @@ class SlabGradient:
             c.set_material(self.material if material is None else material, dt,
                            None if gamma_local is None else gamma_local[i])
         grid = self.problem.grid
-        n0 = grid.shape[0]
-        solo = all(i0 == 0 and i1 == n0 for i0, i1 in self.all_slabs)   # no neighbours
-        self.two_step = (self.peer_stores or solo) and two_step_slabs_ok(
+        self.two_step = self.whole_sweeps and two_step_slabs_ok(
             self.all_slabs, grid.shape[1] * grid.shape[2], [s.support_idx for _, s in self._shots])
         for c in self.ctxs:
             c.set_two_step(1 if self.two_step else 0)
@@ -460,7 +468,7 @@ class SlabGradient:
 
     def _forward_all(self, n_steps, src_local, amp, accumulate, dt):
         no_src = np.zeros((0, n_steps))
-        if self.peer_stores:   # sweeps enqueued on every slab (interleaved), then awaited
+        if self.whole_sweeps:   # sweeps enqueued on every slab (interleaved), then awaited
             for n0, n1 in self._peer_ranges(1, n_steps, 2):
                 for c, s in zip(self.ctxs, src_local):
                     c.sweep_forward_range(n_steps, n0, n1, [] if s is None else [s],
@@ -593,7 +601,7 @@ class SlabGradient:
             total += self.halo.allreduce_sum(cost)
             inject = [spec[0] > 0 for spec in specs]
             src_b = [N.WO_NO_SOURCE if s is None else s for s in src_local]
-            if self.peer_stores:
+            if self.whole_sweeps:
                 for hi, lo in self._peer_ranges(n_steps - 1, 0, -2):
                     for c, s, inj in zip(self.ctxs, src_b, inject):
                         c.sweep_backward_range(n_steps, hi, lo, s, amp[0], inj, True, dt)

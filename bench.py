@@ -1,32 +1,40 @@
 """Headline benchmark: superposed forward+adjoint sensitivity throughput.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+                    [--workload auto|c2|c5] [--scaling weak|strong] [--halo ipc|nccl]
 
 Metric (BASELINE.json): Gcell-updates/s of gradient_superposed, 3D, fp32.
-One bench "step" = one full gradient_superposed evaluation of the C2
-workload: 3D rho-scaled FWI on a 256^3 grid, one source,
-N = 1024 time steps, a 33x33 sensor plane, k = 1e13.  It performs
+
+N = 1 (default): one bench "step" = one full gradient_superposed evaluation
+of the C2 workload: 3D rho-scaled FWI on a 256^3 grid, one
+source, N = 1024 time steps, a 33x33 sensor plane, k = 1e13.  It performs
 2*(N-1)*C cell-updates (forward sweep + superposed backward sweep).
 
 * value  — device-resident: inputs already in HBM (SuperposedPlan.run()),
-           timed with CUDA events on the library stream, max over ranks.
+           timed with CUDA events on the library stream, max over ranks;
+           the timed evaluations run exactly as a user's.
 * e2e    — the public API call gradient_superposed(problem, material, cfg)
            with host (pinned) inputs: gamma/measured H2D and the gradient
            D2H inside the timed region.
-* roofline — the dominant step kernel: SURVEY 8(d)'s 24 algorithmic bytes
-           per fp32 cell-update x the cell-updates of one launch (a two-step
-           pass does 2C) / its mean launch duration, from CUDA events around
-           every 8th step launch of the timed region (bracketing every launch
-           cost ~3.5% of it), against MEASURED_PEAKS.json; the bytes the
-           two-step kernel really streams (10 fields per cell and pass) are
-           reported beside it.
-* cpu_baseline / --impl reference — the CPU oracle port (oracle/, a
-           restatement of the reference's Numba loops pinned bit-exact to
-           it) on the host cores, on a bounded sample of the same workload.
+* roofline — the dominant step kernel (step2_kernel_tma, two time steps per
+           pass): its time per step = ms_per_step x its share of the step's
+           GPU time in the committed ncu launch list of this command
+           (profiles/launch_share.json); achieved = SURVEY 8(d)'s 24 B per
+           fp32 cell-update x the 2C cell-updates of one launch / its launch
+           time; traffic / physical_frac from the committed ncu capture
+           (profiles/ncu_step_kernel.json); peak = MEASURED_PEAKS.json.
+* cpu_baseline / --impl reference — the reference ITSELF (baseline/_ref:
+           the unmodified waveopt package, Python + Numba) on the host cores,
+           one process and one per core, on a bounded sample of the same
+           workload; the pinned C/OpenMP oracle port (oracle/) is reported
+           beside it and replaces it when baseline/_ref is absent.
 
-N > 1 (torchrun): shot-parallel weak scaling — each rank evaluates its own
-shot of the same 256^3 model and the per-shot accumulators are summed with
-one NCCL all-reduce per evaluation (shot-parallel mode).
+N > 1 (torchrun) or --workload c5: SURVEY C5 — one slab of 256 x 2048^2
+cells per GPU (weak scaling; --scaling strong: global 2048^3), N = 200
+steps, peer ghost stores through CUDA IPC (SlabGradient.for_rank, halo
+"ipc"; --halo nccl: send/recv exchanges), two-step passes on the slabs.
+--workload c2 with N > 1: shot-parallel (one 256^3 shot per GPU, one NCCL
+all-reduce of the accumulator per evaluation).
 """
 
 from __future__ import annotations
@@ -330,6 +338,7 @@ def run_reference_arm(args):
         return run_port_arm(args, wl)
     n_sample = args.ref_sample_steps
     ref = ReferenceCPU(R, wl, n_sample)
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
     procs = host_cores()
     one_s = ref.one()                                  # 1 process (1 core)
     for _ in range(args.warmup):
@@ -344,7 +353,10 @@ def run_reference_arm(args):
         "data": "synthetic", "impl": "reference",
         "config": {"workload": wl["name"], "grid": list(wl["shape"]),
                    "n_steps_sampled": n_sample, "shots": procs, "precision": "single",
-                   "l2": "inputs larger than L2 (268 MB working set per process)"},
+                   "l2": "inputs larger than L2 (268 MB working set per process)",
+                   "note": ("per-cell-update rate of the reference on the 256^3 grid (the "
+                            "C5 slabs need >= 43 GB per CPU process: extrapolated, SURVEY "
+                            "8(d))" if world_env > 1 else "same grid as the GPU arm")},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "reference",
                          "sample": ref.describe(procs),
                          "value_1process": ref.updates / one_s / 1e9,

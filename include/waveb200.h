@@ -106,6 +106,11 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
  * captured into a CUDA graph on its second occurrence and replayed from then
  * on (launch-bound small grids gain most); 0 = always launch directly. */
 #define WO_OPT_GRAPHS 6
+/* WO_OPT_CLUSTER (default 1): small 2D grids (>= 32 rows, the whole problem
+ * within one 16-CTA thread-block cluster's shared memory) run every sweep as
+ * ONE cluster-resident launch (fields in distributed shared memory, one
+ * cluster barrier per step, identical arithmetic); 0 = step launches. */
+#define WO_OPT_CLUSTER 7
 int wo_set_option(wo_ctx* ctx, int option, int value);
 /* Device-resident optimisation loop (fwi.py:178-238 with
  * optim.py adam_step / clip_bounds): fp64 parameters (gamma), the Adam

@@ -127,6 +127,7 @@ WO_OPT_FAST_DIV = 1
 WO_OPT_PAIR_KERNEL = 2
 WO_OPT_TMA_KERNEL = 3
 WO_OPT_TWO_STEP = 4
+WO_OPT_CLUSTER = 7
 WO_OPT_PLANE_PART = 5
 WO_OPT_GRAPHS = 6
 WO_SNAP_FREE, WO_SNAP_SAVE, WO_SNAP_RESTORE = 0, 1, 2

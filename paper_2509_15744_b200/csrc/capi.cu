@@ -102,6 +102,10 @@ struct wo_ctx {
     unsigned int t2_seq = 0;           // two-step passes of the current sweep (flag values)
     bool t2_chain_next = false;        // the next pass directly follows one of this sweep
     bool t2_oom = false;               // two-step buffers did not fit: single steps only
+    int cl_state = 0;                  // cluster sweep engine: 0 unknown, 1 ready, -1 no
+    int cl_size = 0, cl_rows = 0;      // CTAs per cluster, rows per CTA
+    double* amp_dev = nullptr;         // source amplitude table of a cluster sweep
+    size_t amp_cap = 0;
     char* stage = nullptr;             // fp64 upload staging (persistent)
     char* hstage = nullptr;            // pinned host staging for field downloads (2 halves)
     char* scratch = nullptr;           // one field (wo_get_field axis reversal)
@@ -935,6 +939,102 @@ int t2_sweep_begin(wo_ctx* ctx) {
     return WO_OK;
 }
 
+// ---- cluster-resident whole sweeps of small 2D grids (cluster_sweep.cuh) ----
+// WB_CLUSTER=0 disables the engine (A/B runs)
+bool cluster_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("WB_CLUSTER");
+        return !e || atoi(e) != 0;
+    }();
+    return on;
+}
+
+template <typename T>
+bool cluster_ready(wo_ctx* ctx) {
+    if (ctx->cl_state == 0) {
+        ctx->cl_state = -1;
+        if (cluster_enabled() && ctx->ndim == 2 && ctx->kn0 == 1 && !ctx->has_lo &&
+            !ctx->has_hi && ctx->kn1 >= 2 * CS_MAX_CLUSTER) {
+            const int rows = (ctx->kn1 + CS_MAX_CLUSTER - 1) / CS_MAX_CLUSTER;
+            const int cl = (ctx->kn1 + rows - 1) / rows;
+            if (cluster_sweep_smem<T>(rows, ctx->kn2) + 1024 <= 227 * 1024) {
+                ClusterSweepArgs<T> a{};
+                a.rows = rows;
+                a.n2 = ctx->kn2;
+                if (launch_cluster_sweep<T>(RHO_SCALED, true, a, cl, ctx->stream, true) ==
+                    cudaSuccess) {
+                    ctx->cl_state = 1;
+                    ctx->cl_size = cl;
+                    ctx->cl_rows = rows;
+                }
+            }
+            (void)cudaGetLastError();
+        }
+    }
+    return ctx->cl_state == 1;
+}
+
+// steps n_first, n_first +- 1, ... (count of them) of an N-step sweep in one
+// launch; the window indices rotate as count single steps would
+template <typename T>
+int run_cluster_sweep(wo_ctx* ctx, int backward, int64_t N, int64_t n_first, int64_t count,
+                      int ns, const long long* sidx, const double* const* amp_rows, bool acc,
+                      double sdt, int sup_mode) {
+    ClusterSweepArgs<T> a{};
+    a.n1 = ctx->kn1;
+    a.n2 = ctx->kn2;
+    a.rows = ctx->cl_rows;
+    a.backward = backward;
+    a.n_first = (int)n_first;
+    a.n_count = (int)count;
+    a.N = N;
+    a.gamma = reinterpret_cast<const T*>(ctx->base0(ctx->gamma));
+    a.u_prev_in = reinterpret_cast<const T*>(ctx->uprev());
+    a.u_cur_in = reinterpret_cast<const T*>(ctx->ucur());
+    if (count % 2) std::swap(ctx->cur, ctx->prv);
+    a.u_prev_out = reinterpret_cast<T*>(ctx->uprev());
+    a.u_cur_out = reinterpret_cast<T*>(ctx->ucur());
+    a.acc = reinterpret_cast<T*>(ctx->acc);
+    a.accumulate = acc;
+    a.mat = mat_scalars<T>(ctx);
+    a.cv = (T)ctx->cv; a.cg = (T)ctx->cg; a.inv2dt = (T)ctx->inv2dt; a.inv2dx = (T)ctx->inv2dx;
+    a.sdt = (T)sdt;
+    a.n_src = 0;
+    std::vector<double> table;
+    for (int s = 0; s < ns; ++s) {
+        const long long f = sidx[s];
+        if (f < 0 || f >= ctx->cells()) continue;
+        a.src_j[a.n_src] = (int)(f / ctx->kn2);
+        a.src_k[a.n_src] = (int)(f % ctx->kn2);
+        table.insert(table.end(), amp_rows[s], amp_rows[s] + N);
+        a.n_src++;
+    }
+    if (a.n_src) {
+        int rc = ensure(ctx, &ctx->amp_dev, &ctx->amp_cap, table.size() * sizeof(double));
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(ctx->amp_dev, table.data(), table.size() * sizeof(double),
+                           cudaMemcpyHostToDevice, ctx->stream));
+        a.src_amp = ctx->amp_dev;
+    }
+    a.sup_mode = ctx->n_sup > 0 ? sup_mode : SUP_NONE;
+    a.n_sup = ctx->n_sup;
+    a.sup_mask = ctx->mask;
+    a.sup_prefix = ctx->prefix;
+    a.store = reinterpret_cast<T*>(ctx->store);
+    a.maxslots = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots);
+    prof_begin(ctx, 0);
+    const cudaError_t e = launch_cluster_sweep<T>(ctx->flavor, acc, a, ctx->cl_size, ctx->stream,
+                                                  false);
+    prof_end(ctx);
+    ctx->launches++;
+    ctx->step_launches++;
+    ctx->t2_chain_next = false;
+    CK(e);
+    CK(cudaGetLastError());
+    if (a.n_src) CK(cudaStreamSynchronize(ctx->stream));   // host table lifetime
+    return WO_OK;
+}
+
 struct PairSpec {
     bool acc = false, check1 = false, check2 = false;
     double sdt = 0.0;
@@ -1150,6 +1250,17 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
             "sweep not initialised (first range must start at n = 1)");
     std::vector<double> vals(std::max(ns, 1));
     auto fcheck = [&](int64_t n) { return (n % STABILITY_CHECK_INTERVAL == 0) || (n == N - 1); };
+    // small 2D grids: the whole range in one cluster-resident launch
+    const bool cluster = !record && ns <= MAX_SRC && ctx->part == 0 && !ctx->p2p &&
+                         n_end > n_begin && cluster_ready<T>(ctx);
+    if (cluster) {
+        std::vector<const double*> rows(ns);
+        for (int s = 0; s < ns; ++s) rows[s] = src_amp + (int64_t)spos[s] * N;
+        rc = run_cluster_sweep<T>(ctx, 0, N, n_begin, n_end - n_begin, ns, sidx.data(), rows.data(),
+                                  accumulate != 0, -dt, gather ? SUP_GATHER : SUP_NONE);
+        if (rc) return rc;
+        n_end = n_begin;   // nothing left for the step loop
+    }
     const bool pairs = ns <= MAX_SRC && !record && pair_ready(ctx);
     // a peer-store slab must launch exactly like its neighbours
     REQUIRE(!(ctx->p2p && ctx->t2_oom),
@@ -1159,7 +1270,7 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
     // graph of this sweep: the key covers everything the launches depend on
     // beyond the state generation
     const bool graphable = ctx->use_graphs && !ctx->prof && ctx->part == 0 && !record &&
-                           !ctx->p2p && ns <= MAX_SRC && n_end - n_begin >= 8;
+                           !ctx->p2p && !cluster && ns <= MAX_SRC && n_end - n_begin >= 8;
     uint64_t gkey = 0;
     bool capturing = false;
     const int64_t l0 = ctx->launches, s0 = ctx->step_launches, p0 = ctx->pair_launches;
@@ -1302,13 +1413,21 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
                              : src_flat >= 0;
     double val = 0.0;
     auto bcheck = [](int64_t n) { return (n % STABILITY_CHECK_INTERVAL == 0) || (n == 1); };
+    const bool cluster = ctx->part == 0 && !ctx->p2p && n_hi > n_lo && cluster_ready<T>(ctx);
+    if (cluster) {
+        const double* row = src_amp;
+        rc = run_cluster_sweep<T>(ctx, 1, N, n_hi, n_hi - n_lo, has_src ? 1 : 0, &sf, &row,
+                                  accumulate != 0, dt, inject ? SUP_INJECT : SUP_NONE);
+        if (rc) return rc;
+        n_hi = n_lo;
+    }
     const bool pairs = pair_ready(ctx);
     REQUIRE(!(ctx->p2p && ctx->t2_oom),
             "two-step buffers do not fit on this peer-store slab: disable two-step passes on "
             "every slab of the decomposition");
     double val2 = 0.0;
-    const bool graphable =
-        ctx->use_graphs && !ctx->prof && ctx->part == 0 && !ctx->p2p && n_hi - n_lo >= 8;
+    const bool graphable = ctx->use_graphs && !ctx->prof && ctx->part == 0 && !ctx->p2p &&
+                           !cluster && n_hi - n_lo >= 8;
     uint64_t gkey = 0;
     bool capturing = false;
     const int64_t l0 = ctx->launches, s0 = ctx->step_launches, p0 = ctx->pair_launches;
@@ -1795,7 +1914,8 @@ void wo_destroy(wo_ctx* ctx) {
                     ctx->flag, ctx->acc, reinterpret_cast<char*>(ctx->in_flags),
                     ctx->mask, ctx->prefix,
                     ctx->store, ctx->measured, ctx->partial, ctx->cost, ctx->maxslots,
-                    ctx->f_idx, ctx->f_vals, ctx->f_dense, ctx->hist, ctx->u3};
+                    ctx->f_idx, ctx->f_vals, ctx->f_dense, ctx->hist, ctx->u3,
+                    reinterpret_cast<char*>(ctx->amp_dev), reinterpret_cast<char*>(ctx->tflags)};
     for (auto& m : ctx->ipc_maps) cudaIpcCloseMemHandle(m.second);
     for (void* b : bufs)
         if (b) cudaFree(b);
@@ -2012,8 +2132,13 @@ int wo_set_option(wo_ctx* ctx, int option, int value) {
     ++ctx->gen;
     REQUIRE(option == WO_OPT_FAST_DIV || option == WO_OPT_PAIR_KERNEL ||
                 option == WO_OPT_TMA_KERNEL || option == WO_OPT_TWO_STEP ||
-                option == WO_OPT_PLANE_PART || option == WO_OPT_GRAPHS,
+                option == WO_OPT_PLANE_PART || option == WO_OPT_GRAPHS ||
+                option == WO_OPT_CLUSTER,
             "unknown option");
+    if (option == WO_OPT_CLUSTER) {
+        ctx->cl_state = value ? 0 : -1;   // 0: probe again on the next sweep
+        return WO_OK;
+    }
     if (option == WO_OPT_GRAPHS) {
         ctx->use_graphs = value != 0;
         return WO_OK;

@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 
+#include "cluster_sweep.cuh"
 #include "step2_kernel.cuh"
 #include "step_kernel.cuh"
 #include "step_kernel_tma.cuh"
@@ -52,6 +53,12 @@ void launch_material4(int flavor, cudaStream_t s, const T* gamma, const MatScala
 // of this process will set, such a load would wait forever.  The peer-store
 // setup (wo_slab_peers) therefore loads them all up front.
 template <typename T> void preload_step_kernels();
+
+// whole sweep of a small 2D grid in one cluster launch (cluster_sweep.cuh);
+// probe = only check that the device can hold the cluster
+template <typename T>
+cudaError_t launch_cluster_sweep(int flavor, bool acc, const ClusterSweepArgs<T>& a, int cl,
+                                 cudaStream_t s, bool probe);
 template <typename T> void preload_step2_kernels();
 
 

@@ -423,6 +423,10 @@ class DeviceGrid:
         """Replay repeated sweeps from captured CUDA graphs (default on)."""
         self._ck(self.L.wo_set_option(self.h, N.WO_OPT_GRAPHS, int(bool(on))), "wo_set_option")
 
+    def set_cluster(self, on):
+        """Cluster-resident whole sweeps of small 2D grids (WO_OPT_CLUSTER)."""
+        self._ck(self.L.wo_set_option(self.h, N.WO_OPT_CLUSTER, int(bool(on))), "wo_set_option")
+
     def slab_abort(self):
         """Release streams waiting on this slab's peer flags (wo_slab_abort)."""
         self._ck(self.L.wo_slab_abort(self.h), "wo_slab_abort")

@@ -108,6 +108,7 @@ def rate_reference(problem, mat, prec, reps=2):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
+    ap.add_argument("--only", default=None, help="comma-separated config prefixes, e.g. C1,C3")
     args = ap.parse_args()
     rows = []
     cases = [
@@ -117,6 +118,9 @@ def main():
         ("C3 TATO 3D 192^3, N=600", lambda: tato((192, 192, 192), 600)),
         ("C4 3D FWI 1024^3, 4 shots, N=128 sample", lambda: fwi((1024, 1024, 1024), 128, 4)),
     ]
+    if args.only:
+        keep = tuple(args.only.split(","))
+        cases = [c for c in cases if c[0].startswith(keep)]
     for name, make in cases:
         problem, mat = make()
         for prec in ("single", "double"):

@@ -339,3 +339,47 @@ def test_two_step_long_chunks(W, knob, prec):
     out = subprocess.run([sys.executable, os.path.join(here, "_long_chunk_case.py"), prec],
                          env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("shape", [(256, 256), (101, 101), (33, 29), (40, 200), (97, 64)])
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_cluster_sweep_engine_bitwise(W, shape, prec):
+    """Small 2D grids: the cluster-resident whole-sweep engine (one launch per
+    sweep, fields in distributed shared memory) gives the step kernels' bits
+    (and the oracle's) for the superposed gradient, FWI with a source near a
+    CTA row boundary and sensors on several CTAs."""
+    from oracle import oracle as O
+    from paper_2509_15744_b200 import engine
+
+    rng = np.random.default_rng(sum(shape))
+    dx, n_steps = 2e-4, 121
+    dt = 0.5 * dx / 6000.0
+    grid = W.build_grid(shape, dx)
+    gamma = rng.uniform(0.3, 1.0, size=shape)
+    mat = W.MaterialModel.rho_scaled(gamma, grid, rho0=2700.0, c0=6000.0)
+    src = W.SourceSpec(node=(shape[0] // 2 + 1, shape[1] // 3), amplitude=1e12, frequency=1.5e6,
+                       cycles=2)
+    nodes = sorted({(i, j) for i in (0, shape[0] // 4, shape[0] - 1)
+                    for j in (0, shape[1] // 2, shape[1] - 1)})
+    meas = rng.normal(scale=1e-9, size=(1, len(nodes), n_steps))
+    problem = W.FwiProblem(grid=grid, time=W.TimeConfig(n_steps, dt), material=mat,
+                           sources=[src], sensors=W.SensorArray(nodes=nodes), measured=meas)
+    cfg = W.SuperpositionConfig(k=1e14, precision=prec)
+    ctx = engine.get_context(grid, W.precision_dtype(prec))
+    try:
+        ctx.set_cluster(True)
+        ctx.reset_stats()
+        on = W.gradient_superposed(problem, mat, cfg)
+        launches_on = ctx.stats()["step_launches"]
+        ctx.set_cluster(False)
+        off = W.gradient_superposed(problem, mat, cfg)
+    finally:
+        ctx.set_cluster(True)
+    assert launches_on == 2        # one launch per sweep
+    assert bits_equal(on.gradient, off.gradient)
+    assert on.cost == off.cost
+    omat = O.Material("rho_scaled", gamma, dx, rho0=2700.0, c0=6000.0)
+    support = np.array([grid.flat_index(n) for n in nodes], dtype=np.int64)
+    shots = [(O.Source(src.node, 1e12, 1.5e6, 2), O.FwiShot(support, meas[0], dt))]
+    _, grad, _ = O.gradient_superposed(omat, dt, n_steps, shots, 1e14, prec)
+    assert bits_equal(on.gradient, grad)

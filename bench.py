@@ -516,6 +516,18 @@ def run_native(args):
     gc.enable()
     print(f"e2e per call (s): {[round(x, 4) for x in per_call]}", file=sys.stderr)
     e2e_value = world * updates / e2e_s / 1e9
+    # the same call from plain pageable numpy arrays (the usual waveopt
+    # caller): two evaluations, reported beside the pinned e2e
+    pageable = None
+    if world == 1:
+        problem.measured = np.array(meas_pinned)
+        mat_pg = model.with_gamma(np.array(gamma_pinned))
+        W.gradient_superposed(problem, mat_pg, cfg)
+        t0 = time.perf_counter()
+        for _ in range(2):
+            W.gradient_superposed(problem, mat_pg, cfg)
+        pageable = updates / ((time.perf_counter() - t0) / 2) / 1e9
+        problem.measured = meas_pinned
     n_sup = len(problem.sensors)
     h2d = C * 8 + n_sup * n_steps * 8
     d2h = C * 4 + 8 + 2 * (n_steps + 2) * 8
@@ -571,7 +583,8 @@ def run_native(args):
                          "traffic_source": NCU_TRAFFIC_SRC,
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+                    "host_buffers": "pinned", "value_pageable": pageable},
             "gpu_launches": int(stats["launches"]),
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,

@@ -106,7 +106,7 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
  * captured into a CUDA graph on its second occurrence and replayed from then
  * on (launch-bound small grids gain most); 0 = always launch directly. */
 #define WO_OPT_GRAPHS 6
-/* WO_OPT_CLUSTER (default 1): small 2D grids (>= 32 rows, the whole problem
+/* WO_OPT_CLUSTER (default 0): small 2D grids (>= 32 rows, the whole problem
  * within one 16-CTA thread-block cluster's shared memory) run every sweep as
  * ONE cluster-resident launch (fields in distributed shared memory, one
  * cluster barrier per step, identical arithmetic); 0 = step launches. */

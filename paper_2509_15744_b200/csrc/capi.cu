@@ -36,6 +36,17 @@ constexpr int STABILITY_CHECK_INTERVAL = 50;     // solver.py:29
 constexpr double STABILITY_GROWTH_FACTOR = 1e6;  // solver.py:30
 thread_local std::string g_create_error;
 
+// cluster-resident sweeps of small 2D grids (cluster_sweep.cuh): default of
+// WO_OPT_CLUSTER for new contexts; WB_CLUSTER=0/1 overrides (A/B runs)
+constexpr bool CLUSTER_DEFAULT = false;
+bool cluster_default() {
+    static const bool on = [] {
+        const char* e = getenv("WB_CLUSTER");
+        return e ? atoi(e) != 0 : CLUSTER_DEFAULT;
+    }();
+    return on;
+}
+
 }  // namespace
 
 struct wo_ctx {
@@ -102,6 +113,7 @@ struct wo_ctx {
     unsigned int t2_seq = 0;           // two-step passes of the current sweep (flag values)
     bool t2_chain_next = false;        // the next pass directly follows one of this sweep
     bool t2_oom = false;               // two-step buffers did not fit: single steps only
+    int use_cluster = cluster_default();   // wo_set_option(WO_OPT_CLUSTER)
     int cl_state = 0;                  // cluster sweep engine: 0 unknown, 1 ready, -1 no
     int cl_size = 0, cl_rows = 0;      // CTAs per cluster, rows per CTA
     double* amp_dev = nullptr;         // source amplitude table of a cluster sweep
@@ -940,24 +952,18 @@ int t2_sweep_begin(wo_ctx* ctx) {
 }
 
 // ---- cluster-resident whole sweeps of small 2D grids (cluster_sweep.cuh) ----
-// WB_CLUSTER=0 disables the engine (A/B runs)
-bool cluster_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("WB_CLUSTER");
-        return !e || atoi(e) != 0;
-    }();
-    return on;
-}
+
 
 template <typename T>
 bool cluster_ready(wo_ctx* ctx) {
     if (ctx->cl_state == 0) {
         ctx->cl_state = -1;
-        if (cluster_enabled() && ctx->ndim == 2 && ctx->kn0 == 1 && !ctx->has_lo &&
+        if (ctx->use_cluster && ctx->ndim == 2 && ctx->kn0 == 1 && !ctx->has_lo &&
             !ctx->has_hi && ctx->kn1 >= 2 * CS_MAX_CLUSTER) {
             const int rows = (ctx->kn1 + CS_MAX_CLUSTER - 1) / CS_MAX_CLUSTER;
             const int cl = (ctx->kn1 + rows - 1) / rows;
-            if (cluster_sweep_smem<T>(rows, ctx->kn2) + 1024 <= 227 * 1024) {
+            if (cluster_sweep_smem<T>(rows, ctx->kn2) + 1024 <= 227 * 1024 &&
+                rows * ctx->kn2 <= CS_MAXC * CS_THREADS) {
                 ClusterSweepArgs<T> a{};
                 a.rows = rows;
                 a.n2 = ctx->kn2;
@@ -1945,7 +1951,7 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
     ctx->flavor = flavor;
     ctx->rho0 = rho0; ctx->rho1 = rho1; ctx->kappa1 = kappa1;
     ctx->rho2 = rho2; ctx->kappa2 = kappa2; ctx->dt_mat = dt; ctx->ratio2 = ratio2;
-    // gamma.astype(T) (solver.py:94/100) on the host: halves H2D bytes in fp32
+    // gamma.astype(T) (solver.py:94/100): fp64 staged up and cast on the device
     const int64_t n = ctx->alloc_cells();
     if (ctx->itemsize == 4) {
         rc = upload_cast_t<float>(ctx, gamma, ctx->gamma, n);
@@ -2136,7 +2142,8 @@ int wo_set_option(wo_ctx* ctx, int option, int value) {
                 option == WO_OPT_CLUSTER,
             "unknown option");
     if (option == WO_OPT_CLUSTER) {
-        ctx->cl_state = value ? 0 : -1;   // 0: probe again on the next sweep
+        ctx->use_cluster = value != 0;
+        ctx->cl_state = 0;   // probe again on the next sweep
         return WO_OK;
     }
     if (option == WO_OPT_GRAPHS) {

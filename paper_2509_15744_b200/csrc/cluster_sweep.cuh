@@ -29,6 +29,7 @@ namespace wb {
 
 constexpr int CS_THREADS = 1024;
 constexpr int CS_MAX_CLUSTER = 16;
+constexpr int CS_MAXC = 12;   // cells per thread (R * n2 <= 12 * 1024)
 
 template <typename T> struct ClusterSweepArgs {
     int n1, n2;                 // kernel-space plane (2D grid: rows j, columns k)
@@ -60,7 +61,9 @@ template <typename T>
 __host__ __device__ constexpr size_t cluster_sweep_smem(int rows, int n2) {
     // U[2][R+2][n2], COEF[R][n2], WJ[R+1][n2], WK[R][n2+1], ACC[R][n2]
     return sizeof(T) * ((size_t)2 * (rows + 2) * n2 + (size_t)rows * n2 + (size_t)(rows + 1) * n2 +
-                        (size_t)rows * (n2 + 1) + (size_t)rows * n2);
+                        (size_t)rows * (n2 + 1) + (size_t)rows * n2) +
+           // support bits of the own rows (+1 word of slack each side)
+           sizeof(unsigned int) * (((size_t)rows * n2 + 31) / 32 + 2);
 }
 
 __device__ __forceinline__ unsigned cs_rank() {
@@ -109,9 +112,19 @@ __global__ void __launch_bounds__(CS_THREADS, 1) cluster_sweep_kernel(const Clus
     T* WJ = CO + (size_t)R * n2;                    // [R+1][n2]: face (j-1, j) of own row r at r
     T* WK = WJ + (size_t)(R + 1) * n2;              // [R][n2+1]: face (k-1, k) at k
     T* AC = WK + (size_t)R * (n2 + 1);              // [R][n2]
+    unsigned int* SB = reinterpret_cast<unsigned int*>(AC + (size_t)R * n2);   // support bits
     __shared__ Bits smax[CS_THREADS / 32];
     const int tid = threadIdx.x;
     const int ncell = own * n2;
+    // this thread's cells, fixed for the sweep: c = tid + i * CS_THREADS
+    const int nmine = ncell > tid ? (ncell - tid + CS_THREADS - 1) / CS_THREADS : 0;
+    int cr[CS_MAXC], ck[CS_MAXC];
+#pragma unroll
+    for (int i = 0; i < CS_MAXC; ++i) {
+        const int c = tid + i * CS_THREADS;
+        cr[i] = c / n2;
+        ck[i] = c - cr[i] * n2;
+    }
 
     // ---- prologue: material, window, accumulator ----
     auto mg = [&](int j, int k) { return P::m(a.mat, __ldg(a.gamma + (long long)j * n2 + k)); };
@@ -134,6 +147,17 @@ __global__ void __launch_bounds__(CS_THREADS, 1) cluster_sweep_kernel(const Clus
     for (int s = 0; s < a.n_src; ++s)
         if (a.src_j[s] >= j0 && a.src_j[s] < j0 + own) my_src |= 1u << s;
     const bool has_sup = a.sup_mode != SUP_NONE && a.n_sup > 0;
+    // support bits of the own cells, local cell index c (bit c of SB)
+    const long long gbase = (long long)j0 * n2;
+    if (has_sup)
+        for (int w = tid; w < (ncell + 31) / 32; w += CS_THREADS) {
+            unsigned int v = 0;
+            for (int b = 0; b < 32 && w * 32 + b < ncell; ++b) {
+                const long long g = gbase + w * 32 + b;
+                v |= ((__ldg(a.sup_mask + (g >> 5)) >> (g & 31)) & 1u) << b;
+            }
+            SB[w] = v;
+        }
     cs_cluster_sync();   // every CTA's rows are loaded before the first halo read
 
     // remote addresses of the neighbours' boundary rows (both level buffers)
@@ -154,20 +178,25 @@ __global__ void __launch_bounds__(CS_THREADS, 1) cluster_sweep_kernel(const Clus
         const bool check = a.backward ? (n % 50 == 0 || n == 1) : (n % 50 == 0 || n == a.N - 1);
         T* srow = has_sup ? a.store + n * a.n_sup : nullptr;
         // ---- 2: the own cells ----
-        for (int c = tid; c < ncell; c += CS_THREADS) {
-            const int r = c / n2, k = c - r * n2, j = j0 + r;
+#pragma unroll
+        for (int i = 0; i < CS_MAXC; ++i) {
+            if (i >= nmine) break;
+            const int r = cr[i], k = ck[i], j = j0 + r;
+            const int c = tid + i * CS_THREADS;
             const size_t o = (size_t)(r + 1) * n2 + k;
             const T uc = cu[o];
             const T up = pv[o];
+            const T uj_m = cu[o - n2], uj_p = cu[o + n2];
+            const T uk_m = k > 0 ? cu[o - 1] : uc, uk_p = k < n2 - 1 ? cu[o + 1] : uc;
             T s = uc - uc;
-            if (j < n1 - 1) s += (cu[o + n2] - uc) * WJ[(size_t)(r + 1) * n2 + k];
-            if (j > 0) s -= (uc - cu[o - n2]) * WJ[(size_t)r * n2 + k];
-            if (k < n2 - 1) s += (cu[o + 1] - uc) * WK[(size_t)r * (n2 + 1) + k + 1];
-            if (k > 0) s -= (uc - cu[o - 1]) * WK[(size_t)r * (n2 + 1) + k];
+            if (j < n1 - 1) s += (uj_p - uc) * WJ[(size_t)(r + 1) * n2 + k];
+            if (j > 0) s -= (uc - uj_m) * WJ[(size_t)r * n2 + k];
+            if (k < n2 - 1) s += (uk_p - uc) * WK[(size_t)r * (n2 + 1) + k + 1];
+            if (k > 0) s -= (uc - uk_m) * WK[(size_t)r * (n2 + 1) + k];
             T out = ((uc + uc) - up) + CO[c] * s;
-            const long long g = (long long)j * n2 + k;
             // nodal sources, then the support (solver.py:167-170)
             if (my_src) {
+                const long long g = gbase + c;
                 for (int q = 0; q < a.n_src; ++q) {
                     if (!((my_src >> q) & 1u) || a.src_j[q] != j || a.src_k[q] != k) continue;
                     const T gam = __ldg(a.gamma + g);
@@ -176,27 +205,26 @@ __global__ void __launch_bounds__(CS_THREADS, 1) cluster_sweep_kernel(const Clus
                     out = out + P::fc(a.mat, gam, kap) * (T)a.src_amp[(long long)q * a.N + n];
                 }
             }
-            if (has_sup) {
+            if (has_sup && ((SB[c >> 5] >> (c & 31)) & 1u)) {
+                const long long g = gbase + c;
                 const unsigned int w = __ldg(a.sup_mask + (g >> 5));
                 const unsigned int bit = (unsigned int)(g & 31);
-                if ((w >> bit) & 1u) {
-                    const int qi = __ldg(a.sup_prefix + (g >> 5)) + __popc(w & ((1u << bit) - 1u));
-                    if (a.sup_mode == SUP_GATHER) {
-                        srow[qi] = uc;                    // trace entry n = u^n
-                    } else {
-                        const T gam = __ldg(a.gamma + g);
-                        T kap;
-                        (void)P::coef(a.mat, gam, kap);
-                        out = out + P::fc(a.mat, gam, kap) * srow[qi];
-                    }
+                const int qi = __ldg(a.sup_prefix + (g >> 5)) + __popc(w & ((1u << bit) - 1u));
+                if (a.sup_mode == SUP_GATHER) {
+                    srow[qi] = uc;                    // trace entry n = u^n
+                } else {
+                    const T gam = __ldg(a.gamma + g);
+                    T kap;
+                    (void)P::coef(a.mat, gam, kap);
+                    out = out + P::fc(a.mat, gam, kap) * srow[qi];
                 }
             }
             if (ACC) {
                 // self-kernel increment; (cv*va)*va is sign-invariant, the
                 // absent axis 0 contributes (0*0) + ... = the 2D sum exactly
                 const T va = (out - up) * a.inv2dt;
-                const T gj = (cu[j < n1 - 1 ? o + n2 : o] - cu[j > 0 ? o - n2 : o]) * a.inv2dx;
-                const T gk = (cu[k < n2 - 1 ? o + 1 : o] - cu[k > 0 ? o - 1 : o]) * a.inv2dx;
+                const T gj = ((j < n1 - 1 ? uj_p : uc) - (j > 0 ? uj_m : uc)) * a.inv2dx;
+                const T gk = (uk_p - uk_m) * a.inv2dx;
                 AC[c] = AC[c] + a.sdt * ((a.cv * va) * va + a.cg * ((gj * gj) + (gk * gk)));
             }
             pv[o] = out;

@@ -168,7 +168,7 @@ def run_forward(material: MaterialModel, time: TimeConfig, sources,
     else:
         traces = (np.zeros((len(sensor_idx), n_steps), dtype=dtype)
                   if sensor_idx is not None else None)
-        up, uc = ctx.get_window()
+        uc = np.zeros(grid.shape, dtype)        # u^1 = 0 after the reset
         peak = 0.0
         for n in range(1, n_steps):
             if traces is not None:
@@ -176,13 +176,14 @@ def run_forward(material: MaterialModel, time: TimeConfig, sources,
             force = (src_flat, amp[:, n]) if len(sources) else None
             check = n % STABILITY_CHECK_INTERVAL == 0 or n == n_steps - 1
             m = ctx.step(force, want_max=check)
-            up, uc = ctx.get_window()
+            uc = ctx.get_field("u_cur").reshape(grid.shape)   # one D2H per step
             if check:
                 peak = max(peak, _check(m, n + 1, scale))
             if history is not None:
                 history[n + 1] = uc
             if on_step is not None:
                 on_step(n, uc)
+        up, uc = ctx.get_window()
     window = SolverWindow(u_prev=up, u_cur=uc, u_next=np.zeros_like(uc), step=n_steps)
     if sensors is not None:
         sensors.traces = traces
@@ -204,8 +205,7 @@ def run_backward(material: MaterialModel, time: TimeConfig, end_window: SolverWi
         if check:
             _check(m, n - 1)
         if on_step is not None:
-            _, u_new = ctx.get_window()
-            on_step(n, u_new)
+            on_step(n, ctx.get_field("u_cur").reshape(grid.shape))
     up, uc = ctx.get_window()
     if copy:
         window = SolverWindow(u_prev=up, u_cur=uc, u_next=np.empty_like(uc))

@@ -8,7 +8,8 @@ Times one superposed gradient (fp32, rho-scaled 3D FWI, one shot) as
   slabsO  `parts` slab contexts on this GPU, loopback halo, split
           boundary/interior steps (the overlapped NCCL schedule)
   slabsW  the same with whole steps then the exchange
-  slabsP  split steps with peer ghost stores + device flags (no exchange)
+  slabsP  peer ghost stores + device flags (no exchange): whole sweeps with
+          two-step passes (interleaved pass by pass: same device)
 Host wall clock around a synchronised run (slabs use one stream each).
 On one GPU the slabs run one after the other, so slabsO/slabsW vs mono1 is
 the price of the decomposition itself (split launches, ghost planes, the

@@ -83,9 +83,9 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
  * grid tiles exactly into 64 x 8 cells (0 = never). */
 #define WO_OPT_TMA_KERNEL 3
 /* WO_OPT_TWO_STEP (default 1; slab contexts 0): advance two time steps per
- * pass over HBM (temporal blocking, identical arithmetic) on fp32 contexts
- * whose plane tiles into 64 x 8 or 32 x 16 cells; 2 = also fp64 contexts;
- * 0 = never.  Sweeps fall back to single steps at odd range ends, while
+ * pass over HBM (temporal blocking, identical arithmetic) on fp32 and fp64
+ * contexts whose plane tiles into 64 x 8 or 32 x 16 cells (2: the same,
+ * kept for compatibility); 0 = never.  Sweeps fall back to single steps at odd range ends, while
  * recording history, and everywhere else.  Slabs take two-step passes only
  * with peer ghost stores and two ghost planes per neighbour; the caller
  * enables them on every slab of a decomposition or on none (all slabs must

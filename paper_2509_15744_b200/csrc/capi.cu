@@ -561,17 +561,34 @@ int p2p_signal(wo_ctx* ctx) {
     return WO_OK;
 }
 
+// where the device supports it, a satisfied wait also flushes the remote
+// (peer / NVLink) writes that arrived before the flag, so the next launch
+// sees the neighbour's ghost-plane stores
+unsigned wait_flags(int device) {
+    static int cached[64];
+    static bool known[64] = {};
+    const int d = device & 63;
+    if (!known[d]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, (cudaDeviceAttr)CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES,
+                               device);
+        (void)cudaGetLastError();
+        cached[d] = v;
+        known[d] = true;
+    }
+    return CU_STREAM_WAIT_VALUE_GEQ | (cached[d] ? CU_STREAM_WAIT_VALUE_FLUSH : 0u);
+}
+
 int p2p_wait(wo_ctx* ctx) {
     auto wait = wait_value32();
     REQUIRE(wait, "stream memory operations unavailable");
     const int par = ctx->p2p_epoch & 1;
+    const unsigned wf = wait_flags(ctx->device);
     if (ctx->peer_lo_flag &&
-        wait((CUstream)ctx->stream, (CUdeviceptr)(ctx->in_flags + 2 * par), ctx->p2p_seq,
-             CU_STREAM_WAIT_VALUE_GEQ))
+        wait((CUstream)ctx->stream, (CUdeviceptr)(ctx->in_flags + 2 * par), ctx->p2p_seq, wf))
         return cu_fail(ctx, "cuStreamWaitValue32 failed");
     if (ctx->peer_hi_flag &&
-        wait((CUstream)ctx->stream, (CUdeviceptr)(ctx->in_flags + 2 * par + 1), ctx->p2p_seq,
-             CU_STREAM_WAIT_VALUE_GEQ))
+        wait((CUstream)ctx->stream, (CUdeviceptr)(ctx->in_flags + 2 * par + 1), ctx->p2p_seq, wf))
         return cu_fail(ctx, "cuStreamWaitValue32 failed");
     return WO_OK;
 }
@@ -786,10 +803,10 @@ bool pair_ready(wo_ctx* ctx) {
     if ((ctx->has_lo && ctx->gl < 2) || (ctx->has_hi && ctx->gh < 2) ||
         ((ctx->has_lo || ctx->has_hi) && ctx->kn0 < 2))
         return false;
-    // fp64 two-step CTAs need 130 KB of shared memory (1 CTA/SM) and measure
-    // slower than the single-step kernel (100.9 vs 106.7 Gcell-upd/s, 256^3):
-    // fp64 takes two-step passes only when forced (option value 2)
-    if (ctx->itemsize == 8 && ctx->use_two_step != 2) return false;
+    // fp64 two-step passes run 2 ring stages at 2 CTAs per SM (98 KB each):
+    // 256^3 125-134 vs 106 Gcell-upd/s single-step, 512^3 127.7 vs 120.8,
+    // 1024^3 125.7 vs 120.2 (profiles/r2/f64_two_step.txt); round 1's
+    // 3-stage, 1-CTA variant was slower, so fp64 used to need option 2
     if (ctx->t2_oom) return false;
     if (ensure_four(ctx) || ensure_mat4(ctx)) {
         // the two extra levels and the material do not fit next to the rest:
@@ -869,7 +886,7 @@ int choose_chunk2(const wo_ctx* ctx) {
     if (forced > 0) {
         best_nz = forced;
     } else {
-        const int slots = ctx->num_sms * (ctx->itemsize == 4 ? T2_CTAS_F32 : 1);
+        const int slots = ctx->num_sms * (ctx->itemsize == 4 ? T2_CTAS_F32 : T2_CTAS_F64);
         const int nz_max = std::min(ctx->kn0, 64);
         // dataflow-chained passes (t2_chain_enabled) overlap one pass's tail
         // with the next pass's start, so partial waves cost their CTAs only:
@@ -1070,7 +1087,7 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     const int nz = choose_layers2(ctx, a.zb);
     a.chunk = 0;
     for (int z = 0; z < nz; ++z) a.chunk = std::max(a.chunk, a.zb[z + 1] - a.zb[z]);
-    a.resident = ctx->num_sms * (ctx->itemsize == 4 ? T2_CTAS_F32 : 1);
+    a.resident = ctx->num_sms * (ctx->itemsize == 4 ? T2_CTAS_F32 : T2_CTAS_F64);
     a.negz = 0x8000000080000000ull;   // (-0.0f, -0.0f): packed fp32 products
     a.mat = mat_scalars<T>(ctx);
     a.cv = (T)ctx->cv; a.cg = (T)ctx->cg; a.inv2dt = (T)ctx->inv2dt; a.inv2dx = (T)ctx->inv2dx;
@@ -2156,7 +2173,7 @@ int wo_set_option(wo_ctx* ctx, int option, int value) {
         return WO_OK;
     }
     if (option == WO_OPT_TWO_STEP) {
-        ctx->use_two_step = value;   // 0 off, 1 fp32 grids, 2 also fp64
+        ctx->use_two_step = value;   // 0 off, 1 (2: same) fp32 and fp64 grids
         return WO_OK;
     }
     if (option == WO_OPT_PAIR_KERNEL) {

@@ -64,7 +64,14 @@ namespace wb {
 #define WB_T2_CTAS 3
 #endif
 constexpr int T2_THREADS = 128;
-constexpr int T2_CTAS_F32 = WB_T2_CTAS;   // resident fp32 CTAs per SM (fp64: 1)
+constexpr int T2_CTAS_F32 = WB_T2_CTAS;   // resident fp32 CTAs per SM
+#ifndef WB_T2_CTAS_F64
+#define WB_T2_CTAS_F64 2
+#endif
+#ifndef WB_T2_STAGES_F64
+#define WB_T2_STAGES_F64 2   // fp64: two ring stages -> two CTAs per SM (98 KB each)
+#endif
+constexpr int T2_CTAS_F64 = WB_T2_CTAS_F64;
 constexpr int T2_MAXZ = 64;          // z layers (chunks along axis 0) per launch
 
 // Packed fp32 pairs (sm_100a FADD2 / FFMA2): the two cells of a thread's row
@@ -100,7 +107,10 @@ __device__ __forceinline__ f2x mul2(f2x a, f2x b, f2x negz) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(negz));
     return r;
 }
-constexpr int T2_NS = WB_T2_STAGES;  // TMA ring stages
+constexpr int T2_NS = WB_T2_STAGES;  // TMA ring stages (fp32)
+template <typename T> __host__ __device__ constexpr int t2_ns() {
+    return sizeof(T) == 8 ? WB_T2_STAGES_F64 : T2_NS;
+}
 constexpr int T2_PF = WB_T2_PREFETCH;   // L2 prefetch distance beyond the ring (planes)
 constexpr int T2_PRODUCER = 32;      // thread issuing TMA (warp 0 carries the extra ring cells)
 
@@ -197,9 +207,9 @@ constexpr int T2_NX = 3;             // u^{n+1} plane buffers (X)
 
 template <typename T, typename G>
 constexpr size_t step2_smem_bytes() {
-    return T2_NS * sizeof(Tma2Stage<T, G>) +
+    return t2_ns<T>() * sizeof(Tma2Stage<T, G>) +
            T2_NX * sizeof(T) * G::R2 * G::template W<T>() /* X planes */ +
-           T2_NS * sizeof(unsigned long long) + 128;
+           t2_ns<T>() * sizeof(unsigned long long) + 128;
 }
 
 // coef and the +k / +j / +i face weights of every cell (0 across the grid
@@ -225,7 +235,7 @@ __global__ void material4_kernel(const T* __restrict__ gamma, MatScalars<T> M, i
 }
 
 template <typename T, typename G, int FLAVOR, bool ACC, int SUP>
-__global__ void __launch_bounds__(T2_THREADS, sizeof(T) == 4 ? T2_CTAS_F32 : 1)
+__global__ void __launch_bounds__(T2_THREADS, sizeof(T) == 4 ? T2_CTAS_F32 : T2_CTAS_F64)
 step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__ Tma2Maps maps) {
     using Tr = FTraits<T>;
     using MP = Mat<T, FLAVOR, false>;   // sparse force coefficients only
@@ -238,6 +248,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     unsigned char* smem_raw =
         smem_dyn + ((128u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_dyn)) & 127u)) & 127u);
     Tma2Stage<T, G>* st = reinterpret_cast<Tma2Stage<T, G>*>(smem_raw);
+    constexpr int T2_NS = t2_ns<T>();   // ring stages of this dtype (shadows the fp32 default)
     T* Xb = reinterpret_cast<T*>(smem_raw + T2_NS * sizeof(Tma2Stage<T, G>));   // X[T2_NX][PL]
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(Xb + T2_NX * PL);
     __shared__ Bits smax[2][T2_THREADS / 32];

@@ -21,7 +21,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--grid", type=int, default=256)
 ap.add_argument("--n-steps", type=int, default=256)
 ap.add_argument("--reps", type=int, default=3)
-ap.add_argument("--two-step", type=int, default=1, help="2: fp64 two-step passes")
+ap.add_argument("--two-step", type=int, default=1, help="0: single steps, 1: two-step passes")
 args = ap.parse_args()
 n = args.grid
 problem, mat = configs.fwi((n, n, n), args.n_steps)

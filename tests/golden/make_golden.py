@@ -238,6 +238,35 @@ def gen_loops(W):
     return out
 
 
+def gen_config_desk(W):
+    """configs/fwi_desk.toml through the reference's own config path
+    (config.py:74-215: parse, assemble, synthesize on the refine = 2 grid)
+    and 3 iterations of its invert with the config's optimizer (alpha 0.02,
+    Adam eps 1e-40: real updates, unlike the FwiProblem defaults) at k = 1e13.
+    The TOML bytes are stored with the outputs (the GPU box has no
+    /root/reference)."""
+    import tomllib
+
+    import waveopt_ref.config as RC
+
+    path = "/root/reference/pkg/configs/fwi_desk.toml"
+    raw_bytes = open(path, "rb").read()
+    cfg = tomllib.loads(raw_bytes.decode())
+    rc = RC.parse_config(cfg)
+    problem, truth = RC.build_fwi(cfg, rc)
+    out = {"toml": np.frombuffer(raw_bytes, dtype=np.uint8), "measured": problem.measured,
+           "truth_gamma": np.asarray(truth.gamma, dtype=np.float64),
+           "sensor_idx": problem.sensors.flat_indices(problem.grid)}
+    for prec in ("double", "single"):
+        t0 = time.time()
+        res = W.invert(problem, method="superposed", k=1e13, iterations=3, precision=prec,
+                       snapshot_every=1)
+        print(f"  config invert {prec} {time.time() - t0:.1f}s")
+        out[f"hist_{prec}"] = np.array(res.gamma_history)
+        _log_arrays(out, f"inv_{prec}", res.log)
+    return out
+
+
 def gen_solver(W):
     """run_forward with co-located sources (solver.py:154-170: numpy fancy
     `+=` keeps the LAST duplicate) and run_backward (solver.py:343-372), from
@@ -340,6 +369,7 @@ def main():
         ("io_dumps", lambda: gen_io(W)),
         ("loops", lambda: gen_loops(W)),
         ("solver", lambda: gen_solver(W)),
+        ("config_desk", lambda: gen_config_desk(W)),
     ]
     only = set(sys.argv[1:])
     for name, fn in jobs:

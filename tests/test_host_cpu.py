@@ -120,3 +120,87 @@ def test_beta_schedule_and_footprint():
         assert len(ws) == count and offs.shape == (count, nd)
         K = O.filter_kernel(1.5, nd)
         assert np.isclose(ws.sum(), K.sum())
+
+
+def test_config_parsing_mirrors_reference(tmp_path):
+    """Host-only part of the config path (config.py:74-191): sections, keys,
+    overrides, sensor ring, truth disks / boxes, error messages."""
+    import numpy as np
+    import pytest
+
+    from paper_2509_15744_b200 import config as C
+    from paper_2509_15744_b200.grids import ConfigError
+
+    toml = b"""
+[problem]
+kind = "fwi"
+[grid]
+n = [21, 17]
+dx = 1.0e-3
+[time]
+n_steps = 40
+dt = 1.0e-8
+[material]
+flavor = "rho_scaled"
+rho0 = 2700.0
+c0 = 6000.0
+[[sources]]
+node = [3, 8]
+amplitude = 1.0e12
+frequency = 1.5e6
+[sensors]
+ring = { inset = 2, stride = 3 }
+[truth]
+disks = [{ center = [10, 8], radius = 2 }]
+boxes = [{ lo = [1, 1], hi = [2, 3] }]
+[gradient]
+k = 1.0e13
+precision = "single"
+"""
+    p = tmp_path / "c.toml"
+    p.write_bytes(toml)
+    rc, raw = C.load_config(p, overrides={"precision": "double", "method": None})
+    assert rc.grid.shape == (21, 17) and rc.time.n_steps == 40
+    assert rc.k == 1e13 and rc.precision == "double" and rc.method == "superposed"
+    assert rc.resolved()["kind"] == "fwi"
+    mat = C.build_material(raw, rc.grid)
+    assert np.all(mat.gamma == 1.0)
+    sens = C.build_sensors(raw, rc.grid)
+    n1, n2, inset, stride = 21, 17, 2, 3
+    lo = inset + stride - 1
+    want = sorted({(inset, j) for j in range(lo, n2 - inset, stride)}
+                  | {(n1 - 1 - inset, j) for j in range(lo, n2 - inset, stride)}
+                  | {(i, inset) for i in range(lo, n1 - inset, stride)}
+                  | {(i, n2 - 1 - inset) for i in range(lo, n1 - inset, stride)})
+    assert list(sens.nodes) == want
+    truth = C.build_truth_gamma(raw, rc.grid, mat)
+    assert truth[10, 8] == mat.eps and truth[1, 3] == mat.eps and truth[0, 0] == 1.0
+    src = C.build_sources(raw)
+    assert src[0].cycles == 2
+    with pytest.raises(ConfigError, match="missing required section"):
+        C.parse_config({"problem": {"kind": "fwi"}})
+    with pytest.raises(ConfigError, match="k must be a number or 'auto'"):
+        C.parse_config(dict(raw, gradient={"k": "big"}))
+
+
+def test_c5_problem_is_never_materialised():
+    """bench.py's C5 problem: the global 2048-plane grids are
+    constant broadcast views (no rank allocates the global gamma); shapes,
+    source and sensor placement; weak vs strong sizes."""
+    import numpy as np
+
+    import bench
+    import paper_2509_15744_b200 as W
+
+    wl = bench.c5_workload(8, "weak", 200)
+    assert wl["shape"] == (2048, 2048, 2048)
+    assert bench.c5_workload(2, "strong", 200)["shape"] == (2048, 2048, 2048)
+    wl = bench.c5_workload(4, "weak", 20)
+    problem, model, truth = bench.build_c5_problem(W, wl)
+    assert model.gamma.strides == (0, 0, 0) and truth.gamma.strides == (0, 0, 0)
+    assert float(truth.gamma[5, 6, 7]) == 0.9 and float(model.gamma[0, 0, 0]) == 1.0
+    assert problem.sources[0].node == (3, 1024, 1024)
+    assert len(problem.sensors) == 33 * 33
+    assert all(n[0] == 1024 - 4 for n in problem.sensors.nodes)
+    assert problem.measured.shape == (1, 33 * 33, 20)
+    assert np.all(problem.measured == 0)

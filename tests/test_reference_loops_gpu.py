@@ -159,3 +159,28 @@ def test_run_backward_matches_reference(W, golden, tag, dt_name, start):
     wb = W.run_backward(mat, tcfg, end, forces)
     assert bits_equal(wb.u_prev, g[f"{pre}_uprev_{key}"])
     assert bits_equal(wb.u_cur, g[f"{pre}_ucur_{key}"])
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_config_desk_runs_unchanged(W, golden, tmp_path, prec):
+    """configs/fwi_desk.toml (bytes from the fixture) through this package's
+    config path: the same problem as the reference's config.py (measured
+    traces synthesized on the refine = 2 grid, bit for bit), then invert with
+    the config's optimizer (alpha 0.02, Adam eps 1e-40) reproduces the
+    reference's gamma after every iteration bit for bit."""
+    from paper_2509_15744_b200 import config as C
+
+    g = golden("config_desk")
+    path = tmp_path / "fwi_desk.toml"
+    path.write_bytes(g["toml"].tobytes())
+    rc, raw = C.load_config(path)
+    assert rc.kind == "fwi" and rc.k == "auto" and rc.precision == "double"
+    problem, truth = C.build_fwi(raw, rc)
+    assert bits_equal(truth.gamma, g["truth_gamma"])
+    assert bits_equal(problem.measured, g["measured"])
+    assert (problem.alpha, problem.adam_eps) == (0.02, 1e-40)
+    res = W.invert(problem, method="superposed", k=1e13, iterations=3, precision=prec,
+                   snapshot_every=1)
+    for a, b in zip(res.gamma_history, g[f"hist_{prec}"]):
+        assert bits_equal(a, b)
+    _check_log(res.log, g, f"inv_{prec}")

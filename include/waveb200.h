@@ -111,11 +111,6 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
  * ONE cluster-resident launch (fields in distributed shared memory, one
  * cluster barrier per step, identical arithmetic); 0 = step launches. */
 #define WO_OPT_CLUSTER 7
-/* WO_OPT_TILE2D (default 1): 2D grids advance up to 8 time steps per launch
- * (temporal tiling in shared memory: a tile plus a ring of 8 cells, the ring
- * shrinking by one per step; identical arithmetic); needs WO_OPT_TWO_STEP
- * (four level buffers). */
-#define WO_OPT_TILE2D 8
 int wo_set_option(wo_ctx* ctx, int option, int value);
 /* Device-resident optimisation loop (fwi.py:178-238 with
  * optim.py adam_step / clip_bounds): fp64 parameters (gamma), the Adam
@@ -350,8 +345,6 @@ int wo_stats(wo_ctx* ctx, int64_t* launches, int64_t* step_launches, double* ste
 int wo_reset_stats(wo_ctx* ctx);
 /* Device bytes held by the context (fields + support storage). */
 int64_t wo_device_bytes(const wo_ctx* ctx);
-/* Launches of the 2D K-steps engine (WO_OPT_TILE2D) since the last reset. */
-int64_t wo_tile_launches(const wo_ctx* ctx);
 /* Solution-sized device buffers the context holds right now: gamma, the
  * window levels (2; 4 once two-step passes ran), the accumulator, the third
  * adjoint level of the reference engine, and the 4 precomputed material

@@ -36,17 +36,6 @@ constexpr int STABILITY_CHECK_INTERVAL = 50;     // solver.py:29
 constexpr double STABILITY_GROWTH_FACTOR = 1e6;  // solver.py:30
 thread_local std::string g_create_error;
 
-// K steps per launch on 2D grids (tile2d_kernel.cuh): default of
-// WO_OPT_TILE2D for new contexts; WB_TILE2D=0/1 overrides (A/B runs)
-constexpr bool TILE2D_DEFAULT = true;
-bool tile2d_default() {
-    static const bool on = [] {
-        const char* e = getenv("WB_TILE2D");
-        return e ? atoi(e) != 0 : TILE2D_DEFAULT;
-    }();
-    return on;
-}
-
 // cluster-resident sweeps of small 2D grids (cluster_sweep.cuh): default of
 // WO_OPT_CLUSTER for new contexts; WB_CLUSTER=0/1 overrides (A/B runs)
 constexpr bool CLUSTER_DEFAULT = false;
@@ -111,7 +100,7 @@ struct wo_ctx {
         uint64_t key = 0, seen = 0;
         cudaGraphExec_t exec = nullptr;
         int cur = 0, prv = 0;
-        int64_t d_launches = 0, d_steps = 0, d_pairs = 0, d_tiles = 0;
+        int64_t d_launches = 0, d_steps = 0, d_pairs = 0;
     } graph[2];                        // forward, backward
     int use_graphs = 1;
     uint64_t gen = 1;
@@ -125,8 +114,6 @@ struct wo_ctx {
     bool t2_chain_next = false;        // the next pass directly follows one of this sweep
     bool t2_oom = false;               // two-step buffers did not fit: single steps only
     int use_cluster = cluster_default();   // wo_set_option(WO_OPT_CLUSTER)
-    int use_tile2d = tile2d_default();     // wo_set_option(WO_OPT_TILE2D)
-    int64_t tile_launches = 0;
     int cl_state = 0;                  // cluster sweep engine: 0 unknown, 1 ready, -1 no
     int cl_size = 0, cl_rows = 0;      // CTAs per cluster, rows per CTA
     double* amp_dev = nullptr;         // source amplitude table of a cluster sweep
@@ -671,7 +658,6 @@ bool graph_replay(wo_ctx* ctx, int dir, uint64_t key) {
     ctx->launches += g.d_launches;
     ctx->step_launches += g.d_steps;
     ctx->pair_launches += g.d_pairs;
-    ctx->tile_launches += g.d_tiles;
     return true;
 }
 
@@ -685,8 +671,7 @@ bool graph_capture_begin(wo_ctx* ctx, int dir, uint64_t key) {
     return cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
 }
 
-int graph_capture_end(wo_ctx* ctx, int dir, uint64_t key, int64_t l0, int64_t s0, int64_t p0,
-                      int64_t t0) {
+int graph_capture_end(wo_ctx* ctx, int dir, uint64_t key, int64_t l0, int64_t s0, int64_t p0) {
     auto& g = ctx->graph[dir];
     cudaGraph_t graph = nullptr;
     CK(cudaStreamEndCapture(ctx->stream, &graph));
@@ -702,7 +687,6 @@ int graph_capture_end(wo_ctx* ctx, int dir, uint64_t key, int64_t l0, int64_t s0
     g.d_launches = ctx->launches - l0;
     g.d_steps = ctx->step_launches - s0;
     g.d_pairs = ctx->pair_launches - p0;
-    g.d_tiles = ctx->tile_launches - t0;
     CK(cudaGraphLaunch(exec, ctx->stream));   // the captured work has not run yet
     return WO_OK;
 }
@@ -1074,69 +1058,6 @@ int run_cluster_sweep(wo_ctx* ctx, int backward, int64_t N, int64_t n_first, int
     return WO_OK;
 }
 
-// ---- K steps per launch on 2D grids (tile2d_kernel.cuh) ----
-bool tile2d_ready(wo_ctx* ctx) {
-    if (!ctx->use_tile2d || !ctx->use_two_step || ctx->ndim != 2 || ctx->kn0 != 1 ||
-        ctx->has_lo || ctx->has_hi || ctx->part != 0 || ctx->p2p || !ctx->material_set ||
-        ctx->t2_oom)
-        return false;
-    return ensure_four(ctx) == WO_OK;
-}
-
-// steps n, n +- 1, ..., (k of them) in one launch; own cells' last two
-// levels go to the two buffers outside the window, which then rotate in
-template <typename T>
-int run_tile2d(wo_ctx* ctx, int backward, int64_t N, int64_t n, int k, int ns,
-               const long long* sidx, const double* const* amp_rows, bool acc, double sdt,
-               int sup_mode) {
-    int x[2], nx = 0;
-    for (int b = 0; b < 4 && nx < 2; ++b)
-        if (b != ctx->cur && b != ctx->prv) x[nx++] = b;
-    Tile2DArgs<T> a{};
-    a.n1 = ctx->kn1;
-    a.n2 = ctx->kn2;
-    a.backward = backward;
-    a.K = k;
-    a.n_first = (int)n;
-    a.N = N;
-    a.gamma = reinterpret_cast<const T*>(ctx->base0(ctx->gamma));
-    a.u_prev = reinterpret_cast<const T*>(ctx->uprev());
-    a.u_cur = reinterpret_cast<const T*>(ctx->ucur());
-    a.o_prev = reinterpret_cast<T*>(ctx->base0(ctx->u[x[0]]));
-    a.o_cur = reinterpret_cast<T*>(ctx->base0(ctx->u[x[1]]));
-    a.acc = reinterpret_cast<T*>(ctx->acc);
-    a.mat = mat_scalars<T>(ctx);
-    a.cv = (T)ctx->cv; a.cg = (T)ctx->cg; a.inv2dt = (T)ctx->inv2dt; a.inv2dx = (T)ctx->inv2dx;
-    a.sdt = (T)sdt;
-    a.n_src = 0;
-    for (int s = 0; s < ns; ++s) {
-        const long long f = sidx[s];
-        if (f < 0 || f >= ctx->cells()) continue;
-        a.src_j[a.n_src] = (int)(f / ctx->kn2);
-        a.src_k[a.n_src] = (int)(f % ctx->kn2);
-        for (int i = 0; i < k; ++i)
-            a.src_val[i][a.n_src] = (T)amp_rows[s][backward ? n - i : n + i];
-        a.n_src++;
-    }
-    a.sup_mode = ctx->n_sup > 0 ? sup_mode : SUP_NONE;
-    a.n_sup = ctx->n_sup;
-    a.sup_mask = ctx->mask;
-    a.sup_prefix = ctx->prefix;
-    a.store = reinterpret_cast<T*>(ctx->store);
-    a.maxslots = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots);
-    prof_begin(ctx, 1);
-    const cudaError_t e = launch_tile2d<T>(ctx->flavor, acc, a, ctx->stream);
-    prof_end(ctx);
-    ctx->launches++;
-    ctx->step_launches++;
-    ctx->tile_launches++;
-    ctx->t2_chain_next = false;
-    CK(e);
-    ctx->prv = x[0];
-    ctx->cur = x[1];
-    return WO_OK;
-}
-
 struct PairSpec {
     bool acc = false, check1 = false, check2 = false;
     double sdt = 0.0;
@@ -1375,8 +1296,7 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
                            !ctx->p2p && !cluster && ns <= MAX_SRC && n_end - n_begin >= 8;
     uint64_t gkey = 0;
     bool capturing = false;
-    const int64_t l0 = ctx->launches, s0 = ctx->step_launches, p0 = ctx->pair_launches,
-                  tl0 = ctx->tile_launches;
+    const int64_t l0 = ctx->launches, s0 = ctx->step_launches, p0 = ctx->pair_launches;
     if (graphable) {
         KeyHash kh;
         kh.val(0); kh.val(N); kh.val(n_begin); kh.val(n_end); kh.val(flags); kh.val(dt);
@@ -1395,18 +1315,7 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
         rc = t2_sweep_begin(ctx);
         if (rc) return rc;
     }
-    const bool tiles = ns <= MAX_SRC && !record && tile2d_ready(ctx);
-    std::vector<const double*> amp_rows(std::max(ns, 1));
-    for (int s = 0; s < ns; ++s) amp_rows[s] = src_amp + (int64_t)spos[s] * N;
     for (int64_t n = n_begin; n < n_end; ++n) {
-        if (tiles && n + 1 < n_end) {   // up to TL_MAXK steps in one launch (2D)
-            const int k = (int)std::min<int64_t>(TL_MAXK, n_end - n);
-            rc = run_tile2d<T>(ctx, 0, N, n, k, ns, sidx.data(), amp_rows.data(),
-                               accumulate != 0, -dt, gather ? SUP_GATHER : SUP_NONE);
-            if (rc) return rc;
-            n += k - 1;
-            continue;
-        }
         if (pairs && n + 1 < n_end) {   // steps n and n+1 in one pass
             PairSpec ps;
             ps.acc = accumulate != 0;
@@ -1469,7 +1378,7 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
         if (ctx->part != 1) std::swap(ctx->cur, ctx->prv);
     }
     if (capturing) {
-        rc = graph_capture_end(ctx, 0, gkey, l0, s0, p0, tl0);
+        rc = graph_capture_end(ctx, 0, gkey, l0, s0, p0);
         if (rc) return rc;
     }
     // split steps and peer-store ranges stay asynchronous (the neighbours'
@@ -1544,8 +1453,7 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
                            !cluster && n_hi - n_lo >= 8;
     uint64_t gkey = 0;
     bool capturing = false;
-    const int64_t l0 = ctx->launches, s0 = ctx->step_launches, p0 = ctx->pair_launches,
-                  tl0 = ctx->tile_launches;
+    const int64_t l0 = ctx->launches, s0 = ctx->step_launches, p0 = ctx->pair_launches;
     if (graphable) {
         KeyHash kh;
         kh.val(1); kh.val(N); kh.val(n_hi); kh.val(n_lo); kh.val(inject); kh.val(accumulate);
@@ -1561,17 +1469,7 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
         rc = t2_sweep_begin(ctx);
         if (rc) return rc;
     }
-    const bool tiles = tile2d_ready(ctx);
-    const double* amp_row = src_amp;
     for (int64_t n = n_hi; n > n_lo; --n) {
-        if (tiles && n - 1 > n_lo) {   // up to TL_MAXK steps in one launch (2D)
-            const int k = (int)std::min<int64_t>(TL_MAXK, n - n_lo);
-            rc = run_tile2d<T>(ctx, 1, N, n, k, has_src ? 1 : 0, &sf, &amp_row, accumulate != 0,
-                               dt, inject ? SUP_INJECT : SUP_NONE);
-            if (rc) return rc;
-            n -= k - 1;
-            continue;
-        }
         if (pairs && n - 1 > n_lo) {   // steps n and n-1 in one pass
             PairSpec ps;
             ps.acc = accumulate != 0;
@@ -1612,7 +1510,7 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
         if (ctx->part != 1) std::swap(ctx->cur, ctx->prv);
     }
     if (capturing) {
-        rc = graph_capture_end(ctx, 1, gkey, l0, s0, p0, tl0);
+        rc = graph_capture_end(ctx, 1, gkey, l0, s0, p0);
         if (rc) return rc;
     }
     if (ctx->part != 0 || (ctx->p2p && !finish)) return WO_OK;
@@ -2258,12 +2156,8 @@ int wo_set_option(wo_ctx* ctx, int option, int value) {
     REQUIRE(option == WO_OPT_FAST_DIV || option == WO_OPT_PAIR_KERNEL ||
                 option == WO_OPT_TMA_KERNEL || option == WO_OPT_TWO_STEP ||
                 option == WO_OPT_PLANE_PART || option == WO_OPT_GRAPHS ||
-                option == WO_OPT_CLUSTER || option == WO_OPT_TILE2D,
+                option == WO_OPT_CLUSTER,
             "unknown option");
-    if (option == WO_OPT_TILE2D) {
-        ctx->use_tile2d = value != 0;
-        return WO_OK;
-    }
     if (option == WO_OPT_CLUSTER) {
         ctx->use_cluster = value != 0;
         ctx->cl_state = 0;   // probe again on the next sweep
@@ -2845,7 +2739,7 @@ int wo_stats(wo_ctx* ctx, int64_t* launches, int64_t* step_launches, double* ste
 
 int wo_reset_stats(wo_ctx* ctx) {
     if (!ctx) return WO_ERR_CONFIG;
-    ctx->launches = ctx->step_launches = ctx->pair_launches = ctx->tile_launches = 0;
+    ctx->launches = ctx->step_launches = ctx->pair_launches = 0;
     ctx->step_ms = 0.0;
     ctx->prof_ms[0] = ctx->prof_ms[1] = 0.0;
     ctx->prof_n[0] = ctx->prof_n[1] = 0;
@@ -2863,8 +2757,6 @@ int wo_field_buffers(const wo_ctx* ctx) {
 }
 
 int64_t wo_pair_launches(const wo_ctx* ctx) { return ctx ? ctx->pair_launches : 0; }
-
-int64_t wo_tile_launches(const wo_ctx* ctx) { return ctx ? ctx->tile_launches : 0; }
 
 int wo_profile_stats(const wo_ctx* ctx, double* single_ms, int64_t* single_n, double* pair_ms,
                      int64_t* pair_n) {

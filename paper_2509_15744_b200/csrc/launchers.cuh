@@ -8,7 +8,6 @@
 #include <cuda_runtime.h>
 
 #include "cluster_sweep.cuh"
-#include "tile2d_kernel.cuh"
 #include "step2_kernel.cuh"
 #include "step_kernel.cuh"
 #include "step_kernel_tma.cuh"
@@ -54,10 +53,6 @@ void launch_material4(int flavor, cudaStream_t s, const T* gamma, const MatScala
 // of this process will set, such a load would wait forever.  The peer-store
 // setup (wo_slab_peers) therefore loads them all up front.
 template <typename T> void preload_step_kernels();
-
-// K (<= TL_MAXK) steps of a 2D grid per launch (tile2d_kernel.cuh)
-template <typename T>
-cudaError_t launch_tile2d(int flavor, bool acc, const Tile2DArgs<T>& a, cudaStream_t s);
 
 // whole sweep of a small 2D grid in one cluster launch (cluster_sweep.cuh);
 // probe = only check that the device can hold the cluster

@@ -427,10 +427,6 @@ class DeviceGrid:
         """Cluster-resident whole sweeps of small 2D grids (WO_OPT_CLUSTER)."""
         self._ck(self.L.wo_set_option(self.h, N.WO_OPT_CLUSTER, int(bool(on))), "wo_set_option")
 
-    def set_tile2d(self, on):
-        """Up to 8 time steps per launch on 2D grids (WO_OPT_TILE2D)."""
-        self._ck(self.L.wo_set_option(self.h, N.WO_OPT_TILE2D, int(bool(on))), "wo_set_option")
-
     def slab_abort(self):
         """Release streams waiting on this slab's peer flags (wo_slab_abort)."""
         self._ck(self.L.wo_slab_abort(self.h), "wo_slab_abort")
@@ -535,7 +531,6 @@ class DeviceGrid:
                                          ctypes.byref(pm), ctypes.byref(pn)), "wo_profile_stats")
         return {"launches": a.value, "step_launches": b.value, "step_kernel_ms": c.value,
                 "pair_launches": int(self.L.wo_pair_launches(self.h)),
-                "tile_launches": int(self.L.wo_tile_launches(self.h)),
                 "profiled_single_ms": sm.value, "profiled_single_n": sn.value,
                 "profiled_pair_ms": pm.value, "profiled_pair_n": pn.value}
 

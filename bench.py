@@ -709,6 +709,9 @@ def run_native_slab(args):
                        "cell_updates_per_step": world * updates,
                        "truth": "homogeneous gamma 0.9 vs model 1.0 (traces synthesized on "
                                 "the slabs, refine = 1)",
+                       "weak_scaling_n1": ("the same per-GPU work on one GPU: python bench.py "
+                                           "--workload c5 (profiles/r2/bench_c5_1gpu_r2b.json); "
+                                           "the default N = 1 line is C2 256^3"),
                        "l2": "inputs larger than L2 (4.3 GB per field per GPU)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

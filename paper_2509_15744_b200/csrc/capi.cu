@@ -1144,6 +1144,12 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
         a.tflags = ctx->tflags;
         a.seq = ++ctx->t2_seq;
         a.chain = ctx->t2_chain_next ? 1 : 0;
+        // WB_T2_ZREV=1: alternate the layer dispatch order from pass to pass
+        static const bool zrev = [] {
+            const char* e = getenv("WB_T2_ZREV");
+            return e && atoi(e) != 0;
+        }();
+        a.zrev = zrev ? (int)(a.seq & 1u) : 0;
     }
     a.max1 = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots) + sp.slot1;
     a.max2 = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots) + sp.slot2;

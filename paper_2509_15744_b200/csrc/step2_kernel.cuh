@@ -169,6 +169,7 @@ template <typename T> struct Step2Args {
     unsigned int* tflags;
     unsigned int seq;
     int chain;
+    int zrev;          // z layers in reverse dispatch order (logical layer = nz-1-blockIdx.z)
     T* plo1;
     T* phi1;
     T* plo2;
@@ -264,8 +265,12 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     const int kA = k0 + 2 * tx, ja = j0 + 2 * ty;
     const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
     const long long plane = (long long)n1 * n2;   // 64-bit plane offsets: grids of >= 2^31 cells
-    const int i0 = a.zb[blockIdx.z];
-    const int i1 = a.zb[blockIdx.z + 1];
+    // logical z layer: consecutive passes may dispatch the layers in opposite
+    // orders (zrev), so a pass starts where the previous one ended (its
+    // outputs still in L2)
+    const int lz = a.zrev ? (int)gridDim.z - 1 - (int)blockIdx.z : (int)blockIdx.z;
+    const int i0 = a.zb[lz];
+    const int i1 = a.zb[lz + 1];
     // step-n planes of this chunk: one recomputed plane beyond each end
     // (a ghost plane at a slab boundary; none at the global ends)
     const int pbeg = (i0 > 0 || a.lo_open) ? i0 - 1 : 0;
@@ -341,7 +346,8 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     if (has_next) {
         nk0 = (nblk % gridDim.x) * TBX;
         nj0 = ((nblk / gridDim.x) % gridDim.y) * TBY;
-        const int nz0 = a.zb[nblk / (gridDim.x * gridDim.y)];
+        const int nbz = nblk / (gridDim.x * gridDim.y);
+        const int nz0 = a.zb[a.zrev ? (int)gridDim.z - 1 - nbz : nbz];
         npb = (nz0 > 0 || a.lo_open) ? nz0 - 1 : 0;
     }
     auto issue = [&](int p, int s) {
@@ -373,7 +379,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         if (tid < 27) {
             const int bx = (int)blockIdx.x + tid % 3 - 1, by = (int)blockIdx.y + (tid / 3) % 3 - 1;
-            const int bz = (int)blockIdx.z + tid / 9 - 1;
+            const int bz = lz + tid / 9 - 1;
             if (bx >= 0 && bx < (int)gridDim.x && by >= 0 && by < (int)gridDim.y && bz >= 0 &&
                 bz < (int)gridDim.z) {
                 const unsigned int* f = a.tflags + ((size_t)bz * gridDim.y + by) * gridDim.x + bx;
@@ -822,7 +828,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         if (tid == 0) {
             asm volatile("fence.proxy.async.global;" ::: "memory");
             __threadfence();
-            unsigned int* f = a.tflags + ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x +
+            unsigned int* f = a.tflags + ((size_t)lz * gridDim.y + blockIdx.y) * gridDim.x +
                               blockIdx.x;
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(a.seq) : "memory");
         }

@@ -302,6 +302,62 @@ class TorchHalo:
         return float(t.item())
 
 
+class HostStagedHalo(TorchHalo):
+    """One slab per process, planes staged through host memory and exchanged
+    with CPU torch.distributed send/recv (gloo): a slab decomposition across
+    processes that never makes one GPU wait on another process (so several
+    ranks may share one GPU — the multi-process test of the slab path), and
+    the fallback where no GPU-aware backend exists.  Whole-step exchanges
+    (overlap=False); maxima and costs reduce on CPU tensors."""
+
+    def exchange(self):
+        import torch
+
+        (first, last, glo, ghi), pb = self.ctx.halo_planes()
+        dt, dev = self.ctx.dtype, self.ctx.device
+        n = pb // dt.itemsize
+        view = lambda p: _device_view(p, pb, dt, dev)  # noqa: E731
+        self.ctx.synchronize()                     # the step's planes are final
+        send_lo = view(first).cpu() if first and self.rank > 0 else None
+        send_hi = view(last).cpu() if last and self.rank < self.world - 1 else None
+        recv_lo = torch.empty(n, dtype=_torch_dtype(dt)) if glo else None
+        recv_hi = torch.empty(n, dtype=_torch_dtype(dt)) if ghi else None
+        exchange_planes(send_lo, send_hi, recv_lo, recv_hi, self.rank, self.world, self.group)
+        for p, b in ((glo, recv_lo), (ghi, recv_hi)):
+            if p:
+                view(p).copy_(b)
+        torch.cuda.synchronize(dev)                # ghosts in place before the next step
+
+    def begin(self):
+        raise ConfigError("HostStagedHalo exchanges whole steps (overlap=False)")
+
+    def allreduce_max(self, arr):
+        if self.world == 1:
+            return arr
+        import torch
+        import torch.distributed as dist
+
+        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return t.numpy()
+
+    def allreduce_sum(self, x):
+        if self.world == 1:
+            return x
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return float(t.item())
+
+
+def _torch_dtype(dt):
+    import torch
+
+    return torch.float32 if np.dtype(dt) == np.float32 else torch.float64
+
+
 def ipc_peer_wiring(rank, world, exports):
     """Which neighbour exports rank opens for wo_slab_peers.
 
@@ -397,15 +453,18 @@ class SlabGradient:
     def for_rank(cls, problem, material, config, rank, world, device=None, group=None,
                  overlap=True, halo="nccl"):
         """One slab per torchrun rank: halo 'nccl' (send/recv of the planes,
-        TorchHalo) or 'ipc' (peer ghost stores through CUDA IPC, IpcPeerHalo;
-        needs overlap)."""
-        if halo not in ("nccl", "ipc"):
+        TorchHalo), 'ipc' (peer ghost stores through CUDA IPC, IpcPeerHalo)
+        or 'staged' (host-staged gloo send/recv, HostStagedHalo, whole
+        steps)."""
+        if halo not in ("nccl", "ipc", "staged"):
             raise ConfigError(f"unknown rank halo {halo!r}")
+        if halo == "staged":
+            overlap = False
         slab = slab_ranges(problem.grid.shape[0], world)[rank]
         dev = rank if device is None else device
         obj = cls(problem, material, config, [slab], [dev], halo=None, overlap=overlap)
         obj.all_slabs = slab_ranges(problem.grid.shape[0], world)
-        make = IpcPeerHalo if halo == "ipc" else TorchHalo
+        make = {"ipc": IpcPeerHalo, "staged": HostStagedHalo}.get(halo, TorchHalo)
         obj.halo = make(obj.ctxs[0], rank, world, group)
         return obj
 

@@ -297,16 +297,27 @@ class ReferenceCPU:
                 f"{procs} concurrent processes; CPU {cpu_model()}")
 
 
+# WB_BENCH_SHARED_GPU=1: every rank on GPU 0 with a gloo process group — a
+# functional dry run of the multi-GPU code path on a one-GPU box (the ranks
+# share the GPU, so the numbers are not a scaling measurement)
+SHARED_GPU = os.environ.get("WB_BENCH_SHARED_GPU", "0") == "1"
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if SHARED_GPU:
+        local = 0
     if world > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARED_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
 
@@ -316,7 +327,7 @@ def max_over_ranks(x, world):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if SHARED_GPU else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

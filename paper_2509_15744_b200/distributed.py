@@ -281,13 +281,19 @@ class TorchHalo:
             for w in works:
                 w.wait()
 
+    def _dev(self):
+        """Where reduction tensors live: the GPU for NCCL, the host for gloo."""
+        import torch.distributed as dist
+
+        return "cpu" if dist.get_backend(self.group) == "gloo" else f"cuda:{self.ctx.device}"
+
     def allreduce_max(self, arr):
         if self.world == 1:
             return arr
         import torch
         import torch.distributed as dist
 
-        t = torch.from_numpy(np.ascontiguousarray(arr)).cuda(self.ctx.device)
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(self._dev())
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         return t.cpu().numpy()
 
@@ -297,7 +303,7 @@ class TorchHalo:
         import torch
         import torch.distributed as dist
 
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{self.ctx.device}")
+        t = torch.tensor([x], dtype=torch.float64, device=self._dev())
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return float(t.item())
 

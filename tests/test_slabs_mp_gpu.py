@@ -108,19 +108,22 @@ def test_slab_ranks_across_processes_bitwise(world, shape, prec):
             assert abs(c - ref.cost) <= 1e-13 * abs(ref.cost)
 
 
-def test_ipc_peer_store_ranks_across_processes_bitwise():
-    """Two ranks (processes) on the one GPU with CUDA-IPC peer ghost stores
-    (IpcPeerHalo): whole sweeps with two-step passes whose launches store
-    into the other process's mapped ghost planes and wait on its flags (on
-    the stream; nothing spins on an SM).  Bitwise the one-context gradient."""
+@pytest.mark.parametrize("world,shape,prec", [(2, (24, 16, 64), "single"),
+                                              (3, (36, 16, 64), "double")])
+def test_ipc_peer_store_ranks_across_processes_bitwise(world, shape, prec):
+    """Ranks (processes) on the one GPU with CUDA-IPC peer ghost stores
+    (IpcPeerHalo, the production multi-GPU path): whole sweeps with two-step
+    passes whose launches store into the other processes' mapped ghost
+    planes and wait on their flags (on the stream; nothing spins on an SM);
+    a middle rank with two neighbours at world 3.  Bitwise the one-context
+    gradient."""
     import multiprocessing as mp
 
     import paper_2509_15744_b200 as W
     from paper_2509_15744_b200 import _native
 
     _native.load(require_device=True)
-    world, shape, prec = 2, (24, 16, 64), "single"
-    seed = 99
+    seed = 99 + world
     problem, mat, cfg = _problem(W, shape, prec, seed, mid_sensor=False)
     ref = W.gradient_superposed(problem, mat, cfg)
     ctx = mp.get_context("spawn")

@@ -1129,7 +1129,10 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     a.check1 = sp.check1; a.check2 = sp.check2;
     // dataflow chaining: only right after a pass of this sweep, with z layers
     // of >= 2 planes (the 3x3x3 block neighbourhood then covers every plane a
-    // block reads or overwrites), PDL launches and no stream operations between
+    // block reads or overwrites), PDL launches and no stream operations
+    // between.  (Single-layer 2D grids measured slower chained: C1 17.9 vs
+    // 24.3 Gcell-upd/s — there the whole-grid dependency resolves faster than
+    // the flag publish + poll; profiles/dev/cycle28.sh)
     int min_layer = n0_min_layer(a.zb, nz);
     const bool chain_ok = t2_chain_enabled() && !ctx->p2p && WB_T2_PDL && min_layer >= 2;
     if (chain_ok && !ctx->tflags) {
@@ -1174,7 +1177,13 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     }
     prof_begin(ctx, 1);
     t_no_pdl = ctx->p2p && !p2p_pdl();
-    launch_step2_engine<T>(StepSel{ctx->flavor, true, sp.acc, false, sup}, ctx->t2_geo, grid,
+    // feature level (T2Mode): peer stores or cell offsets beyond 32 bits ->
+    // T2_FULL; completion flags -> T2_CHAIN; else the lean T2_BASE
+    const bool big = (int64_t)(ctx->kn0 + 2) * ctx->plane() >= (int64_t)INT32_MAX;
+    const int mode = (ctx->p2p || a.plo1 || a.phi1 || big) ? T2_FULL
+                     : a.tflags                           ? T2_CHAIN
+                                                          : T2_BASE;
+    launch_step2_engine<T>(StepSel{ctx->flavor, true, sp.acc, false, sup}, ctx->t2_geo, mode, grid,
                            ctx->stream, a, ctx->t2maps);
     t_no_pdl = false;
     prof_end(ctx);
@@ -1688,7 +1697,7 @@ int misfit_t(wo_ctx* ctx, int64_t N, int kind, const double* measured, double c1
     misfit_kernel<T><<<(unsigned)N, 256, 0, ctx->stream>>>(
         reinterpret_cast<T*>(ctx->store), ctx->measured, (long long)N, (int)ctx->n_sup, kind, c1,
         c2, c3, c4, adj_coef, write_adj, (T)k, ctx->partial);
-    cost_sum_kernel<<<1, 32, 0, ctx->stream>>>(ctx->partial, (long long)N, ctx->cost);
+    cost_sum_kernel<<<1, 256, 0, ctx->stream>>>(ctx->partial, (long long)N, ctx->cost);
     ctx->launches += 2;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(cost_out, ctx->cost, 8, cudaMemcpyDeviceToHost, ctx->stream));

@@ -37,9 +37,20 @@ void launch_step_engine(int engine, const StepSel& k, dim3 grid, dim3 block, cud
 // two-step pass (no divisions on the dense path; checks are runtime flags)
 // geometry: GEO_WIDE (64 x 8 tiles) or GEO_TALL (32 x 16 tiles)
 enum Step2Geo : int { GEO_NONE = 0, GEO_WIDE = 1, GEO_TALL = 2 };
+// one translation unit per (dtype, T2Mode) instantiates launch_step2_mode
+template <typename T, int MODE>
+void launch_step2_mode(const StepSel& k, int geo, dim3 grid, cudaStream_t s,
+                       const Step2Args<T>& a, const Tma2Maps& maps);
+template <typename T, int MODE> void preload_step2_mode();
+
+// mode: T2Mode (step2_kernel.cuh) — the feature level the launch needs
 template <typename T>
-void launch_step2_engine(const StepSel& k, int geo, dim3 grid, cudaStream_t s,
-                         const Step2Args<T>& a, const Tma2Maps& maps);
+inline void launch_step2_engine(const StepSel& k, int geo, int mode, dim3 grid, cudaStream_t s,
+                                const Step2Args<T>& a, const Tma2Maps& maps) {
+    if (mode == T2_FULL) launch_step2_mode<T, T2_FULL>(k, geo, grid, s, a, maps);
+    else if (mode == T2_CHAIN) launch_step2_mode<T, T2_CHAIN>(k, geo, grid, s, a, maps);
+    else launch_step2_mode<T, T2_BASE>(k, geo, grid, s, a, maps);
+}
 
 // coef | +k | +j | +i face arrays (4 consecutive fields at out) of a material
 template <typename T>
@@ -59,7 +70,14 @@ template <typename T> void preload_step_kernels();
 template <typename T>
 cudaError_t launch_cluster_sweep(int flavor, bool acc, const ClusterSweepArgs<T>& a, int cl,
                                  cudaStream_t s, bool probe);
-template <typename T> void preload_step2_kernels();
+template <typename T> void preload_material4_kernels();
+template <typename T>
+inline void preload_step2_kernels() {
+    preload_step2_mode<T, T2_BASE>();
+    preload_step2_mode<T, T2_CHAIN>();
+    preload_step2_mode<T, T2_FULL>();
+    preload_material4_kernels<T>();
+}
 
 
 }  // namespace wb

@@ -74,6 +74,15 @@ constexpr int T2_CTAS_F32 = WB_T2_CTAS;   // resident fp32 CTAs per SM
 constexpr int T2_CTAS_F64 = WB_T2_CTAS_F64;
 constexpr int T2_MAXZ = 64;          // z layers (chunks along axis 0) per launch
 
+// Feature level of a two-step launch (template parameter MODE): the launch-
+// latency-bound grids (2D, one plane per pass) lose 7% to code they never run
+// (C1 24.9 vs 26.6 Gcell-upd/s), so each level compiles only what it needs:
+//   T2_BASE   32-bit cell offsets, whole-grid dependency (griddepcontrol.wait)
+//   T2_CHAIN  + dataflow-chained passes (completion flags, Step2Args::chain)
+//   T2_FULL   + 64-bit offsets (grids of >= 2^31 cells) and peer ghost
+//             stores (peer-store slabs)
+enum T2Mode : int { T2_BASE = 0, T2_CHAIN = 1, T2_FULL = 2 };
+
 // Packed fp32 pairs (sm_100a FADD2 / FFMA2): the two cells of a thread's row
 // run the same IEEE operation sequence, so one f32x2 instruction computes
 // both with the bits of two scalar ones.  Products are fma(a, b, z) with z =
@@ -235,13 +244,16 @@ __global__ void material4_kernel(const T* __restrict__ gamma, MatScalars<T> M, i
     }
 }
 
-template <typename T, typename G, int FLAVOR, bool ACC, int SUP>
+template <typename T, typename G, int FLAVOR, bool ACC, int SUP, int MODE>
 __global__ void __launch_bounds__(T2_THREADS, sizeof(T) == 4 ? T2_CTAS_F32 : T2_CTAS_F64)
 step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__ Tma2Maps maps) {
     using Tr = FTraits<T>;
     using MP = Mat<T, FLAVOR, false>;   // sparse force coefficients only
     using V = typename Pair<T>::V;
     using Bits = typename Tr::Bits;
+    using Off = typename std::conditional<MODE == T2_FULL, long long, int>::type;   // cell offsets
+    using UOff = typename std::make_unsigned<Off>::type;
+    constexpr bool CHAIN = MODE != T2_BASE, PEER = MODE == T2_FULL;
     constexpr int W = G::template W<T>(), HO = th_ho<T>();
     constexpr int TBX = G::TBX, TBY = G::TBY, R2_H = G::R2, R1_H = G::R1, NRING = G::NRING;
     constexpr int PL = R2_H * W;                       // elements of one R2 plane
@@ -264,7 +276,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     const int k0 = blockIdx.x * TBX, j0 = blockIdx.y * TBY;
     const int kA = k0 + 2 * tx, ja = j0 + 2 * ty;
     const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
-    const long long plane = (long long)n1 * n2;   // 64-bit plane offsets: grids of >= 2^31 cells
+    const Off plane = (Off)n1 * n2;   // 64-bit in T2_FULL: grids of >= 2^31 cells
     // logical z layer: consecutive passes may dispatch the layers in opposite
     // orders (zrev), so a pass starts where the previous one ended (its
     // outputs still in L2)
@@ -373,7 +385,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     // while the previous pass drains; nothing above touched global memory.
     // Wait for the previous grid (and its memory) before the first load, and
     // let the next pass start its prologue once every CTA of this one runs.
-    if (a.chain) {
+    if (CHAIN && a.chain) {
         // the next pass may dispatch as soon as all our CTAs run; ours only
         // depend on the previous pass's blocks around this one
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -467,7 +479,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         return add2(accv, mul2(sdt, add2(mul2(mul2(cv, va, NZ), va, NZ), mul2(cg, gg, NZ)), NZ));
     };
     // nodal force coefficient of a cell from its gamma (sparse; solver.py:98,110)
-    auto fcoef = [&](long long flat) {
+    auto fcoef = [&](Off flat) {
         const T g = __ldg(a.gamma + flat);
         T kap;
         (void)MP::coef(a.mat, g, kap);
@@ -482,7 +494,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     // support bit / compact index of cell (p, jj, kk)
     auto sup_index = [&](int p, int jj, int kk) -> int {
         if (SUP == SUP_NONE || p < a.sup_lo || p > a.sup_hi) return -1;
-        const unsigned long long flat = (unsigned long long)(p * plane + jj * n2 + kk);
+        const UOff flat = (UOff)(p * plane + jj * n2 + kk);
         const unsigned w = __ldg(a.sup_mask + (flat >> 5));
         const unsigned bit = (unsigned)(flat & 31u);
         if (!((w >> bit) & 1u)) return -1;
@@ -522,7 +534,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
     V unm_a, unm_b, w0_a = {T(0), T(0)}, w0_b = {T(0), T(0)};   // plane pbeg-1 (mirror at 0)
     T rum[2] = {T(0), T(0)}, rw0[2] = {T(0), T(0)};
     if (has_m0) {
-        const long long gm = (pbeg - 1) * plane;
+        const Off gm = (pbeg - 1) * plane;
         unm_a = __ldg(reinterpret_cast<const V*>(a.u_cur + gm + cofs));
         unm_b = __ldg(reinterpret_cast<const V*>(a.u_cur + gm + cofs + n2));
         w0_a = __ldg(reinterpret_cast<const V*>(a.fi + gm + cofs));
@@ -574,7 +586,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
             o2a = upk2(ra);
             o2b = upk2(rb);
             tile_inject(q1, o2a, o2b, x_0a, x_0b, a.src_val2, a.row2, true);
-            const long long oc = q1 * plane + cofs;
+            const Off oc = q1 * plane + cofs;
             if (ACC) {
                 const f2x fa = kinc2(pk2(acc1_a), pk2(o2a), pk2(un1_a), pk2(xp_a), pk2(x_m1a),
                                      pk2(x_0b), pk2(xu), kpa, kma);
@@ -597,7 +609,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         o2b.y = cell(x_0b.y, xp_b.y, x_m1b.y, xd.y, x_0a.y, xRb, x_0b.x, w1hi_b.y, w1lo_b.y,
                      f1_jhi.y, f1_jab.y, f1_kRb, f1_kIb, c1_b.y, un1_b.y);
         tile_inject(q1, o2a, o2b, x_0a, x_0b, a.src_val2, a.row2, true);
-        const long long oc = q1 * plane + cofs;
+        const Off oc = q1 * plane + cofs;
         if (ACC) {
             V fa, fb;
             fa.x = kinc(acc1_a.x, o2a.x, un1_a.x, xp_a.x, x_m1a.x, x_0b.x, xu.x, x_0a.y, xLa);
@@ -614,13 +626,13 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
         }
         // slab boundary planes: both new levels also go straight into the
         // neighbour's ghost planes (NVLink stores across GPUs)
-        if (q1 < 2 && a.plo1) {
-            const long long oc = q1 * plane + cofs;
+        if (PEER && q1 < 2 && a.plo1) {
+            const Off oc = q1 * plane + cofs;
             stg(a.plo1 + oc, x_0a); stg(a.plo1 + oc + n2, x_0b);
             stg(a.plo2 + oc, o2a); stg(a.plo2 + oc + n2, o2b);
         }
-        if (q1 >= n0 - 2 && a.phi1) {
-            const long long oc = q1 * plane + cofs;
+        if (PEER && q1 >= n0 - 2 && a.phi1) {
+            const Off oc = q1 * plane + cofs;
             stg(a.phi1 + oc, x_0a); stg(a.phi1 + oc + n2, x_0b);
             stg(a.phi2 + oc, o2a); stg(a.phi2 + oc + n2, o2b);
         }
@@ -823,7 +835,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
             }
         }
     }
-    if (a.tflags) {   // publish this block's completion (release: all its writes first)
+    if (CHAIN && a.tflags) {   // publish this block's completion (release: all its writes first)
         __syncthreads();
         if (tid == 0) {
             asm volatile("fence.proxy.async.global;" ::: "memory");

@@ -106,37 +106,38 @@ void launch_step_engine(int engine, const StepSel& k, dim3 grid, dim3 block, cud
     }
 }
 
-template <typename T, typename G, int FL, bool ACC, int SUP>
+template <typename T, typename G, int FL, bool ACC, int SUP, int MODE>
 void go_step2(dim3 grid, cudaStream_t s, const Step2Args<T>& a, const Tma2Maps& maps) {
     const size_t sm = step2_smem_bytes<T, G>();
-    smem_opt_in<step2_kernel_tma<T, G, FL, ACC, SUP>>(sm);
-    launch_pdl(step2_kernel_tma<T, G, FL, ACC, SUP>, grid, dim3(G::TX, G::TY, 1), sm, s, a, maps);
+    smem_opt_in<step2_kernel_tma<T, G, FL, ACC, SUP, MODE>>(sm);
+    launch_pdl(step2_kernel_tma<T, G, FL, ACC, SUP, MODE>, grid, dim3(G::TX, G::TY, 1), sm, s, a,
+               maps);
 }
 
-template <typename T, typename G, int FL, bool ACC>
+template <typename T, typename G, int FL, bool ACC, int MODE>
 void go_step2_sup(int sup, dim3 grid, cudaStream_t s, const Step2Args<T>& a, const Tma2Maps& maps) {
-    if (sup == SUP_GATHER) go_step2<T, G, FL, ACC, SUP_GATHER>(grid, s, a, maps);
-    else if (sup == SUP_INJECT) go_step2<T, G, FL, ACC, SUP_INJECT>(grid, s, a, maps);
-    else go_step2<T, G, FL, ACC, SUP_NONE>(grid, s, a, maps);
+    if (sup == SUP_GATHER) go_step2<T, G, FL, ACC, SUP_GATHER, MODE>(grid, s, a, maps);
+    else if (sup == SUP_INJECT) go_step2<T, G, FL, ACC, SUP_INJECT, MODE>(grid, s, a, maps);
+    else go_step2<T, G, FL, ACC, SUP_NONE, MODE>(grid, s, a, maps);
 }
 
-template <typename T, typename G>
+template <typename T, typename G, int MODE>
 void go_step2_geo(const StepSel& k, dim3 grid, cudaStream_t s, const Step2Args<T>& a,
                   const Tma2Maps& maps) {
     if (k.flavor == RHO_SCALED) {
-        if (k.acc) go_step2_sup<T, G, RHO_SCALED, true>(k.sup, grid, s, a, maps);
-        else go_step2_sup<T, G, RHO_SCALED, false>(k.sup, grid, s, a, maps);
+        if (k.acc) go_step2_sup<T, G, RHO_SCALED, true, MODE>(k.sup, grid, s, a, maps);
+        else go_step2_sup<T, G, RHO_SCALED, false, MODE>(k.sup, grid, s, a, maps);
     } else {
-        if (k.acc) go_step2_sup<T, G, ACOUSTIC, true>(k.sup, grid, s, a, maps);
-        else go_step2_sup<T, G, ACOUSTIC, false>(k.sup, grid, s, a, maps);
+        if (k.acc) go_step2_sup<T, G, ACOUSTIC, true, MODE>(k.sup, grid, s, a, maps);
+        else go_step2_sup<T, G, ACOUSTIC, false, MODE>(k.sup, grid, s, a, maps);
     }
 }
 
-template <typename T>
-void launch_step2_engine(const StepSel& k, int geo, dim3 grid, cudaStream_t s,
-                         const Step2Args<T>& a, const Tma2Maps& maps) {
-    if (geo == GEO_TALL) go_step2_geo<T, GeoTall>(k, grid, s, a, maps);
-    else go_step2_geo<T, GeoWide>(k, grid, s, a, maps);
+template <typename T, int MODE>
+void launch_step2_mode(const StepSel& k, int geo, dim3 grid, cudaStream_t s,
+                       const Step2Args<T>& a, const Tma2Maps& maps) {
+    if (geo == GEO_TALL) go_step2_geo<T, GeoTall, MODE>(k, grid, s, a, maps);
+    else go_step2_geo<T, GeoWide, MODE>(k, grid, s, a, maps);
 }
 
 template <typename T>
@@ -185,27 +186,31 @@ void preload_step_kernels() {
     preload_step_fl<T, ACOUSTIC, true>();
 }
 
-template <typename T, typename G, int FL, bool ACC>
+template <typename T, typename G, int FL, bool ACC, int MODE>
 void preload_step2_variant() {
     const size_t sm = step2_smem_bytes<T, G>();
-    load_kernel(step2_kernel_tma<T, G, FL, ACC, SUP_NONE>);
-    load_kernel(step2_kernel_tma<T, G, FL, ACC, SUP_GATHER>);
-    load_kernel(step2_kernel_tma<T, G, FL, ACC, SUP_INJECT>);
-    smem_opt_in<step2_kernel_tma<T, G, FL, ACC, SUP_NONE>>(sm);
-    smem_opt_in<step2_kernel_tma<T, G, FL, ACC, SUP_GATHER>>(sm);
-    smem_opt_in<step2_kernel_tma<T, G, FL, ACC, SUP_INJECT>>(sm);
+    load_kernel(step2_kernel_tma<T, G, FL, ACC, SUP_NONE, MODE>);
+    load_kernel(step2_kernel_tma<T, G, FL, ACC, SUP_GATHER, MODE>);
+    load_kernel(step2_kernel_tma<T, G, FL, ACC, SUP_INJECT, MODE>);
+    smem_opt_in<step2_kernel_tma<T, G, FL, ACC, SUP_NONE, MODE>>(sm);
+    smem_opt_in<step2_kernel_tma<T, G, FL, ACC, SUP_GATHER, MODE>>(sm);
+    smem_opt_in<step2_kernel_tma<T, G, FL, ACC, SUP_INJECT, MODE>>(sm);
+}
+
+template <typename T, int MODE>
+void preload_step2_mode() {
+    preload_step2_variant<T, GeoWide, RHO_SCALED, false, MODE>();
+    preload_step2_variant<T, GeoWide, RHO_SCALED, true, MODE>();
+    preload_step2_variant<T, GeoWide, ACOUSTIC, false, MODE>();
+    preload_step2_variant<T, GeoWide, ACOUSTIC, true, MODE>();
+    preload_step2_variant<T, GeoTall, RHO_SCALED, false, MODE>();
+    preload_step2_variant<T, GeoTall, RHO_SCALED, true, MODE>();
+    preload_step2_variant<T, GeoTall, ACOUSTIC, false, MODE>();
+    preload_step2_variant<T, GeoTall, ACOUSTIC, true, MODE>();
 }
 
 template <typename T>
-void preload_step2_kernels() {
-    preload_step2_variant<T, GeoWide, RHO_SCALED, false>();
-    preload_step2_variant<T, GeoWide, RHO_SCALED, true>();
-    preload_step2_variant<T, GeoWide, ACOUSTIC, false>();
-    preload_step2_variant<T, GeoWide, ACOUSTIC, true>();
-    preload_step2_variant<T, GeoTall, RHO_SCALED, false>();
-    preload_step2_variant<T, GeoTall, RHO_SCALED, true>();
-    preload_step2_variant<T, GeoTall, ACOUSTIC, false>();
-    preload_step2_variant<T, GeoTall, ACOUSTIC, true>();
+void preload_material4_kernels() {
     load_kernel(material4_kernel<T, RHO_SCALED>);
     load_kernel(material4_kernel<T, ACOUSTIC>);
 }

@@ -520,9 +520,7 @@ int launch_step(wo_ctx* ctx, const StepSpec& sp) {
     }
     prof_begin(ctx, 0);
     const StepSel sel{ctx->flavor, ctx->fast_div, sp.acc, sp.check, a.sup_mode};
-    // (the superseded 256-thread TMA engine has no peer stores)
-    const int engine = tma ? (ctx->use_tma == 2 && !sp.peer ? ENGINE_TMA : ENGINE_TMA4)
-                           : (pair ? ENGINE_PAIR : ENGINE_SCALAR);
+    const int engine = tma ? ENGINE_TMA4 : (pair ? ENGINE_PAIR : ENGINE_SCALAR);
     t_no_pdl = sp.peer && !p2p_pdl();
     ctx->t2_chain_next = false;   // the next two-step pass waits for this whole grid
     launch_step_engine<T>(engine, sel, grid, block, ctx->stream, a, ctx->tmaps);
@@ -2196,7 +2194,7 @@ int wo_set_option(wo_ctx* ctx, int option, int value) {
         return WO_OK;
     }
     if (option == WO_OPT_TMA_KERNEL) {
-        ctx->use_tma = value;   // 0 off, 1 tma4 (default), 2 the 256-thread TMA kernel
+        ctx->use_tma = value != 0;   // 0 off, else the TMA kernels (default)
         return WO_OK;
     }
     ctx->allow_fast_div = value != 0;

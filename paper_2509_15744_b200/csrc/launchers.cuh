@@ -10,12 +10,12 @@
 #include "cluster_sweep.cuh"
 #include "step2_kernel.cuh"
 #include "step_kernel.cuh"
-#include "step_kernel_tma.cuh"
+#include "tma_common.cuh"
 
 namespace wb {
 
 // single-step engines
-enum StepEngine : int { ENGINE_SCALAR = 0, ENGINE_PAIR = 1, ENGINE_TMA = 2, ENGINE_TMA4 = 3 };
+enum StepEngine : int { ENGINE_SCALAR = 0, ENGINE_PAIR = 1, ENGINE_TMA4 = 3 };
 
 struct StepSel {
     int flavor;   // RHO_SCALED / ACOUSTIC

@@ -34,7 +34,7 @@
 
 #include "common.cuh"
 #include "step_kernel.cuh"
-#include "step_kernel_tma.cuh"
+#include "tma_common.cuh"
 #include "step_kernel_v2.cuh"
 
 namespace wb {

@@ -1,9 +1,10 @@
 // TMA-pipelined fused step, 2x2 cells per thread (production kernel on
 // whole-tile grids).
 //
-// Same data movement as step_kernel_tma (4-stage TMA ring of u^n / gamma halo
-// boxes and u^{n-1} / acc tiles, one producer thread, mbarrier completion)
-// with two changes that cut the per-cell instruction count:
+// Data movement (tma_common.cuh): a 4-stage TMA ring of u^n / gamma halo
+// boxes and u^{n-1} / acc tiles, one producer thread, mbarrier completion.
+// Round 1's first TMA kernel (256 threads x 2 cells) was superseded by this
+// layout, which cuts the per-cell instruction count:
 //   * a thread owns a 2x2 block (rows j, j+1 x cells k, k+1): the k-face and
 //     the j-face inside the block live in registers, the outer faces are
 //     computed directly from the shared m-plane (no shared face arrays), and
@@ -19,7 +20,7 @@
 
 #include "common.cuh"
 #include "step_kernel.cuh"
-#include "step_kernel_tma.cuh"
+#include "tma_common.cuh"
 #include "step_kernel_v2.cuh"
 
 namespace wb {

@@ -61,10 +61,6 @@ void go_step(int engine, dim3 grid, dim3 block, cudaStream_t s, const StepArgs<T
         smem_opt_in<step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP>>(sm);
         launch_pdl(step_kernel_tma4<T, FL, FAST, ACC, CHK, SUP>, grid, dim3(32, 4, 1), sm, s, a,
                    maps);
-    } else if (engine == ENGINE_TMA) {   // 256 threads, 2 cells each
-        const size_t sm = tma_smem_bytes<T>();
-        smem_opt_in<step_kernel_tma<T, FL, FAST, ACC, CHK, SUP>>(sm);
-        step_kernel_tma<T, FL, FAST, ACC, CHK, SUP><<<grid, block, sm, s>>>(a, maps);
     } else if (SUP == SUP_NONE) {   // pair / scalar kernels read a.sup_mode at run time
         if (engine == ENGINE_PAIR)
             step_kernel_pair<T, FL, FAST, ACC, CHK><<<grid, block, 0, s>>>(a);
@@ -76,7 +72,7 @@ void go_step(int engine, dim3 grid, dim3 block, cudaStream_t s, const StepArgs<T
 template <typename T, int FL, bool FAST, bool ACC, bool CHK>
 void go_step_sup(int engine, int sup, dim3 grid, dim3 block, cudaStream_t s,
                  const StepArgs<T>& a, const TmaMaps& maps) {
-    if (engine != ENGINE_TMA && engine != ENGINE_TMA4) sup = SUP_NONE;
+    if (engine != ENGINE_TMA4) sup = SUP_NONE;
     if (sup == SUP_GATHER) go_step<T, FL, FAST, ACC, CHK, SUP_GATHER>(engine, grid, block, s, a, maps);
     else if (sup == SUP_INJECT) go_step<T, FL, FAST, ACC, CHK, SUP_INJECT>(engine, grid, block, s, a, maps);
     else go_step<T, FL, FAST, ACC, CHK, SUP_NONE>(engine, grid, block, s, a, maps);

@@ -486,7 +486,7 @@ class DeviceGrid:
                  "wo_set_option")
 
     def set_tma_kernel(self, mode):
-        """0: never; 1/True: 2x2-cell TMA kernel (default); 2: 256-thread TMA kernel."""
+        """0/False: never; 1/True: the TMA kernels on whole-tile grids (default)."""
         self._ck(self.L.wo_set_option(self.h, N.WO_OPT_TMA_KERNEL, int(mode)), "wo_set_option")
 
     def set_two_step(self, mode):

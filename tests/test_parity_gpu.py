@@ -366,7 +366,7 @@ def test_tma_pair_scalar_kernels_agree(W, prec):
     cfg = W.SuperpositionConfig(k=1e13, precision=prec)
     ctx = engine.get_context(grid, W.precision_dtype(prec))
     out = {}
-    for name, tma, pair in (("tma4", 1, True), ("tma", 2, True), ("pair", 0, True),
+    for name, tma, pair in (("tma4", 1, True), ("pair", 0, True),
                             ("scalar", 0, False)):
         ctx.set_tma_kernel(tma)
         ctx.set_pair_kernel(pair)

@@ -75,6 +75,26 @@ __global__ void cost_sum_kernel(const double* partial, long long n_steps, double
     if (threadIdx.x == 0) *out = c;
 }
 
+// Nodal force coefficient fc(gamma) of every support node, in compact
+// (increasing flat index) order: the two-step kernel's adjoint injection
+// (gradients.py:268-269 through solver.py:167-170) multiplies by it instead
+// of recomputing it per step from gamma with two IEEE divisions behind a
+// chain of dependent global loads (C3 TATO 192^3: the objective region's
+// CTAs made the backward sweep 2x the forward one).  Same operations as the
+// kernels' per-cell fcoef, so the products are bit-identical.
+template <typename T, int FLAVOR>
+__global__ void sup_fc_kernel(const T* __restrict__ gamma, MatScalars<T> M,
+                              const long long* __restrict__ flat, long long n, T* __restrict__ out) {
+    using P = Mat<T, FLAVOR, false>;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const T g = gamma[flat[i]];
+        T kap;
+        (void)P::coef(M, g, kap);
+        out[i] = P::fc(M, g, kap);
+    }
+}
+
 template <typename T>
 __global__ void scale_div_kernel(T* acc, long long n, T denom) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;

@@ -152,6 +152,13 @@ struct wo_ctx {
     int64_t n_sup = 0;
     unsigned int* mask = nullptr;
     int* prefix = nullptr;
+    // per-support-node force coefficients fc(gamma), compact order
+    // (sup_fc_kernel; the two-step kernel's adjoint injection)
+    long long* sup_flat = nullptr;     // device copy of the support indices
+    size_t sup_flat_bytes = 0;
+    char* sup_fc = nullptr;
+    size_t sup_fc_bytes = 0;
+    bool sup_fc_valid = false;
     char* store = nullptr;
     size_t store_bytes = 0;
     double* measured = nullptr;
@@ -643,7 +650,7 @@ struct KeyHash {
 void hash_param_buffers(KeyHash& kh, const wo_ctx* ctx) {
     for (auto* b : ctx->u) kh.val(b);
     kh.val(ctx->gamma); kh.val(ctx->acc); kh.val(ctx->mat4); kh.val(ctx->store);
-    kh.val(ctx->maxslots); kh.val(ctx->mask); kh.val(ctx->prefix);
+    kh.val(ctx->maxslots); kh.val(ctx->mask); kh.val(ctx->prefix); kh.val(ctx->sup_fc);
 }
 
 // true: the sweep was replayed from its graph (the caller skips its loop)
@@ -774,6 +781,39 @@ int ensure_mat4(wo_ctx* ctx) {
     return WO_OK;
 }
 
+// fc(gamma) of every support node for the two-step kernel's adjoint
+// injection (sup_fc_kernel), rebuilt when gamma or the support changes;
+// called from pair_ready, i.e. before a sweep's graph capture
+int ensure_sup_fc(wo_ctx* ctx) {
+    if (ctx->sup_fc_valid || ctx->n_sup == 0) return WO_OK;
+    int rc = ensure(ctx, &ctx->sup_fc, &ctx->sup_fc_bytes, (size_t)ctx->n_sup * ctx->itemsize);
+    if (rc) return rc;
+    const char* g = ctx->base0(ctx->gamma);
+    const long long n = ctx->n_sup;
+    const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 592);
+    if (ctx->itemsize == 4) {
+        const MatScalars<float> M = mat_scalars<float>(ctx);
+        const float* gf = reinterpret_cast<const float*>(g);
+        float* o = reinterpret_cast<float*>(ctx->sup_fc);
+        if (ctx->flavor == RHO_SCALED)
+            sup_fc_kernel<float, RHO_SCALED><<<blocks, 256, 0, ctx->stream>>>(gf, M, ctx->sup_flat, n, o);
+        else
+            sup_fc_kernel<float, ACOUSTIC><<<blocks, 256, 0, ctx->stream>>>(gf, M, ctx->sup_flat, n, o);
+    } else {
+        const MatScalars<double> M = mat_scalars<double>(ctx);
+        const double* gd = reinterpret_cast<const double*>(g);
+        double* o = reinterpret_cast<double*>(ctx->sup_fc);
+        if (ctx->flavor == RHO_SCALED)
+            sup_fc_kernel<double, RHO_SCALED><<<blocks, 256, 0, ctx->stream>>>(gd, M, ctx->sup_flat, n, o);
+        else
+            sup_fc_kernel<double, ACOUSTIC><<<blocks, 256, 0, ctx->stream>>>(gd, M, ctx->sup_flat, n, o);
+    }
+    ctx->launches++;
+    CK(cudaGetLastError());
+    ctx->sup_fc_valid = true;
+    return WO_OK;
+}
+
 // tile geometry for a two-step pass: 64 x 8 where it divides the plane, else
 // 32 x 16 (measured equal at 256^3: 214 vs 212 Gcell/s; the tall tile's
 // balanced warps and smaller ring are offset by narrower TMA rows);
@@ -859,6 +899,7 @@ bool pair_ready(wo_ctx* ctx) {
             ctx->t2_geo = geo;
         }
     }
+    if (ctx->t2_state == 1 && ensure_sup_fc(ctx)) return false;   // (out of memory: single steps)
     return ctx->t2_state == 1;
 }
 
@@ -1120,6 +1161,7 @@ int launch_pair(wo_ctx* ctx, const PairSpec& sp) {
     const int sup = ctx->n_sup > 0 ? sp.sup_mode : SUP_NONE;
     a.sup_lo = ctx->sup_lo; a.sup_hi = ctx->sup_hi;
     a.sup_mask = ctx->mask; a.sup_prefix = ctx->prefix;
+    a.sup_fc = reinterpret_cast<const T*>(ctx->sup_fc);
     if (sup != SUP_NONE) {
         a.row1 = reinterpret_cast<T*>(ctx->store) + sp.row1 * ctx->n_sup;
         a.row2 = reinterpret_cast<T*>(ctx->store) + sp.row2 * ctx->n_sup;
@@ -1948,7 +1990,7 @@ void wo_destroy(wo_ctx* ctx) {
                     ctx->snap, ctx->scratch, ctx->opt, ctx->opt_frozen, ctx->opt_partial,
                     ctx->dsn, ctx->dmask, ctx->dfp_off, ctx->dfp_w,
                     ctx->flag, ctx->acc, reinterpret_cast<char*>(ctx->in_flags),
-                    ctx->mask, ctx->prefix,
+                    ctx->mask, ctx->prefix, reinterpret_cast<char*>(ctx->sup_flat), ctx->sup_fc,
                     ctx->store, ctx->measured, ctx->partial, ctx->cost, ctx->maxslots,
                     ctx->f_idx, ctx->f_vals, ctx->f_dense, ctx->hist, ctx->u3,
                     reinterpret_cast<char*>(ctx->amp_dev), reinterpret_cast<char*>(ctx->tflags)};
@@ -1992,6 +2034,7 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
     }
     ctx->material_set = true;
     ctx->mat4_valid = false;
+    ctx->sup_fc_valid = false;
     return verify_fast_div(ctx);
 }
 
@@ -2056,6 +2099,7 @@ int wo_opt_step(wo_ctx* ctx, int t, double* grad_norm) {
     if (grad_norm) *grad_norm = std::sqrt(sq);
     if (ctx->design_active) return WO_OK;   // the material changes in wo_design_material
     ctx->mat4_valid = false;                // gamma changed on the device
+    ctx->sup_fc_valid = false;
     return verify_fast_div(ctx);
 }
 
@@ -2115,6 +2159,7 @@ int wo_design_material(wo_ctx* ctx, double beta, double eta, double t_be, double
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->mat4_valid = false;
+    ctx->sup_fc_valid = false;
     return verify_fast_div(ctx);
 }
 
@@ -2240,6 +2285,12 @@ int wo_set_support(wo_ctx* ctx, int64_t n_sup, const int64_t* flat) {
     }
     CK(cudaMemcpy(ctx->mask, m.data(), words * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->prefix, p.data(), words * 4, cudaMemcpyHostToDevice));
+    if (n_sup) {
+        if ((rc = ensure(ctx, &ctx->sup_flat, &ctx->sup_flat_bytes, (size_t)n_sup * 8))) return rc;
+        static_assert(sizeof(long long) == sizeof(int64_t), "support index width");
+        CK(cudaMemcpy(ctx->sup_flat, flat, (size_t)n_sup * 8, cudaMemcpyHostToDevice));
+    }
+    ctx->sup_fc_valid = false;
     ctx->n_sup = n_sup;
     ++ctx->gen;
     return WO_OK;

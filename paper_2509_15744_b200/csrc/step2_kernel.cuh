@@ -160,6 +160,7 @@ template <typename T> struct Step2Args {
     int sup_lo, sup_hi;
     const unsigned int* sup_mask;
     const int* sup_prefix;
+    const T* sup_fc;   // fc(gamma) per support node, compact order (SUP_INJECT)
     T* row1;           // store row of step 1 (gather: u^n; inject: adj of step 1)
     T* row2;           // store row of step 2 (gather: u^{n+1}; inject: adj of step 2)
     int check1, check2;
@@ -518,7 +519,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
                 const int qi = sup_index(p, jj, kk);
                 if (qi >= 0) {
                     if (SUP == SUP_GATHER) { if (gather_ok) row[qi] = uo[c]; }
-                    else *oo[c] = *oo[c] + fcoef(p * plane + jj * n2 + kk) * ldg(row + qi);
+                    else *oo[c] = *oo[c] + ldg(a.sup_fc + qi) * ldg(row + qi);
                 }
             }
         }
@@ -747,7 +748,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
                 if (my_src) inject_src(p, jj, kk, a.src_val1, v);
                 if (SUP == SUP_INJECT) {
                     const int qi = sup_index(p, jj, kk);
-                    if (qi >= 0) v = v + fcoef(p * plane + jj * n2 + kk) * ldg(a.row1 + qi);
+                    if (qi >= 0) v = v + ldg(a.sup_fc + qi) * ldg(a.row1 + qi);
                 }
             }
             Xc[o] = v;

@@ -899,7 +899,10 @@ bool pair_ready(wo_ctx* ctx) {
             ctx->t2_geo = geo;
         }
     }
-    if (ctx->t2_state == 1 && ensure_sup_fc(ctx)) return false;   // (out of memory: single steps)
+    if (ctx->t2_state == 1 && ensure_sup_fc(ctx)) {   // out of memory: single steps
+        if (ctx->has_lo || ctx->has_hi) ctx->t2_oom = true;   // slabs must launch alike (REQUIRE)
+        return false;
+    }
     return ctx->t2_state == 1;
 }
 

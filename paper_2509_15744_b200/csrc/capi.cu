@@ -1839,8 +1839,9 @@ int upload_cast_t(wo_ctx* ctx, const double* host, char* dev, int64_t n) {
 }
 
 int create_common(wo_ctx* ctx) {
-    // plane offsets are 64-bit in every kernel; in-plane offsets and plane
-    // indices stay 32-bit (n1*n2 < 2^31 per plane)
+    // plane offsets are 64-bit in the single-step kernels and in the
+    // two-step kernel's T2_FULL level (chosen for allocations of >= 2^31
+    // cells); in-plane offsets and plane indices stay 32-bit (n1*n2 < 2^31)
     REQUIRE(ctx->plane() < (1ll << 31), "plane too large (n1*n2 >= 2^31 cells)");
     CK(cudaSetDevice(ctx->device));
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));

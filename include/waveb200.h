@@ -245,6 +245,15 @@ int wo_slab_ghosts(wo_ctx* ctx, void** ghost_lo, void** ghost_hi, void** flags);
 /* Error recovery: set this slab's and its neighbours' flags to the maximum
  * so no stream keeps waiting on a sweep that was only partly enqueued. */
 int wo_slab_abort(wo_ctx* ctx);
+/* Prepare two-step passes now (replaces nothing in the reference: the
+ * launch-kind agreement of a slab decomposition).  Allocates the two extra
+ * level buffers and the precomputed material, builds the tensor maps and the
+ * support forces; *ready = 1 when this context will take two-step passes,
+ * 0 when it will not (option off, grid shape, or the buffers do not fit).
+ * Peer-store slabs must all launch alike: a decomposition whose slabs do not
+ * all report 1 sets WO_OPT_TWO_STEP 0 on every slab. */
+int wo_prepare_two_step(wo_ctx* ctx, int* ready);
+
 /* Diagnostics (no wait on the context's stream): out[0..3] the flag words,
  * out[4] signals sent in the current epoch, out[5] epochs begun, out[6] 1 if
  * the stream is idle. */

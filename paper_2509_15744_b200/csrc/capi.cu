@@ -1344,9 +1344,9 @@ int sweep_forward_t(wo_ctx* ctx, int64_t N, int n_src, const int64_t* src_flat,
     }
     const bool pairs = ns <= MAX_SRC && !record && pair_ready(ctx);
     // a peer-store slab must launch exactly like its neighbours
-    REQUIRE(!(ctx->p2p && ctx->t2_oom),
+    REQUIRE(!(ctx->p2p && ctx->t2_oom && ctx->use_two_step),
             "two-step buffers do not fit on this peer-store slab: disable two-step passes on "
-            "every slab of the decomposition");
+            "every slab of the decomposition (wo_prepare_two_step)");
     std::vector<double> vals2(std::max(ns, 1));
     // graph of this sweep: the key covers everything the launches depend on
     // beyond the state generation
@@ -1503,9 +1503,9 @@ int sweep_backward_t(wo_ctx* ctx, int64_t N, int64_t src_flat, const double* src
         n_hi = n_lo;
     }
     const bool pairs = pair_ready(ctx);
-    REQUIRE(!(ctx->p2p && ctx->t2_oom),
+    REQUIRE(!(ctx->p2p && ctx->t2_oom && ctx->use_two_step),
             "two-step buffers do not fit on this peer-store slab: disable two-step passes on "
-            "every slab of the decomposition");
+            "every slab of the decomposition (wo_prepare_two_step)");
     double val2 = 0.0;
     const bool graphable = ctx->use_graphs && !ctx->prof && ctx->part == 0 && !ctx->p2p &&
                            !cluster && n_hi - n_lo >= 8;
@@ -2517,6 +2517,19 @@ int wo_slab_abort(wo_ctx* ctx) {
 
 // Diagnostics of the peer-store protocol without touching the context's
 // stream: out = {flag words [4], signals sent this epoch, epoch, stream idle}
+int wo_prepare_two_step(wo_ctx* ctx, int* ready) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    REQUIRE(ready, "wo_prepare_two_step: null output");
+    CK(cudaSetDevice(ctx->device));
+    // allocates the extra levels and the material, builds the maps and the
+    // support forces now (pair_ready), so a decomposition can agree on the
+    // launch kind before any peer-store sweep
+    *ready = pair_ready(ctx) ? 1 : 0;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return WO_OK;
+}
+
 int wo_slab_state(wo_ctx* ctx, int64_t* out) {
     int rc = check_ctx(ctx);
     if (rc) return rc;

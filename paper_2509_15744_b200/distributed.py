@@ -504,6 +504,15 @@ class SlabGradient:
             self.all_slabs, grid.shape[1] * grid.shape[2], [s.support_idx for _, s in self._shots])
         for c in self.ctxs:
             c.set_two_step(1 if self.two_step else 0)
+        if self.two_step:
+            # every slab must launch alike: allocate the two-step buffers now
+            # and fall back to single steps everywhere if any slab (of any
+            # rank) cannot hold them (e.g. 2048^3 over two GPUs)
+            short = 0.0 if all(c.prepare_two_step() for c in self.ctxs) else 1.0
+            if self.halo.allreduce_max(np.array([short]))[0] > 0:
+                self.two_step = False
+                for c in self.ctxs:
+                    c.set_two_step(0)
         return self
 
     def set_measured(self, measured):

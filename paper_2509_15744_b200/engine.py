@@ -438,9 +438,17 @@ class DeviceGrid:
         return out.tolist()
 
     def set_two_step(self, on):
-        """Two time steps per HBM pass (WO_OPT_TWO_STEP; slabs: off until the
-        decomposition enables it on every slab)."""
+        """Two time steps per HBM pass where the grid allows it (fp32 and
+        fp64; WO_OPT_TWO_STEP, default on; slabs: off until the decomposition
+        enables it on every slab)."""
         self._ck(self.L.wo_set_option(self.h, N.WO_OPT_TWO_STEP, int(on)), "wo_set_option")
+
+    def prepare_two_step(self):
+        """Allocate and build the two-step buffers now (wo_prepare_two_step):
+        True when this context will take two-step passes."""
+        ready = ctypes.c_int(0)
+        self._ck(self.L.wo_prepare_two_step(self.h, ctypes.byref(ready)), "wo_prepare_two_step")
+        return bool(ready.value)
 
     def set_plane_part(self, part):
         """Split slab steps: 1 boundary planes, 2 interior (+rotation), 0 whole."""
@@ -488,11 +496,6 @@ class DeviceGrid:
     def set_tma_kernel(self, mode):
         """0/False: never; 1/True: the TMA kernels on whole-tile grids (default)."""
         self._ck(self.L.wo_set_option(self.h, N.WO_OPT_TMA_KERNEL, int(mode)), "wo_set_option")
-
-    def set_two_step(self, mode):
-        """Two time steps per HBM pass where the grid allows it: 0/False off,
-        1/True fp32 grids (default), 2 also fp64 grids."""
-        self._ck(self.L.wo_set_option(self.h, N.WO_OPT_TWO_STEP, int(mode)), "wo_set_option")
 
     def fast_div_active(self):
         return bool(self.L.wo_fast_div_active(self.h))

@@ -49,7 +49,10 @@ namespace wb {
 #define WB_T2_STREAM_STORES 0
 #endif
 #ifndef WB_T2_NEXT_PREFETCH
-#define WB_T2_NEXT_PREFETCH 1
+// L2 prefetch of the next block's first planes (round 1, +1% then); with
+// dataflow-chained passes it costs 1-2% (256^3 / 512^3 / 1024^3 / C5 slab,
+// profiles/dev/cycle53.sh): off
+#define WB_T2_NEXT_PREFETCH 0
 #endif
 #ifndef WB_T2_TIMELINE
 #define WB_T2_TIMELINE 0   // dev: per-CTA start / first data / end times (launch_pair dump)

@@ -60,6 +60,9 @@ namespace wb {
 #ifndef WB_T2_PACKED
 #define WB_T2_PACKED 1
 #endif
+#ifndef WB_T2_POLL_NS
+#define WB_T2_POLL_NS 128   // back-off between polls of a neighbour's completion flag
+#endif
 #ifndef WB_T2_PDL
 #define WB_T2_PDL 1   // programmatic dependent launch: overlap the next pass's start with this tail
 #endif
@@ -403,7 +406,7 @@ step2_kernel_tma(const __grid_constant__ Step2Args<T> a, const __grid_constant__
                 for (;;) {
                     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
                     if (v + 1u >= a.seq) break;
-                    __nanosleep(128);
+                    __nanosleep(WB_T2_POLL_NS);
                 }
             }
         }

@@ -259,3 +259,44 @@ def test_ipc_peer_halo_single_rank_is_inert():
     assert s.peers is None and halo.begin() == []
     halo.close()
     assert s.peers is None
+
+
+class _FakeSlabCtx:
+    """Stands in for a slab DeviceGrid in SlabGradient.upload (no GPU)."""
+
+    def __init__(self, fits):
+        self.fits = fits
+        self.two_step = None
+        self.prepared = False
+
+    def set_material(self, material, dt, gamma_local=None):
+        pass
+
+    def set_two_step(self, on):
+        self.two_step = int(on)
+
+    def prepare_two_step(self):
+        self.prepared = True
+        return self.fits
+
+
+@pytest.mark.parametrize("fits,expect", [((True, True, True), 1), ((True, False, True), 0)])
+def test_slabs_agree_on_two_step_passes(fits, expect):
+    """SlabGradient.upload: every slab prepares its two-step buffers and, if
+    any slab cannot hold them, two-step passes go off on every slab (their
+    peer-store launches must match one for one; capi REQUIREs it)."""
+    from types import SimpleNamespace
+
+    sg = D.SlabGradient.__new__(D.SlabGradient)
+    sg.ctxs = [_FakeSlabCtx(f) for f in fits]
+    sg.halo = D.PeerHalo.__new__(D.PeerHalo)          # peer stores, no wiring needed
+    sg.halo.ctxs = sg.ctxs
+    n0 = 8 * len(fits)
+    sg.all_slabs = sg.slabs = [(8 * i, 8 * i + 8) for i in range(len(fits))]
+    sg.problem = SimpleNamespace(time=SimpleNamespace(dt=1e-9),
+                                 grid=SimpleNamespace(shape=(n0, 16, 64)))
+    sg.material = None
+    sg._shots = []
+    sg.upload()
+    assert sg.two_step == bool(expect)
+    assert all(c.two_step == expect for c in sg.ctxs)

@@ -574,7 +574,7 @@ def run_native(args):
                        "shots_per_gpu": 1, "precision": wl["precision"], "k": wl["k"],
                        "parallelism": "shot-parallel" if world > 1 else "single",
                        "cell_updates_per_step": world * updates,
-                       "l2": "inputs larger than L2 (4 x 67 MB fields = 268 MB > 126 MB)"},
+                       "l2": "inputs larger than L2 (a two-step pass streams 10 x 67 MB fields = 671 MB > 126 MB)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": ("wb::step2_kernel_tma (two fused steps per pass)" if two

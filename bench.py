@@ -55,7 +55,7 @@ sys.path.insert(0, ROOT)
 METRIC = "Gcell-updates/s fwd+adjoint sensitivity (3D, 1/2/4/8 B200); % HBM roofline"
 UNIT = "Gcell-updates/s"
 ITEMSIZE = {"single": 4, "double": 8}
-PROFILE_EVERY = 8      # CUDA-event bracket on every 8th step launch of the timed region
+PROFILE_EVERY = 8      # diagnostic: CUDA events around every 8th launch of one extra evaluation
 
 
 def workload(n=256, n_steps=1024):

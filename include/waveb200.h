@@ -106,10 +106,11 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
  * captured into a CUDA graph on its second occurrence and replayed from then
  * on (launch-bound small grids gain most); 0 = always launch directly. */
 #define WO_OPT_GRAPHS 6
-/* WO_OPT_CLUSTER (default 0): small 2D grids (>= 32 rows, the whole problem
- * within one 16-CTA thread-block cluster's shared memory) run every sweep as
- * ONE cluster-resident launch (fields in distributed shared memory, one
- * cluster barrier per step, identical arithmetic); 0 = step launches. */
+/* WO_OPT_CLUSTER (default 2): small 2D grids (up to 65,536 cells: one
+ * 16-CTA thread-block cluster, 2 x 4 cells per thread) run every sweep as ONE
+ * cluster-resident launch (fields in registers, neighbour rows exchanged
+ * through shared memory / st.async into the cluster peers, identical
+ * arithmetic); 1 = on, 0 = step launches, 2 = auto (fp32 contexts only). */
 #define WO_OPT_CLUSTER 7
 int wo_set_option(wo_ctx* ctx, int option, int value);
 /* Device-resident optimisation loop (fwi.py:178-238 with

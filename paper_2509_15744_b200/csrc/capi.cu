@@ -36,15 +36,34 @@ constexpr int STABILITY_CHECK_INTERVAL = 50;     // solver.py:29
 constexpr double STABILITY_GROWTH_FACTOR = 1e6;  // solver.py:30
 thread_local std::string g_create_error;
 
-// cluster-resident sweeps of small 2D grids (cluster_sweep.cuh): default of
-// WO_OPT_CLUSTER for new contexts; WB_CLUSTER=0/1 overrides (A/B runs)
-constexpr bool CLUSTER_DEFAULT = false;
-bool cluster_default() {
-    static const bool on = [] {
+// cluster-resident sweeps of small 2D grids (cluster_reg.cuh): default of
+// WO_OPT_CLUSTER for new contexts, 2 = auto (fp32 contexts: C1 fp32 27.6 ->
+// 37.4 Gcell-upd/s; fp64 stays on two-step passes, 24.1 vs 22.7);
+// WB_CLUSTER=0/1/2 overrides (A/B runs)
+constexpr int CLUSTER_DEFAULT = 2;
+int cluster_default() {
+    static const int on = [] {
         const char* e = getenv("WB_CLUSTER");
-        return e ? atoi(e) != 0 : CLUSTER_DEFAULT;
+        return e ? atoi(e) : CLUSTER_DEFAULT;
     }();
     return on;
+}
+// which cluster engine: the register-resident one (cluster_reg.cuh) unless
+// WB_CLUSTER_ENGINE=smem asks for the shared-memory one (cluster_sweep.cuh)
+bool cluster_smem_engine() {
+    static const bool smem = [] {
+        const char* e = getenv("WB_CLUSTER_ENGINE");
+        return e && strcmp(e, "smem") == 0;
+    }();
+    return smem;
+}
+// packed pairs per thread row of the register-resident engine (WB_CR_PC=1|2)
+int cluster_reg_pc() {
+    static const int pc = [] {
+        const char* e = getenv("WB_CR_PC");
+        return e && atoi(e) == 1 ? 1 : 2;
+    }();
+    return pc;
 }
 
 }  // namespace
@@ -116,6 +135,7 @@ struct wo_ctx {
     int use_cluster = cluster_default();   // wo_set_option(WO_OPT_CLUSTER)
     int cl_state = 0;                  // cluster sweep engine: 0 unknown, 1 ready, -1 no
     int cl_size = 0, cl_rows = 0;      // CTAs per cluster, rows per CTA
+    int cr_state = 0, cr_size = 0, cr_rows = 0;   // register-resident engine (cluster_reg.cuh)
     double* amp_dev = nullptr;         // source amplitude table of a cluster sweep
     size_t amp_cap = 0;
     char* stage = nullptr;             // fp64 upload staging (persistent)
@@ -1013,12 +1033,51 @@ int t2_sweep_begin(wo_ctx* ctx) {
 // ---- cluster-resident whole sweeps of small 2D grids (cluster_sweep.cuh) ----
 
 
+// support slots a register-resident CTA may need (even, for the T array after them)
+int64_t cluster_reg_sup_cap(const wo_ctx* ctx, int rows) {
+    const int64_t cap = std::min<int64_t>(ctx->n_sup, (int64_t)rows * ctx->kn2);
+    return cap + (cap & 1);
+}
+
+// Cluster engine of a sweep: 2 register-resident (cluster_reg.cuh: up to 16
+// CTAs x 1024 threads x 2x2 cells = 65,536 cells), 1 shared-memory
+// (cluster_sweep.cuh, WB_CLUSTER_ENGINE=smem), 0 none.
 template <typename T>
-bool cluster_ready(wo_ctx* ctx) {
+int cluster_engine(wo_ctx* ctx) {
+    const bool on = ctx->use_cluster == 1 || (ctx->use_cluster == 2 && sizeof(T) == 4);
+    const bool shape_ok = on && ctx->ndim == 2 && ctx->kn0 == 1 && !ctx->has_lo &&
+                          !ctx->has_hi;
+    if (ctx->cr_state == 0) {
+        ctx->cr_state = -1;
+        if (shape_ok && !cluster_smem_engine()) {
+            int rows = (ctx->kn1 + CS_MAX_CLUSTER - 1) / CS_MAX_CLUSTER;
+            rows += rows & 1;
+            const int cl = (ctx->kn1 + rows - 1) / rows;
+            const int pc = cluster_reg_pc();
+            if (cr_txn(ctx->kn2, pc) * (rows / 2) <= CR_THREADS / pc &&
+                cluster_reg_smem<T>(rows, ctx->kn2, 0, pc) + 1024 <= 227 * 1024) {
+                ClusterSweepArgs<T> a{};
+                a.reg = 1;
+                a.pc = pc;
+                a.rows = rows;
+                a.n2 = ctx->kn2;
+                if (launch_cluster_sweep<T>(RHO_SCALED, true, a, cl, ctx->stream, true) ==
+                    cudaSuccess) {
+                    ctx->cr_state = 1;
+                    ctx->cr_size = cl;
+                    ctx->cr_rows = rows;
+                }
+            }
+            (void)cudaGetLastError();
+        }
+    }
+    if (ctx->cr_state == 1 &&
+        cluster_reg_smem<T>(ctx->cr_rows, ctx->kn2, cluster_reg_sup_cap(ctx, ctx->cr_rows),
+                            cluster_reg_pc()) + 1024 <= 227 * 1024)
+        return 2;
     if (ctx->cl_state == 0) {
         ctx->cl_state = -1;
-        if (ctx->use_cluster && ctx->ndim == 2 && ctx->kn0 == 1 && !ctx->has_lo &&
-            !ctx->has_hi && ctx->kn1 >= 2 * CS_MAX_CLUSTER) {
+        if (shape_ok && cluster_smem_engine() && ctx->kn1 >= 2 * CS_MAX_CLUSTER) {
             const int rows = (ctx->kn1 + CS_MAX_CLUSTER - 1) / CS_MAX_CLUSTER;
             const int cl = (ctx->kn1 + rows - 1) / rows;
             if (cluster_sweep_smem<T>(rows, ctx->kn2) + 1024 <= 227 * 1024 &&
@@ -1036,7 +1095,11 @@ bool cluster_ready(wo_ctx* ctx) {
             (void)cudaGetLastError();
         }
     }
-    return ctx->cl_state == 1;
+    return ctx->cl_state == 1 ? 1 : 0;
+}
+template <typename T>
+bool cluster_ready(wo_ctx* ctx) {
+    return cluster_engine<T>(ctx) != 0;
 }
 
 // steps n_first, n_first +- 1, ... (count of them) of an N-step sweep in one
@@ -1046,9 +1109,15 @@ int run_cluster_sweep(wo_ctx* ctx, int backward, int64_t N, int64_t n_first, int
                       int ns, const long long* sidx, const double* const* amp_rows, bool acc,
                       double sdt, int sup_mode) {
     ClusterSweepArgs<T> a{};
+    const int engine = cluster_engine<T>(ctx);
+    REQUIRE(engine != 0, "no cluster engine for this context");
+    a.reg = engine == 2;
+    a.pc = cluster_reg_pc();
     a.n1 = ctx->kn1;
     a.n2 = ctx->kn2;
-    a.rows = ctx->cl_rows;
+    a.rows = a.reg ? ctx->cr_rows : ctx->cl_rows;
+    a.sup_cap = a.reg ? (int)cluster_reg_sup_cap(ctx, a.rows) : 0;
+    a.negz2 = 0x8000000080000000ull;
     a.backward = backward;
     a.n_first = (int)n_first;
     a.n_count = (int)count;
@@ -1088,8 +1157,9 @@ int run_cluster_sweep(wo_ctx* ctx, int backward, int64_t N, int64_t n_first, int
     a.store = reinterpret_cast<T*>(ctx->store);
     a.maxslots = reinterpret_cast<typename FTraits<T>::Bits*>(ctx->maxslots);
     prof_begin(ctx, 0);
-    const cudaError_t e = launch_cluster_sweep<T>(ctx->flavor, acc, a, ctx->cl_size, ctx->stream,
-                                                  false);
+    const cudaError_t e = launch_cluster_sweep<T>(ctx->flavor, acc, a,
+                                                  a.reg ? ctx->cr_size : ctx->cl_size,
+                                                  ctx->stream, false);
     prof_end(ctx);
     ctx->launches++;
     ctx->step_launches++;
@@ -2221,8 +2291,9 @@ int wo_set_option(wo_ctx* ctx, int option, int value) {
                 option == WO_OPT_CLUSTER,
             "unknown option");
     if (option == WO_OPT_CLUSTER) {
-        ctx->use_cluster = value != 0;
+        ctx->use_cluster = value == 2 ? 2 : value != 0;
         ctx->cl_state = 0;   // probe again on the next sweep
+        ctx->cr_state = 0;
         return WO_OK;
     }
     if (option == WO_OPT_GRAPHS) {

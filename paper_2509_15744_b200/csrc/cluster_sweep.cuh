@@ -55,6 +55,11 @@ template <typename T> struct ClusterSweepArgs {
     const int* sup_prefix;
     T* store;                   // [N][n_sup]
     typename FTraits<T>::Bits* maxslots;
+    // register-resident engine (cluster_reg.cuh)
+    int reg;                    // 1: cluster_reg_kernel
+    int pc;                     // its packed pairs per thread row (1 or 2)
+    int sup_cap;                // support slots per CTA (even)
+    unsigned long long negz2;   // fp32 (-0, -0) addend of the exact packed products
 };
 
 template <typename T>

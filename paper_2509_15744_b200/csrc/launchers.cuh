@@ -7,7 +7,7 @@
 
 #include <cuda_runtime.h>
 
-#include "cluster_sweep.cuh"
+#include "cluster_reg.cuh"
 #include "step2_kernel.cuh"
 #include "step_kernel.cuh"
 #include "tma_common.cuh"

@@ -424,8 +424,10 @@ class DeviceGrid:
         self._ck(self.L.wo_set_option(self.h, N.WO_OPT_GRAPHS, int(bool(on))), "wo_set_option")
 
     def set_cluster(self, on):
-        """Cluster-resident whole sweeps of small 2D grids (WO_OPT_CLUSTER)."""
-        self._ck(self.L.wo_set_option(self.h, N.WO_OPT_CLUSTER, int(bool(on))), "wo_set_option")
+        """Cluster-resident whole sweeps of small 2D grids (WO_OPT_CLUSTER):
+        True / False, or None for the default (fp32 contexts only)."""
+        v = 2 if on is None else int(bool(on))
+        self._ck(self.L.wo_set_option(self.h, N.WO_OPT_CLUSTER, v), "wo_set_option")
 
     def slab_abort(self):
         """Release streams waiting on this slab's peer flags (wo_slab_abort)."""

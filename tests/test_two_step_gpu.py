@@ -87,6 +87,7 @@ def test_two_step_gradient_bitexact(W, shape, flavor, prec, n_steps):
     problem, mat, omat, dt, shots = _problem(W, shape, flavor, n_steps, sum(shape) + n_steps)
     cfg = W.SuperpositionConfig(k=1e13 if flavor == "rho_scaled" else 1e3, precision=prec)
     ctx = engine.get_context(problem.grid, W.precision_dtype(prec))
+    ctx.set_cluster(False)   # the step kernels themselves (small 2D fp32 grids default to the cluster engine)
     out = {}
     for two in (True, False):
         ctx.set_two_step(2 if two else 0)   # 2: fp64 grids too
@@ -98,6 +99,7 @@ def test_two_step_gradient_bitexact(W, shape, flavor, prec, n_steps):
         if not two:
             assert pairs == 0
     ctx.set_two_step(1)
+    ctx.set_cluster(None)
     assert bits_equal(out[True].gradient, out[False].gradient)
     cost, grad, _ = O.gradient_superposed(omat, dt, n_steps, shots, cfg.k, prec)
     assert bits_equal(out[True].gradient, grad)
@@ -115,6 +117,7 @@ def test_two_step_forward_traces_and_window(W, shape, dn):
     problem, mat, omat, dt, shots = _problem(W, shape, "rho_scaled", 73, 3)
     ctx = engine.get_context(problem.grid, dtype)
     ctx.set_two_step(2)
+    ctx.set_cluster(False)
     try:
         ctx.reset_stats()
         res = W.run_forward(mat, problem.time, problem.sources,
@@ -122,6 +125,7 @@ def test_two_step_forward_traces_and_window(W, shape, dn):
         assert ctx.stats()["pair_launches"] > 0
     finally:
         ctx.set_two_step(1)
+        ctx.set_cluster(None)
     sup = np.array([problem.grid.flat_index(n) for n in problem.sensors.nodes], dtype=np.int64)
     osrc = [s for s, _ in shots]
     u_prev, u_cur, traces, _, peak = O.run_forward(omat, dt, 73, osrc, sensor_idx=sup,
@@ -267,6 +271,7 @@ def test_two_step_random_cases(W, seed):
 
     ctx = engine.get_context(grid, W.precision_dtype(prec))
     ctx.set_two_step(2)
+    ctx.set_cluster(False)
     try:
         ctx.reset_stats()
         k = 1e13 if flavor == "rho_scaled" else 1e3
@@ -274,6 +279,7 @@ def test_two_step_random_cases(W, seed):
         assert ctx.stats()["pair_launches"] > 0
     finally:
         ctx.set_two_step(1)
+        ctx.set_cluster(None)
     support = np.array([grid.flat_index(n) for n in sens], dtype=np.int64)
     shots = [(O.Source(node, amp, 0.05 / dt, 2), O.FwiShot(support, meas[0], dt))]
     cost, grad, _ = O.gradient_superposed(omat, dt, n_steps, shots, k, prec)
@@ -283,7 +289,8 @@ def test_two_step_random_cases(W, seed):
 
 # ------------------------------------------------ sweep graphs (WO_OPT_GRAPHS)
 @pytest.mark.parametrize("shape", [(40, 8, 64), (64, 128), (33, 64)])
-def test_sweep_graph_replay_matches_direct_launches(W, shape):
+@pytest.mark.parametrize("cluster", [False, None])
+def test_sweep_graph_replay_matches_direct_launches(W, shape, cluster):
     """Repeated evaluations replay captured sweep graphs; a new gamma (same
     scalars: data, graph kept), new measured data, a new k and a new source
     frequency (new key: recapture) must all give the direct-launch bits."""
@@ -294,6 +301,7 @@ def test_sweep_graph_replay_matches_direct_launches(W, shape):
                            sources=problem.sources[:1], sensors=problem.sensors,
                            measured=problem.measured[:1])
     ctx = engine.get_context(problem.grid, np.float32)
+    ctx.set_cluster(cluster)   # None: the default (2D: the cluster engine, no graphs)
     cfg = W.SuperpositionConfig(k=1e13, precision="single")
 
     def both(prob, m, c):
@@ -318,6 +326,7 @@ def test_sweep_graph_replay_matches_direct_launches(W, shape):
                                             frequency=s0.frequency * 1.3, cycles=2)],
                       sensors=problem.sensors, measured=problem.measured)
     both(p3, mat2, cfg)
+    ctx.set_cluster(None)
 
 
 @pytest.mark.parametrize("knob", [("WB_T2_NZ", "1"), ("WB_T2_NZ", "2"), ("WB_T2_NZ", "3"),
@@ -374,7 +383,7 @@ def test_cluster_sweep_engine_bitwise(W, shape, prec):
         ctx.set_cluster(False)
         off = W.gradient_superposed(problem, mat, cfg)
     finally:
-        ctx.set_cluster(True)
+        ctx.set_cluster(None)
     assert launches_on == 2        # one launch per sweep
     assert bits_equal(on.gradient, off.gradient)
     assert on.cost == off.cost

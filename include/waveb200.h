@@ -277,6 +277,10 @@ int wo_ipc_open(wo_ctx* ctx, const void* handle, int64_t offset, void** ptr);
 int wo_sweep_adjoint_reference(wo_ctx* ctx, int64_t n_steps, double dt, int64_t* fail_step,
                                double* fail_max);
 int wo_free_history(wo_ctx* ctx);
+/* Levels u^{n_first} .. u^{n_first+n_count-1} of the history recorded by a
+ * WO_FWD_HISTORY forward sweep, C order, to host memory (run_forward's
+ * full_history / on_step: solver.py:306-336 in one fused sweep). */
+int wo_get_history(wo_ctx* ctx, int64_t n_first, int64_t n_count, void* out);
 
 /* Per-step shot cost and compact adjoint store from the recorded support
  * values (fwi.py:57-63, tato.py:154-163, gradients.py:231-239, 263):

@@ -27,7 +27,7 @@ EXPORTS = (
     "wo_zero_accumulator", "wo_get_accumulator", "wo_set_accumulator", "wo_sweep_forward",
     "wo_shot_misfit", "wo_get_store", "wo_sweep_backward", "wo_get_gradient", "wo_step",
     "wo_apply_step", "wo_apply_kernel_increment", "wo_set_profiling", "wo_stats",
-    "wo_reset_stats", "wo_device_bytes", "wo_field_buffers", "wo_slab_abort", "wo_slab_state", "wo_prepare_two_step", "wo_sweep_adjoint_reference", "wo_free_history",
+    "wo_reset_stats", "wo_device_bytes", "wo_field_buffers", "wo_slab_abort", "wo_slab_state", "wo_prepare_two_step", "wo_sweep_adjoint_reference", "wo_free_history", "wo_get_history",
     "wo_design_filter", "wo_design_project", "wo_design_chain", "wo_timer_mark",
     "wo_timer_elapsed", "wo_synchronize", "wo_accumulator_ptr", "wo_set_option",
     "wo_fast_div_active", "wo_sweep_forward_range", "wo_sweep_backward_range",
@@ -86,6 +86,7 @@ _SIGS = {
     "wo_prepare_two_step": (c_int, [c_vp, ctypes.POINTER(c_int)]),
     "wo_sweep_adjoint_reference": (c_int, [c_vp, c_i64, c_dbl, P_i64, P_dbl]),
     "wo_free_history": (c_int, [c_vp]),
+    "wo_get_history": (c_int, [c_vp, c_i64, c_i64, c_vp]),
     "wo_design_filter": (c_int, [c_int, P_i64, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_int]),
     "wo_design_project": (c_int, [c_i64, c_vp, c_dbl, c_dbl, c_dbl, c_dbl, c_vp, c_vp, c_int]),
     "wo_design_chain": (c_int, [c_int, P_i64, c_vp, c_vp, c_dbl, c_dbl, c_dbl, c_vp, c_int,

@@ -2784,6 +2784,16 @@ int wo_sweep_adjoint_reference(wo_ctx* ctx, int64_t n_steps, double dt, int64_t*
     return DISPATCH(ctx, sweep_adjoint_reference_t, ctx, n_steps, dt, fail_step, fail_max);
 }
 
+int wo_get_history(wo_ctx* ctx, int64_t n_first, int64_t n_count, void* out) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    const size_t fb = ctx->field_bytes();
+    REQUIRE(n_first >= 0 && n_count >= 0 &&
+                (size_t)(n_first + n_count) * fb <= ctx->hist_bytes,
+            "history levels out of range (record them with WO_FWD_HISTORY)");
+    return download_field(ctx, out, ctx->hist + (size_t)n_first * fb, (size_t)n_count * fb);
+}
+
 int wo_free_history(wo_ctx* ctx) {
     int rc = check_ctx(ctx);
     if (rc) return rc;

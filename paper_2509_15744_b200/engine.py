@@ -469,6 +469,14 @@ class DeviceGrid:
             raise SolverInstabilityError(int(fstep.value), fmax.value)
         self._ck(rc, "wo_sweep_adjoint_reference")
 
+    def get_history(self, n_first, out):
+        """Recorded levels u^{n_first} .. into out ([k] + grid shape, C order)."""
+        assert out.dtype == self.dtype and out.flags.c_contiguous
+        k = out.shape[0]
+        self._ck(self.L.wo_get_history(self.h, int(n_first), int(k), N.ptr(out)),
+                 "wo_get_history")
+        return out
+
     def free_history(self):
         self._ck(self.L.wo_free_history(self.h), "wo_free_history")
 

@@ -19,6 +19,9 @@ from .grids import ConfigError, Grid, MaterialModel, SensorArray, SourceSpec, Ti
 STABILITY_CHECK_INTERVAL = 50            # solver.py:29
 STABILITY_GROWTH_FACTOR = 1e6            # solver.py:30
 DEFAULT_HISTORY_BUDGET = 4 * 1024**3     # solver.py:31
+MAX_KERNEL_SOURCES = 8                   # source nodes a recording sweep injects in-kernel
+DEVICE_HISTORY_CAP = 16 * 1024**3        # on_step without full_history: device levels recorded
+HISTORY_CHUNK_BYTES = 256 * 1024**2      # on_step levels read back per host copy
 
 __all__ = [
     "ResourceBudgetError", "SolverInstabilityError", "SolverWindow", "ForwardResult",
@@ -123,9 +126,13 @@ def run_forward(material: MaterialModel, time: TimeConfig, sources,
                 on_step=None) -> ForwardResult:
     """N steps from u^0 = u^1 = 0 with trace recording (solver.py:282-340).
 
-    Trace entry j records level u^j (entry 0 stays 0).  The plain path is
-    one native sweep; recorder_mode='full_history' or an on_step callback
-    stream every level back to the host."""
+    Trace entry j records level u^j (entry 0 stays 0).  One native sweep;
+    with recorder_mode='full_history' or an on_step callback the sweep also
+    records every level on the device and the levels come back in bulk
+    afterwards (the callback runs after the sweep, in step order; a sweep that
+    fails its stability check raises before any callback).  More than 8
+    source nodes, or an on_step history beyond DEVICE_HISTORY_CAP, step
+    level by level with one read-back per step."""
     grid = material.grid
     n_steps = time.n_steps
     for s in sources:
@@ -153,17 +160,38 @@ def run_forward(material: MaterialModel, time: TimeConfig, sources,
     traces = None
     sensor_idx = sensors.flat_indices(grid) if sensors is not None else None
 
-    if history is None and on_step is None:
+    level_bytes = grid.n_nodes * dtype.itemsize
+    fused_levels = (len(set(src_flat.tolist())) <= MAX_KERNEL_SOURCES and
+                    (history is not None or (n_steps + 1) * level_bytes <= DEVICE_HISTORY_CAP))
+    if (history is None and on_step is None) or fused_levels:
+        # one native sweep; with a history / callback the levels are recorded
+        # on the device during the sweep (WO_FWD_HISTORY) and read back in
+        # bulk afterwards instead of one step launch + one D2H per step
         if sensor_idx is not None:
             order = ctx.set_support(sensor_idx)
         else:
             ctx.clear_support()
-        peak = ctx.sweep_forward(n_steps, src_flat, amp, accumulate=False, dt=time.dt,
-                                 scale=scale)
-        if sensor_idx is not None:
-            store = ctx.get_store(n_steps)            # [N][n_sup], device order
-            traces = np.empty((len(sensor_idx), n_steps), dtype=dtype)
-            traces[order] = store.T
+        record = history is not None or on_step is not None
+        try:
+            peak = ctx.sweep_forward(n_steps, src_flat, amp, accumulate=False, dt=time.dt,
+                                     scale=scale, history=record)
+            if sensor_idx is not None:
+                store = ctx.get_store(n_steps)            # [N][n_sup], device order
+                traces = np.empty((len(sensor_idx), n_steps), dtype=dtype)
+                traces[order] = store.T
+            if history is not None:
+                ctx.get_history(0, history)
+            if on_step is not None:
+                chunk = max(1, min(n_steps - 1, HISTORY_CHUNK_BYTES // level_bytes))
+                for n0 in range(1, n_steps, chunk):
+                    k = min(chunk, n_steps - n0)
+                    levels = (history[n0 + 1:n0 + 1 + k] if history is not None else
+                              ctx.get_history(n0 + 1, np.empty((k,) + grid.shape, dtype)))
+                    for i in range(k):
+                        on_step(n0 + i, levels[i])
+        finally:
+            if record:
+                ctx.free_history()
         up, uc = ctx.get_window()
     else:
         traces = (np.zeros((len(sensor_idx), n_steps), dtype=dtype)

@@ -427,3 +427,50 @@ def test_superposed_matches_reference_engine(W, golden):
     sup = W.gradient_superposed(problem, mat, W.SuperpositionConfig(k=c["k"]))
     ref = W.gradient_reference(problem, mat)
     assert W.rel_mse(sup.gradient, ref.gradient) < 0.05
+
+
+# ------------------------------------------ run_forward history / on_step
+@pytest.mark.parametrize("shape", [(37, 29), (12, 16, 64)])
+@pytest.mark.parametrize("dn", ["f32", "f64"])
+@pytest.mark.parametrize("fused", [True, False])
+def test_run_forward_full_history_and_on_step(W, shape, dn, fused, monkeypatch):
+    """recorder_mode='full_history' and on_step (solver.py:306-336): every
+    level u^0..u^N and every callback (n, u^{n+1}) bit-exact vs the oracle's
+    run_forward history, through the fused recording sweep (levels read back
+    in chunks) and through the per-step fallback."""
+    from paper_2509_15744_b200 import solver
+
+    if not fused:   # more nodes than a recording sweep injects in-kernel: per step
+        monkeypatch.setattr(solver, "MAX_KERNEL_SOURCES", 0)
+    monkeypatch.setattr(solver, "HISTORY_CHUNK_BYTES", 7 * int(np.prod(shape)) * 8)
+    dx, n_steps = 2e-4, 57
+    dt = 0.45 * dx / 6000.0 / np.sqrt(len(shape))
+    grid = W.build_grid(shape, dx)
+    rng = np.random.default_rng(len(shape) + n_steps)
+    gamma = rng.uniform(0.3, 1.0, size=shape)
+    mat = W.MaterialModel.rho_scaled(gamma, grid, rho0=2700.0, c0=6000.0)
+    node = tuple(n // 2 for n in shape)
+    src = W.SourceSpec(node=node, amplitude=1e12, frequency=3e6, cycles=2)
+    sens = [tuple(max(0, c - 3) for c in node), tuple(n - 1 for n in shape)]
+    time = W.TimeConfig(n_steps, dt)
+    seen = []
+    res = W.run_forward(mat, time, [src], W.SensorArray(nodes=sens),
+                        recorder_mode="full_history", dtype=_dt(dn),
+                        on_step=lambda n, u: seen.append((n, u.copy())))
+    omat = O.Material("rho_scaled", gamma, dx, rho0=2700.0, c0=6000.0)
+    sidx = np.array([grid.flat_index(s) for s in sens], dtype=np.int64)
+    up, uc, tr, hist, _ = O.run_forward(omat, dt, n_steps, [O.Source(node, 1e12, 3e6, 2)], sidx,
+                                        dtype=_dt(dn), full_history=True)
+    assert bits_equal(res.history, hist)
+    assert bits_equal(res.traces, tr)
+    assert bits_equal(res.window.u_cur, uc) and bits_equal(res.window.u_prev, up)
+    assert [n for n, _ in seen] == list(range(1, n_steps))
+    for n, u in seen:
+        assert bits_equal(u, hist[n + 1])
+    # on_step alone (no host history): levels straight from the device history
+    seen2 = []
+    W.run_forward(mat, time, [src], None, dtype=_dt(dn),
+                  on_step=lambda n, u: seen2.append((n, u.copy())))
+    assert len(seen2) == n_steps - 1
+    for n, u in seen2:
+        assert bits_equal(u, hist[n + 1])

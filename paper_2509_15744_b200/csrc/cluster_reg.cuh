@@ -48,13 +48,13 @@ template <> struct CR2<float> {
         return r;
     }
     __device__ static __forceinline__ float lo(V v) {
-        float a, b;
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+        float a;
+        asm("{\n.reg .f32 t;\nmov.b64 {%0, t}, %1;\n}" : "=f"(a) : "l"(v));
         return a;
     }
     __device__ static __forceinline__ float hi(V v) {
-        float a, b;
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+        float b;
+        asm("{\n.reg .f32 t;\nmov.b64 {t, %0}, %1;\n}" : "=f"(b) : "l"(v));
         return b;
     }
     __device__ static __forceinline__ V add(V a, V b) {
@@ -132,19 +132,6 @@ template <> struct CR2<double> {
             : "memory");
     }
 };
-
-// wait for a phase of a local mbarrier that cluster peers complete (st.async)
-__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* bar, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
 
 // one element global -> shared, asynchronous (LDGSTS)
 template <typename E> __device__ __forceinline__ void cp_async_el(E* dst, const E* src) {
@@ -394,7 +381,7 @@ __global__ void __launch_bounds__(CR_THREADS / PC, 1) cluster_reg_kernel(const C
         }
         // ---- 2: plane n visible in the CTA, the neighbours' rows arrived ----
         __syncthreads();
-        if (recv) mbar_wait_cluster(MB + b, (it >> 1) & 1);
+        if (recv) mbar_wait(MB + b, (it >> 1) & 1);
         // neighbours of pair p in row i: rows from registers / X, columns
         // from registers / X, mirrored at the grid edge
         auto nbrs = [&](int i, int p, V& ujm, V& ujp, V& ukm, V& ukp) {

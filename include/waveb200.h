@@ -110,7 +110,7 @@ int wo_set_material(wo_ctx* ctx, int flavor, const double* gamma, double rho0, d
  * 16-CTA thread-block cluster, 2 x 4 cells per thread) run every sweep as ONE
  * cluster-resident launch (fields in registers, neighbour rows exchanged
  * through shared memory / st.async into the cluster peers, identical
- * arithmetic); 1 = on, 0 = step launches, 2 = auto (fp32 contexts only). */
+ * arithmetic); 1 = on, 0 = step launches, 2 = the default (on). */
 #define WO_OPT_CLUSTER 7
 int wo_set_option(wo_ctx* ctx, int option, int value);
 /* Device-resident optimisation loop (fwi.py:178-238 with

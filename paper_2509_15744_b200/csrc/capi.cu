@@ -37,9 +37,9 @@ constexpr double STABILITY_GROWTH_FACTOR = 1e6;  // solver.py:30
 thread_local std::string g_create_error;
 
 // cluster-resident sweeps of small 2D grids (cluster_reg.cuh): default of
-// WO_OPT_CLUSTER for new contexts, 2 = auto (fp32 contexts: C1 fp32 27.6 ->
-// 37.4 Gcell-upd/s; fp64 stays on two-step passes, 24.1 vs 22.7);
-// WB_CLUSTER=0/1/2 overrides (A/B runs)
+// WO_OPT_CLUSTER for new contexts, 2 = the default (on: C1 fp32 27.6 -> 42.3,
+// fp64 24.1 -> 26.7 Gcell-upd/s against two-step passes); WB_CLUSTER=0/1/2
+// overrides (A/B runs)
 constexpr int CLUSTER_DEFAULT = 2;
 int cluster_default() {
     static const int on = [] {
@@ -1044,7 +1044,7 @@ int64_t cluster_reg_sup_cap(const wo_ctx* ctx, int rows) {
 // (cluster_sweep.cuh, WB_CLUSTER_ENGINE=smem), 0 none.
 template <typename T>
 int cluster_engine(wo_ctx* ctx) {
-    const bool on = ctx->use_cluster == 1 || (ctx->use_cluster == 2 && sizeof(T) == 4);
+    const bool on = ctx->use_cluster != 0;
     const bool shape_ok = on && ctx->ndim == 2 && ctx->kn0 == 1 && !ctx->has_lo &&
                           !ctx->has_hi;
     if (ctx->cr_state == 0) {

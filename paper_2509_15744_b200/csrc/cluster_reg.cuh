@@ -317,17 +317,20 @@ __global__ void __launch_bounds__(CR_THREADS / PC, 1) cluster_reg_kernel(const C
     const int oa = (r0 + 1) * XW + 2 + c0, ob = oa + XW;
     cs_cluster_sync();   // every mbarrier initialised before the first push
 
-    // pairs (bit i * PC + p) holding a source or a support cell: their kernel
-    // increment waits for the injections (step 4); all others run inline
+    // pairs (bit i * PC + p) with an injection (a source, or an adjoint
+    // support cell): injected right after their stencil, before the kernel
+    // increment; support cells of a gathering sweep only store their u^n
+    const bool inject = a.sup_mode == SUP_INJECT;
+    const unsigned gmask = inject ? 0u : smask;
     unsigned pmask = 0;
 #pragma unroll
     for (int e = 0; e < 2 * CW; ++e)
-        if ((smask >> e) & 1u) pmask |= 1u << (e / CW * PC + (e % CW) / 2);
+        if (inject && ((smask >> e) & 1u)) pmask |= 1u << (e / CW * PC + (e % CW) / 2);
     for (unsigned bb = tsrc; bb; bb &= bb - 1) {
         const int q = __ffs(bb) - 1;
         pmask |= 1u << ((a.src_j[q] - ja) * PC + (a.src_k[q] - c0) / 2);
     }
-    const bool special = pmask != 0;
+    const bool special = (pmask | gmask) != 0;
     // opaque to the compiler, so it stays in a register instead of being
     // rematerialised (S2R SR_CgaCtaId + LEA) at every use
     unsigned xs0, mt0;
@@ -382,6 +385,19 @@ __global__ void __launch_bounds__(CR_THREADS / PC, 1) cluster_reg_kernel(const C
         // ---- 2: plane n visible in the CTA, the neighbours' rows arrived ----
         __syncthreads();
         if (recv) mbar_wait(MB + b, (it >> 1) & 1);
+        if (special) {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            if (gmask) {   // trace entries n = u^n (gradients.py:237)
+                T* srow = a.store + (long long)n * a.n_sup;
+                int s0 = sbase;
+#pragma unroll
+                for (int e = 0; e < 2 * CW; ++e)
+                    if ((gmask >> e) & 1u) {
+                        const V u = uc[e / CW][(e % CW) / 2];
+                        srow[SQ[s0++]] = (e & 1) ? O::hi(u) : O::lo(u);
+                    }
+            }
+        }
         // neighbours of pair p in row i: rows from registers / X, columns
         // from registers / X, mirrored at the grid edge
         auto nbrs = [&](int i, int p, V& ujm, V& ujp, V& ukm, V& ukp) {
@@ -414,8 +430,8 @@ __global__ void __launch_bounds__(CR_THREADS / PC, 1) cluster_reg_kernel(const C
                                  O::mul(cgv, O::add(O::mul(gj, gj, nz), O::mul(gk, gk, nz)), nz));
             ac[i][p] = O::add(ac[i][p], O::mul(sdv, inc, nz));
         };
-        // ---- 3: stencil of the 2 x CW cells (kernels.py:30-44); the kernel
-        //      increment right away unless the block injects (then after 4) ----
+        // ---- 3: stencil of the 2 x CW cells (kernels.py:30-44), injections,
+        //      kernel increment ----
         V nu[2][PC];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
@@ -436,17 +452,8 @@ __global__ void __launch_bounds__(CR_THREADS / PC, 1) cluster_reg_kernel(const C
                 s = O::add(s, O::mul(O::sub(ukp, u), mt(4 * PC + i * PC + p, wkr[i][p]), nz));
                 s = O::sub(s, O::mul(O::sub(u, ukm), mt(2 * PC + i * PC + p, wkl[i][p]), nz));
                 nu[i][p] = O::add(O::sub(O::add(u, u), up[i][p]), O::mul(mt(i * PC + p, co[i][p]), s, nz));
-                if (ACC && !((pmask >> (i * PC + p)) & 1u)) kinc(i, p, nu[i][p], ujm, ujp, ukm, ukp);
-            }
-        // ---- 4: nodal sources, then the support (solver.py:167-170), per cell ----
-        if (special) {
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            T* srow = a.store + (long long)n * a.n_sup;
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-                for (int p = 0; p < PC; ++p) {
-                    if (!((pmask >> (i * PC + p)) & 1u)) continue;
+                if ((pmask >> (i * PC + p)) & 1u) {
+                    // nodal sources, then the support (solver.py:167-170), per cell
                     T v[2] = {O::lo(nu[i][p]), O::hi(nu[i][p])};
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
@@ -455,22 +462,15 @@ __global__ void __launch_bounds__(CR_THREADS / PC, 1) cluster_reg_kernel(const C
                             const int q = __ffs(bb) - 1;
                             if (a.src_j[q] == j && a.src_k[q] == k) v[h] = v[h] + SRCFC[q] * (T)SAMP[q];
                         }
-                        if ((smask >> e) & 1u) {
+                        if (inject && ((smask >> e) & 1u)) {   // adjoint force (gradients.py:268)
                             const int s0 = sbase + __popc(smask & ((1u << e) - 1u));
-                            if (a.sup_mode == SUP_GATHER)   // trace entry n = u^n
-                                srow[SQ[s0]] = h ? O::hi(uc[i][p]) : O::lo(uc[i][p]);
-                            else
-                                v[h] = v[h] + SFC[s0] * SFV[s0];
+                            v[h] = v[h] + SFC[s0] * SFV[s0];
                         }
                     }
                     nu[i][p] = O::mk(v[0], v[1]);
-                    if (ACC) {   // neighbours again (X still holds plane n)
-                        V ujm, ujp, ukm, ukp;
-                        nbrs(i, p, ujm, ujp, ukm, ukp);
-                        kinc(i, p, nu[i][p], ujm, ujp, ukm, ukp);
-                    }
                 }
-        }
+                if (ACC) kinc(i, p, nu[i][p], ujm, ujp, ukm, ukp);
+            }
         if (n % 50 == 0 || n == nlast) {   // stability max (solver.py:180-186), block-uniform
 #pragma unroll
             for (int i = 0; i < 2; ++i)

@@ -425,7 +425,7 @@ class DeviceGrid:
 
     def set_cluster(self, on):
         """Cluster-resident whole sweeps of small 2D grids (WO_OPT_CLUSTER):
-        True / False, or None for the default (fp32 contexts only)."""
+        True / False, or None for the default (on)."""
         v = 2 if on is None else int(bool(on))
         self._ck(self.L.wo_set_option(self.h, N.WO_OPT_CLUSTER, v), "wo_set_option")
 

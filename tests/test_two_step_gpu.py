@@ -369,7 +369,10 @@ def test_cluster_sweep_engine_bitwise(W, shape, prec):
     src = W.SourceSpec(node=(shape[0] // 2 + 1, shape[1] // 3), amplitude=1e12, frequency=1.5e6,
                        cycles=2)
     nodes = sorted({(i, j) for i in (0, shape[0] // 4, shape[0] - 1)
-                    for j in (0, shape[1] // 2, shape[1] - 1)})
+                    for j in (0, shape[1] // 2, shape[1] - 1)}
+                   # a sensor in the source's packed pair: the forward sweep
+                   # only gathers there, the backward sweep injects both
+                   | {(src.node[0], src.node[1] ^ 1)})
     meas = rng.normal(scale=1e-9, size=(1, len(nodes), n_steps))
     problem = W.FwiProblem(grid=grid, time=W.TimeConfig(n_steps, dt), material=mat,
                            sources=[src], sensors=W.SensorArray(nodes=nodes), measured=meas)
@@ -380,6 +383,8 @@ def test_cluster_sweep_engine_bitwise(W, shape, prec):
         ctx.reset_stats()
         on = W.gradient_superposed(problem, mat, cfg)
         launches_on = ctx.stats()["step_launches"]
+        again = W.gradient_superposed(problem, mat, cfg)   # shared memory left by a backward sweep
+        assert bits_equal(again.gradient, on.gradient) and again.cost == on.cost
         ctx.set_cluster(False)
         off = W.gradient_superposed(problem, mat, cfg)
     finally:

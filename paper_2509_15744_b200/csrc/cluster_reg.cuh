@@ -1,33 +1,34 @@
 // Register-resident whole sweeps of small 2D grids: one thread-block cluster
-// of up to 16 CTAs, every field in REGISTERS, one cluster barrier per step.
+// of up to 16 CTAs runs all N steps of a sweep in ONE launch, every field in
+// registers.
 //
 // The first cluster engine (cluster_sweep.cuh) kept the window, coef, the
 // faces and the accumulator in shared memory: ~14 shared-memory accesses and
 // a scalar, branchy stencil per cell left it at ~4.7 us per step for C1
 // (2D 256^2, N = 3200), slower than 148-SM two-step launches.
-// Here thread t of CTA r owns a 2 x 2 block of cells (rows r0, r0+1 of the
-// CTA's R rows, columns c0, c0+1) and keeps u^{n-1}, u^n and the accumulator
-// of its four cells in registers as packed pairs (fp32: one f32x2 register
-// per row, FADD2 / FFMA2; fp64: two doubles), coef and the five face weights
-// in registers (fp32) or in a thread-major shared-memory table (fp64, which
-// has no room for them at 64 registers per thread).  Per step:
-//   1. publish u^n of the own 2 x 2 block into the exchange plane X[n & 1]
-//      (two 8/16-byte stores), and prefetch the step's adjoint forces /
-//      source amplitudes into registers (their global loads overlap 2.)
-//   2. one cluster barrier (arrive.release / wait.acquire): every CTA's
-//      plane n is visible cluster-wide; because X is double-buffered, the
-//      plane written at step n+1 is one nobody reads any more
-//   3. the four neighbours: left/right columns and the rows above/below from
-//      X (local shared memory, or the neighbour CTA's X through DSMEM,
-//      ld.shared::cluster, for the CTA's first/last row); the rows inside the
-//      block and the two columns inside a pair come from registers
-//   4. stencil, sources, support gather / adjoint injection, self-kernel
-//      increment and the stability max, in the reference's per-cell
-//      operation order (kernels.py:30-44, solver.py:154-186,
-//      gradients.py:237, 268, kernels.py:86-102), so results are
-//      bit-identical to the step kernels.  A face leading out of the grid
-//      has weight 0 and its neighbour is mirrored (u - u = +0), which is
-//      bit-identical to skipping the term (step_kernel.cuh).
+// Here thread t of CTA r owns a 2 x 2PC block of cells (rows r0, r0+1 of the
+// CTA's R rows; PC packed pairs of columns, PC = 2 by default: 512 threads)
+// and keeps u^{n-1}, u^n and the accumulator of its cells in registers as
+// packed pairs (fp32: one f32x2 register per pair, FADD2 / FFMA2; fp64: two
+// doubles), coef and the face weights in registers (fp32) or in a
+// thread-major shared-memory table (fp64).  Per step:
+//   1. publish u^n of the own block into the exchange plane X[n & 1] (the
+//      grid-edge threads also write their mirror copies into the pad / halo
+//      slots); the CTA's first / last row-pair pushes its boundary row into
+//      the neighbour CTA's halo row with st.async (complete_tx on the
+//      receiver's mbarrier); source amplitudes and adjoint forces are
+//      prefetched with cp.async
+//   2. one __syncthreads; the boundary row-pairs wait on the halo mbarrier.
+//      X is double-buffered, so a plane is rewritten two steps later, after
+//      every reader has published the step in between (no cluster barrier)
+//   3. per packed pair: neighbours from registers / X, stencil, sources,
+//      adjoint injection, self-kernel increment; trace gather and the
+//      stability max — in the reference's per-cell operation order
+//      (kernels.py:30-44, solver.py:154-186, gradients.py:237, 268,
+//      kernels.py:86-102), so results are bit-identical to the step kernels.
+//      A face leading out of the grid has weight 0 and its neighbour is
+//      mirrored (u - u = +0), bit-identical to skipping the term
+//      (step_kernel.cuh).
 // The window and the accumulator go back to global memory at the end.
 #pragma once
 

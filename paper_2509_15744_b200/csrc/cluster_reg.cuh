@@ -350,23 +350,26 @@ __global__ void __launch_bounds__(CR_THREADS / PC, 1) cluster_reg_kernel(const C
         auto xa = [&](int off) { return xb + off * (unsigned)sizeof(T); };
         // ---- 1: publish u^n (own plane, neighbours' halo rows); prefetch
         //      this step's forces / amplitudes ----
-        if (live) {
+        // rows beyond the grid publish nothing: the slot below the grid's
+        // last row holds that row's mirror copy (a partial last CTA)
+        if (acta) {
 #pragma unroll
             for (int p = 0; p < PC; ++p) {
                 O::sts(xa(oa + 2 * p), uc[0][p]);
-                O::sts(xa(ob + 2 * p), uc[1][p]);
                 // mirrored neighbours of the grid's edge cells (u - u = +0)
                 if (top) O::sts(xa(oa - XW + 2 * p), uc[0][p]);
+            }
+            if (medge) O::sts1(xa(oa - 1), O::lo(uc[0][0]));
+            if (pedge) O::sts1(xa(oa + CW), O::hi(uc[0][PC - 1]));
+        }
+        if (actb) {
+#pragma unroll
+            for (int p = 0; p < PC; ++p) {
+                O::sts(xa(ob + 2 * p), uc[1][p]);
                 if (bot) O::sts(xa(ob + XW + 2 * p), uc[1][p]);
             }
-            if (medge) {
-                O::sts1(xa(oa - 1), O::lo(uc[0][0]));
-                O::sts1(xa(ob - 1), O::lo(uc[1][0]));
-            }
-            if (pedge) {
-                O::sts1(xa(oa + CW), O::hi(uc[0][PC - 1]));
-                O::sts1(xa(ob + CW), O::hi(uc[1][PC - 1]));
-            }
+            if (medge) O::sts1(xa(ob - 1), O::lo(uc[1][0]));
+            if (pedge) O::sts1(xa(ob + CW), O::hi(uc[1][PC - 1]));
         }
 #pragma unroll
         for (int p = 0; p < PC; ++p) {

@@ -350,7 +350,8 @@ def test_two_step_long_chunks(W, knob, prec):
     assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
 
 
-@pytest.mark.parametrize("shape", [(256, 256), (101, 101), (33, 29), (40, 200), (97, 64)])
+@pytest.mark.parametrize("shape", [(256, 256), (101, 101), (33, 29), (40, 200), (97, 64),
+                                   (200, 200), (70, 96)])   # partial last CTAs
 @pytest.mark.parametrize("prec", ["single", "double"])
 def test_cluster_sweep_engine_bitwise(W, shape, prec):
     """Small 2D grids: the cluster-resident whole-sweep engine (one launch per

@@ -398,3 +398,43 @@ def test_cluster_sweep_engine_bitwise(W, shape, prec):
     shots = [(O.Source(src.node, 1e12, 1.5e6, 2), O.FwiShot(support, meas[0], dt))]
     _, grad, _ = O.gradient_superposed(omat, dt, n_steps, shots, 1e14, prec)
     assert bits_equal(on.gradient, grad)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_cluster_sweep_random_shapes(W, seed):
+    """Random 2D shapes that fit one cluster (odd widths, partial last CTAs,
+    a handful of rows), random source / sensors: the cluster sweep equals the
+    step kernels bit for bit, fp32 and fp64."""
+    from paper_2509_15744_b200 import engine
+
+    rng = np.random.default_rng(500 + seed)
+    while True:
+        shape = (int(rng.integers(3, 300)), int(rng.integers(3, 300)))
+        if shape[0] * shape[1] <= 65536:
+            break
+    dx, n_steps = 2e-4, int(rng.integers(20, 90))
+    dt = 0.5 * dx / 6000.0
+    grid = W.build_grid(shape, dx)
+    gamma = rng.uniform(0.3, 1.0, size=shape)
+    mat = W.MaterialModel.rho_scaled(gamma, grid, rho0=2700.0, c0=6000.0)
+    src = W.SourceSpec(node=tuple(int(rng.integers(0, n)) for n in shape), amplitude=1e12,
+                       frequency=3e6, cycles=2)
+    nodes = sorted({tuple(int(rng.integers(0, n)) for n in shape) for _ in range(12)})
+    meas = rng.normal(scale=1e-9, size=(1, len(nodes), n_steps))
+    problem = W.FwiProblem(grid=grid, time=W.TimeConfig(n_steps, dt), material=mat,
+                           sources=[src], sensors=W.SensorArray(nodes=nodes), measured=meas)
+    for prec in ("single", "double"):
+        cfg = W.SuperpositionConfig(k=1e14, precision=prec)
+        ctx = engine.get_context(grid, W.precision_dtype(prec))
+        try:
+            ctx.set_cluster(True)
+            ctx.reset_stats()
+            on = W.gradient_superposed(problem, mat, cfg)
+            launches = ctx.stats()["step_launches"]
+            ctx.set_cluster(False)
+            off = W.gradient_superposed(problem, mat, cfg)
+        finally:
+            ctx.set_cluster(None)
+        assert launches == 2, shape
+        assert bits_equal(on.gradient, off.gradient), (shape, prec)
+        assert on.cost == off.cost, (shape, prec)

@@ -408,9 +408,11 @@ def test_cluster_sweep_random_shapes(W, seed):
     from paper_2509_15744_b200 import engine
 
     rng = np.random.default_rng(500 + seed)
-    while True:
+    while True:   # one cluster: 16 CTAs of <= 512 threads with 2 x 4 cells each
         shape = (int(rng.integers(3, 300)), int(rng.integers(3, 300)))
-        if shape[0] * shape[1] <= 65536:
+        rows = -(-shape[0] // 16)
+        rows += rows % 2
+        if -(-shape[1] // 4) * (rows // 2) <= 512:
             break
     dx, n_steps = 2e-4, int(rng.integers(20, 90))
     dt = 0.5 * dx / 6000.0

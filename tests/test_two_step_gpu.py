@@ -408,11 +408,10 @@ def test_cluster_sweep_random_shapes(W, seed):
     from paper_2509_15744_b200 import engine
 
     rng = np.random.default_rng(500 + seed)
-    while True:   # one cluster: 16 CTAs of <= 512 threads with 2 x 4 cells each
+    while True:   # one cluster: 16 CTAs, threads of 2 (fp64) / 4 (fp32) rows x 4 cells
         shape = (int(rng.integers(3, 300)), int(rng.integers(3, 300)))
         rows = -(-shape[0] // 16)
-        rows += rows % 2
-        if -(-shape[1] // 4) * (rows // 2) <= 512:
+        if all(-(-shape[1] // 4) * (-(-rows // rt) * rt) <= 1024 for rt in (2, 4)):
             break
     dx, n_steps = 2e-4, int(rng.integers(20, 90))
     dt = 0.5 * dx / 6000.0
